@@ -1,0 +1,69 @@
+/* mtnlg_gemm.h — C ABI of the sm_100a tcgen05 GEMM used by every contraction of the
+ * tensor-sliced transformer layer (column-parallel QKV / fc1, row-parallel attention-out /
+ * fc2, their dgrad and wgrad, and the batched attention contractions).
+ *
+ * The reference (arxiv/paper_2201_11990, `proj/`) has no GEMM: the layer math is restated
+ * from PAPER.md:133-150 (Megatron tensor slicing). This header is the kernel-level boundary;
+ * the layer-level boundary is mtnlg.h.
+ *
+ * Logical problem, per batch index b in [0, batch):
+ *     D[b][m][n] = epilogue( alpha * sum_k A[b][m][k] * B[b][n][k] )
+ * A and B are bf16. "K-major" means k is the contiguous index:
+ *     A(m,k) = a[b*a_batch_stride + m*lda + k]          (a_mn_major = 0)
+ *     A(m,k) = a[b*a_batch_stride + k*lda + m]          (a_mn_major = 1)
+ * and likewise for B(n,k). D(m,n) = d[b*d_batch_stride + m*ldd + n]. All strides in elements.
+ * Requirements: 16-byte aligned base pointers and leading dimensions (multiples of 8 elements).
+ */
+#ifndef MTNLG_GEMM_H
+#define MTNLG_GEMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum mt_epilogue {
+  MT_EPI_STORE_BF16 = 0,   /* D = bf16(alpha*acc [+ bias[n]])                                  */
+  MT_EPI_BIAS_GELU = 1,    /* aux = bf16(acc + bias[n]) (pre-activation), D = bf16(gelu(aux))   */
+  MT_EPI_GELU_BWD = 2,     /* D = bf16(acc * gelu'(aux[m][n]))   (aux = saved pre-activation)    */
+  MT_EPI_STORE_F32 = 3,    /* D(f32) = alpha*acc                                                */
+  MT_EPI_ACCUM_F32 = 4     /* D(f32) += alpha*acc   (fp32 gradient accumulation across microbatches) */
+};
+
+enum mt_causal {
+  MT_CAUSAL_NONE = 0,
+  MT_CAUSAL_SKIP_UPPER_TILES = 1, /* skip D tiles entirely above the diagonal (n_begin > m_end-1)   */
+  MT_CAUSAL_K_LE_M = 2,           /* A is lower-triangular in (m,k): contract k < m_tile_end only    */
+  MT_CAUSAL_K_GE_M = 3            /* A is upper-triangular in (m,k): contract k >= m_tile_begin only */
+};
+
+typedef struct mt_gemm_args {
+  const void* a;
+  int64_t lda, a_batch_stride;
+  int32_t a_mn_major;
+  const void* b;
+  int64_t ldb, b_batch_stride;
+  int32_t b_mn_major;
+  void* d;
+  int64_t ldd, d_batch_stride;
+  int64_t m, n, k, batch;
+  float alpha;
+  int32_t epilogue; /* enum mt_epilogue */
+  int32_t causal;   /* enum mt_causal */
+  const void* bias; /* bf16[n] or NULL */
+  void* aux;        /* bf16, ld = ld_aux (pre-activation for the GeLU epilogues) */
+  int64_t ld_aux;
+  int32_t block_n;  /* 0 = auto; else 64/128/160/256 */
+} mt_gemm_args;
+
+/* Launches on `stream` (a cudaStream_t). Returns 0 on success, 1 on bad arguments, 2 on CUDA error. */
+int mt_gemm(const mt_gemm_args* args, void* stream);
+
+/* Number of kernel launches mt_gemm issues per call (always 1). */
+int mt_gemm_launches_per_call(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

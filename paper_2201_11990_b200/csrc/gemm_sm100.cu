@@ -1,0 +1,421 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a (bf16 in, fp32 accumulate in TMEM).
+//
+// Roles (256 threads, one CTA per SM):
+//   warp 0 lane 0 : TMA producer   — global -> smem ring of kStages {A,B} tiles (128B swizzle)
+//   warp 1 lane 0 : MMA issuer     — tcgen05.mma.cta_group::1 M=128, N=BN, K=16, accumulator in TMEM
+//   warp 2        : TMEM allocator — 2 accumulator buffers (double-buffered so the epilogue of
+//                                    tile i overlaps the main loop of tile i+1)
+//   warps 4..7    : epilogue       — tcgen05.ld TMEM -> registers, fused bias / GeLU / GeLU' /
+//                                    fp32 accumulate, vectorised global stores
+// Both operands may be K-major or MN-major (the UMMA descriptor major bits), which covers the
+// forward (TN), dgrad (NN) and wgrad (TT) products of the layer and the attention contractions
+// without any transpose kernels. The layer math these serve is restated from PAPER.md:133-150.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "../../include/mtnlg_gemm.h"
+#include "sm100_ptx.cuh"
+
+namespace mt {
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kThreads = 256;
+constexpr int kSmemBudget = 232448;  // 227 KB opt-in maximum per CTA
+
+struct GemmParams {
+  int m, n, k, batch;
+  int mblocks, nblocks, kblocks, total_tiles;
+  float alpha;
+  int epilogue, causal;
+  __nv_bfloat16* d_bf16;
+  float* d_f32;
+  long long ldd, d_batch_stride;
+  const __nv_bfloat16* bias;
+  __nv_bfloat16* aux;
+  long long ld_aux;
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int kBNAlloc = (BN + 63) / 64 * 64;
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = kBNAlloc * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 256;
+  static constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
+  static constexpr uint32_t kAccStride = kTmemCols / 2;  // column offset of accumulator buffer 1
+};
+
+__device__ __forceinline__ void tile_coords(const GemmParams& p, int t, int& b, int& mb, int& nb) {
+  const int per_batch = p.mblocks * p.nblocks;
+  b = t / per_batch;
+  const int rem = t - b * per_batch;
+  nb = rem / p.mblocks;
+  mb = rem - nb * p.mblocks;
+}
+
+template <int BN>
+__device__ __forceinline__ bool tile_valid(const GemmParams& p, int mb, int nb) {
+  if (p.causal == MT_CAUSAL_SKIP_UPPER_TILES) return nb * BN <= mb * kBM + kBM - 1;
+  return true;
+}
+
+__device__ __forceinline__ void k_range(const GemmParams& p, int mb, int& kb0, int& kb1) {
+  kb0 = 0;
+  kb1 = p.kblocks;
+  if (p.causal == MT_CAUSAL_K_LE_M) {
+    const int kend = min(p.k, (mb + 1) * kBM);
+    kb1 = (kend + kBK - 1) / kBK;
+  } else if (p.causal == MT_CAUSAL_K_GE_M) {
+    kb0 = (mb * kBM) / kBK;
+  }
+}
+
+template <int BN>
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int b, int row, int col0, uint32_t (&r)[32]) {
+  if (row >= p.m) return;
+  const float alpha = p.alpha;
+  const int ep = p.epilogue;
+  if (ep == MT_EPI_STORE_F32 || ep == MT_EPI_ACCUM_F32) {
+    float* dst = p.d_f32 + (long long)b * p.d_batch_stride + (long long)row * p.ldd + col0;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int c = col0 + v * 4;
+      if (c >= p.n) break;
+      float4 o = make_float4(alpha * __uint_as_float(r[4 * v + 0]), alpha * __uint_as_float(r[4 * v + 1]),
+                             alpha * __uint_as_float(r[4 * v + 2]), alpha * __uint_as_float(r[4 * v + 3]));
+      float4* q = reinterpret_cast<float4*>(dst + v * 4);
+      if (ep == MT_EPI_ACCUM_F32) {
+        const float4 old = *q;
+        o.x += old.x;
+        o.y += old.y;
+        o.z += old.z;
+        o.w += old.w;
+      }
+      *q = o;
+    }
+    return;
+  }
+  __nv_bfloat16* dst = p.d_bf16 + (long long)b * p.d_batch_stride + (long long)row * p.ldd + col0;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int c = col0 + v * 8;
+    if (c >= p.n) break;
+    float x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = __uint_as_float(r[8 * v + j]);
+    if (ep == MT_EPI_STORE_BF16) {
+      if (p.bias != nullptr) {
+        const uint4 bv = *reinterpret_cast<const uint4*>(p.bias + c);
+        const uint32_t bw[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = unpack_bf16x2(bw[j]);
+          x[2 * j] = alpha * x[2 * j] + f.x;
+          x[2 * j + 1] = alpha * x[2 * j + 1] + f.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] *= alpha;
+      }
+    } else if (ep == MT_EPI_BIAS_GELU) {
+      const uint4 bv = *reinterpret_cast<const uint4*>(p.bias + c);
+      const uint32_t bw[4] = {bv.x, bv.y, bv.z, bv.w};
+      uint32_t pre[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = unpack_bf16x2(bw[j]);
+        pre[j] = pack_bf16x2(alpha * x[2 * j] + f.x, alpha * x[2 * j + 1] + f.y);
+        const float2 pr = unpack_bf16x2(pre[j]);  // GeLU of the stored (bf16) pre-activation
+        x[2 * j] = gelu_tanh(pr.x);
+        x[2 * j + 1] = gelu_tanh(pr.y);
+      }
+      *reinterpret_cast<uint4*>(p.aux + (long long)row * p.ld_aux + c) = make_uint4(pre[0], pre[1], pre[2], pre[3]);
+    } else {  // MT_EPI_GELU_BWD
+      const uint4 av = *reinterpret_cast<const uint4*>(p.aux + (long long)row * p.ld_aux + c);
+      const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = unpack_bf16x2(aw[j]);
+        x[2 * j] = alpha * x[2 * j] * gelu_tanh_grad(f.x);
+        x[2 * j + 1] = alpha * x[2 * j + 1] * gelu_tanh_grad(f.y);
+      }
+    }
+    *reinterpret_cast<uint4*>(dst + v * 8) =
+        make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]), pack_bf16x2(x[6], x[7]));
+  }
+}
+
+template <int BN, bool kAMN, bool kBMN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                      const GemmParams p) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_base = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  // bars[0..S) full, bars[S..2S) empty, bars[2S..2S+2) tmem_full, bars[2S+2..2S+4) tmem_empty
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(smem_u32(&bars[s]), 1);
+      mbar_init(smem_u32(&bars[C::kStages + s]), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&bars[2 * C::kStages + a]), 1);
+      mbar_init(smem_u32(&bars[2 * C::kStages + 2 + a]), 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<C::kTmemCols>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      constexpr uint32_t kTx = C::kABytes + (kBMN ? C::kBBytes : BN * kBK * 2);
+      uint32_t stage = 0, phase = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        int b, mb, nb;
+        tile_coords(p, t, b, mb, nb);
+        if (!tile_valid<BN>(p, mb, nb)) continue;
+        int kb0, kb1;
+        k_range(p, mb, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(smem_u32(&bars[C::kStages + stage]), phase ^ 1);
+          const uint32_t full = smem_u32(&bars[stage]);
+          mbar_arrive_expect_tx(full, kTx);
+          const uint32_t sa = smem_u32(stage_base + stage * C::kStageBytes);
+          const uint32_t sb = sa + C::kABytes;
+          if (kAMN) {
+            tma_load_3d(sa, &tmap_a, full, mb * kBM, kb * kBK, b);
+            tma_load_3d(sa + 8192, &tmap_a, full, mb * kBM + 64, kb * kBK, b);
+          } else {
+            tma_load_3d(sa, &tmap_a, full, kb * kBK, mb * kBM, b);
+          }
+          if (kBMN) {
+#pragma unroll
+            for (int c = 0; c < C::kBNAlloc / 64; ++c) tma_load_3d(sb + c * 8192, &tmap_b, full, nb * BN + c * 64, kb * kBK, b);
+          } else {
+            tma_load_3d(sb, &tmap_b, full, kb * kBK, nb * BN, b);
+          }
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN, kAMN ? 1 : 0, kBMN ? 1 : 0);
+      uint32_t stage = 0, phase = 0, it = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        int b, mb, nb;
+        tile_coords(p, t, b, mb, nb);
+        if (!tile_valid<BN>(p, mb, nb)) continue;
+        int kb0, kb1;
+        k_range(p, mb, kb0, kb1);
+        const uint32_t acc = it & 1, acc_phase = (it >> 1) & 1;
+        mbar_wait(smem_u32(&bars[2 * C::kStages + 2 + acc]), acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * C::kAccStride;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(smem_u32(&bars[stage]), phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(stage_base + stage * C::kStageBytes);
+          const uint32_t sb = sa + C::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t ad = kAMN ? umma_desc_sw128(sa + kk * 2048, 8192, 1024) : umma_desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t bd = kBMN ? umma_desc_sw128(sb + kk * 2048, 8192, 1024) : umma_desc_sw128(sb + kk * 32, 16, 1024);
+            umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(smem_u32(&bars[C::kStages + stage]));
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(smem_u32(&bars[2 * C::kStages + acc]));
+        ++it;
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------------- epilogue
+    const uint32_t quad = warp - 4;
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      int b, mb, nb;
+      tile_coords(p, t, b, mb, nb);
+      if (!tile_valid<BN>(p, mb, nb)) continue;
+      const uint32_t acc = it & 1, acc_phase = (it >> 1) & 1;
+      mbar_wait(smem_u32(&bars[2 * C::kStages + acc]), acc_phase);
+      tc_fence_after();
+      const int row = mb * kBM + quad * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((quad * 32) << 16) + acc * C::kAccStride + c * 32, r);
+        tmem_ld_wait();
+        epilogue_chunk<BN>(p, b, row, nb * BN + c * 32, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
+      ++it;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<C::kTmemCols>(tmem_base);
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(ptr);
+  });
+  return fn;
+}
+
+// 3-D bf16 tensor map: dims (inner, outer, batch), 128B swizzle, box (64, box_outer, 1).
+bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t batch, uint64_t ld,
+              uint64_t batch_stride, uint32_t box_outer) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {inner, outer, batch};
+  uint64_t bs = batch_stride;
+  if (batch <= 1) bs = (ld * outer + 7) / 8 * 8;
+  if (bs == 0) bs = 8;
+  cuuint64_t strides[2] = {ld * 2, bs * 2};
+  cuuint32_t box[3] = {64, box_outer, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, bool kAMN, bool kBMN>
+int launch(const mt_gemm_args& a, cudaStream_t stream) {
+  using C = Cfg<BN>;
+  CUtensorMap ma, mb;
+  const int m = (int)a.m, n = (int)a.n, k = (int)a.k, batch = (int)a.batch;
+  bool ok = kAMN ? make_map(&ma, a.a, m, k, batch, a.lda, a.a_batch_stride, 64)
+                 : make_map(&ma, a.a, k, m, batch, a.lda, a.a_batch_stride, kBM);
+  ok = ok && (kBMN ? make_map(&mb, a.b, n, k, batch, a.ldb, a.b_batch_stride, 64)
+                   : make_map(&mb, a.b, k, n, batch, a.ldb, a.b_batch_stride, BN));
+  if (!ok) return 1;
+  GemmParams p{};
+  p.m = m;
+  p.n = n;
+  p.k = k;
+  p.batch = batch;
+  p.mblocks = (m + kBM - 1) / kBM;
+  p.nblocks = (n + BN - 1) / BN;
+  p.kblocks = (k + kBK - 1) / kBK;
+  p.total_tiles = p.mblocks * p.nblocks * batch;
+  p.alpha = a.alpha;
+  p.epilogue = a.epilogue;
+  p.causal = a.causal;
+  p.d_bf16 = static_cast<__nv_bfloat16*>(a.d);
+  p.d_f32 = static_cast<float*>(a.d);
+  p.ldd = a.ldd;
+  p.d_batch_stride = a.d_batch_stride;
+  p.bias = static_cast<const __nv_bfloat16*>(a.bias);
+  p.aux = static_cast<__nv_bfloat16*>(a.aux);
+  p.ld_aux = a.ld_aux;
+  auto kern = gemm_sm100_kernel<BN, kAMN, kBMN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
+      return 2;
+    attr_set = true;
+  }
+  const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
+  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+template <int BN>
+int dispatch_major(const mt_gemm_args& a, cudaStream_t s) {
+  if (a.a_mn_major) return a.b_mn_major ? launch<BN, true, true>(a, s) : launch<BN, true, false>(a, s);
+  return a.b_mn_major ? launch<BN, false, true>(a, s) : launch<BN, false, false>(a, s);
+}
+
+}  // namespace
+}  // namespace mt
+
+extern "C" int mt_gemm_launches_per_call(void) { return 1; }
+
+extern "C" int mt_gemm(const mt_gemm_args* args, void* stream) {
+  if (args == nullptr) return 1;
+  const mt_gemm_args& a = *args;
+  if (a.m <= 0 || a.n <= 0 || a.k <= 0 || a.batch <= 0) return 1;
+  if (a.a == nullptr || a.b == nullptr || a.d == nullptr) return 1;
+  if ((a.n % 8) != 0 || (a.lda % 8) != 0 || (a.ldb % 8) != 0 || (a.ldd % 8) != 0) return 1;
+  if ((reinterpret_cast<uintptr_t>(a.a) | reinterpret_cast<uintptr_t>(a.b) | reinterpret_cast<uintptr_t>(a.d)) & 15)
+    return 1;
+  if ((a.epilogue == MT_EPI_BIAS_GELU || a.epilogue == MT_EPI_GELU_BWD) && (a.aux == nullptr || a.ld_aux % 8))
+    return 1;
+  if (a.epilogue == MT_EPI_BIAS_GELU && a.bias == nullptr) return 1;
+  if ((a.epilogue == MT_EPI_BIAS_GELU || a.epilogue == MT_EPI_GELU_BWD) && a.batch != 1) return 1;
+  if (a.epilogue < 0 || a.epilogue > MT_EPI_ACCUM_F32 || a.causal < 0 || a.causal > MT_CAUSAL_K_GE_M) return 1;
+  int bn = a.block_n;
+  if (bn == 0) bn = a.n <= 64 ? 64 : (a.n <= 128 ? 128 : (a.n == 160 ? 160 : 256));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (bn) {
+    case 64:
+      return mt::dispatch_major<64>(a, s);
+    case 128:
+      return mt::dispatch_major<128>(a, s);
+    case 160:
+      return mt::dispatch_major<160>(a, s);
+    case 256:
+      return mt::dispatch_major<256>(a, s);
+    default:
+      return 1;
+  }
+}
