@@ -1,0 +1,181 @@
+/* mtnlg.h — C ABI of the B200-native MT-NLG training-step runtime (libmtnlg.so).
+ *
+ * Drop-in boundary for the hot path of arxiv/paper_2201_11990: the reference keeps only the
+ * analytical planner (proj/include/curator/planner.hpp:7-128, C++, statically linked) and has no
+ * runtime below it. This ABI exposes (1) the planner's partition and
+ * schedule functions in plain C so any FFI can bind them, and (2) the GPU runtime that executes
+ * the layout the planner decides: the tensor-sliced transformer layer forward/backward on sm_100a
+ * kernels, its TP all-reduces, the 1F1B pipeline and the DP gradient all-reduce over NCCL.
+ *
+ * Conventions: plain pointers and sizes, no exceptions across the boundary.
+ * Every function returns MT_OK (0), MT_ERR_CONFIG (1: bad argument / layout — the reference's
+ * ConfigError / std::invalid_argument) or MT_ERR_DATA (2: CUDA / NCCL / data failure — the
+ * reference's DataError); mt_last_error() holds the message (thread-local).
+ * Streams are cudaStream_t passed as void*. The caller owns host buffers and device buffers it
+ * passes in; the library owns what *_create allocates and frees it in *_destroy.
+ */
+#ifndef MTNLG_H
+#define MTNLG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "mtnlg_gemm.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { MT_OK = 0, MT_ERR_CONFIG = 1, MT_ERR_DATA = 2 };
+
+const char* mt_last_error(void);
+const char* mt_version(void);
+
+/* ------------------------------------------------------------------ planner (host, pure) */
+/* Mirrors curator::ClusterTopology / ParallelConfig / RankPlacement (planner.hpp:18-36, 84-90). */
+typedef struct mt_cluster_topology {
+  int32_t nodes, gpus_per_node;
+  double intra_node_bw, inter_node_bw, peak_flops_per_gpu;
+} mt_cluster_topology;
+
+typedef struct mt_parallel_config {
+  int32_t tensor, pipeline, data, batch, micro_batches;
+} mt_parallel_config;
+
+typedef struct mt_rank_placement {
+  int32_t data, pipeline, tensor, node, gpu;
+} mt_rank_placement;
+
+typedef struct mt_model_shape {
+  double parameters;
+  int32_t layers, hidden, heads, sequence, vocab;
+} mt_model_shape;
+
+/* curator::map_topology (reference proj/src/planner.cpp:84-128). Writes min(cap, n) placements,
+ * *n = TP*PP*DP. Errors: MT_ERR_CONFIG with the reference's message. */
+int mt_map_topology(const mt_cluster_topology* topo, const mt_parallel_config* par, mt_rank_placement* out,
+                    int64_t cap, int64_t* n);
+/* curator::pipeline_efficiency (planner.cpp:27-32) */
+int mt_pipeline_efficiency(int32_t micro_batches, int32_t stages, double* out);
+/* curator::estimated_tflops_per_gpu (planner.cpp:39-57) */
+int mt_estimated_tflops_per_gpu(const mt_model_shape* shape, const mt_parallel_config* par,
+                                const mt_cluster_topology* topo, double iteration_seconds, double* out);
+/* curator::weight_init_std, activation_bytes, model_state_bytes, lr_at, batch_size_at */
+int mt_weight_init_std(double hidden, double* out);
+int mt_activation_bytes(double batch, double layers, double sequence, double hidden, double* out);
+int mt_model_state_bytes(double parameters, double* out);
+int mt_lr_at(double tokens_seen, double* out);
+int mt_batch_size_at(double tokens_seen, int32_t* out);
+/* curator::parse_planner_config + build_plan_report + render_plan_report: writes up to cap bytes
+ * (NUL-terminated) of the rendered report; *len = full length. */
+int mt_plan_report(const char* config_path, int32_t as_json, char* out, int64_t cap, int64_t* len);
+
+/* 1F1B (PipeDream-Flush) op order of one stage: warmup = min(PP-stage-1, MB)
+ * forwards, then MB-warmup (F, B) pairs, then warmup backwards. kind 0 = forward, 1 = backward. */
+typedef struct mt_pipe_op {
+  int32_t kind, micro_batch;
+} mt_pipe_op;
+int mt_pipeline_schedule(int32_t stage, int32_t stages, int32_t micro_batches, mt_pipe_op* out, int32_t cap,
+                         int32_t* n);
+/* Unit-cost simulation of the 1F1B schedule over all stages with integer op costs; *makespan in
+ * cost units. Pins pipeline_efficiency: makespan == (MB + PP - 1) * (t_fwd + t_bwd). */
+int mt_pipeline_simulate(int32_t stages, int32_t micro_batches, int32_t t_fwd, int32_t t_bwd, int64_t* makespan);
+
+/* ------------------------------------------------------------------ layer parameters */
+enum mt_param {
+  MT_P_LN1_GAMMA = 0, MT_P_LN1_BETA, MT_P_QKV_W, MT_P_QKV_B, MT_P_PROJ_W, MT_P_PROJ_B,
+  MT_P_LN2_GAMMA, MT_P_LN2_BETA, MT_P_FC1_W, MT_P_FC1_B, MT_P_FC2_W, MT_P_FC2_B, MT_P_COUNT
+};
+
+typedef struct mt_layer_desc {
+  int32_t hidden, heads, seq, micro_batch; /* h, H, s, b */
+  int32_t tp_size, tp_rank;
+  int32_t ffn_mult;                         /* 4 */
+  float dropout_hidden, dropout_attn, ln_eps;
+  uint64_t seed;
+  uint32_t layer_index;                     /* global layer id: keys weights and dropout sites */
+} mt_layer_desc;
+
+/* TP shard of parameter `param` (Megatron layout): global [rows, cols], this
+ * rank's block starts at (row0, col0) with shape [shard_rows, shard_cols]. Pure. */
+int mt_param_shard(const mt_layer_desc* d, int32_t param, int64_t global_shape[2], int64_t shard_origin[2],
+                   int64_t shard_shape[2]);
+/* Seed key of a parameter / synthetic stream: mix64(seed, fnv1a64(name) ^ (layer << 32 | micro_batch)). */
+uint64_t mt_stream_key(uint64_t seed, const char* name, uint32_t layer, uint32_t micro_batch);
+/* Dropout threshold used by the mask definition in include/curator/dropout.hpp. */
+uint32_t mt_dropout_threshold16(double p);
+
+/* ------------------------------------------------------------------ runtime */
+typedef struct mt_ctx mt_ctx;
+typedef struct mt_layer mt_layer;
+
+int mt_ctx_create(int32_t device, mt_ctx** out);
+int mt_ctx_destroy(mt_ctx* ctx);
+/* NCCL bootstrap: rank 0 creates the id, the caller broadcasts the 128 bytes (e.g. over
+ * torch.distributed's store), every rank calls mt_ctx_init_comm. The TP / PP / DP communicators
+ * are split from the world communicator by curator::map_topology(nodes=1, gpus_per_node=world). */
+int mt_nccl_unique_id(unsigned char out[128]);
+int mt_ctx_init_comm(mt_ctx* ctx, const unsigned char id[128], int32_t world_size, int32_t rank,
+                     const mt_parallel_config* par);
+int mt_ctx_placement(const mt_ctx* ctx, mt_rank_placement* out);
+
+int mt_layer_create(mt_ctx* ctx, const mt_layer_desc* d, mt_layer** out);
+int mt_layer_destroy(mt_layer* l);
+/* On-device seeded init of this rank's shard (weights ~ N(0, sqrt(1/(3h))), biases and LN beta
+ * ~ N(0, 0.02), LN gamma ~ 1 + N(0, 0.02)); identical global tensors for every TP degree. */
+int mt_layer_init_params(mt_layer* l, void* stream);
+/* Copy this rank's shard out of a full (global, row-major, bf16) host tensor. */
+int mt_layer_set_param(mt_layer* l, int32_t param, const void* host_global_bf16);
+/* Read back this rank's bf16 parameter shard (shard_shape elements, raw bf16 bits). */
+int mt_layer_get_param(mt_layer* l, int32_t param, void* host_shard_bf16);
+/* Read back this rank's fp32 gradient shard (shard_shape elements). */
+int mt_layer_get_grad(mt_layer* l, int32_t param, float* host_shard);
+int mt_layer_zero_grads(mt_layer* l, void* stream);
+/* Forward of one microbatch: x, y device bf16 [b*s, h]. x must stay valid until the matching
+ * backward (it is the LayerNorm-1 input the backward re-reads). Activations are saved per
+ * microbatch id. */
+int mt_layer_forward(mt_layer* l, const void* x, void* y, uint32_t micro_batch, void* stream);
+/* Backward of one microbatch (frees its saved activations): dy -> dx (device bf16 [b*s, h]);
+ * parameter gradients accumulate in fp32. */
+int mt_layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t micro_batch, void* stream);
+/* Kernel launches one forward / backward issues (for the bench's gpu_launches claim). */
+int mt_layer_launch_counts(const mt_layer* l, int32_t* fwd, int32_t* bwd);
+/* Device pointer to the flat fp32 gradient buffer of the layer and its element count. */
+int mt_layer_grad_buffer(mt_layer* l, float** ptr, int64_t* n);
+
+/* loss += sum 0.5 (y - t)^2 / n and dy = (y - t) / n over n bf16 elements. */
+int mt_mse_loss(const void* y, const void* t, void* dy, float* loss_dev, int64_t n, void* stream);
+/* out[i] = bf16(mean + std * normal_at(key, i)), i < n. */
+int mt_fill_normal(void* out, int64_t n, uint64_t key, float mean, float std, void* stream);
+
+/* Collectives on the context's groups (device buffers, stream-ordered). */
+int mt_tp_allreduce_bf16(mt_ctx* ctx, void* buf, int64_t n, void* stream);
+int mt_dp_allreduce_f32(mt_ctx* ctx, float* buf, int64_t n, int32_t average, void* stream);
+int mt_pp_send_bf16(mt_ctx* ctx, const void* buf, int64_t n, int32_t peer_stage, void* stream);
+int mt_pp_recv_bf16(mt_ctx* ctx, void* buf, int64_t n, int32_t peer_stage, void* stream);
+
+/* ------------------------------------------------------------------ pipeline stage (1F1B driver) */
+typedef struct mt_stage mt_stage;
+typedef struct mt_stage_desc {
+  mt_layer_desc layer;          /* template: layer_index is filled per layer; tp fields from ctx */
+  int32_t layers;               /* total transformer layers of the model (split evenly over PP) */
+  int32_t micro_batches;        /* MB per iteration per DP replica */
+} mt_stage_desc;
+
+int mt_stage_create(mt_ctx* ctx, const mt_stage_desc* d, mt_stage** out);
+int mt_stage_destroy(mt_stage* st);
+int mt_stage_layer(mt_stage* st, int32_t i, mt_layer** out);
+/* One training iteration of this rank: zero grads, 1F1B over MB microbatches (first stage reads
+ * inputs_host[mb] — host bf16 [b*s*h] per microbatch, copied in-stream; last stage computes the
+ * synthetic MSE loss against targets_host), PP send/recv, TP all-reduces inside the layers, then
+ * the DP gradient all-reduce (mean). *loss_out = summed loss over microbatches (last stage,
+ * DP-averaged), else 0. Host buffers should be pinned. If inputs_host is NULL the stage
+ * generates inputs/targets on device from the seed (no host traffic). */
+int mt_stage_train_step(mt_stage* st, const void* inputs_host, const void* targets_host, float* loss_out,
+                        void* stream);
+int mt_stage_launch_count(const mt_stage* st, int64_t* launches_per_step);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,4 +1,4 @@
-"""ctypes binding of libmtnlg.so (the C ABI declared in include/*.h).
+"""ctypes binding of libmtnlg.so (the C ABI declared in include/mtnlg.h and include/mtnlg_gemm.h).
 
 The product path has no fallback: if the library is missing, every entry point raises.
 """
@@ -9,6 +9,8 @@ from pathlib import Path
 
 _LIB_PATH = Path(__file__).resolve().parent / "libmtnlg.so"
 _lib = None
+
+MT_OK, MT_ERR_CONFIG, MT_ERR_DATA = 0, 1, 2
 
 
 class GemmArgs(C.Structure):
@@ -26,16 +28,123 @@ EPI_STORE_BF16, EPI_BIAS_GELU, EPI_GELU_BWD, EPI_STORE_F32, EPI_ACCUM_F32 = rang
 CAUSAL_NONE, CAUSAL_SKIP_UPPER_TILES, CAUSAL_K_LE_M, CAUSAL_K_GE_M = range(4)
 
 
+class ClusterTopology(C.Structure):
+    _fields_ = [("nodes", C.c_int32), ("gpus_per_node", C.c_int32), ("intra_node_bw", C.c_double),
+                ("inter_node_bw", C.c_double), ("peak_flops_per_gpu", C.c_double)]
+
+
+class ParallelConfig(C.Structure):
+    _fields_ = [("tensor", C.c_int32), ("pipeline", C.c_int32), ("data", C.c_int32), ("batch", C.c_int32),
+                ("micro_batches", C.c_int32)]
+
+
+class RankPlacement(C.Structure):
+    _fields_ = [("data", C.c_int32), ("pipeline", C.c_int32), ("tensor", C.c_int32), ("node", C.c_int32),
+                ("gpu", C.c_int32)]
+
+
+class ModelShape(C.Structure):
+    _fields_ = [("parameters", C.c_double), ("layers", C.c_int32), ("hidden", C.c_int32), ("heads", C.c_int32),
+                ("sequence", C.c_int32), ("vocab", C.c_int32)]
+
+
+class PipeOp(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("micro_batch", C.c_int32)]
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [("hidden", C.c_int32), ("heads", C.c_int32), ("seq", C.c_int32), ("micro_batch", C.c_int32),
+                ("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("ffn_mult", C.c_int32),
+                ("dropout_hidden", C.c_float), ("dropout_attn", C.c_float), ("ln_eps", C.c_float),
+                ("seed", C.c_uint64), ("layer_index", C.c_uint32)]
+
+
+class StageDesc(C.Structure):
+    _fields_ = [("layer", LayerDesc), ("layers", C.c_int32), ("micro_batches", C.c_int32)]
+
+
+P = C.c_void_p
+I32, I64, U32, U64, F32, F64 = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_float, C.c_double
+PI32, PI64, PF32, PF64 = C.POINTER(I32), C.POINTER(I64), C.POINTER(F32), C.POINTER(F64)
+
+_SIGS = {
+    "mt_gemm": (C.c_int, [C.POINTER(GemmArgs), P]),
+    "mt_gemm_launches_per_call": (C.c_int, []),
+    "mt_last_error": (C.c_char_p, []),
+    "mt_version": (C.c_char_p, []),
+    "mt_map_topology": (C.c_int, [C.POINTER(ClusterTopology), C.POINTER(ParallelConfig), C.POINTER(RankPlacement),
+                                  I64, PI64]),
+    "mt_pipeline_efficiency": (C.c_int, [I32, I32, PF64]),
+    "mt_estimated_tflops_per_gpu": (C.c_int, [C.POINTER(ModelShape), C.POINTER(ParallelConfig),
+                                              C.POINTER(ClusterTopology), F64, PF64]),
+    "mt_weight_init_std": (C.c_int, [F64, PF64]),
+    "mt_activation_bytes": (C.c_int, [F64, F64, F64, F64, PF64]),
+    "mt_model_state_bytes": (C.c_int, [F64, PF64]),
+    "mt_lr_at": (C.c_int, [F64, PF64]),
+    "mt_batch_size_at": (C.c_int, [F64, PI32]),
+    "mt_plan_report": (C.c_int, [C.c_char_p, I32, C.c_char_p, I64, PI64]),
+    "mt_pipeline_schedule": (C.c_int, [I32, I32, I32, C.POINTER(PipeOp), I32, PI32]),
+    "mt_pipeline_simulate": (C.c_int, [I32, I32, I32, I32, PI64]),
+    "mt_param_shard": (C.c_int, [C.POINTER(LayerDesc), I32, PI64, PI64, PI64]),
+    "mt_stream_key": (U64, [U64, C.c_char_p, U32, U32]),
+    "mt_dropout_threshold16": (U32, [F64]),
+    "mt_ctx_create": (C.c_int, [I32, C.POINTER(P)]),
+    "mt_ctx_destroy": (C.c_int, [P]),
+    "mt_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "mt_ctx_init_comm": (C.c_int, [P, C.c_char_p, I32, I32, C.POINTER(ParallelConfig)]),
+    "mt_ctx_placement": (C.c_int, [P, C.POINTER(RankPlacement)]),
+    "mt_layer_create": (C.c_int, [P, C.POINTER(LayerDesc), C.POINTER(P)]),
+    "mt_layer_destroy": (C.c_int, [P]),
+    "mt_layer_init_params": (C.c_int, [P, P]),
+    "mt_layer_set_param": (C.c_int, [P, I32, P]),
+    "mt_layer_get_grad": (C.c_int, [P, I32, PF32]),
+    "mt_layer_get_param": (C.c_int, [P, I32, P]),
+    "mt_layer_zero_grads": (C.c_int, [P, P]),
+    "mt_layer_forward": (C.c_int, [P, P, P, U32, P]),
+    "mt_layer_backward": (C.c_int, [P, P, P, U32, P]),
+    "mt_layer_launch_counts": (C.c_int, [P, PI32, PI32]),
+    "mt_layer_grad_buffer": (C.c_int, [P, C.POINTER(PF32), PI64]),
+    "mt_mse_loss": (C.c_int, [P, P, P, P, I64, P]),
+    "mt_fill_normal": (C.c_int, [P, I64, U64, F32, F32, P]),
+    "mt_tp_allreduce_bf16": (C.c_int, [P, P, I64, P]),
+    "mt_dp_allreduce_f32": (C.c_int, [P, P, I64, I32, P]),
+    "mt_pp_send_bf16": (C.c_int, [P, P, I64, I32, P]),
+    "mt_pp_recv_bf16": (C.c_int, [P, P, I64, I32, P]),
+    "mt_stage_create": (C.c_int, [P, C.POINTER(StageDesc), C.POINTER(P)]),
+    "mt_stage_destroy": (C.c_int, [P]),
+    "mt_stage_layer": (C.c_int, [P, I32, C.POINTER(P)]),
+    "mt_stage_train_step": (C.c_int, [P, P, P, PF32, P]),
+    "mt_stage_launch_count": (C.c_int, [P, PI64]),
+}
+
+EXPORTED = sorted(_SIGS)
+
+
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
         if not _LIB_PATH.exists():
             raise RuntimeError(f"native library {_LIB_PATH} is missing: run `python -m paper_2201_11990_b200.build`")
-        _lib = C.CDLL(str(_LIB_PATH))
-        _declare(_lib)
+        L = C.CDLL(str(_LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype, fn.argtypes = res, args
+        _lib = L
     return _lib
 
 
-def _declare(L: C.CDLL) -> None:
-    L.mt_gemm.argtypes = [C.POINTER(GemmArgs), C.c_void_p]
-    L.mt_gemm.restype = C.c_int
+class ConfigError(ValueError):
+    """Status 1: bad configuration / argument (the reference's ConfigError / std::invalid_argument)."""
+
+
+class DataError(RuntimeError):
+    """Status 2: CUDA / NCCL / data failure (the reference's DataError)."""
+
+
+def check(rc: int) -> None:
+    if rc == MT_OK:
+        return
+    msg = (lib().mt_last_error() or b"").decode()
+    if rc == MT_ERR_CONFIG:
+        raise ConfigError(msg)
+    raise DataError(msg)

@@ -1,0 +1,574 @@
+// HBM-bound kernels of the tensor-sliced transformer layer (sm_100a).
+//
+// All kernels move bf16 in 16-byte vectors (8 elements per thread per access), reduce with warp
+// shuffles, and keep row data in registers between the passes of a row reduction, so every
+// element is read from HBM once and written once. Column reductions (bias / LayerNorm parameter
+// gradients) are two-stage and deterministic: per-split partials in a workspace, then a fixed-order
+// sum into the fp32 gradient accumulator.
+//
+// Layer math restated from PAPER.md:133-150 (Megatron tensor slicing) — the reference has no
+// implementation of it; the CPU restatement the tests compare against is oracle/layer_oracle.cpp.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "curator/dropout.hpp"
+#include "kernels.cuh"
+
+namespace mt {
+namespace {
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[j]);
+    const float2 p = __bfloat1622float2(h);
+    f[2 * j] = p.x;
+    f[2 * j + 1] = p.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+    w[j] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Sum over the block; `red` is >= 32 floats of shared memory, reused across calls.
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float t = lane < nw ? red[lane] : 0.f;
+  return warp_sum(t);
+}
+
+// Drop mask for 8 consecutive elements starting at idx (idx % 4 == 0): two mix64 groups.
+__device__ __forceinline__ uint32_t keep_mask8(uint64_t seed, uint64_t idx, uint32_t thresh16) {
+  if (thresh16 == 0) return 0xffu;
+  uint32_t m = 0;
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const uint64_t bits = curator::mix64(seed, (idx >> 2) + g);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (((bits >> (16 * q)) & 0xffffu) >= thresh16) m |= 1u << (4 * g + q);
+  }
+  return m;
+}
+
+// ------------------------------------------------------------------ LayerNorm
+template <int VPT>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const uint4* __restrict__ x, const uint4* __restrict__ gamma,
+                                                     const uint4* __restrict__ beta, uint4* __restrict__ y,
+                                                     float* __restrict__ mean, float* __restrict__ rstd, int nvec,
+                                                     float inv_h, float eps) {
+  __shared__ float red[32];
+  const size_t row = blockIdx.x;
+  const uint4* xr = x + row * nvec;
+  float v[VPT][8];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int idx = i * blockDim.x + threadIdx.x;
+    if (idx < nvec) {
+      unpack8(xr[idx], v[i]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[i][j];
+    }
+  }
+  const float mu = block_sum(s, red) * inv_h;
+  float sq = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int idx = i * blockDim.x + threadIdx.x;
+    if (idx < nvec) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float d = v[i][j] - mu;
+        sq += d * d;
+      }
+    }
+  }
+  const float rs = rsqrtf(block_sum(sq, red) * inv_h + eps);
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int idx = i * blockDim.x + threadIdx.x;
+    if (idx < nvec) {
+      float g[8], b[8], o[8];
+      unpack8(gamma[idx], g);
+      unpack8(beta[idx], b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mu) * rs * g[j] + b[j];
+      y[row * nvec + idx] = pack8(o);
+    }
+  }
+  if (threadIdx.x == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+template <int VPT>
+__global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ x,
+                                                        const uint4* __restrict__ gamma, const float* __restrict__ mean,
+                                                        const float* __restrict__ rstd, const uint4* __restrict__ resid,
+                                                        uint4* __restrict__ dx, int nvec, float inv_h) {
+  __shared__ float red[32];
+  const size_t row = blockIdx.x;
+  const float mu = mean[row], rs = rstd[row];
+  float g[VPT][8], xh[VPT][8];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int idx = i * blockDim.x + threadIdx.x;
+    if (idx < nvec) {
+      float d[8], xv[8], gm[8];
+      unpack8(dy[row * nvec + idx], d);
+      unpack8(x[row * nvec + idx], xv);
+      unpack8(gamma[idx], gm);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        xh[i][j] = (xv[j] - mu) * rs;
+        g[i][j] = d[j] * gm[j];
+        s1 += g[i][j];
+        s2 += g[i][j] * xh[i][j];
+      }
+    }
+  }
+  const float m1 = block_sum(s1, red) * inv_h;
+  const float m2 = block_sum(s2, red) * inv_h;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int idx = i * blockDim.x + threadIdx.x;
+    if (idx < nvec) {
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = rs * (g[i][j] - m1 - xh[i][j] * m2);
+      if (resid != nullptr) {
+        float r[8];
+        unpack8(resid[row * nvec + idx], r);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] += r[j];
+      }
+      dx[row * nvec + idx] = pack8(o);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ column reductions
+// Stage 1: block (32 x 8): threadIdx.x -> 8-column vector, threadIdx.y -> row lane.
+// Each (blockIdx.y) split covers rows [split*rows_per, ...). Partials -> ws[out][split][col].
+constexpr int kColTY = 8;
+
+enum ColOp { kColSum = 0, kColLnParams = 1, kColDropout = 2 };
+
+template <int OP>
+__global__ void __launch_bounds__(256) colsum_stage1(const uint4* __restrict__ a, long long lda_vec,
+                                                     const uint4* __restrict__ xin, const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, uint4* __restrict__ out_dz,
+                                                     float* __restrict__ ws, int rows, int nvec, int rows_per,
+                                                     uint64_t seed, uint32_t thresh16, float scale) {
+  constexpr int NO = OP == kColLnParams ? 2 : 1;
+  __shared__ float part[NO][kColTY][32][9];
+  const int cv = blockIdx.x * 32 + threadIdx.x;
+  const int split = blockIdx.y;
+  const int r0 = split * rows_per, r1 = min(rows, r0 + rows_per);
+  float acc[NO][8];
+#pragma unroll
+  for (int o = 0; o < NO; ++o)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[o][j] = 0.f;
+  if (cv < nvec) {
+    for (int r = r0 + threadIdx.y; r < r1; r += kColTY) {
+      float v[8];
+      unpack8(a[(long long)r * lda_vec + cv], v);
+      if (OP == kColSum) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[0][j] += v[j];
+      } else if (OP == kColLnParams) {
+        float xv[8];
+        unpack8(xin[(long long)r * nvec + cv], xv);
+        const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc[0][j] += v[j] * ((xv[j] - mu) * rs);
+          acc[1][j] += v[j];
+        }
+      } else {
+        const uint64_t idx = ((uint64_t)r * nvec + cv) * 8;
+        const uint32_t keep = keep_mask8(seed, idx, thresh16);
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = ((keep >> j) & 1u) ? v[j] * scale : 0.f;
+        const uint4 packed = pack8(o);
+        out_dz[(long long)r * nvec + cv] = packed;
+        float ob[8];
+        unpack8(packed, ob);  // bias grad of the stored (bf16) dz
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[0][j] += ob[j];
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < NO; ++o)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) part[o][threadIdx.y][threadIdx.x][j] = acc[o][j];
+  __syncthreads();
+  // 256 threads reduce 32 vectors x 8 lanes = 256 outputs per op (fixed order over threadIdx.y)
+  const int t = threadIdx.y * 32 + threadIdx.x;
+  const int vec = t >> 3, lane = t & 7;
+  const int col = (blockIdx.x * 32 + vec) * 8 + lane;
+  if (blockIdx.x * 32 + vec < nvec) {
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      float s = 0.f;
+#pragma unroll
+      for (int y = 0; y < kColTY; ++y) s += part[o][y][vec][lane];
+      ws[((size_t)o * gridDim.y + split) * (size_t)nvec * 8 + col] = s;
+    }
+  }
+}
+
+__global__ void colsum_stage2(const float* __restrict__ ws, float* __restrict__ out0, float* __restrict__ out1, int n,
+                              int splits) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n) return;
+  float s0 = 0.f;
+  for (int sp = 0; sp < splits; ++sp) s0 += ws[(size_t)sp * n + col];
+  out0[col] += s0;
+  if (out1 != nullptr) {
+    float s1 = 0.f;
+    for (int sp = 0; sp < splits; ++sp) s1 += ws[((size_t)splits + sp) * n + col];
+    out1[col] += s1;
+  }
+}
+
+int col_splits(int rows) {
+  int s = rows / 64;
+  return s < 1 ? 1 : (s > 64 ? 64 : s);
+}
+
+// ------------------------------------------------------------------ bias + dropout + residual
+__global__ void bias_dropout_residual_kernel(const uint4* __restrict__ z, const uint4* __restrict__ bias,
+                                             const uint4* __restrict__ resid, uint4* __restrict__ out, long long nvec_total,
+                                             int nvec_row, uint64_t seed, uint32_t thresh16, float scale) {
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvec_total;
+       v += (long long)gridDim.x * blockDim.x) {
+    float a[8], b[8], r[8], o[8];
+    unpack8(z[v], a);
+    unpack8(bias[v % nvec_row], b);
+    unpack8(resid[v], r);
+    const uint32_t keep = keep_mask8(seed, (uint64_t)v * 8, thresh16);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = r[j] + (((keep >> j) & 1u) ? (a[j] + b[j]) * scale : 0.f);
+    out[v] = pack8(o);
+  }
+}
+
+// ------------------------------------------------------------------ causal softmax
+template <int VPL>
+__global__ void __launch_bounds__(256) softmax_fwd_kernel(const uint4* __restrict__ S, uint4* __restrict__ P,
+                                                          float* __restrict__ lse, int rows_total, int seq,
+                                                          long long head_base, uint64_t seed, uint32_t thresh16,
+                                                          float scale) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows_total) return;
+  const int bh = warp / seq, i = warp - bh * seq;
+  const int nvec_row = seq >> 3;
+  const uint4* srow = S + (size_t)warp * nvec_row;
+  uint4* prow = P + (size_t)warp * nvec_row;
+  const int nvalid = i + 1, nvec = (nvalid + 7) >> 3;
+  float x[VPL][8];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    const int v = lane + 32 * t;
+    if (v < nvec) {
+      unpack8(srow[v], x[t]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (v * 8 + j >= nvalid) x[t][j] = -INFINITY;
+        mx = fmaxf(mx, x[t][j]);
+      }
+    }
+  }
+  mx = warp_max(mx);
+  float sum = 0.f;
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    const int v = lane + 32 * t;
+    if (v < nvec) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        x[t][j] = __expf(x[t][j] - mx);
+        sum += x[t][j];
+      }
+    }
+  }
+  sum = warp_sum(sum);
+  const float inv = 1.f / sum;
+  const uint64_t base_idx = ((uint64_t)(head_base + bh) * seq + i) * (uint64_t)seq;
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    const int v = lane + 32 * t;
+    if (v < nvec) {
+      const uint32_t keep = keep_mask8(seed, base_idx + v * 8, thresh16);
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = ((keep >> j) & 1u) ? x[t][j] * inv * scale : 0.f;
+      prow[v] = pack8(o);
+    }
+  }
+  const int zend = min(seq, (i / 256 + 1) * 256) >> 3;
+  for (int v = nvec + lane; v < zend; v += 32) prow[v] = make_uint4(0, 0, 0, 0);
+  if (lane == 0) lse[warp] = mx + logf(sum);
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(const uint4* __restrict__ S, const float* __restrict__ lse,
+                                                          uint4* __restrict__ dP, int rows_total, int seq,
+                                                          long long head_base, uint64_t seed, uint32_t thresh16,
+                                                          float scale, float alpha) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows_total) return;
+  const int bh = warp / seq, i = warp - bh * seq;
+  const int nvec_row = seq >> 3;
+  const uint4* srow = S + (size_t)warp * nvec_row;
+  uint4* drow = dP + (size_t)warp * nvec_row;
+  const int nvalid = i + 1, nvec = (nvalid + 7) >> 3;
+  const float l = lse[warp];
+  const uint64_t base_idx = ((uint64_t)(head_base + bh) * seq + i) * (uint64_t)seq;
+  float y[VPL][8], g[VPL][8];
+  float dot = 0.f;
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    const int v = lane + 32 * t;
+    if (v < nvec) {
+      float sv[8];
+      unpack8(srow[v], sv);
+      unpack8(drow[v], g[t]);
+      const uint32_t keep = keep_mask8(seed, base_idx + v * 8, thresh16);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool valid = v * 8 + j < nvalid;
+        y[t][j] = valid ? __expf(sv[j] - l) : 0.f;
+        g[t][j] = (valid && ((keep >> j) & 1u)) ? g[t][j] * scale : 0.f;
+        dot += y[t][j] * g[t][j];
+      }
+    }
+  }
+  dot = warp_sum(dot);
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    const int v = lane + 32 * t;
+    if (v < nvec) {
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = alpha * y[t][j] * (g[t][j] - dot);
+      drow[v] = pack8(o);
+    }
+  }
+  const int zend = min(seq, (i / 256 + 1) * 256) >> 3;
+  for (int v = nvec + lane; v < zend; v += 32) drow[v] = make_uint4(0, 0, 0, 0);
+}
+
+// ------------------------------------------------------------------ loss, init
+__global__ void mse_loss_kernel(const uint4* __restrict__ y, const uint4* __restrict__ t, uint4* __restrict__ dy,
+                                float* __restrict__ loss, long long nvec, float inv_n) {
+  __shared__ float red[32];
+  float acc = 0.f;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvec; v += (long long)gridDim.x * blockDim.x) {
+    float a[8], b[8], o[8];
+    unpack8(y[v], a);
+    unpack8(t[v], b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float d = a[j] - b[j];
+      acc += 0.5f * d * d;
+      o[j] = d * inv_n;
+    }
+    dy[v] = pack8(o);
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) atomicAdd(loss, acc * inv_n);
+}
+
+__global__ void fill_normal_kernel(__nv_bfloat16* __restrict__ out, long long rows, long long cols,
+                                   long long global_cols, long long row0, long long col0, uint64_t key, float mean,
+                                   float std) {
+  const long long n = rows * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cols, c = e - r * cols;
+    const uint64_t gidx = (uint64_t)(row0 + r) * (uint64_t)global_cols + (uint64_t)(col0 + c);
+    const float z = (float)curator::normal_at(key, gidx);
+    out[e] = __float2bfloat16_rn(mean + std * z);
+  }
+}
+
+__global__ void fill_zero_kernel(float* p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = 0.f;
+}
+
+int grid_for(long long work, int block) {
+  long long g = (work + block - 1) / block;
+  const long long cap = 148LL * 16;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+#define MT_VPT_DISPATCH(VPT_NEEDED, LAUNCH) \
+  do {                                      \
+    if ((VPT_NEEDED) <= 1) {                \
+      LAUNCH(1);                            \
+    } else if ((VPT_NEEDED) <= 2) {         \
+      LAUNCH(2);                            \
+    } else if ((VPT_NEEDED) <= 4) {         \
+      LAUNCH(4);                            \
+    } else if ((VPT_NEEDED) <= 8) {         \
+      LAUNCH(8);                            \
+    } else if ((VPT_NEEDED) <= 12) {        \
+      LAUNCH(12);                           \
+    } else {                                \
+      LAUNCH(16);                           \
+    }                                       \
+  } while (0)
+
+static void row_launch_shape(int h, int& threads, int& vpt) {
+  const int nvec = h / 8;
+  threads = ((nvec + 31) / 32) * 32;
+  if (threads > 256) threads = 256;
+  vpt = (nvec + threads - 1) / threads;
+}
+
+void ln_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int rows, int h,
+            float eps, cudaStream_t s) {
+  int threads, vpt;
+  row_launch_shape(h, threads, vpt);
+#define L(V)                                                                                                   \
+  ln_fwd_kernel<V><<<rows, threads, 0, s>>>((const uint4*)x, (const uint4*)gamma, (const uint4*)beta, (uint4*)y, \
+                                            mean, rstd, h / 8, 1.f / h, eps)
+  MT_VPT_DISPATCH(vpt, L);
+#undef L
+}
+
+void ln_bwd_dx(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
+               const void* resid, void* dx, int rows, int h, cudaStream_t s) {
+  int threads, vpt;
+  row_launch_shape(h, threads, vpt);
+#define L(V)                                                                                                     \
+  ln_bwd_dx_kernel<V><<<rows, threads, 0, s>>>((const uint4*)dy, (const uint4*)x, (const uint4*)gamma, mean, rstd, \
+                                               (const uint4*)resid, (uint4*)dx, h / 8, 1.f / h)
+  MT_VPT_DISPATCH(vpt, L);
+#undef L
+}
+
+size_t colsum_workspace_floats(int rows, int n) { return (size_t)2 * col_splits(rows) * n; }
+
+void ln_bwd_params(const void* dy, const void* x, const float* mean, const float* rstd, float* dgamma, float* dbeta,
+                   int rows, int h, float* ws, cudaStream_t s) {
+  const int nvec = h / 8, splits = col_splits(rows);
+  dim3 grid((nvec + 31) / 32, splits), block(32, kColTY);
+  colsum_stage1<kColLnParams><<<grid, block, 0, s>>>((const uint4*)dy, nvec, (const uint4*)x, mean, rstd, nullptr, ws,
+                                                     rows, nvec, (rows + splits - 1) / splits, 0, 0, 1.f);
+  colsum_stage2<<<(h + 255) / 256, 256, 0, s>>>(ws, dgamma, dbeta, h, splits);
+}
+
+void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, float* ws, cudaStream_t s) {
+  const int nvec = n / 8, splits = col_splits(rows);
+  dim3 grid((nvec + 31) / 32, splits), block(32, kColTY);
+  colsum_stage1<kColSum><<<grid, block, 0, s>>>((const uint4*)x, ldx / 8, nullptr, nullptr, nullptr, nullptr, ws, rows,
+                                                nvec, (rows + splits - 1) / splits, 0, 0, 1.f);
+  colsum_stage2<<<(n + 255) / 256, 256, 0, s>>>(ws, dbias, nullptr, n, splits);
+}
+
+void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int h, uint64_t seed, uint32_t thresh16,
+                           float scale, float* ws, cudaStream_t s) {
+  const int nvec = h / 8, splits = col_splits(rows);
+  dim3 grid((nvec + 31) / 32, splits), block(32, kColTY);
+  colsum_stage1<kColDropout><<<grid, block, 0, s>>>((const uint4*)dy, nvec, nullptr, nullptr, nullptr, (uint4*)dz, ws,
+                                                    rows, nvec, (rows + splits - 1) / splits, seed, thresh16, scale);
+  colsum_stage2<<<(h + 255) / 256, 256, 0, s>>>(ws, dbias, nullptr, h, splits);
+}
+
+void bias_dropout_residual(const void* z, const void* bias, const void* resid, void* out, int rows, int h,
+                           uint64_t seed, uint32_t thresh16, float scale, cudaStream_t s) {
+  const long long nvec = (long long)rows * h / 8;
+  bias_dropout_residual_kernel<<<grid_for(nvec, 256), 256, 0, s>>>((const uint4*)z, (const uint4*)bias,
+                                                                   (const uint4*)resid, (uint4*)out, nvec, h / 8, seed,
+                                                                   thresh16, scale);
+}
+
+#define MT_VPL_DISPATCH(SEQ, LAUNCH) \
+  do {                               \
+    const int need = ((SEQ) + 255) / 256; \
+    if (need <= 1) LAUNCH(1);        \
+    else if (need <= 2) LAUNCH(2);   \
+    else if (need <= 4) LAUNCH(4);   \
+    else if (need <= 8) LAUNCH(8);   \
+    else LAUNCH(16);                 \
+  } while (0)
+
+void softmax_fwd(const void* S, void* P, float* lse, int batch_heads, int seq, long long head_base, uint64_t seed,
+                 uint32_t thresh16, float scale, cudaStream_t s) {
+  const int rows = batch_heads * seq;
+  const int blocks = (rows + 7) / 8;
+#define L(V)                                                                                                     \
+  softmax_fwd_kernel<V><<<blocks, 256, 0, s>>>((const uint4*)S, (uint4*)P, lse, rows, seq, head_base, seed, thresh16, \
+                                               scale)
+  MT_VPL_DISPATCH(seq, L);
+#undef L
+}
+
+void softmax_bwd(const void* S, const float* lse, void* dP, int batch_heads, int seq, long long head_base,
+                 uint64_t seed, uint32_t thresh16, float scale, float alpha, cudaStream_t s) {
+  const int rows = batch_heads * seq;
+  const int blocks = (rows + 7) / 8;
+#define L(V)                                                                                                      \
+  softmax_bwd_kernel<V><<<blocks, 256, 0, s>>>((const uint4*)S, lse, (uint4*)dP, rows, seq, head_base, seed, thresh16, \
+                                               scale, alpha)
+  MT_VPL_DISPATCH(seq, L);
+#undef L
+}
+
+void mse_loss(const void* y, const void* t, void* dy, float* loss, long long n, cudaStream_t s) {
+  const long long nvec = n / 8;
+  mse_loss_kernel<<<grid_for(nvec, 256), 256, 0, s>>>((const uint4*)y, (const uint4*)t, (uint4*)dy, loss, nvec,
+                                                      1.f / (float)n);
+}
+
+void fill_normal(void* out, long long rows, long long cols, long long global_cols, long long row0, long long col0,
+                 uint64_t key, float mean, float std, cudaStream_t s) {
+  fill_normal_kernel<<<grid_for(rows * cols, 256), 256, 0, s>>>((__nv_bfloat16*)out, rows, cols, global_cols, row0,
+                                                                col0, key, mean, std);
+}
+
+void fill_zero_f32(float* p, size_t n, cudaStream_t s) {
+  fill_zero_kernel<<<grid_for((long long)n, 256), 256, 0, s>>>(p, n);
+}
+
+}  // namespace mt

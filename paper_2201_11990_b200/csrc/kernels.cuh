@@ -1,0 +1,54 @@
+// Launchers of the HBM-bound kernels of the tensor-sliced layer (LayerNorm fwd/bwd, causal
+// scaled-masked softmax fwd/bwd with attention dropout, bias+dropout+residual, bias-grad column
+// sums, synthetic loss, seeded init). All take bf16 activations and an explicit stream.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mt {
+
+typedef unsigned short bf16_t;  // raw bf16 bits on the host side of the launchers
+
+// y = LN(x) * gamma + beta ; saves mean and rstd (fp32, one per row).
+void ln_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int rows, int h,
+            float eps, cudaStream_t s);
+// dx = rstd * (g - mean(g) - xhat * mean(g * xhat)) [+ resid], g = dy * gamma.
+void ln_bwd_dx(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
+               const void* resid, void* dx, int rows, int h, cudaStream_t s);
+// dgamma += sum_rows dy * xhat ; dbeta += sum_rows dy   (fp32 accumulate, deterministic)
+void ln_bwd_params(const void* dy, const void* x, const float* mean, const float* rstd, float* dgamma, float* dbeta,
+                   int rows, int h, float* workspace, cudaStream_t s);
+
+// out = resid + dropout(z + bias)
+void bias_dropout_residual(const void* z, const void* bias, const void* resid, void* out, int rows, int h,
+                           uint64_t site_seed, uint32_t thresh16, float scale, cudaStream_t s);
+// dz = dropout'(dy) ; dbias += sum_rows dz
+void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int h, uint64_t site_seed,
+                           uint32_t thresh16, float scale, float* workspace, cudaStream_t s);
+// dbias += sum_rows x   (x bf16 [rows, n])
+void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, float* workspace, cudaStream_t s);
+size_t colsum_workspace_floats(int rows, int n);
+
+// Causal softmax over S (already scaled by 1/sqrt(hd)), rows of `batch_heads` independent
+// [seq x seq] blocks. P = dropout(softmax(S)); zeros above the diagonal up to the next
+// multiple of 256 columns (what the causal GEMMs read); lse saved per row.
+// Attention dropout element index = ((head_base + bh) * seq + i) * seq + j, where bh is the
+// block index and head_base maps local blocks to global (microbatch-row, head) ids.
+void softmax_fwd(const void* S, void* P, float* lse, int batch_heads, int seq, long long head_base,
+                 uint64_t site_seed, uint32_t thresh16, float scale, cudaStream_t s);
+// In place: dP (dropped-prob grad) -> dS * alpha.
+void softmax_bwd(const void* S, const float* lse, void* dP, int batch_heads, int seq, long long head_base,
+                 uint64_t site_seed, uint32_t thresh16, float scale, float alpha, cudaStream_t s);
+
+// loss += sum 0.5 (y - t)^2 / n ; dy = (y - t) / n     (n = rows * h)
+void mse_loss(const void* y, const void* t, void* dy, float* loss, long long n, cudaStream_t s);
+
+// Seeded normal init of a TP shard of a row-major [global_rows x global_cols] tensor:
+// out[r][c] = bf16(mean + std * normal_at(key, (row0 + r) * global_cols + col0 + c)).
+void fill_normal(void* out, long long rows, long long cols, long long global_cols, long long row0, long long col0,
+                 uint64_t key, float mean, float std, cudaStream_t s);
+void fill_zero_f32(float* p, size_t n, cudaStream_t s);
+
+}  // namespace mt

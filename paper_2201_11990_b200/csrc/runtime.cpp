@@ -1,0 +1,651 @@
+// Tensor-sliced transformer layer runtime: context, NCCL groups, parameter shards, layer forward
+// and backward (PAPER.md:133-150 restated), and their C ABI.
+//
+// Per layer and microbatch (M = b*s tokens, t = TP, local widths h/t, 3h/t, 4h/t):
+//   forward   LN1 -> QKV GEMM(+bias) -> [S = QK^T/sqrt(d) -> causal softmax+dropout -> P V] per head
+//             -> attn-out GEMM -> TP all-reduce -> bias+dropout+residual -> LN2
+//             -> fc1 GEMM(+bias, GeLU) -> fc2 GEMM -> TP all-reduce -> bias+dropout+residual
+//   backward  the transposed chain with dgrad GEMMs (MN-major weight operand), wgrad GEMMs
+//             (both operands MN-major, fp32 accumulation in the epilogue), the GeLU derivative fused
+//             into the fc2-dgrad epilogue, softmax backward, LayerNorm backward, bias-grad column
+//             sums, and the TP all-reduce of the LN inputs' gradients ("f" operator).
+#include "runtime.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "curator/dropout.hpp"
+#include "curator/errors.hpp"
+#include "curator/hashing.hpp"
+#include "kernels.cuh"
+
+namespace mt {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& e) { g_last_error = e; }
+const char* last_error() { return g_last_error.c_str(); }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw RuntimeFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void check_nccl(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw RuntimeFailure(std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+DeviceBuffer::DeviceBuffer(size_t n) { ensure(n); }
+DeviceBuffer::~DeviceBuffer() {
+  if (ptr) cudaFree(ptr);
+}
+void DeviceBuffer::ensure(size_t n) {
+  if (n <= bytes) return;
+  if (ptr) check_cuda(cudaFree(ptr), "cudaFree");
+  ptr = nullptr;
+  bytes = 0;
+  check_cuda(cudaMalloc(&ptr, n), "cudaMalloc");
+  bytes = n;
+}
+
+// Runs `f`, mapping exceptions to the ABI's status codes.
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MT_OK;
+  } catch (const curator::ConfigError& e) {
+    set_error(e.what());
+    return MT_ERR_CONFIG;
+  } catch (const std::invalid_argument& e) {
+    set_error(e.what());
+    return MT_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return MT_ERR_DATA;
+  }
+}
+
+namespace {
+
+// --------------------------------------------------------------------------- GEMM helper
+struct Gemm {
+  mt_gemm_args a{};
+  Gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn, void* D, int64_t ldd, int64_t m,
+       int64_t n, int64_t k) {
+    a.a = A;
+    a.lda = lda;
+    a.a_mn_major = a_mn;
+    a.b = B;
+    a.ldb = ldb;
+    a.b_mn_major = b_mn;
+    a.d = D;
+    a.ldd = ldd;
+    a.m = m;
+    a.n = n;
+    a.k = k;
+    a.batch = 1;
+    a.alpha = 1.f;
+    a.epilogue = MT_EPI_STORE_BF16;
+  }
+  Gemm& epi(int e) {
+    a.epilogue = e;
+    return *this;
+  }
+  Gemm& bias(const void* b) {
+    a.bias = b;
+    return *this;
+  }
+  Gemm& aux(void* p, int64_t ld) {
+    a.aux = p;
+    a.ld_aux = ld;
+    return *this;
+  }
+  Gemm& alpha(float v) {
+    a.alpha = v;
+    return *this;
+  }
+  Gemm& batched(int64_t b, int64_t abs, int64_t bbs, int64_t dbs) {
+    a.batch = b;
+    a.a_batch_stride = abs;
+    a.b_batch_stride = bbs;
+    a.d_batch_stride = dbs;
+    return *this;
+  }
+  Gemm& causal(int c) {
+    a.causal = c;
+    return *this;
+  }
+  void run(cudaStream_t s, int& launches) {
+    const int rc = mt_gemm(&a, s);
+    if (rc == 1) throw std::invalid_argument("mt_gemm: invalid arguments");
+    if (rc != 0) throw RuntimeFailure(std::string("mt_gemm: ") + cudaGetErrorString(cudaGetLastError()));
+    ++launches;
+  }
+};
+
+uint64_t key_of(uint64_t seed, const char* name, uint32_t layer, uint32_t mb) {
+  return curator::site_seed(seed, name, layer, mb);
+}
+
+const char* kParamNames[MT_P_COUNT] = {"ln1.gamma", "ln1.beta", "qkv.weight", "qkv.bias", "proj.weight", "proj.bias",
+                                       "ln2.gamma", "ln2.beta", "fc1.weight", "fc1.bias", "fc2.weight", "fc2.bias"};
+
+struct ShardInfo {
+  int64_t grows, gcols, r0, c0, rows, cols;
+};
+
+ShardInfo shard_info(const mt_layer_desc& d, int p) {
+  const auto sh = curator::layer_shard(d.hidden, d.heads, d.ffn_mult, d.tp_size, d.tp_rank);
+  const int64_t h = d.hidden, ff = int64_t{d.ffn_mult} * d.hidden;
+  switch (p) {
+    case MT_P_LN1_GAMMA:
+    case MT_P_LN1_BETA:
+    case MT_P_LN2_GAMMA:
+    case MT_P_LN2_BETA:
+    case MT_P_PROJ_B:
+    case MT_P_FC2_B:
+      return {1, h, 0, 0, 1, h};
+    case MT_P_QKV_W:
+      return {3 * h, h, sh.qkv_rows.begin, 0, sh.qkv_rows.size(), h};
+    case MT_P_QKV_B:
+      return {1, 3 * h, 0, sh.qkv_rows.begin, 1, sh.qkv_rows.size()};
+    case MT_P_PROJ_W:
+      return {h, h, 0, sh.proj_cols.begin, h, sh.proj_cols.size()};
+    case MT_P_FC1_W:
+      return {ff, h, sh.fc1_rows.begin, 0, sh.fc1_rows.size(), h};
+    case MT_P_FC1_B:
+      return {1, ff, 0, sh.fc1_rows.begin, 1, sh.fc1_rows.size()};
+    case MT_P_FC2_W:
+      return {h, ff, 0, sh.fc2_cols.begin, h, sh.fc2_cols.size()};
+    default:
+      throw std::invalid_argument("unknown parameter id");
+  }
+}
+
+void validate_desc(const mt_layer_desc& d) {
+  if (d.hidden <= 0 || d.heads <= 0 || d.seq <= 0 || d.micro_batch <= 0 || d.ffn_mult <= 0)
+    throw std::invalid_argument("layer dimensions must be positive");
+  if (d.hidden % 64 != 0) throw std::invalid_argument("hidden must be a multiple of 64");
+  if (d.seq % 64 != 0) throw std::invalid_argument("sequence must be a multiple of 64");
+  if ((d.hidden / d.heads) % 16 != 0) throw std::invalid_argument("head dim must be a multiple of 16");
+  if (d.dropout_hidden < 0 || d.dropout_hidden >= 1 || d.dropout_attn < 0 || d.dropout_attn >= 1)
+    throw std::invalid_argument("dropout must be in [0, 1)");
+  (void)curator::layer_shard(d.hidden, d.heads, d.ffn_mult, d.tp_size, d.tp_rank);
+  if ((int64_t{d.hidden} / d.tp_size) % 8 != 0) throw std::invalid_argument("h / TP must be a multiple of 8");
+}
+
+}  // namespace
+}  // namespace mt
+
+using namespace mt;
+
+// =========================================================================== context & comm
+extern "C" const char* mt_last_error(void) { return mt::last_error(); }
+extern "C" const char* mt_version(void) { return "mtnlg-b200 0.1 (sm_100a)"; }
+
+extern "C" int mt_ctx_create(int32_t device, mt_ctx** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("null out");
+    check_cuda(cudaSetDevice(device), "cudaSetDevice");
+    auto* c = new mt_ctx();
+    c->device = device;
+    *out = c;
+  });
+}
+
+extern "C" int mt_ctx_destroy(mt_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    for (ncclComm_t* cm : {&c->tp, &c->pp, &c->dp, &c->world})
+      if (*cm) ncclCommDestroy(*cm);
+    delete c;
+  });
+}
+
+extern "C" int mt_nccl_unique_id(unsigned char out[128]) {
+  return guarded([&] {
+    ncclUniqueId id;
+    check_nccl(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+  });
+}
+
+extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], int32_t world_size, int32_t rank,
+                                const mt_parallel_config* par) {
+  return guarded([&] {
+    if (!c || !par) throw std::invalid_argument("null argument");
+    curator::ClusterTopology topo;
+    topo.nodes = 1;
+    topo.gpus_per_node = world_size;
+    curator::ParallelConfig p;
+    p.tensor = par->tensor;
+    p.pipeline = par->pipeline;
+    p.data = par->data;
+    p.batch = par->batch;
+    p.micro_batches = par->micro_batches;
+    const auto ranks = curator::map_topology(topo, p);  // throws invalid_argument on bad layouts
+    if (rank < 0 || rank >= world_size) throw std::invalid_argument("rank out of range");
+    c->world_size = world_size;
+    c->rank = rank;
+    c->par = p;
+    c->place = ranks[rank];
+    check_cuda(cudaSetDevice(c->device), "cudaSetDevice");
+    if (world_size == 1) return;
+    ncclUniqueId id;
+    std::memcpy(&id, id_bytes, 128);
+    check_nccl(ncclCommInitRank(&c->world, world_size, id, rank), "ncclCommInitRank");
+    const auto& me = c->place;
+    // TP group: same (dp, pp); PP group: same (dp, tp); DP group: same (pp, tp).
+    const int tp_color = me.pipeline * p.data + me.data;
+    const int pp_color = me.data * p.tensor + me.tensor;
+    const int dp_color = me.pipeline * p.tensor + me.tensor;
+    check_nccl(ncclCommSplit(c->world, tp_color, me.tensor, &c->tp, nullptr), "ncclCommSplit(tp)");
+    check_nccl(ncclCommSplit(c->world, pp_color, me.pipeline, &c->pp, nullptr), "ncclCommSplit(pp)");
+    check_nccl(ncclCommSplit(c->world, dp_color, me.data, &c->dp, nullptr), "ncclCommSplit(dp)");
+  });
+}
+
+extern "C" int mt_ctx_placement(const mt_ctx* c, mt_rank_placement* out) {
+  return guarded([&] {
+    if (!c || !out) throw std::invalid_argument("null argument");
+    out->data = c->place.data;
+    out->pipeline = c->place.pipeline;
+    out->tensor = c->place.tensor;
+    out->node = c->place.node;
+    out->gpu = c->place.gpu;
+  });
+}
+
+extern "C" int mt_tp_allreduce_bf16(mt_ctx* c, void* buf, int64_t n, void* stream) {
+  return guarded([&] {
+    if (c->par.tensor <= 1) return;
+    check_nccl(ncclAllReduce(buf, buf, n, ncclBfloat16, ncclSum, c->tp, (cudaStream_t)stream), "ncclAllReduce(tp)");
+  });
+}
+
+extern "C" int mt_dp_allreduce_f32(mt_ctx* c, float* buf, int64_t n, int32_t average, void* stream) {
+  return guarded([&] {
+    if (c->par.data <= 1) return;
+    check_nccl(ncclAllReduce(buf, buf, n, ncclFloat32, average ? ncclAvg : ncclSum, c->dp, (cudaStream_t)stream),
+               "ncclAllReduce(dp)");
+  });
+}
+
+extern "C" int mt_pp_send_bf16(mt_ctx* c, const void* buf, int64_t n, int32_t peer, void* stream) {
+  return guarded([&] {
+    check_nccl(ncclSend(buf, n, ncclBfloat16, peer, c->pp, (cudaStream_t)stream), "ncclSend(pp)");
+  });
+}
+
+extern "C" int mt_pp_recv_bf16(mt_ctx* c, void* buf, int64_t n, int32_t peer, void* stream) {
+  return guarded([&] {
+    check_nccl(ncclRecv(buf, n, ncclBfloat16, peer, c->pp, (cudaStream_t)stream), "ncclRecv(pp)");
+  });
+}
+
+// =========================================================================== parameters
+extern "C" int mt_param_shard(const mt_layer_desc* d, int32_t p, int64_t g[2], int64_t o[2], int64_t s[2]) {
+  return guarded([&] {
+    if (!d) throw std::invalid_argument("null desc");
+    const ShardInfo si = shard_info(*d, p);
+    g[0] = si.grows;
+    g[1] = si.gcols;
+    o[0] = si.r0;
+    o[1] = si.c0;
+    s[0] = si.rows;
+    s[1] = si.cols;
+  });
+}
+
+extern "C" uint64_t mt_stream_key(uint64_t seed, const char* name, uint32_t layer, uint32_t mb) {
+  return key_of(seed, name, layer, mb);
+}
+
+extern "C" uint32_t mt_dropout_threshold16(double p) { return curator::dropout_threshold16(p); }
+
+extern "C" int mt_layer_create(mt_ctx* c, const mt_layer_desc* d, mt_layer** out) {
+  return guarded([&] {
+    if (!c || !d || !out) throw std::invalid_argument("null argument");
+    validate_desc(*d);
+    check_cuda(cudaSetDevice(c->device), "cudaSetDevice");
+    auto l = std::make_unique<mt_layer>();
+    l->ctx = c;
+    l->d = *d;
+    l->M = int64_t{d->micro_batch} * d->seq;
+    l->h = d->hidden;
+    l->hl = d->hidden / d->tp_size;
+    l->ffl = int64_t{d->ffn_mult} * d->hidden / d->tp_size;
+    l->qkvl = 3 * l->hl;
+    l->heads_local = d->heads / d->tp_size;
+    l->head_dim = d->hidden / d->heads;
+    l->shard = curator::layer_shard(d->hidden, d->heads, d->ffn_mult, d->tp_size, d->tp_rank);
+    int64_t off = 0;
+    for (int p = 0; p < MT_P_COUNT; ++p) {
+      const ShardInfo si = shard_info(*d, p);
+      l->param_off[p] = off;
+      l->param_rows[p] = si.rows;
+      l->param_cols[p] = si.cols;
+      off += (si.rows * si.cols + 63) / 64 * 64;  // 128-byte aligned bf16 slices
+    }
+    l->param_total = off;
+    l->params.ensure(off * 2);
+    l->grads.ensure(off * 4);
+    check_cuda(cudaMemset(l->grads.ptr, 0, off * 4), "cudaMemset");
+    // shared scratch
+    const int64_t M = l->M;
+    for (auto& b : c->scratch_h) b.ensure(M * l->h * 2);
+    c->scratch_ffn.ensure(M * l->ffl * 2);
+    c->scratch_ctx.ensure(M * l->hl * 2);
+    c->scratch_qkv.ensure(M * l->qkvl * 2);
+    c->scratch_attn.ensure(l->heads_local * int64_t{d->seq} * d->seq * 2);
+    size_t ws = 0;
+    for (int64_t n : {l->h, l->ffl, l->qkvl}) ws = std::max(ws, mt::colsum_workspace_floats((int)M, (int)n));
+    c->scratch_ws.ensure(ws * 4);
+    *out = l.release();
+  });
+}
+
+extern "C" int mt_layer_destroy(mt_layer* l) {
+  return guarded([&] { delete l; });
+}
+
+extern "C" int mt_layer_init_params(mt_layer* l, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = (cudaStream_t)stream;
+    const double wstd = curator::weight_init_std(l->d.hidden);
+    for (int p = 0; p < MT_P_COUNT; ++p) {
+      const ShardInfo si = shard_info(l->d, p);
+      const uint64_t key = key_of(l->d.seed, kParamNames[p], l->d.layer_index, 0);
+      float mean = 0.f, std = 0.02f;
+      if (p == MT_P_QKV_W || p == MT_P_PROJ_W || p == MT_P_FC1_W || p == MT_P_FC2_W) std = (float)wstd;
+      if (p == MT_P_LN1_GAMMA || p == MT_P_LN2_GAMMA) mean = 1.f;
+      mt::fill_normal(l->param_ptr(p), si.rows, si.cols, si.gcols, si.r0, si.c0, key, mean, std, s);
+    }
+    check_cuda(cudaGetLastError(), "fill_normal");
+  });
+}
+
+extern "C" int mt_layer_set_param(mt_layer* l, int32_t p, const void* host_global) {
+  return guarded([&] {
+    const ShardInfo si = shard_info(l->d, p);
+    const uint16_t* src = static_cast<const uint16_t*>(host_global) + si.r0 * si.gcols + si.c0;
+    check_cuda(cudaMemcpy2D(l->param_ptr(p), si.cols * 2, src, si.gcols * 2, si.cols * 2, si.rows,
+                            cudaMemcpyHostToDevice),
+               "cudaMemcpy2D(param)");
+  });
+}
+
+extern "C" int mt_layer_get_param(mt_layer* l, int32_t p, void* host) {
+  return guarded([&] {
+    if (p < 0 || p >= MT_P_COUNT) throw std::invalid_argument("unknown parameter id");
+    check_cuda(cudaDeviceSynchronize(), "sync");
+    check_cuda(cudaMemcpy(host, l->param_ptr(p), l->param_rows[p] * l->param_cols[p] * 2, cudaMemcpyDeviceToHost),
+               "cudaMemcpy(param)");
+  });
+}
+
+extern "C" int mt_layer_get_grad(mt_layer* l, int32_t p, float* host) {
+  return guarded([&] {
+    if (p < 0 || p >= MT_P_COUNT) throw std::invalid_argument("unknown parameter id");
+    check_cuda(cudaDeviceSynchronize(), "sync");
+    check_cuda(cudaMemcpy(host, l->grad_ptr(p), l->param_rows[p] * l->param_cols[p] * 4, cudaMemcpyDeviceToHost),
+               "cudaMemcpy(grad)");
+  });
+}
+
+extern "C" int mt_layer_zero_grads(mt_layer* l, void* stream) {
+  return guarded([&] {
+    check_cuda(cudaMemsetAsync(l->grads.ptr, 0, l->param_total * 4, (cudaStream_t)stream), "cudaMemsetAsync");
+  });
+}
+
+extern "C" int mt_layer_grad_buffer(mt_layer* l, float** ptr, int64_t* n) {
+  return guarded([&] {
+    *ptr = l->grads.as<float>();
+    *n = l->param_total;
+  });
+}
+
+extern "C" int mt_layer_launch_counts(const mt_layer* l, int32_t* f, int32_t* b) {
+  return guarded([&] {
+    *f = l->fwd_launches;
+    *b = l->bwd_launches;
+  });
+}
+
+// =========================================================================== forward
+namespace {
+
+mt_layer::Saved& acquire_slot(mt_layer* l, uint32_t mb) {
+  if (l->saved.count(mb)) throw std::invalid_argument("microbatch already has saved activations");
+  std::unique_ptr<mt_layer::Saved> sv;
+  if (!l->free_slots.empty()) {
+    sv = std::move(l->free_slots.back());
+    l->free_slots.pop_back();
+  } else {
+    sv = std::make_unique<mt_layer::Saved>();
+  }
+  const int64_t M = l->M, b = l->d.micro_batch, s = l->d.seq, Hl = l->heads_local;
+  sv->ln1.ensure(M * l->h * 2);
+  sv->qkv.ensure(M * l->qkvl * 2);
+  sv->S.ensure(b * Hl * s * s * 2);
+  sv->P.ensure(b * Hl * s * s * 2);
+  sv->lse.ensure(b * Hl * s * 4);
+  sv->ctx.ensure(M * l->hl * 2);
+  sv->x1.ensure(M * l->h * 2);
+  sv->ln2.ensure(M * l->h * 2);
+  sv->pre.ensure(M * l->ffl * 2);
+  sv->act.ensure(M * l->ffl * 2);
+  sv->stats.ensure(4 * M * 4);
+  auto& ref = *sv;
+  l->saved[mb] = std::move(sv);
+  return ref;
+}
+
+void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t st) {
+  mt_ctx* c = l->ctx;
+  const mt_layer_desc& d = l->d;
+  const int64_t M = l->M, h = l->h, hl = l->hl, ffl = l->ffl, ld3 = l->qkvl, s = d.seq, Hl = l->heads_local,
+                hd = l->head_dim;
+  auto& sv = acquire_slot(l, mb);
+  sv.x = x;
+  float* mean1 = sv.stats.as<float>();
+  float* rstd1 = mean1 + M;
+  float* mean2 = rstd1 + M;
+  float* rstd2 = mean2 + M;
+  int n = 0;
+  const float scale_h = 1.f / (1.f - d.dropout_hidden), scale_a = 1.f / (1.f - d.dropout_attn);
+  const uint32_t th_h = curator::dropout_threshold16(d.dropout_hidden);
+  const uint32_t th_a = curator::dropout_threshold16(d.dropout_attn);
+  const uint64_t site_attn = key_of(d.seed, "attn.probs", d.layer_index, mb);
+  const uint64_t site_out1 = key_of(d.seed, "attn.out", d.layer_index, mb);
+  const uint64_t site_out2 = key_of(d.seed, "mlp.out", d.layer_index, mb);
+  void* z = c->scratch_h[0].ptr;
+
+  ln_fwd(x, l->param_ptr(MT_P_LN1_GAMMA), l->param_ptr(MT_P_LN1_BETA), sv.ln1.ptr, mean1, rstd1, (int)M, (int)h,
+         d.ln_eps, st);
+  ++n;
+  Gemm(sv.ln1.ptr, h, false, l->param_ptr(MT_P_QKV_W), h, false, sv.qkv.ptr, ld3, M, ld3, h)
+      .bias(l->param_ptr(MT_P_QKV_B))
+      .run(st, n);
+  const float alpha = 1.f / std::sqrt((float)hd);
+  for (int64_t bb = 0; bb < d.micro_batch; ++bb) {
+    const uint16_t* q = sv.qkv.as<uint16_t>() + bb * s * ld3;
+    uint16_t* S = sv.S.as<uint16_t>() + bb * Hl * s * s;
+    uint16_t* P = sv.P.as<uint16_t>() + bb * Hl * s * s;
+    float* lse = sv.lse.as<float>() + bb * Hl * s;
+    Gemm(q, ld3, false, q + hd, ld3, false, S, s, s, s, hd)
+        .batched(Hl, 3 * hd, 3 * hd, s * s)
+        .alpha(alpha)
+        .causal(MT_CAUSAL_SKIP_UPPER_TILES)
+        .run(st, n);
+    const long long head_base = bb * d.heads + int64_t{d.tp_rank} * Hl;
+    softmax_fwd(S, P, lse, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, st);
+    ++n;
+    Gemm(P, s, false, q + 2 * hd, ld3, true, sv.ctx.as<uint16_t>() + bb * s * hl, hl, s, hd, s)
+        .batched(Hl, s * s, 3 * hd, hd)
+        .causal(MT_CAUSAL_K_LE_M)
+        .run(st, n);
+  }
+  Gemm(sv.ctx.ptr, hl, false, l->param_ptr(MT_P_PROJ_W), hl, false, z, h, M, h, hl).run(st, n);
+  if (d.tp_size > 1) {
+    check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(attn.out)");
+    ++n;
+  }
+  bias_dropout_residual(z, l->param_ptr(MT_P_PROJ_B), x, sv.x1.ptr, (int)M, (int)h, site_out1, th_h, scale_h, st);
+  ++n;
+  ln_fwd(sv.x1.ptr, l->param_ptr(MT_P_LN2_GAMMA), l->param_ptr(MT_P_LN2_BETA), sv.ln2.ptr, mean2, rstd2, (int)M,
+         (int)h, d.ln_eps, st);
+  ++n;
+  Gemm(sv.ln2.ptr, h, false, l->param_ptr(MT_P_FC1_W), h, false, sv.act.ptr, ffl, M, ffl, h)
+      .epi(MT_EPI_BIAS_GELU)
+      .bias(l->param_ptr(MT_P_FC1_B))
+      .aux(sv.pre.ptr, ffl)
+      .run(st, n);
+  Gemm(sv.act.ptr, ffl, false, l->param_ptr(MT_P_FC2_W), ffl, false, z, h, M, h, ffl).run(st, n);
+  if (d.tp_size > 1) {
+    check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(mlp.out)");
+    ++n;
+  }
+  bias_dropout_residual(z, l->param_ptr(MT_P_FC2_B), sv.x1.ptr, y, (int)M, (int)h, site_out2, th_h, scale_h, st);
+  ++n;
+  check_cuda(cudaGetLastError(), "layer forward launch");
+  l->fwd_launches = n;
+}
+
+void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStream_t st) {
+  mt_ctx* c = l->ctx;
+  const mt_layer_desc& d = l->d;
+  auto it = l->saved.find(mb);
+  if (it == l->saved.end()) throw std::invalid_argument("backward without a saved forward for this microbatch");
+  auto& sv = *it->second;
+  const int64_t M = l->M, h = l->h, hl = l->hl, ffl = l->ffl, ld3 = l->qkvl, s = d.seq, Hl = l->heads_local,
+                hd = l->head_dim;
+  float* mean1 = sv.stats.as<float>();
+  float* rstd1 = mean1 + M;
+  float* mean2 = rstd1 + M;
+  float* rstd2 = mean2 + M;
+  float* ws = c->scratch_ws.as<float>();
+  int n = 0;
+  const float scale_h = 1.f / (1.f - d.dropout_hidden), scale_a = 1.f / (1.f - d.dropout_attn);
+  const uint32_t th_h = curator::dropout_threshold16(d.dropout_hidden);
+  const uint32_t th_a = curator::dropout_threshold16(d.dropout_attn);
+  const uint64_t site_attn = key_of(d.seed, "attn.probs", d.layer_index, mb);
+  const uint64_t site_out1 = key_of(d.seed, "attn.out", d.layer_index, mb);
+  const uint64_t site_out2 = key_of(d.seed, "mlp.out", d.layer_index, mb);
+  void* dm = c->scratch_h[0].ptr;   // mlp-out grad, later attn-out grad (dz)
+  void* dln = c->scratch_h[1].ptr;  // grad wrt LN2 / LN1 output
+  void* dx1 = c->scratch_h[2].ptr;  // grad wrt residual stream x1
+  void* dpre = c->scratch_ffn.ptr;
+  void* dctx = c->scratch_ctx.ptr;
+  void* dqkv = c->scratch_qkv.ptr;
+  uint16_t* dP = c->scratch_attn.as<uint16_t>();
+
+  // ---- MLP block
+  dropout_bwd_bias_grad(dy, dm, l->grad_ptr(MT_P_FC2_B), (int)M, (int)h, site_out2, th_h, scale_h, ws, st);
+  n += 2;
+  Gemm(dm, h, false, l->param_ptr(MT_P_FC2_W), ffl, true, dpre, ffl, M, ffl, h)
+      .epi(MT_EPI_GELU_BWD)
+      .aux(sv.pre.ptr, ffl)
+      .run(st, n);
+  Gemm(dm, h, true, sv.act.ptr, ffl, true, l->grad_ptr(MT_P_FC2_W), ffl, h, ffl, M).epi(MT_EPI_ACCUM_F32).run(st, n);
+  bias_grad(dpre, l->grad_ptr(MT_P_FC1_B), (int)M, (int)ffl, ffl, ws, st);
+  n += 2;
+  Gemm(dpre, ffl, true, sv.ln2.ptr, h, true, l->grad_ptr(MT_P_FC1_W), h, ffl, h, M).epi(MT_EPI_ACCUM_F32).run(st, n);
+  Gemm(dpre, ffl, false, l->param_ptr(MT_P_FC1_W), h, true, dln, h, M, h, ffl).run(st, n);
+  if (d.tp_size > 1) {
+    check_nccl(ncclAllReduce(dln, dln, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(ln2.grad)");
+    ++n;
+  }
+  ln_bwd_dx(dln, sv.x1.ptr, l->param_ptr(MT_P_LN2_GAMMA), mean2, rstd2, dy, dx1, (int)M, (int)h, st);
+  ln_bwd_params(dln, sv.x1.ptr, mean2, rstd2, l->grad_ptr(MT_P_LN2_GAMMA), l->grad_ptr(MT_P_LN2_BETA), (int)M, (int)h,
+                ws, st);
+  n += 3;
+  // ---- attention block
+  void* dz = dm;
+  dropout_bwd_bias_grad(dx1, dz, l->grad_ptr(MT_P_PROJ_B), (int)M, (int)h, site_out1, th_h, scale_h, ws, st);
+  n += 2;
+  Gemm(dz, h, false, l->param_ptr(MT_P_PROJ_W), hl, true, dctx, hl, M, hl, h).run(st, n);
+  Gemm(dz, h, true, sv.ctx.ptr, hl, true, l->grad_ptr(MT_P_PROJ_W), hl, h, hl, M).epi(MT_EPI_ACCUM_F32).run(st, n);
+  const float alpha = 1.f / std::sqrt((float)hd);
+  for (int64_t bb = 0; bb < d.micro_batch; ++bb) {
+    const uint16_t* q = sv.qkv.as<uint16_t>() + bb * s * ld3;
+    uint16_t* dq = static_cast<uint16_t*>(dqkv) + bb * s * ld3;
+    const uint16_t* dc = static_cast<const uint16_t*>(dctx) + bb * s * hl;
+    const uint16_t* S = sv.S.as<uint16_t>() + bb * Hl * s * s;
+    const uint16_t* P = sv.P.as<uint16_t>() + bb * Hl * s * s;
+    const float* lse = sv.lse.as<float>() + bb * Hl * s;
+    // dP_dropped = dctx_h V_h^T
+    Gemm(dc, hl, false, q + 2 * hd, ld3, false, dP, s, s, s, hd)
+        .batched(Hl, hd, 3 * hd, s * s)
+        .causal(MT_CAUSAL_SKIP_UPPER_TILES)
+        .run(st, n);
+    // dV_h = P_h^T dctx_h
+    Gemm(P, s, true, dc, hl, true, dq + 2 * hd, ld3, s, hd, s)
+        .batched(Hl, s * s, hd, 3 * hd)
+        .causal(MT_CAUSAL_K_GE_M)
+        .run(st, n);
+    const long long head_base = bb * d.heads + int64_t{d.tp_rank} * Hl;
+    softmax_bwd(S, lse, dP, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, alpha, st);
+    ++n;
+    // dQ_h = dS_h K_h ; dK_h = dS_h^T Q_h   (dS already carries the 1/sqrt(d) factor)
+    Gemm(dP, s, false, q + hd, ld3, true, dq, ld3, s, hd, s)
+        .batched(Hl, s * s, 3 * hd, 3 * hd)
+        .causal(MT_CAUSAL_K_LE_M)
+        .run(st, n);
+    Gemm(dP, s, true, q, ld3, true, dq + hd, ld3, s, hd, s)
+        .batched(Hl, s * s, 3 * hd, 3 * hd)
+        .causal(MT_CAUSAL_K_GE_M)
+        .run(st, n);
+  }
+  bias_grad(dqkv, l->grad_ptr(MT_P_QKV_B), (int)M, (int)ld3, ld3, ws, st);
+  n += 2;
+  Gemm(dqkv, ld3, true, sv.ln1.ptr, h, true, l->grad_ptr(MT_P_QKV_W), h, ld3, h, M).epi(MT_EPI_ACCUM_F32).run(st, n);
+  Gemm(dqkv, ld3, false, l->param_ptr(MT_P_QKV_W), h, true, dln, h, M, h, ld3).run(st, n);
+  if (d.tp_size > 1) {
+    check_nccl(ncclAllReduce(dln, dln, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(ln1.grad)");
+    ++n;
+  }
+  ln_bwd_dx(dln, sv.x, l->param_ptr(MT_P_LN1_GAMMA), mean1, rstd1, dx1, dx, (int)M, (int)h, st);
+  ln_bwd_params(dln, sv.x, mean1, rstd1, l->grad_ptr(MT_P_LN1_GAMMA), l->grad_ptr(MT_P_LN1_BETA), (int)M, (int)h, ws,
+                st);
+  n += 3;
+  check_cuda(cudaGetLastError(), "layer backward launch");
+  l->bwd_launches = n;
+  l->free_slots.push_back(std::move(it->second));
+  l->saved.erase(it);
+}
+
+}  // namespace
+
+extern "C" int mt_layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, void* stream) {
+  return guarded([&] {
+    if (!l || !x || !y) throw std::invalid_argument("null argument");
+    layer_forward(l, x, y, mb, (cudaStream_t)stream);
+  });
+}
+
+extern "C" int mt_layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, void* stream) {
+  return guarded([&] {
+    if (!l || !dy || !dx) throw std::invalid_argument("null argument");
+    layer_backward(l, dy, dx, mb, (cudaStream_t)stream);
+  });
+}
+
+extern "C" int mt_mse_loss(const void* y, const void* t, void* dy, float* loss, int64_t n, void* stream) {
+  return guarded([&] {
+    if (n % 8) throw std::invalid_argument("n must be a multiple of 8");
+    mt::mse_loss(y, t, dy, loss, n, (cudaStream_t)stream);
+    check_cuda(cudaGetLastError(), "mse_loss");
+  });
+}
+
+extern "C" int mt_fill_normal(void* out, int64_t n, uint64_t key, float mean, float std, void* stream) {
+  return guarded([&] {
+    mt::fill_normal(out, 1, n, n, 0, 0, key, mean, std, (cudaStream_t)stream);
+    check_cuda(cudaGetLastError(), "fill_normal");
+  });
+}

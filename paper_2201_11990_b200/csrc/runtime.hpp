@@ -1,0 +1,84 @@
+// Internal C++ runtime objects behind the C ABI (mtnlg.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "curator/planner.hpp"
+#include "curator/schedule.hpp"
+#include "mtnlg.h"
+
+namespace mt {
+
+// Failed CUDA / NCCL call -> DataError-class status 2.
+struct RuntimeFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void check_cuda(cudaError_t e, const char* what);
+void check_nccl(ncclResult_t r, const char* what);
+
+// Device buffer owned by the runtime.
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(size_t n);
+  ~DeviceBuffer();
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : ptr(o.ptr), bytes(o.bytes) {
+    o.ptr = nullptr;
+    o.bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(ptr);
+  }
+  void ensure(size_t n);  // grow (contents discarded)
+};
+
+}  // namespace mt
+
+struct mt_ctx {
+  int device = 0;
+  int world_size = 1, rank = 0;
+  curator::ParallelConfig par;
+  curator::RankPlacement place;
+  ncclComm_t world = nullptr, tp = nullptr, pp = nullptr, dp = nullptr;
+  // scratch shared by all layers of this context (sized to the largest layer)
+  mt::DeviceBuffer scratch_h[4];   // [M, h] bf16 temporaries
+  mt::DeviceBuffer scratch_ffn;    // [M, ffn/t] bf16
+  mt::DeviceBuffer scratch_ctx;    // [M, h/t] bf16
+  mt::DeviceBuffer scratch_qkv;    // [M, 3h/t] bf16
+  mt::DeviceBuffer scratch_attn;   // [heads/t, s, s] bf16
+  mt::DeviceBuffer scratch_ws;     // fp32 column-reduction workspace
+};
+
+struct mt_layer {
+  mt_ctx* ctx = nullptr;
+  mt_layer_desc d{};
+  int64_t M = 0, h = 0, hl = 0, ffl = 0, qkvl = 0, heads_local = 0, head_dim = 0;
+  curator::LayerShard shard;
+  int64_t param_off[MT_P_COUNT] = {};  // element offsets into params / grads
+  int64_t param_rows[MT_P_COUNT] = {}, param_cols[MT_P_COUNT] = {};
+  int64_t param_total = 0;
+  mt::DeviceBuffer params;  // bf16
+  mt::DeviceBuffer grads;   // fp32
+  struct Saved {
+    const void* x = nullptr;
+    mt::DeviceBuffer ln1, qkv, S, P, lse, ctx, x1, ln2, pre, act, stats;  // stats: mean1,rstd1,mean2,rstd2
+  };
+  std::map<uint32_t, std::unique_ptr<Saved>> saved;
+  std::vector<std::unique_ptr<Saved>> free_slots;
+  int fwd_launches = 0, bwd_launches = 0;
+  void* param_ptr(int p) const { return static_cast<uint16_t*>(params.ptr) + param_off[p]; }
+  float* grad_ptr(int p) const { return grads.as<float>() + param_off[p]; }
+};

@@ -1,0 +1,263 @@
+// Pipeline stage driver: one training iteration of one rank under the 3D layout.
+//
+// The op order is curator::one_f_one_b (PipeDream-Flush 1F1B). Point-to-point
+// transfers follow the Megatron pairing so neighbouring stages never wait on each other's sends:
+// in the steady phase a stage posts "send activation forward + receive gradient backward" as one
+// NCCL group, and "send gradient backward + receive next activation" as another. After the last
+// backward the fp32 parameter gradients are all-reduced (mean) over the data-parallel group
+// (PAPER.md:103-131). TP all-reduces happen inside the layers.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "curator/dropout.hpp"
+#include "curator/schedule.hpp"
+#include "kernels.cuh"
+#include "runtime.hpp"
+
+namespace mt {
+void set_error(const std::string& e);
+}
+
+struct mt_stage {
+  mt_ctx* ctx = nullptr;
+  mt_stage_desc d{};
+  int stage = 0, stages = 1;
+  std::vector<mt_layer*> layers;
+  int64_t M = 0, h = 0;
+  std::vector<std::vector<mt::DeviceBuffer>> act;  // [mb][layer+1] bf16 [M, h]
+  mt::DeviceBuffer grad[2];                        // ping-pong [M, h]
+  mt::DeviceBuffer target;                         // [M, h]
+  mt::DeviceBuffer loss;                           // fp32 scalar
+  int64_t launches = 0;
+};
+
+namespace {
+
+template <class F>
+int call(F&& f) {
+  try {
+    f();
+    return MT_OK;
+  } catch (const std::invalid_argument& e) {
+    mt::set_error(e.what());
+    return MT_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    mt::set_error(e.what());
+    return MT_ERR_DATA;
+  }
+}
+
+void ok(int rc) {
+  if (rc == MT_ERR_CONFIG) throw std::invalid_argument(mt_last_error());
+  if (rc != MT_OK) throw mt::RuntimeFailure(mt_last_error());
+}
+
+struct Step {
+  mt_stage* st;
+  cudaStream_t s;
+  const uint16_t* in_host;
+  const uint16_t* tgt_host;
+  int64_t launches = 0;
+  bool first() const { return st->stage == 0; }
+  bool last() const { return st->stage == st->stages - 1; }
+  size_t bytes() const { return static_cast<size_t>(st->M * st->h * 2); }
+  int64_t elems() const { return st->M * st->h; }
+  ncclComm_t pp() const { return st->ctx->pp; }
+
+  void load_input(int mb) {
+    void* dst = st->act[mb][0].ptr;
+    if (in_host) {
+      mt::check_cuda(cudaMemcpyAsync(dst, in_host + mb * elems(), bytes(), cudaMemcpyHostToDevice, s), "H2D input");
+    } else {
+      const uint64_t key = mt_stream_key(st->d.layer.seed, "input", 0, (uint32_t)mb);
+      mt::fill_normal(dst, 1, elems(), elems(), 0, 0, key, 0.f, 1.f, s);
+      ++launches;
+    }
+  }
+  void forward(int mb) {
+    for (size_t i = 0; i < st->layers.size(); ++i) {
+      ok(mt_layer_forward(st->layers[i], st->act[mb][i].ptr, st->act[mb][i + 1].ptr, (uint32_t)mb, s));
+      int32_t f, b;
+      mt_layer_launch_counts(st->layers[i], &f, &b);
+      launches += f;
+    }
+    if (last()) {
+      void* y = st->act[mb][st->layers.size()].ptr;
+      if (tgt_host) {
+        mt::check_cuda(cudaMemcpyAsync(st->target.ptr, tgt_host + mb * elems(), bytes(), cudaMemcpyHostToDevice, s),
+                       "H2D target");
+      } else {
+        const uint64_t key = mt_stream_key(st->d.layer.seed, "target", 0, (uint32_t)mb);
+        mt::fill_normal(st->target.ptr, 1, elems(), elems(), 0, 0, key, 0.f, 1.f, s);
+        ++launches;
+      }
+      mt::mse_loss(y, st->target.ptr, y, st->loss.as<float>(), elems(), s);  // dy overwrites y in place
+      ++launches;
+    }
+  }
+  // Backward of microbatch mb; gradient arrives in g (last stage: in act[mb][L]). Returns dx buffer.
+  void* backward(int mb, void* g) {
+    void* cur = g;
+    for (size_t i = st->layers.size(); i-- > 0;) {
+      void* out = (cur == st->grad[0].ptr) ? st->grad[1].ptr : st->grad[0].ptr;
+      ok(mt_layer_backward(st->layers[i], cur, out, (uint32_t)mb, s));
+      int32_t f, b;
+      mt_layer_launch_counts(st->layers[i], &f, &b);
+      launches += b;
+      cur = out;
+    }
+    return cur;
+  }
+  void recv_fwd(int mb) {
+    mt::check_nccl(ncclRecv(st->act[mb][0].ptr, elems(), ncclBfloat16, st->stage - 1, pp(), s), "recv fwd");
+    ++launches;
+  }
+  void send_fwd(int mb) {
+    mt::check_nccl(ncclSend(st->act[mb][st->layers.size()].ptr, elems(), ncclBfloat16, st->stage + 1, pp(), s),
+                   "send fwd");
+    ++launches;
+  }
+  void* grad_in_buffer() { return st->grad[0].ptr; }
+};
+
+}  // namespace
+
+extern "C" int mt_stage_create(mt_ctx* c, const mt_stage_desc* d, mt_stage** out) {
+  return call([&] {
+    if (!c || !d || !out) throw std::invalid_argument("null argument");
+    auto st = new mt_stage();
+    st->ctx = c;
+    st->d = *d;
+    st->stage = c->place.pipeline;
+    st->stages = c->par.pipeline;
+    const curator::Range own = curator::stage_layers(d->layers, st->stages, st->stage);
+    mt_layer_desc ld = d->layer;
+    ld.tp_size = c->par.tensor;
+    ld.tp_rank = c->place.tensor;
+    for (int64_t li = own.begin; li < own.end; ++li) {
+      ld.layer_index = static_cast<uint32_t>(li);
+      mt_layer* l = nullptr;
+      const int rc = mt_layer_create(c, &ld, &l);
+      if (rc != MT_OK) {
+        for (auto* x : st->layers) mt_layer_destroy(x);
+        delete st;
+        ok(rc);
+      }
+      st->layers.push_back(l);
+    }
+    st->M = int64_t{ld.micro_batch} * ld.seq;
+    st->h = ld.hidden;
+    const size_t bytes = static_cast<size_t>(st->M * st->h * 2);
+    st->act.resize(d->micro_batches);
+    for (auto& v : st->act) {
+      v.resize(st->layers.size() + 1);
+      for (auto& b : v) b.ensure(bytes);
+    }
+    for (auto& g : st->grad) g.ensure(bytes);
+    st->target.ensure(bytes);
+    st->loss.ensure(4);
+    *out = st;
+  });
+}
+
+extern "C" int mt_stage_destroy(mt_stage* st) {
+  return call([&] {
+    if (!st) return;
+    for (auto* l : st->layers) mt_layer_destroy(l);
+    delete st;
+  });
+}
+
+extern "C" int mt_stage_layer(mt_stage* st, int32_t i, mt_layer** out) {
+  return call([&] {
+    if (!st || !out || i < 0 || i >= (int32_t)st->layers.size()) throw std::invalid_argument("bad layer index");
+    *out = st->layers[i];
+  });
+}
+
+extern "C" int mt_stage_launch_count(const mt_stage* st, int64_t* n) {
+  return call([&] { *n = st->launches; });
+}
+
+extern "C" int mt_stage_train_step(mt_stage* st, const void* inputs_host, const void* targets_host, float* loss_out,
+                                   void* stream) {
+  return call([&] {
+    if (!st) throw std::invalid_argument("null stage");
+    Step k{st, (cudaStream_t)stream, static_cast<const uint16_t*>(inputs_host),
+           static_cast<const uint16_t*>(targets_host)};
+    const int MB = st->d.micro_batches;
+    for (auto* l : st->layers) ok(mt_layer_zero_grads(l, stream));
+    mt::check_cuda(cudaMemsetAsync(st->loss.ptr, 0, 4, k.s), "memset loss");
+    const int warmup = std::min(st->stages - st->stage - 1, MB);
+    const int steady = MB - warmup;
+    int next_f = 0, next_b = 0;
+    // warmup forwards
+    for (int i = 0; i < warmup; ++i) {
+      const int mb = next_f++;
+      k.first() ? k.load_input(mb) : k.recv_fwd(mb);
+      k.forward(mb);
+      k.send_fwd(mb);  // warmup > 0 implies not the last stage
+    }
+    if (steady > 0) k.first() ? k.load_input(next_f) : k.recv_fwd(next_f);
+    for (int i = 0; i < steady; ++i) {
+      const int mb = next_f++;
+      k.forward(mb);
+      // send activation forward + receive the gradient of the oldest in-flight microbatch
+      const int bmb = next_b++;
+      void* g = k.last() ? st->act[bmb][st->layers.size()].ptr : k.grad_in_buffer();
+      if (!k.last()) {
+        mt::check_nccl(ncclGroupStart(), "group");
+        mt::check_nccl(ncclSend(st->act[mb][st->layers.size()].ptr, k.elems(), ncclBfloat16, st->stage + 1, k.pp(), k.s),
+                       "send fwd");
+        mt::check_nccl(ncclRecv(g, k.elems(), ncclBfloat16, st->stage + 1, k.pp(), k.s), "recv bwd");
+        mt::check_nccl(ncclGroupEnd(), "group");
+        ++k.launches;
+      }
+      void* dx = k.backward(bmb, g);
+      const bool more = i + 1 < steady;
+      if (!k.first()) {
+        mt::check_nccl(ncclGroupStart(), "group");
+        mt::check_nccl(ncclSend(dx, k.elems(), ncclBfloat16, st->stage - 1, k.pp(), k.s), "send bwd");
+        if (more) mt::check_nccl(ncclRecv(st->act[next_f][0].ptr, k.elems(), ncclBfloat16, st->stage - 1, k.pp(), k.s),
+                                 "recv fwd");
+        mt::check_nccl(ncclGroupEnd(), "group");
+        ++k.launches;
+      } else if (more) {
+        k.load_input(next_f);
+      }
+    }
+    // cooldown backwards
+    for (int i = 0; i < warmup; ++i) {
+      const int bmb = next_b++;
+      void* g = k.grad_in_buffer();
+      mt::check_nccl(ncclRecv(g, k.elems(), ncclBfloat16, st->stage + 1, k.pp(), k.s), "recv bwd");
+      ++k.launches;
+      void* dx = k.backward(bmb, g);
+      if (!k.first()) {
+        mt::check_nccl(ncclSend(dx, k.elems(), ncclBfloat16, st->stage - 1, k.pp(), k.s), "send bwd");
+        ++k.launches;
+      }
+    }
+    // data-parallel gradient all-reduce (mean)
+    if (st->ctx->par.data > 1) {
+      for (auto* l : st->layers) {
+        ok(mt_dp_allreduce_f32(st->ctx, l->grads.as<float>(), l->param_total, 1, stream));
+        ++k.launches;
+      }
+    }
+    if (loss_out) {
+      float host = 0.f;
+      if (k.last()) {
+        if (st->ctx->par.data > 1) {
+          ok(mt_dp_allreduce_f32(st->ctx, st->loss.as<float>(), 1, 1, stream));
+          ++k.launches;
+        }
+        mt::check_cuda(cudaMemcpyAsync(&host, st->loss.ptr, 4, cudaMemcpyDeviceToHost, k.s), "D2H loss");
+        mt::check_cuda(cudaStreamSynchronize(k.s), "sync");
+      }
+      *loss_out = host;
+    }
+    st->launches = k.launches;
+  });
+}

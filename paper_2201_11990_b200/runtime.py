@@ -1,0 +1,124 @@
+"""Host-side Python handles over the C++ runtime in libmtnlg.so (include/mtnlg.h).
+
+`Context` = one GPU (+ its NCCL TP/PP/DP groups derived from curator::map_topology), `Layer` = one
+tensor-sliced transformer layer shard, `Stage` = this rank's pipeline stage with the 1F1B driver.
+Device buffers are passed as raw pointers (e.g. torch tensors' data_ptr()); streams as cudaStream_t.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from ._native import LayerDesc, ParallelConfig, RankPlacement, StageDesc, check, lib
+from .planner import layer_desc  # noqa: F401  (re-export)
+
+
+def _stream(stream) -> C.c_void_p:
+    if stream is None:
+        return C.c_void_p(0)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(getattr(stream, "cuda_stream", stream))
+
+
+class Context:
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        check(lib().mt_ctx_create(device, C.byref(self._h)))
+        self.device = device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().mt_nccl_unique_id(buf))
+        return buf.raw
+
+    def init_comm(self, nccl_id: bytes, world_size: int, rank: int, tensor=1, pipeline=1, data=1, batch=1,
+                  micro_batches=1) -> None:
+        par = ParallelConfig(tensor, pipeline, data, batch, micro_batches)
+        check(lib().mt_ctx_init_comm(self._h, nccl_id, world_size, rank, C.byref(par)))
+
+    def placement(self) -> RankPlacement:
+        p = RankPlacement()
+        check(lib().mt_ctx_placement(self._h, C.byref(p)))
+        return p
+
+    def close(self) -> None:
+        if self._h:
+            lib().mt_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+class Layer:
+    def __init__(self, ctx: Context, desc: LayerDesc):
+        self.ctx, self.desc = ctx, desc
+        self._h = C.c_void_p()
+        check(lib().mt_layer_create(ctx._h, C.byref(desc), C.byref(self._h)))
+
+    def init_params(self, stream=None) -> None:
+        check(lib().mt_layer_init_params(self._h, _stream(stream)))
+
+    def set_param(self, param: int, host_global_bf16_ptr: int) -> None:
+        check(lib().mt_layer_set_param(self._h, param, C.c_void_p(host_global_bf16_ptr)))
+
+    def get_param(self, param: int, host_u16_ptr: int) -> None:
+        check(lib().mt_layer_get_param(self._h, param, C.c_void_p(host_u16_ptr)))
+
+    def get_grad(self, param: int, host_f32_ptr: int) -> None:
+        check(lib().mt_layer_get_grad(self._h, param, C.cast(C.c_void_p(host_f32_ptr), C.POINTER(C.c_float))))
+
+    def zero_grads(self, stream=None) -> None:
+        check(lib().mt_layer_zero_grads(self._h, _stream(stream)))
+
+    def forward(self, x_ptr: int, y_ptr: int, micro_batch: int = 0, stream=None) -> None:
+        check(lib().mt_layer_forward(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), micro_batch, _stream(stream)))
+
+    def backward(self, dy_ptr: int, dx_ptr: int, micro_batch: int = 0, stream=None) -> None:
+        check(lib().mt_layer_backward(self._h, C.c_void_p(dy_ptr), C.c_void_p(dx_ptr), micro_batch, _stream(stream)))
+
+    def launch_counts(self) -> tuple[int, int]:
+        f, b = C.c_int32(), C.c_int32()
+        check(lib().mt_layer_launch_counts(self._h, C.byref(f), C.byref(b)))
+        return f.value, b.value
+
+    def close(self) -> None:
+        if self._h:
+            lib().mt_layer_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+class Stage:
+    """This rank's pipeline stage: layers [stage*L/PP, (stage+1)*L/PP) of the model."""
+
+    def __init__(self, ctx: Context, layer: LayerDesc, layers: int, micro_batches: int):
+        self.ctx = ctx
+        self.desc = StageDesc(layer, layers, micro_batches)
+        self._h = C.c_void_p()
+        check(lib().mt_stage_create(ctx._h, C.byref(self.desc), C.byref(self._h)))
+
+    def layer(self, i: int) -> Layer:
+        h = C.c_void_p()
+        check(lib().mt_stage_layer(self._h, i, C.byref(h)))
+        lay = Layer.__new__(Layer)
+        lay.ctx, lay.desc, lay._h = self.ctx, None, h
+        return lay
+
+    def init_params(self, n_layers: int, stream=None) -> None:
+        for i in range(n_layers):
+            self.layer(i).init_params(stream)
+
+    def train_step(self, inputs_host_ptr: int | None = None, targets_host_ptr: int | None = None,
+                   stream=None, want_loss: bool = True) -> float:
+        loss = C.c_float(0.0)
+        check(lib().mt_stage_train_step(self._h, C.c_void_p(inputs_host_ptr or 0), C.c_void_p(targets_host_ptr or 0),
+                                        C.byref(loss) if want_loss else None, _stream(stream)))
+        return loss.value
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        check(lib().mt_stage_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    def close(self) -> None:
+        if self._h:
+            lib().mt_stage_destroy(self._h)
+            self._h = C.c_void_p()

@@ -1,0 +1,120 @@
+"""GPU parity of the tensor-sliced layer (forward + backward) against the CPU oracle.
+
+The GPU path runs entirely through the C ABI of libmtnlg.so (mt_layer_forward / mt_layer_backward);
+the oracle is oracle/layer_oracle.cpp on the same seeded bf16 inputs and parameters.
+
+Tolerances, relative Frobenius error:
+  vs bf16-emulated oracle : activations <= 5e-3, gradients <= 1e-2
+  vs fp32 oracle          : activations <= 2e-2, gradients <= 3e-2
+Dropout masks are bit-identical by construction (tests/test_oracle.py pins the mask definition).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from paper_2201_11990_b200 import planner as PL  # noqa: E402
+from paper_2201_11990_b200.runtime import Context, Layer  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+SEED = 20260808
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def bf16_tensor(a: np.ndarray) -> "torch.Tensor":
+    bits = O.to_bf16_bits(a)
+    return torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def to_np(t: "torch.Tensor") -> np.ndarray:
+    return t.float().cpu().numpy()
+
+
+CASES = [
+    # hidden, heads, seq, micro_batch, dropout
+    (256, 4, 128, 4, 0.1),     # BASELINE configs[0] shape (tiny GPT layer), hd = 64
+    (256, 4, 128, 4, 0.0),
+    (1024, 8, 256, 1, 0.1),    # hd = 128
+    (640, 4, 256, 1, 0.1),     # hd = 160 (MT-NLG head size)
+]
+
+
+@pytest.mark.parametrize("hidden,heads,seq,mb,p", CASES)
+def test_layer_matches_oracle(hidden, heads, seq, mb, p):
+    ctx = Context(0)
+    desc = PL.layer_desc(hidden, heads, seq, mb, dropout_hidden=p, dropout_attn=p, seed=SEED, layer_index=3)
+    layer = Layer(ctx, desc)
+    params = O.init_params(hidden, SEED, 3)
+    keep = []
+    for i, prm in enumerate(params):
+        bits = np.ascontiguousarray(O.to_bf16_bits(prm))
+        keep.append(bits)
+        layer.set_param(i, bits.ctypes.data)
+    M = mb * seq
+    x = O.normal(O.site_seed(SEED, "input", 0, 0), M, hidden)
+    g = O.normal(O.site_seed(SEED, "grad", 0, 0), M, hidden, std=1e-2)
+    xd, gd = bf16_tensor(x), bf16_tensor(g)
+    yd = torch.empty_like(xd)
+    dxd = torch.empty_like(xd)
+    s = torch.cuda.current_stream()
+    layer.forward(xd.data_ptr(), yd.data_ptr(), 0, s)
+    layer.backward(gd.data_ptr(), dxd.data_ptr(), 0, s)
+    torch.cuda.synchronize()
+    y, dx = to_np(yd), to_np(dxd)
+    grads = []
+    for i, prm in enumerate(params):
+        out = np.empty(prm.size, np.float32)
+        layer.get_grad(i, out.ctypes.data)
+        grads.append(out.reshape(prm.shape))
+
+    for emu, tol_a, tol_g in ((True, 5e-3, 1e-2), (False, 2e-2, 3e-2)):
+        ol = O.OracleLayer(hidden, heads, seq, mb, 1, dropout_hidden=p, dropout_attn=p, seed=SEED, layer_index=3,
+                           bf16_emulate=emu, params=params)
+        y_ref = ol.forward(x)
+        dx_ref = ol.backward(g)
+        assert rel(y, y_ref) < tol_a, ("y", emu, rel(y, y_ref))
+        assert rel(dx, dx_ref) < tol_a * 2, ("dx", emu, rel(dx, dx_ref))
+        for i, name in enumerate(O.PARAM_NAMES):
+            assert rel(grads[i], ol.grads[i]) < tol_g, (name, emu, rel(grads[i], ol.grads[i]))
+    layer.close()
+    ctx.close()
+
+
+def test_device_init_matches_oracle_streams():
+    """mt_layer_init_params draws, shard by shard, the same global tensors as the oracle's host
+    generator (so TP=t and TP=1 runs start from identical weights)."""
+    hidden, heads = 256, 4
+    ctx = Context(0)
+    ref = O.init_params(hidden, SEED, 5)
+    for tp in (1, 2):
+        for r in range(tp):
+            desc = PL.layer_desc(hidden, heads, 128, 1, tp_size=tp, tp_rank=r, seed=SEED, layer_index=5)
+            layer = Layer(ctx, desc)
+            layer.init_params(torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            for i in range(len(ref)):
+                _, (r0, c0), (nr, nc) = PL.param_shard(desc, i)
+                got = np.empty(nr * nc, np.uint16)
+                layer.get_param(i, got.ctypes.data)
+                want = O.to_bf16_bits(ref[i][r0:r0 + nr, c0:c0 + nc]).ravel()
+                # device (libdevice) and host (glibc) log/sin/cos may differ in the last double ulp;
+                # after rounding to bf16 that flips at most a handful of values by one ulp.
+                diff = np.abs(got.astype(np.int32) - want.astype(np.int32))
+                assert diff.max() <= 1 and (diff > 0).mean() < 1e-3, (tp, r, i)
+            layer.close()
+    ctx.close()
+
+
+def test_layer_rejects_bad_config():
+    ctx = Context(0)
+    with pytest.raises(PL.ConfigError):
+        Layer(ctx, PL.layer_desc(256, 3, 128, 1))  # heads do not divide hidden
+    with pytest.raises(PL.ConfigError):
+        Layer(ctx, PL.layer_desc(256, 4, 128, 1, tp_size=8, tp_rank=0))  # heads % TP
+    ctx.close()
