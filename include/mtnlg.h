@@ -118,6 +118,11 @@ int mt_nccl_unique_id(unsigned char out[128]);
 int mt_ctx_init_comm(mt_ctx* ctx, const unsigned char id[128], int32_t world_size, int32_t rank,
                      const mt_parallel_config* par);
 int mt_ctx_placement(const mt_ctx* ctx, mt_rank_placement* out);
+/* Per-GEMM CUDA-event timing of every tcgen05 GEMM the context's layers launch (stream-ordered
+ * events around each launch). _read synchronises, returns the summed kernel time, summed
+ * algorithmic FLOPs and launch count since enabling / the last read, and resets. */
+int mt_ctx_gemm_timing(mt_ctx* ctx, int32_t enable);
+int mt_ctx_gemm_timing_read(mt_ctx* ctx, double* total_ms, double* total_flops, int64_t* launches);
 
 int mt_layer_create(mt_ctx* ctx, const mt_layer_desc* d, mt_layer** out);
 int mt_layer_destroy(mt_layer* l);
@@ -173,6 +178,11 @@ int mt_stage_layer(mt_stage* st, int32_t i, mt_layer** out);
  * generates inputs/targets on device from the seed (no host traffic). */
 int mt_stage_train_step(mt_stage* st, const void* inputs_host, const void* targets_host, float* loss_out,
                         void* stream);
+/* Same iteration with device-resident inputs: inputs_dev / targets_dev are device bf16
+ * [MB][b*s*h] (first / last stage; may be NULL on other stages); no host copies, no host sync.
+ * The summed loss stays on device in *loss_dev (may be NULL). */
+int mt_stage_train_step_dev(mt_stage* st, const void* inputs_dev, const void* targets_dev, float* loss_dev,
+                            void* stream);
 int mt_stage_launch_count(const mt_stage* st, int64_t* launches_per_step);
 
 #ifdef __cplusplus

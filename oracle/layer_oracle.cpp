@@ -57,48 +57,101 @@ struct Ctx {
   void round(Vec& v) const { round(v.data(), v.size()); }
 };
 
-// C[m][n] = sum_k A[m*lda + k] * B[n*ldb + k]  (both operands contiguous in k)
-void gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int64_t m, int64_t n,
-             int64_t k) {
-  constexpr int RB = 4, CB = 4;
-#pragma omp parallel for collapse(2) schedule(dynamic)
-  for (int64_t i0 = 0; i0 < m; i0 += RB) {
-    for (int64_t j0 = 0; j0 < n; j0 += CB) {
-      float acc[RB][CB] = {};
-      const int64_t ri = std::min<int64_t>(RB, m - i0), cj = std::min<int64_t>(CB, n - j0);
-      if (ri == RB && cj == CB) {
-        const float* a[RB];
-        const float* b[CB];
-        for (int r = 0; r < RB; ++r) a[r] = A + (i0 + r) * lda;
-        for (int c = 0; c < CB; ++c) b[c] = B + (j0 + c) * ldb;
-        for (int r = 0; r < RB; ++r)
-          for (int c = 0; c < CB; ++c) {
-            float s = 0.f;
-#pragma omp simd reduction(+ : s)
-            for (int64_t q = 0; q < k; ++q) s += a[r][q] * b[c][q];
-            acc[r][c] = s;
-          }
-      } else {
-        for (int r = 0; r < ri; ++r)
-          for (int c = 0; c < cj; ++c) {
-            float s = 0.f;
-            for (int64_t q = 0; q < k; ++q) s += A[(i0 + r) * lda + q] * B[(j0 + c) * ldb + q];
-            acc[r][c] = s;
-          }
+// Packed, register-blocked fp32 GEMM (Goto-style): C[m][n] (+)= sum_q A(m,q) B(q,n) with
+//   A(m,q) = a_t ? A[q*lda + m] : A[m*lda + q],   B(q,n) = b_t ? B[n*ldb + q] : B[q*ldb + n].
+// A is packed once into 6-row slivers, B per 16-column panel and 256-deep k-block; the 6x16
+// micro-kernel keeps its accumulators in vector registers. OpenMP over column panels.
+constexpr int kMR = 6, kNR = 16, kKC = 256;
+
+void micro_kernel_scalar(const float* __restrict__ ap, const float* __restrict__ bp, int kc, float* __restrict__ out) {
+  float acc[kMR][kNR] = {};
+  for (int q = 0; q < kc; ++q)
+    for (int r = 0; r < kMR; ++r)
+      for (int j = 0; j < kNR; ++j) acc[r][j] += ap[q * kMR + r] * bp[q * kNR + j];
+  for (int r = 0; r < kMR; ++r)
+    for (int j = 0; j < kNR; ++j) out[r * kNR + j] = acc[r][j];
+}
+
+typedef float v8 __attribute__((vector_size(32), aligned(4)));
+
+// 6x16 block, 12 ymm accumulators, one broadcast + two FMAs per (row, k).
+__attribute__((target("avx2,fma"))) void micro_kernel_avx2(const float* __restrict__ ap, const float* __restrict__ bp,
+                                                           int kc, float* __restrict__ out) {
+  v8 c0a = {}, c0b = {}, c1a = {}, c1b = {}, c2a = {}, c2b = {}, c3a = {}, c3b = {}, c4a = {}, c4b = {}, c5a = {},
+     c5b = {};
+  for (int q = 0; q < kc; ++q) {
+    const v8 b0 = *reinterpret_cast<const v8*>(bp + q * kNR);
+    const v8 b1 = *reinterpret_cast<const v8*>(bp + q * kNR + 8);
+    const float* a = ap + q * kMR;
+#define MT_ROW(R, CA, CB)      \
+  {                            \
+    const float av = a[R];     \
+    const v8 vv = {av, av, av, av, av, av, av, av}; \
+    CA += vv * b0;             \
+    CB += vv * b1;             \
+  }
+    MT_ROW(0, c0a, c0b) MT_ROW(1, c1a, c1b) MT_ROW(2, c2a, c2b) MT_ROW(3, c3a, c3b) MT_ROW(4, c4a, c4b)
+    MT_ROW(5, c5a, c5b)
+#undef MT_ROW
+  }
+  const v8* rows[kMR][2] = {{&c0a, &c0b}, {&c1a, &c1b}, {&c2a, &c2b}, {&c3a, &c3b}, {&c4a, &c4b}, {&c5a, &c5b}};
+  for (int r = 0; r < kMR; ++r) {
+    *reinterpret_cast<v8*>(out + r * kNR) = *rows[r][0];
+    *reinterpret_cast<v8*>(out + r * kNR + 8) = *rows[r][1];
+  }
+}
+
+void micro_kernel(const float* __restrict__ ap, const float* __restrict__ bp, int kc, float* __restrict__ out) {
+  static const bool avx2 = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma");
+  if (avx2)
+    micro_kernel_avx2(ap, bp, kc, out);
+  else
+    micro_kernel_scalar(ap, bp, kc, out);
+}
+
+void gemm(bool a_t, bool b_t, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+          int64_t ldb, float* C, int64_t ldc, bool accumulate) {
+  const int64_t mb = (m + kMR - 1) / kMR, nb = (n + kNR - 1) / kNR;
+  // pack A: Ap[ib][q][r]
+  std::vector<float> Ap(static_cast<size_t>(mb * k * kMR));
+#pragma omp parallel for schedule(static)
+  for (int64_t ib = 0; ib < mb; ++ib)
+    for (int64_t q = 0; q < k; ++q)
+      for (int r = 0; r < kMR; ++r) {
+        const int64_t i = ib * kMR + r;
+        Ap[(ib * k + q) * kMR + r] = i < m ? (a_t ? A[q * lda + i] : A[i * lda + q]) : 0.f;
       }
-      for (int r = 0; r < ri; ++r)
-        for (int c = 0; c < cj; ++c) C[(i0 + r) * ldc + j0 + c] = acc[r][c];
+#pragma omp parallel
+  {
+    std::vector<float> Bp(static_cast<size_t>(kKC) * kNR);
+    float blk[kMR * kNR];
+#pragma omp for schedule(dynamic)
+    for (int64_t jb = 0; jb < nb; ++jb) {
+      const int64_t j0 = jb * kNR, nj = std::min<int64_t>(kNR, n - j0);
+      for (int64_t q0 = 0; q0 < k; q0 += kKC) {
+        const int kc = static_cast<int>(std::min<int64_t>(kKC, k - q0));
+        for (int q = 0; q < kc; ++q)
+          for (int j = 0; j < kNR; ++j)
+            Bp[q * kNR + j] = j < nj ? (b_t ? B[(j0 + j) * ldb + q0 + q] : B[(q0 + q) * ldb + j0 + j]) : 0.f;
+        const bool first = q0 == 0 && !accumulate;
+        for (int64_t ib = 0; ib < mb; ++ib) {
+          micro_kernel(&Ap[(ib * k + q0) * kMR], Bp.data(), kc, blk);
+          const int64_t i0 = ib * kMR, ni = std::min<int64_t>(kMR, m - i0);
+          for (int64_t r = 0; r < ni; ++r)
+            for (int64_t j = 0; j < nj; ++j) {
+              float& c = C[(i0 + r) * ldc + j0 + j];
+              c = first ? blk[r * kNR + j] : c + blk[r * kNR + j];
+            }
+        }
+      }
     }
   }
 }
 
-// out[c][r] = in[r][c]   (in: rows x cols, leading dimension ld)
-Vec transpose(const float* in, int64_t rows, int64_t cols, int64_t ld) {
-  Vec out(static_cast<size_t>(rows * cols));
-#pragma omp parallel for schedule(static)
-  for (int64_t c = 0; c < cols; ++c)
-    for (int64_t r = 0; r < rows; ++r) out[c * rows + r] = in[r * ld + c];
-  return out;
+// C[m][n] = sum_k A[m*lda + k] * B[n*ldb + k]
+void gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int64_t m, int64_t n,
+             int64_t k) {
+  gemm(false, true, m, n, k, A, lda, B, ldb, C, ldc, false);
 }
 
 float gelu(float x) { return 0.5f * x * (1.f + std::tanh(0.7978845608028654f * x * (1.f + 0.044715f * x * x))); }
@@ -123,7 +176,7 @@ typedef struct or_layer_desc {
 struct or_layer {
   or_layer_desc d;
   Ctx cx;
-  std::vector<Vec> p;  // 12 global parameters
+  std::vector<const float*> p;  // 12 global parameters (caller-owned, non-owning views)
   struct Saved {
     Vec x, ln1, mean1, rstd1, qkv, S, P, lse, ctx, x1, ln2, mean2, rstd2, pre, act;
   };
@@ -145,9 +198,7 @@ or_layer* or_layer_create(const or_layer_desc* d, const float* const* params) {
   l->d = *d;
   l->cx.emu = d->bf16_emulate != 0;
   for (int i = 0; i < P_N; ++i) {
-    int64_t r, c;
-    or_param_shape(d, i, &r, &c);
-    l->p.emplace_back(params[i], params[i] + r * c);
+    l->p.push_back(params[i]);
   }
   return l;
 }
@@ -179,7 +230,7 @@ Dims dims(const or_layer_desc& d) {
   return x;
 }
 
-void layer_norm(const Ctx& cx, const Vec& x, const Vec& g, const Vec& be, Vec& y, Vec& mean, Vec& rstd, int64_t M,
+void layer_norm(const Ctx& cx, const Vec& x, const float* g, const float* be, Vec& y, Vec& mean, Vec& rstd, int64_t M,
                 int64_t h, float eps) {
   y.assign(M * h, 0.f);
   mean.assign(M, 0.f);
@@ -201,7 +252,7 @@ void layer_norm(const Ctx& cx, const Vec& x, const Vec& g, const Vec& be, Vec& y
 }
 
 // y = resid + dropout(z + bias)
-void bias_dropout_residual(const Ctx& cx, const Vec& z, const Vec& bias, const Vec& resid, Vec& y, int64_t M, int64_t h,
+void bias_dropout_residual(const Ctx& cx, const Vec& z, const float* bias, const Vec& resid, Vec& y, int64_t M, int64_t h,
                            uint64_t site, uint32_t th, float scale) {
   y.assign(M * h, 0.f);
 #pragma omp parallel for schedule(static)
@@ -214,13 +265,6 @@ void bias_dropout_residual(const Ctx& cx, const Vec& z, const Vec& bias, const V
 
 uint64_t site(const or_layer_desc& d, const char* name, uint32_t mb) {
   return curator::site_seed(d.seed, name, d.layer_index, mb);
-}
-
-// Slice rows [r0, r0+nr) x cols [c0, c0+nc) of a row-major matrix with `cols` columns.
-Vec slice(const Vec& m, int64_t cols, int64_t r0, int64_t nr, int64_t c0, int64_t nc) {
-  Vec o(nr * nc);
-  for (int64_t r = 0; r < nr; ++r) std::copy_n(&m[(r0 + r) * cols + c0], nc, &o[r * nc]);
-  return o;
 }
 
 }  // namespace
@@ -240,7 +284,7 @@ extern "C" void or_layer_forward(or_layer* l, const float* x_in, float* y_out, u
   // column-parallel QKV: the full output is the concatenation of the TP shards, so it is computed
   // at once (rows of the global weight in (head, {q,k,v}, hd) order).
   sv.qkv.assign(D.M * 3 * D.h, 0.f);
-  gemm_nt(sv.ln1.data(), D.h, P[P_QKVW].data(), D.h, sv.qkv.data(), 3 * D.h, D.M, 3 * D.h, D.h);
+  gemm_nt(sv.ln1.data(), D.h, P[P_QKVW], D.h, sv.qkv.data(), 3 * D.h, D.M, 3 * D.h, D.h);
   for (int64_t r = 0; r < D.M; ++r)
     for (int64_t c = 0; c < 3 * D.h; ++c) sv.qkv[r * 3 * D.h + c] += P[P_QKVB][c];
   cx.round(sv.qkv);
@@ -293,13 +337,13 @@ extern "C" void or_layer_forward(or_layer* l, const float* x_in, float* y_out, u
   cx.round(sv.ctx);
 
   // row-parallel attn-out: per TP shard partial (rounded like the GPU epilogue), summed (the all-reduce)
-  auto row_parallel = [&](const Vec& in, int64_t in_cols, const Vec& W, int64_t shard_cols, Vec& out) {
+  auto row_parallel = [&](const Vec& in, int64_t in_cols, const float* W, int64_t shard_cols, Vec& out) {
     out.assign(D.M * D.h, 0.f);
     Vec part(D.M * D.h);
     for (int64_t r = 0; r < D.t; ++r) {
-      const Vec in_s = slice(in, in_cols, 0, D.M, r * shard_cols, shard_cols);
-      const Vec w_s = slice(W, in_cols, 0, D.h, r * shard_cols, shard_cols);
-      gemm_nt(in_s.data(), shard_cols, w_s.data(), shard_cols, part.data(), D.h, D.M, D.h, shard_cols);
+      // shard r: input columns / weight columns [r*shard_cols, (r+1)*shard_cols)
+      gemm_nt(in.data() + r * shard_cols, in_cols, W + r * shard_cols, in_cols, part.data(), D.h, D.M, D.h,
+              shard_cols);
       cx.round(part);
       for (int64_t i = 0; i < D.M * D.h; ++i) out[i] += part[i];
     }
@@ -310,7 +354,7 @@ extern "C" void or_layer_forward(or_layer* l, const float* x_in, float* y_out, u
   bias_dropout_residual(cx, z, P[P_PROJB], sv.x, sv.x1, D.M, D.h, site(d, "attn.out", mb), th_h, scale_h);
   layer_norm(cx, sv.x1, P[P_LN2G], P[P_LN2B], sv.ln2, sv.mean2, sv.rstd2, D.M, D.h, d.ln_eps);
   sv.pre.assign(D.M * D.ff, 0.f);
-  gemm_nt(sv.ln2.data(), D.h, P[P_FC1W].data(), D.h, sv.pre.data(), D.ff, D.M, D.ff, D.h);
+  gemm_nt(sv.ln2.data(), D.h, P[P_FC1W], D.h, sv.pre.data(), D.ff, D.M, D.ff, D.h);
   sv.act.assign(D.M * D.ff, 0.f);
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < D.M * D.ff; ++i) {
@@ -329,23 +373,18 @@ extern "C" void or_layer_forward(or_layer* l, const float* x_in, float* y_out, u
 
 namespace {
 
-// dX = dY * W where W is [n, k] row-major (dY [M, n]) -> [M, k]; via the transposed weight.
+// dX[M][k] = dY[M][n] * W[n][k]
 void dgrad(const float* dY, int64_t n, const float* W, int64_t k, float* dX, int64_t M) {
-  const Vec Wt = transpose(W, n, k, k);  // [k, n]
-  gemm_nt(dY, n, Wt.data(), n, dX, k, M, k, n);
+  gemm(false, false, M, k, n, dY, n, W, k, dX, k, false);
 }
 
 // dW[n][k] += sum_tok dY[tok][n] * X[tok][k]
 void wgrad_acc(const float* dY, int64_t n, const float* X, int64_t k, float* dW, int64_t M) {
-  const Vec dYt = transpose(dY, M, n, n);  // [n, M]
-  const Vec Xt = transpose(X, M, k, k);    // [k, M]
-  Vec tmp(n * k);
-  gemm_nt(dYt.data(), M, Xt.data(), M, tmp.data(), k, n, k, M);
-#pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < n * k; ++i) dW[i] += tmp[i];
+  gemm(true, false, n, k, M, dY, n, X, k, dW, k, true);
 }
 
 void colsum_acc(const Vec& x, int64_t M, int64_t n, float* out) {
+#pragma omp parallel for schedule(static)
   for (int64_t c = 0; c < n; ++c) {
     double s = 0;
     for (int64_t r = 0; r < M; ++r) s += x[r * n + c];
@@ -354,7 +393,7 @@ void colsum_acc(const Vec& x, int64_t M, int64_t n, float* out) {
 }
 
 // LayerNorm backward: returns dx (+resid), accumulates dgamma, dbeta.
-void ln_backward(const Ctx& cx, const Vec& dy, const Vec& x, const Vec& g, const Vec& mean, const Vec& rstd,
+void ln_backward(const Ctx& cx, const Vec& dy, const Vec& x, const float* g, const Vec& mean, const Vec& rstd,
                  const Vec* resid, Vec& dx, float* dg, float* db, int64_t M, int64_t h) {
   dx.assign(M * h, 0.f);
 #pragma omp parallel for schedule(static)
@@ -373,6 +412,7 @@ void ln_backward(const Ctx& cx, const Vec& dy, const Vec& x, const Vec& g, const
       dx[r * h + c] = rstd[r] * (gg - m1 - xh * m2) + (resid ? (*resid)[r * h + c] : 0.f);
     }
   }
+#pragma omp parallel for schedule(static)
   for (int64_t c = 0; c < h; ++c) {
     double sg = 0, sb = 0;
     for (int64_t r = 0; r < M; ++r) {
@@ -410,13 +450,13 @@ extern "C" void or_layer_backward(or_layer* l, const float* dy_in, float* dx_out
   Vec dy(dy_in, dy_in + M * h);
 
   // column-parallel "f" backward: per-shard dgrad partials rounded, summed, rounded (the TP all-reduce)
-  auto col_parallel_dgrad = [&](const Vec& dout, int64_t out_cols, const Vec& W, int64_t shard_rows, Vec& din) {
+  auto col_parallel_dgrad = [&](const Vec& dout, int64_t out_cols, const float* W, int64_t shard_rows, Vec& din) {
     din.assign(M * h, 0.f);
     Vec part(M * h);
     for (int64_t r = 0; r < D.t; ++r) {
-      const Vec do_s = slice(dout, out_cols, 0, M, r * shard_rows, shard_rows);
-      const Vec w_s = slice(W, h, r * shard_rows, shard_rows, 0, h);
-      dgrad(do_s.data(), shard_rows, w_s.data(), h, part.data(), M);
+      // shard r: output columns of dout / rows of W [r*shard_rows, (r+1)*shard_rows)
+      gemm(false, false, M, h, shard_rows, dout.data() + r * shard_rows, out_cols, W + r * shard_rows * h, h,
+           part.data(), h, false);
       cx.round(part);
       for (int64_t i = 0; i < M * h; ++i) din[i] += part[i];
     }
@@ -428,7 +468,7 @@ extern "C" void or_layer_backward(or_layer* l, const float* dy_in, float* dx_out
   dropout_bwd(cx, dy, dm, M * h, site(d, "mlp.out", mb), th_h, scale_h);
   colsum_acc(dm, M, h, grads[P_FC2B]);
   Vec dpre(M * ff);
-  dgrad(dm.data(), h, P[P_FC2W].data(), ff, dpre.data(), M);
+  dgrad(dm.data(), h, P[P_FC2W], ff, dpre.data(), M);
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < M * ff; ++i) dpre[i] *= gelu_grad(sv.pre[i]);
   cx.round(dpre);
@@ -445,7 +485,7 @@ extern "C" void or_layer_backward(or_layer* l, const float* dy_in, float* dx_out
   dropout_bwd(cx, dx1, dz, M * h, site(d, "attn.out", mb), th_h, scale_h);
   colsum_acc(dz, M, h, grads[P_PROJB]);
   Vec dctx(M * h);
-  dgrad(dz.data(), h, P[P_PROJW].data(), h, dctx.data(), M);
+  dgrad(dz.data(), h, P[P_PROJW], h, dctx.data(), M);
   cx.round(dctx);
   wgrad_acc(dz.data(), h, sv.ctx.data(), h, grads[P_PROJW], M);
 

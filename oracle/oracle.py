@@ -107,6 +107,7 @@ class OracleLayer:
         self.desc = OrDesc(hidden, heads, seq, micro_batch, tp_size, ffn_mult, dropout_hidden, dropout_attn, ln_eps,
                            seed, layer_index, int(bf16_emulate))
         self.hidden, self.M = hidden, micro_batch * seq
+        # the native object keeps raw pointers into these arrays (no copy): they live as long as self
         self.params = [np.ascontiguousarray(p, dtype=np.float32) for p in
                        (params if params is not None else init_params(hidden, seed, layer_index, ffn_mult))]
         ptrs = (C.POINTER(C.c_float) * 12)(*[p.ctypes.data_as(C.POINTER(C.c_float)) for p in self.params])

@@ -93,6 +93,8 @@ _SIGS = {
     "mt_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "mt_ctx_init_comm": (C.c_int, [P, C.c_char_p, I32, I32, C.POINTER(ParallelConfig)]),
     "mt_ctx_placement": (C.c_int, [P, C.POINTER(RankPlacement)]),
+    "mt_ctx_gemm_timing": (C.c_int, [P, I32]),
+    "mt_ctx_gemm_timing_read": (C.c_int, [P, PF64, PF64, PI64]),
     "mt_layer_create": (C.c_int, [P, C.POINTER(LayerDesc), C.POINTER(P)]),
     "mt_layer_destroy": (C.c_int, [P]),
     "mt_layer_init_params": (C.c_int, [P, P]),
@@ -114,6 +116,7 @@ _SIGS = {
     "mt_stage_destroy": (C.c_int, [P]),
     "mt_stage_layer": (C.c_int, [P, I32, C.POINTER(P)]),
     "mt_stage_train_step": (C.c_int, [P, P, P, PF32, P]),
+    "mt_stage_train_step_dev": (C.c_int, [P, P, P, P, P]),
     "mt_stage_launch_count": (C.c_int, [P, PI64]),
 }
 

@@ -24,6 +24,7 @@ namespace mt {
 
 namespace {
 thread_local std::string g_last_error;
+thread_local mt_ctx* tl_ctx = nullptr;  // context of the layer call in progress (GEMM timing)
 }
 
 void set_error(const std::string& e) { g_last_error = e; }
@@ -117,10 +118,31 @@ struct Gemm {
     a.causal = c;
     return *this;
   }
+  // Algorithmic FLOPs of this call (causal contractions count the lower triangle only).
+  double flops() const {
+    double f = 2.0 * double(a.m) * double(a.n) * double(a.k) * double(a.batch);
+    if (a.causal != MT_CAUSAL_NONE) f *= (double(a.m) + 1.0) / (2.0 * double(a.m));
+    return f;
+  }
   void run(cudaStream_t s, int& launches) {
+    mt_ctx* c = tl_ctx;
+    const bool timed = c && c->gemm_timing;
+    if (timed) {
+      while (c->ev_pool.size() < c->ev_used + 2) {
+        cudaEvent_t e;
+        check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+        c->ev_pool.push_back(e);
+      }
+      check_cuda(cudaEventRecord(c->ev_pool[c->ev_used], s), "cudaEventRecord");
+    }
     const int rc = mt_gemm(&a, s);
     if (rc == 1) throw std::invalid_argument("mt_gemm: invalid arguments");
     if (rc != 0) throw RuntimeFailure(std::string("mt_gemm: ") + cudaGetErrorString(cudaGetLastError()));
+    if (timed) {
+      check_cuda(cudaEventRecord(c->ev_pool[c->ev_used + 1], s), "cudaEventRecord");
+      c->ev_used += 2;
+      c->ev_flops.push_back(flops());
+    }
     ++launches;
   }
 };
@@ -200,6 +222,7 @@ extern "C" int mt_ctx_destroy(mt_ctx* c) {
     if (!c) return;
     for (ncclComm_t* cm : {&c->tp, &c->pp, &c->dp, &c->world})
       if (*cm) ncclCommDestroy(*cm);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     delete c;
   });
 }
@@ -245,6 +268,34 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
     check_nccl(ncclCommSplit(c->world, tp_color, me.tensor, &c->tp, nullptr), "ncclCommSplit(tp)");
     check_nccl(ncclCommSplit(c->world, pp_color, me.pipeline, &c->pp, nullptr), "ncclCommSplit(pp)");
     check_nccl(ncclCommSplit(c->world, dp_color, me.data, &c->dp, nullptr), "ncclCommSplit(dp)");
+  });
+}
+
+extern "C" int mt_ctx_gemm_timing(mt_ctx* c, int32_t enable) {
+  return guarded([&] {
+    if (!c) throw std::invalid_argument("null ctx");
+    c->gemm_timing = enable != 0;
+    c->ev_used = 0;
+    c->ev_flops.clear();
+  });
+}
+
+extern "C" int mt_ctx_gemm_timing_read(mt_ctx* c, double* total_ms, double* total_flops, int64_t* launches) {
+  return guarded([&] {
+    if (!c) throw std::invalid_argument("null ctx");
+    check_cuda(cudaDeviceSynchronize(), "sync");
+    double ms = 0, fl = 0;
+    for (size_t i = 0; i + 1 < c->ev_used; i += 2) {
+      float t = 0;
+      check_cuda(cudaEventElapsedTime(&t, c->ev_pool[i], c->ev_pool[i + 1]), "cudaEventElapsedTime");
+      ms += t;
+    }
+    for (double f : c->ev_flops) fl += f;
+    if (total_ms) *total_ms = ms;
+    if (total_flops) *total_flops = fl;
+    if (launches) *launches = static_cast<int64_t>(c->ev_flops.size());
+    c->ev_used = 0;
+    c->ev_flops.clear();
   });
 }
 
@@ -447,6 +498,7 @@ mt_layer::Saved& acquire_slot(mt_layer* l, uint32_t mb) {
 
 void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t st) {
   mt_ctx* c = l->ctx;
+  tl_ctx = c;
   const mt_layer_desc& d = l->d;
   const int64_t M = l->M, h = l->h, hl = l->hl, ffl = l->ffl, ld3 = l->qkvl, s = d.seq, Hl = l->heads_local,
                 hd = l->head_dim;
@@ -518,6 +570,7 @@ void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_
 
 void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStream_t st) {
   mt_ctx* c = l->ctx;
+  tl_ctx = c;
   const mt_layer_desc& d = l->d;
   auto it = l->saved.find(mb);
   if (it == l->saved.end()) throw std::invalid_argument("backward without a saved forward for this microbatch");

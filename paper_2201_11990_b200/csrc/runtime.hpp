@@ -60,6 +60,11 @@ struct mt_ctx {
   mt::DeviceBuffer scratch_qkv;    // [M, 3h/t] bf16
   mt::DeviceBuffer scratch_attn;   // [heads/t, s, s] bf16
   mt::DeviceBuffer scratch_ws;     // fp32 column-reduction workspace
+  // optional per-GEMM CUDA-event timing (bench.py's live roofline measurement)
+  bool gemm_timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<double> ev_flops;
 };
 
 struct mt_layer {

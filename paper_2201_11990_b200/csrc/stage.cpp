@@ -58,6 +58,8 @@ struct Step {
   cudaStream_t s;
   const uint16_t* in_host;
   const uint16_t* tgt_host;
+  const uint16_t* in_dev = nullptr;   // device-resident inputs (train_step_dev)
+  const uint16_t* tgt_dev = nullptr;
   int64_t launches = 0;
   bool first() const { return st->stage == 0; }
   bool last() const { return st->stage == st->stages - 1; }
@@ -65,7 +67,11 @@ struct Step {
   int64_t elems() const { return st->M * st->h; }
   ncclComm_t pp() const { return st->ctx->pp; }
 
+  const void* input(int mb) const {
+    return (in_dev && first()) ? static_cast<const void*>(in_dev + mb * elems()) : st->act[mb][0].ptr;
+  }
   void load_input(int mb) {
+    if (in_dev) return;  // read in place by layer 0
     void* dst = st->act[mb][0].ptr;
     if (in_host) {
       mt::check_cuda(cudaMemcpyAsync(dst, in_host + mb * elems(), bytes(), cudaMemcpyHostToDevice, s), "H2D input");
@@ -77,14 +83,18 @@ struct Step {
   }
   void forward(int mb) {
     for (size_t i = 0; i < st->layers.size(); ++i) {
-      ok(mt_layer_forward(st->layers[i], st->act[mb][i].ptr, st->act[mb][i + 1].ptr, (uint32_t)mb, s));
+      const void* x = i == 0 ? input(mb) : st->act[mb][i].ptr;
+      ok(mt_layer_forward(st->layers[i], x, st->act[mb][i + 1].ptr, (uint32_t)mb, s));
       int32_t f, b;
       mt_layer_launch_counts(st->layers[i], &f, &b);
       launches += f;
     }
     if (last()) {
       void* y = st->act[mb][st->layers.size()].ptr;
-      if (tgt_host) {
+      const void* tgt = st->target.ptr;
+      if (tgt_dev) {
+        tgt = tgt_dev + mb * elems();
+      } else if (tgt_host) {
         mt::check_cuda(cudaMemcpyAsync(st->target.ptr, tgt_host + mb * elems(), bytes(), cudaMemcpyHostToDevice, s),
                        "H2D target");
       } else {
@@ -92,7 +102,7 @@ struct Step {
         mt::fill_normal(st->target.ptr, 1, elems(), elems(), 0, 0, key, 0.f, 1.f, s);
         ++launches;
       }
-      mt::mse_loss(y, st->target.ptr, y, st->loss.as<float>(), elems(), s);  // dy overwrites y in place
+      mt::mse_loss(y, tgt, y, st->loss.as<float>(), elems(), s);  // dy overwrites y in place
       ++launches;
     }
   }
@@ -180,84 +190,107 @@ extern "C" int mt_stage_launch_count(const mt_stage* st, int64_t* n) {
   return call([&] { *n = st->launches; });
 }
 
+namespace {
+
+void run_iteration(Step& k, mt_stage* st, void* stream) {
+  const int MB = st->d.micro_batches;
+  for (auto* l : st->layers) ok(mt_layer_zero_grads(l, stream));
+  mt::check_cuda(cudaMemsetAsync(st->loss.ptr, 0, 4, k.s), "memset loss");
+  const int warmup = std::min(st->stages - st->stage - 1, MB);
+  const int steady = MB - warmup;
+  int next_f = 0, next_b = 0;
+  // warmup forwards
+  for (int i = 0; i < warmup; ++i) {
+    const int mb = next_f++;
+    k.first() ? k.load_input(mb) : k.recv_fwd(mb);
+    k.forward(mb);
+    k.send_fwd(mb);  // warmup > 0 implies not the last stage
+  }
+  if (steady > 0) k.first() ? k.load_input(next_f) : k.recv_fwd(next_f);
+  for (int i = 0; i < steady; ++i) {
+    const int mb = next_f++;
+    k.forward(mb);
+    // send activation forward + receive the gradient of the oldest in-flight microbatch
+    const int bmb = next_b++;
+    void* g = k.last() ? st->act[bmb][st->layers.size()].ptr : k.grad_in_buffer();
+    if (!k.last()) {
+      mt::check_nccl(ncclGroupStart(), "group");
+      mt::check_nccl(ncclSend(st->act[mb][st->layers.size()].ptr, k.elems(), ncclBfloat16, st->stage + 1, k.pp(), k.s),
+                     "send fwd");
+      mt::check_nccl(ncclRecv(g, k.elems(), ncclBfloat16, st->stage + 1, k.pp(), k.s), "recv bwd");
+      mt::check_nccl(ncclGroupEnd(), "group");
+      ++k.launches;
+    }
+    void* dx = k.backward(bmb, g);
+    const bool more = i + 1 < steady;
+    if (!k.first()) {
+      mt::check_nccl(ncclGroupStart(), "group");
+      mt::check_nccl(ncclSend(dx, k.elems(), ncclBfloat16, st->stage - 1, k.pp(), k.s), "send bwd");
+      if (more)
+        mt::check_nccl(ncclRecv(st->act[next_f][0].ptr, k.elems(), ncclBfloat16, st->stage - 1, k.pp(), k.s),
+                       "recv fwd");
+      mt::check_nccl(ncclGroupEnd(), "group");
+      ++k.launches;
+    } else if (more) {
+      k.load_input(next_f);
+    }
+  }
+  // cooldown backwards
+  for (int i = 0; i < warmup; ++i) {
+    const int bmb = next_b++;
+    void* g = k.grad_in_buffer();
+    mt::check_nccl(ncclRecv(g, k.elems(), ncclBfloat16, st->stage + 1, k.pp(), k.s), "recv bwd");
+    ++k.launches;
+    void* dx = k.backward(bmb, g);
+    if (!k.first()) {
+      mt::check_nccl(ncclSend(dx, k.elems(), ncclBfloat16, st->stage - 1, k.pp(), k.s), "send bwd");
+      ++k.launches;
+    }
+  }
+  // data-parallel gradient all-reduce (mean)
+  if (st->ctx->par.data > 1) {
+    for (auto* l : st->layers) {
+      ok(mt_dp_allreduce_f32(st->ctx, l->grads.as<float>(), l->param_total, 1, stream));
+      ++k.launches;
+    }
+    if (k.last()) {
+      ok(mt_dp_allreduce_f32(st->ctx, st->loss.as<float>(), 1, 1, stream));
+      ++k.launches;
+    }
+  }
+}
+
+}  // namespace
+
 extern "C" int mt_stage_train_step(mt_stage* st, const void* inputs_host, const void* targets_host, float* loss_out,
                                    void* stream) {
   return call([&] {
     if (!st) throw std::invalid_argument("null stage");
     Step k{st, (cudaStream_t)stream, static_cast<const uint16_t*>(inputs_host),
            static_cast<const uint16_t*>(targets_host)};
-    const int MB = st->d.micro_batches;
-    for (auto* l : st->layers) ok(mt_layer_zero_grads(l, stream));
-    mt::check_cuda(cudaMemsetAsync(st->loss.ptr, 0, 4, k.s), "memset loss");
-    const int warmup = std::min(st->stages - st->stage - 1, MB);
-    const int steady = MB - warmup;
-    int next_f = 0, next_b = 0;
-    // warmup forwards
-    for (int i = 0; i < warmup; ++i) {
-      const int mb = next_f++;
-      k.first() ? k.load_input(mb) : k.recv_fwd(mb);
-      k.forward(mb);
-      k.send_fwd(mb);  // warmup > 0 implies not the last stage
-    }
-    if (steady > 0) k.first() ? k.load_input(next_f) : k.recv_fwd(next_f);
-    for (int i = 0; i < steady; ++i) {
-      const int mb = next_f++;
-      k.forward(mb);
-      // send activation forward + receive the gradient of the oldest in-flight microbatch
-      const int bmb = next_b++;
-      void* g = k.last() ? st->act[bmb][st->layers.size()].ptr : k.grad_in_buffer();
-      if (!k.last()) {
-        mt::check_nccl(ncclGroupStart(), "group");
-        mt::check_nccl(ncclSend(st->act[mb][st->layers.size()].ptr, k.elems(), ncclBfloat16, st->stage + 1, k.pp(), k.s),
-                       "send fwd");
-        mt::check_nccl(ncclRecv(g, k.elems(), ncclBfloat16, st->stage + 1, k.pp(), k.s), "recv bwd");
-        mt::check_nccl(ncclGroupEnd(), "group");
-        ++k.launches;
-      }
-      void* dx = k.backward(bmb, g);
-      const bool more = i + 1 < steady;
-      if (!k.first()) {
-        mt::check_nccl(ncclGroupStart(), "group");
-        mt::check_nccl(ncclSend(dx, k.elems(), ncclBfloat16, st->stage - 1, k.pp(), k.s), "send bwd");
-        if (more) mt::check_nccl(ncclRecv(st->act[next_f][0].ptr, k.elems(), ncclBfloat16, st->stage - 1, k.pp(), k.s),
-                                 "recv fwd");
-        mt::check_nccl(ncclGroupEnd(), "group");
-        ++k.launches;
-      } else if (more) {
-        k.load_input(next_f);
-      }
-    }
-    // cooldown backwards
-    for (int i = 0; i < warmup; ++i) {
-      const int bmb = next_b++;
-      void* g = k.grad_in_buffer();
-      mt::check_nccl(ncclRecv(g, k.elems(), ncclBfloat16, st->stage + 1, k.pp(), k.s), "recv bwd");
-      ++k.launches;
-      void* dx = k.backward(bmb, g);
-      if (!k.first()) {
-        mt::check_nccl(ncclSend(dx, k.elems(), ncclBfloat16, st->stage - 1, k.pp(), k.s), "send bwd");
-        ++k.launches;
-      }
-    }
-    // data-parallel gradient all-reduce (mean)
-    if (st->ctx->par.data > 1) {
-      for (auto* l : st->layers) {
-        ok(mt_dp_allreduce_f32(st->ctx, l->grads.as<float>(), l->param_total, 1, stream));
-        ++k.launches;
-      }
-    }
+    run_iteration(k, st, stream);
     if (loss_out) {
       float host = 0.f;
-      if (k.last()) {
-        if (st->ctx->par.data > 1) {
-          ok(mt_dp_allreduce_f32(st->ctx, st->loss.as<float>(), 1, 1, stream));
-          ++k.launches;
-        }
-        mt::check_cuda(cudaMemcpyAsync(&host, st->loss.ptr, 4, cudaMemcpyDeviceToHost, k.s), "D2H loss");
-        mt::check_cuda(cudaStreamSynchronize(k.s), "sync");
-      }
+      if (k.last()) mt::check_cuda(cudaMemcpyAsync(&host, st->loss.ptr, 4, cudaMemcpyDeviceToHost, k.s), "D2H loss");
+      mt::check_cuda(cudaStreamSynchronize(k.s), "sync");
       *loss_out = host;
     }
+    st->launches = k.launches;
+  });
+}
+
+extern "C" int mt_stage_train_step_dev(mt_stage* st, const void* inputs_dev, const void* targets_dev, float* loss_dev,
+                                       void* stream) {
+  return call([&] {
+    if (!st) throw std::invalid_argument("null stage");
+    Step k{st, (cudaStream_t)stream, nullptr, nullptr};
+    k.in_dev = static_cast<const uint16_t*>(inputs_dev);
+    k.tgt_dev = static_cast<const uint16_t*>(targets_dev);
+    if (k.first() && !k.in_dev) throw std::invalid_argument("first stage needs device inputs");
+    if (k.last() && !k.tgt_dev) throw std::invalid_argument("last stage needs device targets");
+    run_iteration(k, st, stream);
+    if (loss_dev && k.last())
+      mt::check_cuda(cudaMemcpyAsync(loss_dev, st->loss.ptr, 4, cudaMemcpyDeviceToDevice, k.s), "D2D loss");
     st->launches = k.launches;
   });
 }

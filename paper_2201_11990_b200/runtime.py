@@ -113,6 +113,12 @@ class Stage:
                                         C.byref(loss) if want_loss else None, _stream(stream)))
         return loss.value
 
+    def train_step_dev(self, inputs_dev_ptr: int, targets_dev_ptr: int, loss_dev_ptr: int | None = None,
+                       stream=None) -> None:
+        """Iteration with device-resident inputs / targets ([MB][b*s*h] bf16); asynchronous."""
+        check(lib().mt_stage_train_step_dev(self._h, C.c_void_p(inputs_dev_ptr or 0), C.c_void_p(targets_dev_ptr or 0),
+                                            C.c_void_p(loss_dev_ptr or 0), _stream(stream)))
+
     def launch_count(self) -> int:
         n = C.c_int64()
         check(lib().mt_stage_launch_count(self._h, C.byref(n)))
