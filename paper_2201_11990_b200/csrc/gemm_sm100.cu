@@ -46,9 +46,10 @@ struct Cfg {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = kBNAlloc * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagesRaw = (kSmemBudget - 2048) / kStageBytes;
+  static constexpr int kEpiBytes = 4 * 2 * 4096;  // 4 epilogue warps x 2 staging buffers x (32 rows x 128 B)
+  static constexpr int kStagesRaw = (kSmemBudget - 2048 - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 256;
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kEpiBytes + 256;
   static constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
   static constexpr uint32_t kAccStride = kTmemCols / 2;  // column offset of accumulator buffer 1
 };
@@ -78,90 +79,63 @@ __device__ __forceinline__ void k_range(const GemmParams& p, int mb, int& kb0, i
   }
 }
 
-template <int BN>
-__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int b, int row, int col0, uint32_t (&r)[32]) {
-  if (row >= p.m) return;
-  const float alpha = p.alpha;
-  const int ep = p.epilogue;
-  if (ep == MT_EPI_STORE_F32 || ep == MT_EPI_ACCUM_F32) {
-    float* dst = p.d_f32 + (long long)b * p.d_batch_stride + (long long)row * p.ldd + col0;
+// Epilogue of one 32-row x 32-column piece held by one warp (thread t = row t, r[j] = column j):
+// apply the fused epilogue, write the piece into a swizzled staging buffer and hand it to the TMA
+// engine (store, or reduce-add into fp32 gradients). Rows/columns outside D are clipped by TMA.
+struct EpiMaps {
+  const CUtensorMap* d;
+  const CUtensorMap* aux;
+};
+
+// bf16 piece: 32 rows x 64 B, SWIZZLE_64B (16-byte chunk j of row t lands at chunk j ^ ((t >> 1) & 3)).
+__device__ __forceinline__ void stage_bf16(uint32_t buf, uint32_t lane, const float (&x)[32]) {
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const int c = col0 + v * 4;
-      if (c >= p.n) break;
-      float4 o = make_float4(alpha * __uint_as_float(r[4 * v + 0]), alpha * __uint_as_float(r[4 * v + 1]),
-                             alpha * __uint_as_float(r[4 * v + 2]), alpha * __uint_as_float(r[4 * v + 3]));
-      float4* q = reinterpret_cast<float4*>(dst + v * 4);
-      if (ep == MT_EPI_ACCUM_F32) {
-        const float4 old = *q;
-        o.x += old.x;
-        o.y += old.y;
-        o.z += old.z;
-        o.w += old.w;
-      }
-      *q = o;
-    }
-    return;
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t pos = j ^ ((lane >> 1) & 3);
+    st_shared_v4(buf + lane * 64 + pos * 16, pack_bf16x2(x[8 * j], x[8 * j + 1]), pack_bf16x2(x[8 * j + 2], x[8 * j + 3]),
+                 pack_bf16x2(x[8 * j + 4], x[8 * j + 5]), pack_bf16x2(x[8 * j + 6], x[8 * j + 7]));
   }
-  __nv_bfloat16* dst = p.d_bf16 + (long long)b * p.d_batch_stride + (long long)row * p.ldd + col0;
+}
+// fp32 piece: 32 rows x 128 B, SWIZZLE_128B (chunk j of row t lands at chunk j ^ (t & 7)).
+__device__ __forceinline__ void stage_f32(uint32_t buf, uint32_t lane, const float (&x)[32]) {
 #pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    const int c = col0 + v * 8;
-    if (c >= p.n) break;
-    float x[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = __uint_as_float(r[8 * v + j]);
-    if (ep == MT_EPI_STORE_BF16) {
-      if (p.bias != nullptr) {
-        const uint4 bv = *reinterpret_cast<const uint4*>(p.bias + c);
-        const uint32_t bw[4] = {bv.x, bv.y, bv.z, bv.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = unpack_bf16x2(bw[j]);
-          x[2 * j] = alpha * x[2 * j] + f.x;
-          x[2 * j + 1] = alpha * x[2 * j + 1] + f.y;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] *= alpha;
-      }
-    } else if (ep == MT_EPI_BIAS_GELU) {
-      const uint4 bv = *reinterpret_cast<const uint4*>(p.bias + c);
-      const uint32_t bw[4] = {bv.x, bv.y, bv.z, bv.w};
-      uint32_t pre[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = unpack_bf16x2(bw[j]);
-        pre[j] = pack_bf16x2(alpha * x[2 * j] + f.x, alpha * x[2 * j + 1] + f.y);
-        const float2 pr = unpack_bf16x2(pre[j]);  // GeLU of the stored (bf16) pre-activation
-        x[2 * j] = gelu_tanh(pr.x);
-        x[2 * j + 1] = gelu_tanh(pr.y);
-      }
-      *reinterpret_cast<uint4*>(p.aux + (long long)row * p.ld_aux + c) = make_uint4(pre[0], pre[1], pre[2], pre[3]);
-    } else {  // MT_EPI_GELU_BWD
-      const uint4 av = *reinterpret_cast<const uint4*>(p.aux + (long long)row * p.ld_aux + c);
-      const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = unpack_bf16x2(aw[j]);
-        x[2 * j] = alpha * x[2 * j] * gelu_tanh_grad(f.x);
-        x[2 * j + 1] = alpha * x[2 * j + 1] * gelu_tanh_grad(f.y);
-      }
-    }
-    *reinterpret_cast<uint4*>(dst + v * 8) =
-        make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]), pack_bf16x2(x[6], x[7]));
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t pos = j ^ (lane & 7);
+    st_shared_v4(buf + lane * 128 + pos * 16, __float_as_uint(x[4 * j]), __float_as_uint(x[4 * j + 1]),
+                 __float_as_uint(x[4 * j + 2]), __float_as_uint(x[4 * j + 3]));
   }
+}
+
+// Issue the TMA op for the staged piece from lane 0 once all lanes' smem writes are visible.
+__device__ __forceinline__ void flush_piece(const CUtensorMap* map, uint32_t buf, uint32_t lane, int col, int row, int b,
+                                            bool reduce) {
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    if (reduce)
+      tma_reduce_add_3d(map, buf, col, row, b);
+    else
+      tma_store_3d(map, buf, col, row, b);
+    bulk_commit();
+  }
+}
+// Before overwriting a staging buffer: at most one older bulk group may still be reading smem.
+__device__ __forceinline__ void reuse_wait(uint32_t lane) {
+  if (lane == 0) bulk_wait_read<1>();
+  __syncwarp();
 }
 
 template <int BN, bool kAMN, bool kBMN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                      const __grid_constant__ CUtensorMap tmap_d, const __grid_constant__ CUtensorMap tmap_aux,
                       const GemmParams p) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint8_t* epi_base = smem + C::kStages * C::kStageBytes;  // 1024-aligned (stage bytes are 1 KB multiples)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + C::kEpiBytes);
   // bars[0..S) full, bars[S..2S) empty, bars[2S..2S+2) tmem_full, bars[2S+2..2S+4) tmem_empty
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4);
 
@@ -171,6 +145,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
+    tma_prefetch_desc(&tmap_d);
+    if (p.epilogue == MT_EPI_BIAS_GELU) tma_prefetch_desc(&tmap_aux);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(smem_u32(&bars[s]), 1);
       mbar_init(smem_u32(&bars[C::kStages + s]), 1);
@@ -262,6 +238,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
     const uint32_t quad = warp - 4;
+    const uint32_t stg = smem_u32(epi_base) + quad * 8192;  // two 4 KB staging buffers
+    uint32_t bi = 0;
+    const int ep = p.epilogue;
+    const bool f32 = ep == MT_EPI_STORE_F32 || ep == MT_EPI_ACCUM_F32;
+    const float alpha = p.alpha;
     uint32_t it = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
       int b, mb, nb;
@@ -270,19 +251,83 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t acc = it & 1, acc_phase = (it >> 1) & 1;
       mbar_wait(smem_u32(&bars[2 * C::kStages + acc]), acc_phase);
       tc_fence_after();
-      const int row = mb * kBM + quad * 32 + lane;
+      const int row0 = mb * kBM + quad * 32;
+      const int row = row0 + lane;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
+        const int col0 = nb * BN + c * 32;
+        if (col0 >= p.n) break;
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((quad * 32) << 16) + acc * C::kAccStride + c * 32, r);
         tmem_ld_wait();
-        epilogue_chunk<BN>(p, b, row, nb * BN + c * 32, r);
+        float x[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = alpha * __uint_as_float(r[j]);
+        if (f32) {
+          reuse_wait(lane);
+          stage_f32(stg + bi * 4096, lane, x);
+          flush_piece(&tmap_d, stg + bi * 4096, lane, col0, row0, b, ep == MT_EPI_ACCUM_F32);
+          bi ^= 1;
+          continue;
+        }
+        if (ep == MT_EPI_STORE_BF16 || ep == MT_EPI_BIAS_GELU) {
+          if (p.bias != nullptr) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              if (col0 + 8 * v < p.n) {
+                const uint4 bv = __ldg(reinterpret_cast<const uint4*>(p.bias + col0 + 8 * v));
+                const uint32_t bw[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float2 f = unpack_bf16x2(bw[q]);
+                  x[8 * v + 2 * q] += f.x;
+                  x[8 * v + 2 * q + 1] += f.y;
+                }
+              }
+            }
+          }
+          if (ep == MT_EPI_BIAS_GELU) {
+            // pre-activation (bf16) goes to aux; GeLU is applied to the rounded value the backward sees
+            reuse_wait(lane);
+            stage_bf16(stg + bi * 4096, lane, x);
+            flush_piece(&tmap_aux, stg + bi * 4096, lane, col0, row0, 0, false);
+            bi ^= 1;
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const float2 pr = unpack_bf16x2(pack_bf16x2(x[j], x[j + 1]));
+              x[j] = gelu_tanh(pr.x);
+              x[j + 1] = gelu_tanh(pr.y);
+            }
+          }
+        } else {  // MT_EPI_GELU_BWD: D = acc * gelu'(aux)
+          if (row < p.m) {
+            const __nv_bfloat16* ap = p.aux + (long long)row * p.ld_aux + col0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              if (col0 + 8 * v < p.n) {
+                const uint4 av = *reinterpret_cast<const uint4*>(ap + 8 * v);
+                const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float2 f = unpack_bf16x2(aw[q]);
+                  x[8 * v + 2 * q] *= gelu_tanh_grad(f.x);
+                  x[8 * v + 2 * q + 1] *= gelu_tanh_grad(f.y);
+                }
+              }
+            }
+          }
+        }
+        reuse_wait(lane);
+        stage_bf16(stg + bi * 4096, lane, x);
+        flush_piece(&tmap_d, stg + bi * 4096, lane, col0, row0, b, false);
+        bi ^= 1;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
       ++it;
     }
+    if (lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
@@ -309,22 +354,37 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// 3-D bf16 tensor map: dims (inner, outer, batch), 128B swizzle, box (64, box_outer, 1).
-bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t batch, uint64_t ld,
-              uint64_t batch_stride, uint32_t box_outer) {
+// 3-D tensor map: dims (inner, outer, batch) with element size `esize`, box (box_inner, box_outer, 1).
+bool make_map_ex(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t batch, uint64_t ld,
+                 uint64_t batch_stride, uint32_t box_inner, uint32_t box_outer, bool f32, CUtensorMapSwizzle swz) {
   EncodeFn enc = encode_fn();
   if (!enc) return false;
+  const uint64_t es = f32 ? 4 : 2;
   cuuint64_t dims[3] = {inner, outer, batch};
   uint64_t bs = batch_stride;
   if (batch <= 1) bs = (ld * outer + 7) / 8 * 8;
   if (bs == 0) bs = 8;
-  cuuint64_t strides[2] = {ld * 2, bs * 2};
-  cuuint32_t box[3] = {64, box_outer, 1};
+  cuuint64_t strides[2] = {ld * es, bs * es};
+  cuuint32_t box[3] = {box_inner, box_outer, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// Operand map: bf16, 128B swizzle, box (64, box_outer).
+bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t batch, uint64_t ld,
+              uint64_t batch_stride, uint32_t box_outer) {
+  return make_map_ex(map, base, inner, outer, batch, ld, batch_stride, 64, box_outer, false,
+                     CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// Epilogue store map: 32 x 32 pieces; bf16 rows are 64 B (64B swizzle), fp32 rows 128 B (128B swizzle).
+bool make_store_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t m, uint64_t batch, uint64_t ld,
+                    uint64_t batch_stride, bool f32) {
+  return make_map_ex(map, base, n, m, batch, ld, batch_stride, 32, 32, f32,
+                     f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 int num_sms() {
@@ -347,6 +407,13 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
                  : make_map(&ma, a.a, k, m, batch, a.lda, a.a_batch_stride, kBM);
   ok = ok && (kBMN ? make_map(&mb, a.b, n, k, batch, a.ldb, a.b_batch_stride, 64)
                    : make_map(&mb, a.b, k, n, batch, a.ldb, a.b_batch_stride, BN));
+  const bool f32 = a.epilogue == MT_EPI_STORE_F32 || a.epilogue == MT_EPI_ACCUM_F32;
+  CUtensorMap md, maux;
+  ok = ok && make_store_map(&md, a.d, n, m, batch, a.ldd, a.d_batch_stride, f32);
+  if (a.epilogue == MT_EPI_BIAS_GELU)
+    ok = ok && make_store_map(&maux, a.aux, n, m, 1, a.ld_aux, 0, false);
+  else
+    maux = md;
   if (!ok) return 1;
   GemmParams p{};
   p.m = m;
@@ -375,7 +442,7 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
     attr_set = true;
   }
   const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
-  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, p);
+  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, md, maux, p);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -396,6 +463,7 @@ extern "C" int mt_gemm(const mt_gemm_args* args, void* stream) {
   if (a.m <= 0 || a.n <= 0 || a.k <= 0 || a.batch <= 0) return 1;
   if (a.a == nullptr || a.b == nullptr || a.d == nullptr) return 1;
   if ((a.n % 8) != 0 || (a.lda % 8) != 0 || (a.ldb % 8) != 0 || (a.ldd % 8) != 0) return 1;
+  if ((a.a_batch_stride % 8) != 0 || (a.b_batch_stride % 8) != 0 || (a.d_batch_stride % 8) != 0) return 1;
   if ((reinterpret_cast<uintptr_t>(a.a) | reinterpret_cast<uintptr_t>(a.b) | reinterpret_cast<uintptr_t>(a.d)) & 15)
     return 1;
   if ((a.epilogue == MT_EPI_BIAS_GELU || a.epilogue == MT_EPI_GELU_BWD) && (a.aux == nullptr || a.ld_aux % 8))

@@ -250,16 +250,16 @@ __global__ void __launch_bounds__(256) colsum_stage1(const uint4* __restrict__ a
 }
 
 __global__ void colsum_stage2(const float* __restrict__ ws, float* __restrict__ out0, float* __restrict__ out1, int n,
-                              int splits) {
+                              int splits, int accumulate) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= n) return;
   float s0 = 0.f;
   for (int sp = 0; sp < splits; ++sp) s0 += ws[(size_t)sp * n + col];
-  out0[col] += s0;
+  out0[col] = accumulate ? out0[col] + s0 : s0;
   if (out1 != nullptr) {
     float s1 = 0.f;
     for (int sp = 0; sp < splits; ++sp) s1 += ws[((size_t)splits + sp) * n + col];
-    out1[col] += s1;
+    out1[col] = accumulate ? out1[col] + s1 : s1;
   }
 }
 
@@ -490,29 +490,30 @@ void ln_bwd_dx(const void* dy, const void* x, const void* gamma, const float* me
 size_t colsum_workspace_floats(int rows, int n) { return (size_t)2 * col_splits(rows) * n; }
 
 void ln_bwd_params(const void* dy, const void* x, const float* mean, const float* rstd, float* dgamma, float* dbeta,
-                   int rows, int h, float* ws, cudaStream_t s) {
+                   int rows, int h, float* ws, bool accumulate, cudaStream_t s) {
   const int nvec = h / 8, splits = col_splits(rows);
   dim3 grid((nvec + 31) / 32, splits), block(32, kColTY);
   colsum_stage1<kColLnParams><<<grid, block, 0, s>>>((const uint4*)dy, nvec, (const uint4*)x, mean, rstd, nullptr, ws,
                                                      rows, nvec, (rows + splits - 1) / splits, 0, 0, 1.f);
-  colsum_stage2<<<(h + 255) / 256, 256, 0, s>>>(ws, dgamma, dbeta, h, splits);
+  colsum_stage2<<<(h + 255) / 256, 256, 0, s>>>(ws, dgamma, dbeta, h, splits, accumulate);
 }
 
-void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, float* ws, cudaStream_t s) {
+void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, float* ws, bool accumulate,
+               cudaStream_t s) {
   const int nvec = n / 8, splits = col_splits(rows);
   dim3 grid((nvec + 31) / 32, splits), block(32, kColTY);
   colsum_stage1<kColSum><<<grid, block, 0, s>>>((const uint4*)x, ldx / 8, nullptr, nullptr, nullptr, nullptr, ws, rows,
                                                 nvec, (rows + splits - 1) / splits, 0, 0, 1.f);
-  colsum_stage2<<<(n + 255) / 256, 256, 0, s>>>(ws, dbias, nullptr, n, splits);
+  colsum_stage2<<<(n + 255) / 256, 256, 0, s>>>(ws, dbias, nullptr, n, splits, accumulate);
 }
 
 void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int h, uint64_t seed, uint32_t thresh16,
-                           float scale, float* ws, cudaStream_t s) {
+                           float scale, float* ws, bool accumulate, cudaStream_t s) {
   const int nvec = h / 8, splits = col_splits(rows);
   dim3 grid((nvec + 31) / 32, splits), block(32, kColTY);
   colsum_stage1<kColDropout><<<grid, block, 0, s>>>((const uint4*)dy, nvec, nullptr, nullptr, nullptr, (uint4*)dz, ws,
                                                     rows, nvec, (rows + splits - 1) / splits, seed, thresh16, scale);
-  colsum_stage2<<<(h + 255) / 256, 256, 0, s>>>(ws, dbias, nullptr, h, splits);
+  colsum_stage2<<<(h + 255) / 256, 256, 0, s>>>(ws, dbias, nullptr, h, splits, accumulate);
 }
 
 void bias_dropout_residual(const void* z, const void* bias, const void* resid, void* out, int rows, int h,

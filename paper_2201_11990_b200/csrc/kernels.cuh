@@ -17,18 +17,19 @@ void ln_fwd(const void* x, const void* gamma, const void* beta, void* y, float* 
 // dx = rstd * (g - mean(g) - xhat * mean(g * xhat)) [+ resid], g = dy * gamma.
 void ln_bwd_dx(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
                const void* resid, void* dx, int rows, int h, cudaStream_t s);
-// dgamma += sum_rows dy * xhat ; dbeta += sum_rows dy   (fp32 accumulate, deterministic)
+// dgamma (+)= sum_rows dy * xhat ; dbeta (+)= sum_rows dy   (fp32, deterministic; += when accumulate)
 void ln_bwd_params(const void* dy, const void* x, const float* mean, const float* rstd, float* dgamma, float* dbeta,
-                   int rows, int h, float* workspace, cudaStream_t s);
+                   int rows, int h, float* workspace, bool accumulate, cudaStream_t s);
 
 // out = resid + dropout(z + bias)
 void bias_dropout_residual(const void* z, const void* bias, const void* resid, void* out, int rows, int h,
                            uint64_t site_seed, uint32_t thresh16, float scale, cudaStream_t s);
-// dz = dropout'(dy) ; dbias += sum_rows dz
+// dz = dropout'(dy) ; dbias (+)= sum_rows dz
 void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int h, uint64_t site_seed,
-                           uint32_t thresh16, float scale, float* workspace, cudaStream_t s);
-// dbias += sum_rows x   (x bf16 [rows, n])
-void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, float* workspace, cudaStream_t s);
+                           uint32_t thresh16, float scale, float* workspace, bool accumulate, cudaStream_t s);
+// dbias (+)= sum_rows x   (x bf16 [rows, n])
+void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, float* workspace, bool accumulate,
+               cudaStream_t s);
 size_t colsum_workspace_floats(int rows, int n);
 
 // Causal softmax over S (already scaled by 1/sqrt(hd)), rows of `batch_heads` independent

@@ -203,6 +203,14 @@ void validate_desc(const mt_layer_desc& d) {
 
 using namespace mt;
 
+// Materialise logically-zero gradients before anyone reads the buffer.
+static void settle_fresh_grads(mt_layer* l, cudaStream_t s) {
+  if (!l->grads_fresh) return;
+  check_cuda(cudaMemsetAsync(l->grads.ptr, 0, l->param_total * 4, s), "cudaMemsetAsync");
+  l->grads_fresh = false;
+}
+
+
 // =========================================================================== context & comm
 extern "C" const char* mt_last_error(void) { return mt::last_error(); }
 extern "C" const char* mt_version(void) { return "mtnlg-b200 0.1 (sm_100a)"; }
@@ -441,6 +449,7 @@ extern "C" int mt_layer_get_param(mt_layer* l, int32_t p, void* host) {
 extern "C" int mt_layer_get_grad(mt_layer* l, int32_t p, float* host) {
   return guarded([&] {
     if (p < 0 || p >= MT_P_COUNT) throw std::invalid_argument("unknown parameter id");
+    settle_fresh_grads(l, nullptr);
     check_cuda(cudaDeviceSynchronize(), "sync");
     check_cuda(cudaMemcpy(host, l->grad_ptr(p), l->param_rows[p] * l->param_cols[p] * 4, cudaMemcpyDeviceToHost),
                "cudaMemcpy(grad)");
@@ -449,12 +458,15 @@ extern "C" int mt_layer_get_grad(mt_layer* l, int32_t p, float* host) {
 
 extern "C" int mt_layer_zero_grads(mt_layer* l, void* stream) {
   return guarded([&] {
-    check_cuda(cudaMemsetAsync(l->grads.ptr, 0, l->param_total * 4, (cudaStream_t)stream), "cudaMemsetAsync");
+    if (!l) throw std::invalid_argument("null layer");
+    (void)stream;
+    l->grads_fresh = true;  // the next backward stores instead of accumulating
   });
 }
 
 extern "C" int mt_layer_grad_buffer(mt_layer* l, float** ptr, int64_t* n) {
   return guarded([&] {
+    settle_fresh_grads(l, nullptr);
     *ptr = l->grads.as<float>();
     *n = l->param_total;
   });
@@ -596,18 +608,21 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
   void* dctx = c->scratch_ctx.ptr;
   void* dqkv = c->scratch_qkv.ptr;
   uint16_t* dP = c->scratch_attn.as<uint16_t>();
+  const bool acc = !l->grads_fresh;  // accumulate into the fp32 grads, or overwrite them
+  l->grads_fresh = false;
+  const int wg_epi = acc ? MT_EPI_ACCUM_F32 : MT_EPI_STORE_F32;
 
   // ---- MLP block
-  dropout_bwd_bias_grad(dy, dm, l->grad_ptr(MT_P_FC2_B), (int)M, (int)h, site_out2, th_h, scale_h, ws, st);
+  dropout_bwd_bias_grad(dy, dm, l->grad_ptr(MT_P_FC2_B), (int)M, (int)h, site_out2, th_h, scale_h, ws, acc, st);
   n += 2;
   Gemm(dm, h, false, l->param_ptr(MT_P_FC2_W), ffl, true, dpre, ffl, M, ffl, h)
       .epi(MT_EPI_GELU_BWD)
       .aux(sv.pre.ptr, ffl)
       .run(st, n);
-  Gemm(dm, h, true, sv.act.ptr, ffl, true, l->grad_ptr(MT_P_FC2_W), ffl, h, ffl, M).epi(MT_EPI_ACCUM_F32).run(st, n);
-  bias_grad(dpre, l->grad_ptr(MT_P_FC1_B), (int)M, (int)ffl, ffl, ws, st);
+  Gemm(dm, h, true, sv.act.ptr, ffl, true, l->grad_ptr(MT_P_FC2_W), ffl, h, ffl, M).epi(wg_epi).run(st, n);
+  bias_grad(dpre, l->grad_ptr(MT_P_FC1_B), (int)M, (int)ffl, ffl, ws, acc, st);
   n += 2;
-  Gemm(dpre, ffl, true, sv.ln2.ptr, h, true, l->grad_ptr(MT_P_FC1_W), h, ffl, h, M).epi(MT_EPI_ACCUM_F32).run(st, n);
+  Gemm(dpre, ffl, true, sv.ln2.ptr, h, true, l->grad_ptr(MT_P_FC1_W), h, ffl, h, M).epi(wg_epi).run(st, n);
   Gemm(dpre, ffl, false, l->param_ptr(MT_P_FC1_W), h, true, dln, h, M, h, ffl).run(st, n);
   if (d.tp_size > 1) {
     check_nccl(ncclAllReduce(dln, dln, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(ln2.grad)");
@@ -615,14 +630,14 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
   }
   ln_bwd_dx(dln, sv.x1.ptr, l->param_ptr(MT_P_LN2_GAMMA), mean2, rstd2, dy, dx1, (int)M, (int)h, st);
   ln_bwd_params(dln, sv.x1.ptr, mean2, rstd2, l->grad_ptr(MT_P_LN2_GAMMA), l->grad_ptr(MT_P_LN2_BETA), (int)M, (int)h,
-                ws, st);
+                ws, acc, st);
   n += 3;
   // ---- attention block
   void* dz = dm;
-  dropout_bwd_bias_grad(dx1, dz, l->grad_ptr(MT_P_PROJ_B), (int)M, (int)h, site_out1, th_h, scale_h, ws, st);
+  dropout_bwd_bias_grad(dx1, dz, l->grad_ptr(MT_P_PROJ_B), (int)M, (int)h, site_out1, th_h, scale_h, ws, acc, st);
   n += 2;
   Gemm(dz, h, false, l->param_ptr(MT_P_PROJ_W), hl, true, dctx, hl, M, hl, h).run(st, n);
-  Gemm(dz, h, true, sv.ctx.ptr, hl, true, l->grad_ptr(MT_P_PROJ_W), hl, h, hl, M).epi(MT_EPI_ACCUM_F32).run(st, n);
+  Gemm(dz, h, true, sv.ctx.ptr, hl, true, l->grad_ptr(MT_P_PROJ_W), hl, h, hl, M).epi(wg_epi).run(st, n);
   const float alpha = 1.f / std::sqrt((float)hd);
   for (int64_t bb = 0; bb < d.micro_batch; ++bb) {
     const uint16_t* q = sv.qkv.as<uint16_t>() + bb * s * ld3;
@@ -654,9 +669,9 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
         .causal(MT_CAUSAL_K_GE_M)
         .run(st, n);
   }
-  bias_grad(dqkv, l->grad_ptr(MT_P_QKV_B), (int)M, (int)ld3, ld3, ws, st);
+  bias_grad(dqkv, l->grad_ptr(MT_P_QKV_B), (int)M, (int)ld3, ld3, ws, acc, st);
   n += 2;
-  Gemm(dqkv, ld3, true, sv.ln1.ptr, h, true, l->grad_ptr(MT_P_QKV_W), h, ld3, h, M).epi(MT_EPI_ACCUM_F32).run(st, n);
+  Gemm(dqkv, ld3, true, sv.ln1.ptr, h, true, l->grad_ptr(MT_P_QKV_W), h, ld3, h, M).epi(wg_epi).run(st, n);
   Gemm(dqkv, ld3, false, l->param_ptr(MT_P_QKV_W), h, true, dln, h, M, h, ld3).run(st, n);
   if (d.tp_size > 1) {
     check_nccl(ncclAllReduce(dln, dln, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(ln1.grad)");
@@ -664,7 +679,7 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
   }
   ln_bwd_dx(dln, sv.x, l->param_ptr(MT_P_LN1_GAMMA), mean1, rstd1, dx1, dx, (int)M, (int)h, st);
   ln_bwd_params(dln, sv.x, mean1, rstd1, l->grad_ptr(MT_P_LN1_GAMMA), l->grad_ptr(MT_P_LN1_BETA), (int)M, (int)h, ws,
-                st);
+                acc, st);
   n += 3;
   check_cuda(cudaGetLastError(), "layer backward launch");
   l->bwd_launches = n;

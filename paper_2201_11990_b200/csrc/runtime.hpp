@@ -84,6 +84,9 @@ struct mt_layer {
   std::map<uint32_t, std::unique_ptr<Saved>> saved;
   std::vector<std::unique_ptr<Saved>> free_slots;
   int fwd_launches = 0, bwd_launches = 0;
+  // Logically zero gradients: the next backward writes (=) instead of accumulating (+=), which
+  // saves both the memset and the read half of the fp32 read-modify-write in the wgrad epilogues.
+  bool grads_fresh = false;
   void* param_ptr(int p) const { return static_cast<uint16_t*>(params.ptr) + param_off[p]; }
   float* grad_ptr(int p) const { return grads.as<float>() + param_off[p]; }
 };
