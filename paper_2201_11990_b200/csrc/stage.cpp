@@ -66,6 +66,11 @@ struct Step {
   size_t bytes() const { return static_cast<size_t>(st->M * st->h * 2); }
   int64_t elems() const { return st->M * st->h; }
   ncclComm_t pp() const { return st->ctx->pp; }
+  // Global microbatch id (data-parallel replicas see different samples): keys the synthetic
+  // inputs/targets and the dropout masks of the microbatch.
+  uint32_t gid(int mb) const {
+    return static_cast<uint32_t>(st->ctx->place.data * st->d.micro_batches + mb);
+  }
 
   const void* input(int mb) const {
     return (in_dev && first()) ? static_cast<const void*>(in_dev + mb * elems()) : st->act[mb][0].ptr;
@@ -76,7 +81,7 @@ struct Step {
     if (in_host) {
       mt::check_cuda(cudaMemcpyAsync(dst, in_host + mb * elems(), bytes(), cudaMemcpyHostToDevice, s), "H2D input");
     } else {
-      const uint64_t key = mt_stream_key(st->d.layer.seed, "input", 0, (uint32_t)mb);
+      const uint64_t key = mt_stream_key(st->d.layer.seed, "input", 0, gid(mb));
       mt::fill_normal(dst, 1, elems(), elems(), 0, 0, key, 0.f, 1.f, s);
       ++launches;
     }
@@ -84,7 +89,7 @@ struct Step {
   void forward(int mb) {
     for (size_t i = 0; i < st->layers.size(); ++i) {
       const void* x = i == 0 ? input(mb) : st->act[mb][i].ptr;
-      ok(mt_layer_forward(st->layers[i], x, st->act[mb][i + 1].ptr, (uint32_t)mb, s));
+      ok(mt_layer_forward(st->layers[i], x, st->act[mb][i + 1].ptr, gid(mb), s));
       int32_t f, b;
       mt_layer_launch_counts(st->layers[i], &f, &b);
       launches += f;
@@ -98,7 +103,7 @@ struct Step {
         mt::check_cuda(cudaMemcpyAsync(st->target.ptr, tgt_host + mb * elems(), bytes(), cudaMemcpyHostToDevice, s),
                        "H2D target");
       } else {
-        const uint64_t key = mt_stream_key(st->d.layer.seed, "target", 0, (uint32_t)mb);
+        const uint64_t key = mt_stream_key(st->d.layer.seed, "target", 0, gid(mb));
         mt::fill_normal(st->target.ptr, 1, elems(), elems(), 0, 0, key, 0.f, 1.f, s);
         ++launches;
       }
@@ -111,7 +116,7 @@ struct Step {
     void* cur = g;
     for (size_t i = st->layers.size(); i-- > 0;) {
       void* out = (cur == st->grad[0].ptr) ? st->grad[1].ptr : st->grad[0].ptr;
-      ok(mt_layer_backward(st->layers[i], cur, out, (uint32_t)mb, s));
+      ok(mt_layer_backward(st->layers[i], cur, out, gid(mb), s));
       int32_t f, b;
       mt_layer_launch_counts(st->layers[i], &f, &b);
       launches += b;

@@ -1,0 +1,196 @@
+"""Multi-GPU parity (needs >= 2 GPUs; skipped otherwise): TP=2 layer, PP=2 1F1B stage pipeline, DP=2
+gradient all-reduce — all through the C ABI with NCCL over NVLink, compared against the CPU oracle.
+
+Tolerances as tests/test_layer_gpu.py (bf16-emulated oracle: activations 5e-3, gradients 1e-2 rel-Frobenius;
+loss 5e-3 relative).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+SEED = 20260808
+H, HEADS, S, B = 512, 8, 256, 1
+
+
+def _need(n):
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _worker(rank, world, port, mode, q):
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2201_11990_b200 import planner as PL
+    from paper_2201_11990_b200.runtime import Context, Layer, Stage
+    try:
+        torch.cuda.set_device(rank)
+        os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        obj = [Context.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = Context(rank)
+        s = torch.cuda.current_stream()
+        out = {}
+        if mode == "tp":
+            ctx.init_comm(obj[0], world, rank, tensor=world)
+            d = PL.layer_desc(H, HEADS, S, B, tp_size=world, tp_rank=rank, seed=SEED, layer_index=0)
+            lay = Layer(ctx, d)
+            params = O.init_params(H, SEED, 0)
+            bits = [np.ascontiguousarray(O.to_bf16_bits(p)) for p in params]
+            for i, b in enumerate(bits):
+                lay.set_param(i, b.ctypes.data)
+            x = O.normal(O.site_seed(SEED, "input", 0, 0), B * S, H)
+            g = O.normal(O.site_seed(SEED, "grad", 0, 0), B * S, H, std=1e-2)
+            dev = lambda a: torch.from_numpy(O.to_bf16_bits(a).view(np.int16)).view(torch.bfloat16).cuda()  # noqa
+            xd, gd = dev(x), dev(g)
+            yd, dxd = torch.empty_like(xd), torch.empty_like(xd)
+            lay.forward(xd.data_ptr(), yd.data_ptr(), 0, s)
+            lay.backward(gd.data_ptr(), dxd.data_ptr(), 0, s)
+            torch.cuda.synchronize()
+            out["y"], out["dx"] = yd.float().cpu().numpy(), dxd.float().cpu().numpy()
+            grads = []
+            for i, p in enumerate(params):
+                _, _, (nr, nc) = PL.param_shard(d, i)
+                a = np.empty(nr * nc, np.float32)
+                lay.get_grad(i, a.ctypes.data)
+                grads.append(a.reshape(nr, nc))
+            out["grads"] = grads
+            lay.close()
+        else:
+            tp, pp, dp = (1, world, 1) if mode == "pp" else (1, 1, world)
+            layers, MB = (2 * pp, 4) if mode == "pp" else (1, 2)
+            ctx.init_comm(obj[0], world, rank, tensor=tp, pipeline=pp, data=dp, batch=B * MB * dp, micro_batches=MB)
+            place = ctx.placement()
+            d = PL.layer_desc(H, HEADS, S, B, seed=SEED)
+            st = Stage(ctx, d, layers, MB)
+            per = layers // pp
+            for li in range(per):
+                params = O.init_params(H, SEED, place.pipeline * per + li)
+                for i, p in enumerate(params):
+                    b = np.ascontiguousarray(O.to_bf16_bits(p))
+                    st.layer(li).set_param(i, b.ctypes.data)
+            gids = [place.data * MB + m for m in range(MB)]
+            xs = np.stack([O.normal(O.site_seed(SEED, "input", 0, gi), B * S, H) for gi in gids])
+            ts = np.stack([O.normal(O.site_seed(SEED, "target", 0, gi), B * S, H) for gi in gids])
+            xh = torch.from_numpy(O.to_bf16_bits(xs).view(np.int16)).pin_memory()
+            th = torch.from_numpy(O.to_bf16_bits(ts).view(np.int16)).pin_memory()
+            for _ in range(2):  # the second iteration must reproduce the first (grads re-zeroed)
+                loss = st.train_step(xh.data_ptr(), th.data_ptr(), s)
+            out["loss"], out["place"] = loss, (place.data, place.pipeline, place.tensor)
+            out["grads"] = []
+            for li in range(per):
+                gl = []
+                for i, p in enumerate(O.param_shapes(H)):
+                    a = np.empty(p[0] * p[1], np.float32)
+                    st.layer(li).get_grad(i, a.ctypes.data)
+                    gl.append(a.reshape(p))
+                out["grads"].append(gl)
+            st.close()
+        ctx.close()
+        q.put((rank, out))
+    except Exception as e:  # pragma: no cover
+        import traceback
+        q.put((rank, {"error": traceback.format_exc() + repr(e)}))
+    finally:
+        try:
+            dist.destroy_process_group()
+        except Exception:
+            pass
+
+
+def _run(mode, world=2):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    for r, o in res.items():
+        assert "error" not in o, o.get("error")
+    return res
+
+
+@pytest.mark.timeout(900)
+def test_tensor_parallel_layer_two_gpus():
+    _need(2)
+    from oracle import oracle as O
+    res = _run("tp")
+    ol = O.OracleLayer(H, HEADS, S, B, 2, dropout_hidden=0.1, dropout_attn=0.1, seed=SEED, layer_index=0,
+                       bf16_emulate=True)
+    x = O.normal(O.site_seed(SEED, "input", 0, 0), B * S, H)
+    g = O.normal(O.site_seed(SEED, "grad", 0, 0), B * S, H, std=1e-2)
+    y, dx = ol.forward(x), ol.backward(g)
+    for r in (0, 1):
+        assert rel(res[r]["y"], y) < 5e-3 and rel(res[r]["dx"], dx) < 1e-2
+    from paper_2201_11990_b200 import planner as PL
+    for i in range(12):
+        full = np.zeros_like(ol.grads[i])
+        for r in (0, 1):
+            d = PL.layer_desc(H, HEADS, S, B, tp_size=2, tp_rank=r)
+            _, (r0, c0), (nr, nc) = PL.param_shard(d, i)
+            full[r0:r0 + nr, c0:c0 + nc] = res[r]["grads"][i]
+            if nr * nc == H:  # replicated parameter: both ranks hold the full gradient
+                assert rel(res[r]["grads"][i], ol.grads[i]) < 1e-2
+        assert rel(full, ol.grads[i]) < 1e-2, (i, rel(full, ol.grads[i]))
+
+
+def _oracle_step(layer_ids, gids):
+    from oracle import oracle as O
+    ls = [O.OracleLayer(H, HEADS, S, B, 1, dropout_hidden=0.1, dropout_attn=0.1, seed=SEED, layer_index=li,
+                        bf16_emulate=True) for li in layer_ids]
+    loss = 0.0
+    for gi in gids:
+        a = O.normal(O.site_seed(SEED, "input", 0, gi), B * S, H)
+        for l in ls:
+            a = l.forward(a, gi)
+        lv, dy = O.mse_loss(a, O.normal(O.site_seed(SEED, "target", 0, gi), B * S, H))
+        loss += lv
+        for l in reversed(ls):
+            dy = l.backward(O.from_bf16_bits(O.to_bf16_bits(dy)), gi)
+    return loss, [l.grads for l in ls]
+
+
+@pytest.mark.timeout(900)
+def test_pipeline_parallel_1f1b_two_gpus():
+    _need(2)
+    res = _run("pp")
+    loss, grads = _oracle_step([0, 1, 2, 3], range(4))
+    assert abs(res[1]["loss"] - loss) / loss < 5e-3, (res[1]["loss"], loss)
+    for r in (0, 1):
+        for li in range(2):
+            for i in range(12):
+                assert rel(res[r]["grads"][li][i], grads[2 * r + li][i]) < 2e-2, (r, li, i)
+
+
+@pytest.mark.timeout(900)
+def test_data_parallel_gradient_allreduce_two_gpus():
+    _need(2)
+    res = _run("dp")
+    loss, grads = _oracle_step([0], range(4))
+    for r in (0, 1):
+        assert abs(res[r]["loss"] - loss / 2) / loss < 5e-3
+        for i in range(12):
+            assert rel(res[r]["grads"][0][i], grads[0][i] / 2) < 2e-2, (r, i)
