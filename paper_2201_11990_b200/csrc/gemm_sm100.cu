@@ -32,6 +32,7 @@ struct GemmParams {
   int mblocks, nblocks, kblocks, total_tiles;
   float alpha;
   int epilogue, causal;
+  int n_fastest;  // tile raster: 0 = m-blocks vary fastest (B tile shared by concurrent CTAs), 1 = n-blocks
   __nv_bfloat16* d_bf16;
   float* d_f32;
   long long ldd, d_batch_stride;
@@ -58,8 +59,13 @@ __device__ __forceinline__ void tile_coords(const GemmParams& p, int t, int& b, 
   const int per_batch = p.mblocks * p.nblocks;
   b = t / per_batch;
   const int rem = t - b * per_batch;
-  nb = rem / p.mblocks;
-  mb = rem - nb * p.mblocks;
+  if (p.n_fastest) {
+    mb = rem / p.nblocks;
+    nb = rem - mb * p.nblocks;
+  } else {
+    nb = rem / p.mblocks;
+    mb = rem - nb * p.mblocks;
+  }
 }
 
 template <int BN>
@@ -427,6 +433,10 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   p.alpha = a.alpha;
   p.epilogue = a.epilogue;
   p.causal = a.causal;
+  // Raster so the larger operand is streamed once: concurrently resident CTAs then share the tile
+  // of the larger operand, and the smaller operand stays L2-resident across the sweep (e.g. the
+  // wgrad of fc1, M = 4h/t >> N = h, would otherwise re-read its 200 MB A operand per n-block).
+  p.n_fastest = (m > n) ? 1 : 0;
   p.d_bf16 = static_cast<__nv_bfloat16*>(a.d);
   p.d_f32 = static_cast<float*>(a.d);
   p.ldd = a.ldd;

@@ -1,0 +1,41 @@
+"""Run one GEMM of the layer (GPT-3 TP=1 shapes) `reps` times — a clean target for ncu.
+
+    python tools/gemm_one.py fc1_fwd|fc2_fwd|qkv_fwd|fc1_dgrad|fc1_wgrad [reps]
+"""
+import ctypes as C
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2201_11990_b200 import _native as N  # noqa: E402
+
+h, M = 12288, 2048
+SHAPES = {  # name: (m, n, k, a_mn, b_mn, epilogue)
+    "qkv_fwd": (M, 3 * h, h, 0, 0, N.EPI_STORE_BF16),
+    "fc1_fwd": (M, 4 * h, h, 0, 0, N.EPI_STORE_BF16),
+    "fc2_fwd": (M, h, 4 * h, 0, 0, N.EPI_STORE_BF16),
+    "fc1_dgrad": (M, h, 4 * h, 0, 1, N.EPI_STORE_BF16),
+    "fc1_wgrad": (4 * h, h, M, 1, 1, N.EPI_STORE_F32),
+    "fc1_wgrad_acc": (4 * h, h, M, 1, 1, N.EPI_ACCUM_F32),
+}
+name = sys.argv[1]
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+m, n, k, amn, bmn, epi = SHAPES[name]
+A = torch.randn((k, m) if amn else (m, k), device="cuda").bfloat16()
+B = torch.randn((k, n) if bmn else (n, k), device="cuda").bfloat16()
+D = torch.zeros(m, n, device="cuda", dtype=torch.float32 if epi >= 3 else torch.bfloat16)
+a = N.GemmArgs()
+a.a, a.b, a.d = A.data_ptr(), B.data_ptr(), D.data_ptr()
+a.lda, a.ldb, a.ldd = (m if amn else k), (n if bmn else k), n
+a.a_mn_major, a.b_mn_major = amn, bmn
+a.m, a.n, a.k, a.batch, a.alpha, a.epilogue = m, n, k, 1, 1.0, epi
+s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+for i in range(reps):
+    ev[0].record()
+    assert N.lib().mt_gemm(C.byref(a), s) == 0
+    ev[1].record()
+    torch.cuda.synchronize()
+    print(f"{name} rep {i}: {ev[0].elapsed_time(ev[1])*1e3:.1f} us, {2*m*n*k/ev[0].elapsed_time(ev[1])/1e9:.0f} TFLOP/s")
