@@ -13,7 +13,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/mtnlg_gemm.h"
@@ -41,10 +43,14 @@ struct GemmParams {
   long long ld_aux;
 };
 
-template <int BN>
+// kPair: 2-CTA (cta_group::2) tiles of 256 x BN — each CTA of the pair holds 128 rows of A and
+// BN/2 rows of B in its smem and 128 x BN of the accumulator in its TMEM.
+template <int BN, bool kPair = false>
 struct Cfg {
-  static constexpr int kBNAlloc = (BN + 63) / 64 * 64;
-  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kTileM = kPair ? 256 : 128;   // rows of the (pair) tile
+  static constexpr int kBRows = kPair ? BN / 2 : BN;  // B rows (n) held by one CTA
+  static constexpr int kBNAlloc = (kBRows + 63) / 64 * 64;
+  static constexpr int kABytes = 128 * kBK * 2;  // one CTA always holds 128 rows of A
   static constexpr int kBBytes = kBNAlloc * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kEpiBytes = 4 * 2 * 4096;  // 4 epilogue warps x 2 staging buffers x (32 rows x 128 B)
@@ -68,20 +74,21 @@ __device__ __forceinline__ void tile_coords(const GemmParams& p, int t, int& b, 
   }
 }
 
-template <int BN>
+template <int BN, int BMT>
 __device__ __forceinline__ bool tile_valid(const GemmParams& p, int mb, int nb) {
-  if (p.causal == MT_CAUSAL_SKIP_UPPER_TILES) return nb * BN <= mb * kBM + kBM - 1;
+  if (p.causal == MT_CAUSAL_SKIP_UPPER_TILES) return nb * BN <= mb * BMT + BMT - 1;
   return true;
 }
 
+template <int BMT>
 __device__ __forceinline__ void k_range(const GemmParams& p, int mb, int& kb0, int& kb1) {
   kb0 = 0;
   kb1 = p.kblocks;
   if (p.causal == MT_CAUSAL_K_LE_M) {
-    const int kend = min(p.k, (mb + 1) * kBM);
+    const int kend = min(p.k, (mb + 1) * BMT);
     kb1 = (kend + kBK - 1) / kBK;
   } else if (p.causal == MT_CAUSAL_K_GE_M) {
-    kb0 = (mb * kBM) / kBK;
+    kb0 = (mb * BMT) / kBK;
   }
 }
 
@@ -131,12 +138,13 @@ __device__ __forceinline__ void reuse_wait(uint32_t lane) {
   __syncwarp();
 }
 
-template <int BN, bool kAMN, bool kBMN>
+template <int BN, bool kAMN, bool kBMN, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                       const __grid_constant__ CUtensorMap tmap_d, const __grid_constant__ CUtensorMap tmap_aux,
                       const GemmParams p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, kPair>;
+  constexpr int BMT = C::kTileM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
@@ -147,6 +155,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  const uint32_t rank = kPair ? cluster_ctarank() : 0;  // position in the CTA pair
+  const bool leader = rank == 0;
+  const int t_first = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int t_stride = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
@@ -159,44 +171,61 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&bars[2 * C::kStages + a]), 1);
-      mbar_init(smem_u32(&bars[2 * C::kStages + 2 + a]), 4);
+      mbar_init(smem_u32(&bars[2 * C::kStages + 2 + a]), kPair ? 8 : 4);  // epilogue warps (of both CTAs)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<C::kTmemCols>(smem_u32(tmem_slot));
+  if (warp == 2) {
+    if (kPair)
+      tmem_alloc_pair<C::kTmemCols>(smem_u32(tmem_slot));
+    else
+      tmem_alloc<C::kTmemCols>(smem_u32(tmem_slot));
+  }
   tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
-      constexpr uint32_t kTx = C::kABytes + (kBMN ? C::kBBytes : BN * kBK * 2);
+      // bytes landing per stage on the (leader's) full barrier: both CTAs' halves in pair mode
+      constexpr uint32_t kTx = (C::kABytes + (kBMN ? C::kBBytes : C::kBRows * kBK * 2)) * (kPair ? 2 : 1);
       uint32_t stage = 0, phase = 0;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      for (int t = t_first; t < p.total_tiles; t += t_stride) {
         int b, mb, nb;
         tile_coords(p, t, b, mb, nb);
-        if (!tile_valid<BN>(p, mb, nb)) continue;
+        if (!tile_valid<BN, BMT>(p, mb, nb)) continue;
         int kb0, kb1;
-        k_range(p, mb, kb0, kb1);
+        k_range<BMT>(p, mb, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(smem_u32(&bars[C::kStages + stage]), phase ^ 1);
           const uint32_t full = smem_u32(&bars[stage]);
-          mbar_arrive_expect_tx(full, kTx);
+          if (leader) mbar_arrive_expect_tx(full, kTx);
           const uint32_t sa = smem_u32(stage_base + stage * C::kStageBytes);
           const uint32_t sb = sa + C::kABytes;
+          const int m_off = mb * BMT + (int)rank * kBM;        // this CTA's 128 rows of A
+          const int n_off = nb * BN + (int)rank * C::kBRows;   // this CTA's rows of B
+          auto load = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1) {
+            if (kPair)
+              tma_load_3d_pair(dst, map, full, c0, c1, b);
+            else
+              tma_load_3d(dst, map, full, c0, c1, b);
+          };
           if (kAMN) {
-            tma_load_3d(sa, &tmap_a, full, mb * kBM, kb * kBK, b);
-            tma_load_3d(sa + 8192, &tmap_a, full, mb * kBM + 64, kb * kBK, b);
+            load(sa, &tmap_a, m_off, kb * kBK);
+            load(sa + 8192, &tmap_a, m_off + 64, kb * kBK);
           } else {
-            tma_load_3d(sa, &tmap_a, full, kb * kBK, mb * kBM, b);
+            load(sa, &tmap_a, kb * kBK, m_off);
           }
           if (kBMN) {
 #pragma unroll
-            for (int c = 0; c < C::kBNAlloc / 64; ++c) tma_load_3d(sb + c * 8192, &tmap_b, full, nb * BN + c * 64, kb * kBK, b);
+            for (int c = 0; c < C::kBNAlloc / 64; ++c) load(sb + c * 8192, &tmap_b, n_off + c * 64, kb * kBK);
           } else {
-            tma_load_3d(sb, &tmap_b, full, kb * kBK, nb * BN, b);
+            load(sb, &tmap_b, kb * kBK, n_off);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -206,16 +235,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN, kAMN ? 1 : 0, kBMN ? 1 : 0);
+    if (lane == 0 && leader) {
+      // ------------------------------------------------------------ MMA issuer (pair leader only)
+      constexpr uint32_t idesc = umma_idesc_bf16(BMT, BN, kAMN ? 1 : 0, kBMN ? 1 : 0);
       uint32_t stage = 0, phase = 0, it = 0;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      for (int t = t_first; t < p.total_tiles; t += t_stride) {
         int b, mb, nb;
         tile_coords(p, t, b, mb, nb);
-        if (!tile_valid<BN>(p, mb, nb)) continue;
+        if (!tile_valid<BN, BMT>(p, mb, nb)) continue;
         int kb0, kb1;
-        k_range(p, mb, kb0, kb1);
+        k_range<BMT>(p, mb, kb0, kb1);
         const uint32_t acc = it & 1, acc_phase = (it >> 1) & 1;
         mbar_wait(smem_u32(&bars[2 * C::kStages + 2 + acc]), acc_phase ^ 1);
         tc_fence_after();
@@ -229,15 +258,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < kBK / 16; ++kk) {
             const uint64_t ad = kAMN ? umma_desc_sw128(sa + kk * 2048, 8192, 1024) : umma_desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t bd = kBMN ? umma_desc_sw128(sb + kk * 2048, 8192, 1024) : umma_desc_sw128(sb + kk * 32, 16, 1024);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            if (kPair)
+              umma_bf16_pair(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            else
+              umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
           }
-          tc_commit(smem_u32(&bars[C::kStages + stage]));
+          if (kPair)
+            tc_commit_pair_mc(smem_u32(&bars[C::kStages + stage]), 0x3);  // frees the stage in both CTAs
+          else
+            tc_commit(smem_u32(&bars[C::kStages + stage]));
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(smem_u32(&bars[2 * C::kStages + acc]));
+        if (kPair)
+          tc_commit_pair_mc(smem_u32(&bars[2 * C::kStages + acc]), 0x3);
+        else
+          tc_commit(smem_u32(&bars[2 * C::kStages + acc]));
         ++it;
       }
     }
@@ -250,14 +288,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool f32 = ep == MT_EPI_STORE_F32 || ep == MT_EPI_ACCUM_F32;
     const float alpha = p.alpha;
     uint32_t it = 0;
-    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+    for (int t = t_first; t < p.total_tiles; t += t_stride) {
       int b, mb, nb;
       tile_coords(p, t, b, mb, nb);
-      if (!tile_valid<BN>(p, mb, nb)) continue;
+      if (!tile_valid<BN, BMT>(p, mb, nb)) continue;
       const uint32_t acc = it & 1, acc_phase = (it >> 1) & 1;
       mbar_wait(smem_u32(&bars[2 * C::kStages + acc]), acc_phase);
       tc_fence_after();
-      const int row0 = mb * kBM + quad * 32;
+      const int row0 = mb * BMT + (int)rank * kBM + quad * 32;
       const int row = row0 + lane;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
@@ -330,16 +368,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
+      if (lane == 0) {
+        if (kPair)
+          mbar_arrive_cluster(smem_u32(&bars[2 * C::kStages + 2 + acc]), 0);  // the leader's tmem_empty
+        else
+          mbar_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
+      }
       ++it;
     }
     if (lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<C::kTmemCols>(tmem_base);
+  if (warp == 2) {
+    if (kPair)
+      tmem_dealloc_pair<C::kTmemCols>(tmem_base);
+    else
+      tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -404,15 +455,15 @@ int num_sms() {
   return n;
 }
 
-template <int BN, bool kAMN, bool kBMN>
+template <int BN, bool kAMN, bool kBMN, bool kPair>
 int launch(const mt_gemm_args& a, cudaStream_t stream) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, kPair>;
   CUtensorMap ma, mb;
   const int m = (int)a.m, n = (int)a.n, k = (int)a.k, batch = (int)a.batch;
   bool ok = kAMN ? make_map(&ma, a.a, m, k, batch, a.lda, a.a_batch_stride, 64)
                  : make_map(&ma, a.a, k, m, batch, a.lda, a.a_batch_stride, kBM);
   ok = ok && (kBMN ? make_map(&mb, a.b, n, k, batch, a.ldb, a.b_batch_stride, 64)
-                   : make_map(&mb, a.b, k, n, batch, a.ldb, a.b_batch_stride, BN));
+                   : make_map(&mb, a.b, k, n, batch, a.ldb, a.b_batch_stride, C::kBRows));
   const bool f32 = a.epilogue == MT_EPI_STORE_F32 || a.epilogue == MT_EPI_ACCUM_F32;
   CUtensorMap md, maux;
   ok = ok && make_store_map(&md, a.d, n, m, batch, a.ldd, a.d_batch_stride, f32);
@@ -426,7 +477,7 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   p.n = n;
   p.k = k;
   p.batch = batch;
-  p.mblocks = (m + kBM - 1) / kBM;
+  p.mblocks = (m + C::kTileM - 1) / C::kTileM;
   p.nblocks = (n + BN - 1) / BN;
   p.kblocks = (k + kBK - 1) / kBK;
   p.total_tiles = p.mblocks * p.nblocks * batch;
@@ -444,22 +495,49 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   p.bias = static_cast<const __nv_bfloat16*>(a.bias);
   p.aux = static_cast<__nv_bfloat16*>(a.aux);
   p.ld_aux = a.ld_aux;
-  auto kern = gemm_sm100_kernel<BN, kAMN, kBMN>;
+  auto kern = gemm_sm100_kernel<BN, kAMN, kBMN, kPair>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
       return 2;
     attr_set = true;
   }
-  const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
-  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, md, maux, p);
+  if (!kPair) {
+    const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
+    kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, md, maux, p);
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+  }
+  const int pairs = std::min(p.total_tiles, num_sms() / 2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, md, maux, p) != cudaSuccess) return 2;
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
-template <int BN>
+template <int BN, bool kPair>
 int dispatch_major(const mt_gemm_args& a, cudaStream_t s) {
-  if (a.a_mn_major) return a.b_mn_major ? launch<BN, true, true>(a, s) : launch<BN, true, false>(a, s);
-  return a.b_mn_major ? launch<BN, false, true>(a, s) : launch<BN, false, false>(a, s);
+  if (a.a_mn_major)
+    return a.b_mn_major ? launch<BN, true, true, kPair>(a, s) : launch<BN, true, false, kPair>(a, s);
+  return a.b_mn_major ? launch<BN, false, true, kPair>(a, s) : launch<BN, false, false, kPair>(a, s);
+}
+
+bool pair_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MT_GEMM_PAIR");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 }  // namespace
@@ -484,15 +562,17 @@ extern "C" int mt_gemm(const mt_gemm_args* args, void* stream) {
   int bn = a.block_n;
   if (bn == 0) bn = a.n <= 64 ? 64 : (a.n <= 128 ? 128 : (a.n == 160 ? 160 : 256));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // 2-CTA 256-row tiles whenever M fills them (BN 128 / 256); 1-CTA 128-row tiles otherwise.
+  const bool pair = mt::pair_enabled() && a.m >= 256 && (bn == 128 || bn == 256);
   switch (bn) {
     case 64:
-      return mt::dispatch_major<64>(a, s);
+      return mt::dispatch_major<64, false>(a, s);
     case 128:
-      return mt::dispatch_major<128>(a, s);
+      return pair ? mt::dispatch_major<128, true>(a, s) : mt::dispatch_major<128, false>(a, s);
     case 160:
-      return mt::dispatch_major<160>(a, s);
+      return mt::dispatch_major<160, false>(a, s);
     case 256:
-      return mt::dispatch_major<256>(a, s);
+      return pair ? mt::dispatch_major<256, true>(a, s) : mt::dispatch_major<256, false>(a, s);
     default:
       return 1;
   }
