@@ -34,6 +34,7 @@ struct GemmParams {
   int mblocks, nblocks, kblocks, total_tiles;
   float alpha;
   int epilogue, causal;
+  int hints;      // L2 eviction hints on the operand loads (MT_GEMM_HINTS=1 enables; A/B only)
   int n_fastest;  // tile raster: 0 = m-blocks vary fastest (B tile shared by concurrent CTAs), 1 = n-blocks
   __nv_bfloat16* d_bf16;
   float* d_f32;
@@ -194,6 +195,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------------------------------ TMA producer
       // bytes landing per stage on the (leader's) full barrier: both CTAs' halves in pair mode
       constexpr uint32_t kTx = (C::kABytes + (kBMN ? C::kBBytes : C::kBRows * kBK * 2)) * (kPair ? 2 : 1);
+      // The operand re-read across the raster sweep is kept in L2 (evict_last); the one whose tile is
+      // shared by the concurrently resident CTAs streams through once (evict_first).
+      const uint64_t pol_a = !p.hints ? kEvictNormal : (p.n_fastest ? kEvictFirst : kEvictLast);
+      const uint64_t pol_b = !p.hints ? kEvictNormal : (p.n_fastest ? kEvictLast : kEvictFirst);
       uint32_t stage = 0, phase = 0;
       for (int t = t_first; t < p.total_tiles; t += t_stride) {
         int b, mb, nb;
@@ -209,23 +214,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sb = sa + C::kABytes;
           const int m_off = mb * BMT + (int)rank * kBM;        // this CTA's 128 rows of A
           const int n_off = nb * BN + (int)rank * C::kBRows;   // this CTA's rows of B
-          auto load = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1) {
+          auto load = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t pol) {
             if (kPair)
-              tma_load_3d_pair(dst, map, full, c0, c1, b);
+              tma_load_3d_pair(dst, map, full, c0, c1, b, pol);
             else
-              tma_load_3d(dst, map, full, c0, c1, b);
+              tma_load_3d(dst, map, full, c0, c1, b, pol);
           };
           if (kAMN) {
-            load(sa, &tmap_a, m_off, kb * kBK);
-            load(sa + 8192, &tmap_a, m_off + 64, kb * kBK);
+            load(sa, &tmap_a, m_off, kb * kBK, pol_a);
+            load(sa + 8192, &tmap_a, m_off + 64, kb * kBK, pol_a);
           } else {
-            load(sa, &tmap_a, kb * kBK, m_off);
+            load(sa, &tmap_a, kb * kBK, m_off, pol_a);
           }
           if (kBMN) {
 #pragma unroll
-            for (int c = 0; c < C::kBNAlloc / 64; ++c) load(sb + c * 8192, &tmap_b, n_off + c * 64, kb * kBK);
+            for (int c = 0; c < C::kBNAlloc / 64; ++c) load(sb + c * 8192, &tmap_b, n_off + c * 64, kb * kBK, pol_b);
           } else {
-            load(sb, &tmap_b, kb * kBK, n_off);
+            load(sb, &tmap_b, kb * kBK, n_off, pol_b);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -488,6 +493,12 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   // of the larger operand, and the smaller operand stays L2-resident across the sweep (e.g. the
   // wgrad of fc1, M = 4h/t >> N = h, would otherwise re-read its 200 MB A operand per n-block).
   p.n_fastest = (m > n) ? 1 : 0;
+  // Off by default: A/B on B200 (tools/gemm_ab.sh) measured evict_first/evict_last hints 0-7% slower.
+  static const int hints = [] {
+    const char* e = getenv("MT_GEMM_HINTS");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  p.hints = hints;
   p.d_bf16 = static_cast<__nv_bfloat16*>(a.d);
   p.d_f32 = static_cast<float*>(a.d);
   p.ldd = a.ldd;
@@ -531,6 +542,40 @@ int dispatch_major(const mt_gemm_args& a, cudaStream_t s) {
   return a.b_mn_major ? launch<BN, false, true, kPair>(a, s) : launch<BN, false, false, kPair>(a, s);
 }
 
+bool pair_enabled();
+
+bool use_pair(const mt_gemm_args& a, int bn) {
+  return pair_enabled() && a.m >= 256 && (bn == 128 || bn == 192 || bn == 256);
+}
+
+// Tile width: N <= 64/128 and the head dim 160 map directly; otherwise pick the width whose last
+// wave of (pair) tiles is fullest, weighted by the measured per-tile rate of narrower tiles
+// (tools/gemm_ab.sh: BN 192 and 128 run at 87% and 68% of BN 256's rate, so 256 nearly always wins;
+// the last-wave loss, e.g. N = 12288 at M = 2048 -> 384 tiles = 5.19 waves of 74 pairs, is left to
+// a split-K tail).
+int choose_block_n(const mt_gemm_args& a) {
+  if (a.n <= 64) return 64;
+  if (a.n <= 128) return 128;
+  if (a.n == 160) return 160;
+  const int units = pair_enabled() && a.m >= 256 ? num_sms() / 2 : num_sms();
+  const int tile_m = pair_enabled() && a.m >= 256 ? 256 : 128;
+  const long long mblocks = (a.m + tile_m - 1) / tile_m;
+  const int cand[3] = {256, 192, 128};
+  const double weight[3] = {1.0, 0.87, 0.68};  // measured per-tile rates relative to BN = 256 (B200)
+  int best = 256;
+  double best_eff = -1.0;
+  for (int i = 0; i < 3; ++i) {
+    const long long tiles = mblocks * ((a.n + cand[i] - 1) / cand[i]) * a.batch;
+    const long long waves = (tiles + units - 1) / units;
+    const double eff = weight[i] * double(tiles) / double(waves * units);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = cand[i];
+    }
+  }
+  return best;
+}
+
 bool pair_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -560,10 +605,10 @@ extern "C" int mt_gemm(const mt_gemm_args* args, void* stream) {
   if ((a.epilogue == MT_EPI_BIAS_GELU || a.epilogue == MT_EPI_GELU_BWD) && a.batch != 1) return 1;
   if (a.epilogue < 0 || a.epilogue > MT_EPI_ACCUM_F32 || a.causal < 0 || a.causal > MT_CAUSAL_K_GE_M) return 1;
   int bn = a.block_n;
-  if (bn == 0) bn = a.n <= 64 ? 64 : (a.n <= 128 ? 128 : (a.n == 160 ? 160 : 256));
+  if (bn == 0) bn = mt::choose_block_n(a);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // 2-CTA 256-row tiles whenever M fills them (BN 128 / 256); 1-CTA 128-row tiles otherwise.
-  const bool pair = mt::pair_enabled() && a.m >= 256 && (bn == 128 || bn == 256);
+  // 2-CTA 256-row tiles whenever M fills them; 1-CTA 128-row tiles otherwise.
+  const bool pair = mt::use_pair(a, bn);
   switch (bn) {
     case 64:
       return mt::dispatch_major<64, false>(a, s);
@@ -571,6 +616,8 @@ extern "C" int mt_gemm(const mt_gemm_args* args, void* stream) {
       return pair ? mt::dispatch_major<128, true>(a, s) : mt::dispatch_major<128, false>(a, s);
     case 160:
       return mt::dispatch_major<160, false>(a, s);
+    case 192:
+      return pair ? mt::dispatch_major<192, true>(a, s) : mt::dispatch_major<192, false>(a, s);
     case 256:
       return pair ? mt::dispatch_major<256, true>(a, s) : mt::dispatch_major<256, false>(a, s);
     default:

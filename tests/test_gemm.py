@@ -42,7 +42,7 @@ def _close(out, ref, tol=1e-2):
 
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
-@pytest.mark.parametrize("bn", [64, 128, 160, 256])
+@pytest.mark.parametrize("bn", [64, 128, 160, 192, 256])
 @pytest.mark.parametrize("mnk", [(256, 512, 256), (296, 328, 200), (128, 160, 64)])
 def test_gemm_majors(a_mn, b_mn, bn, mnk):
     m, n, k = mnk

@@ -1,8 +1,7 @@
 #!/bin/bash
-# A/B of the 1-CTA and 2-CTA GEMM paths on the same box (interleaved to cancel clock drift).
-for i in 1 2; do
-  for pair in 0 1; do
-    echo "== MT_GEMM_PAIR=$pair"
-    for g in qkv_fwd fc1_fwd fc2_fwd fc1_dgrad fc1_wgrad; do MT_GEMM_PAIR=$pair python tools/gemm_one.py $g 4 | tail -1; done
-  done
+# A/B of GEMM variants on the same box. Usage: tools/gemm_ab.sh "ENV1" "ENV2" ... (each a set of env assignments)
+SHAPES=${SHAPES:-"qkv_fwd fc1_fwd fc2_fwd proj_fwd fc1_dgrad fc1_wgrad mt_qkv_fwd mt_proj_fwd mt_fc1_fwd mt_fc2_fwd mt_fc1_wgrad"}
+for cfg in "$@"; do
+  echo "== $cfg"
+  for g in $SHAPES; do env $cfg python tools/gemm_one.py $g 4 | tail -1; done
 done

@@ -19,6 +19,13 @@ SHAPES = {  # name: (m, n, k, a_mn, b_mn, epilogue)
     "fc1_dgrad": (M, h, 4 * h, 0, 1, N.EPI_STORE_BF16),
     "fc1_wgrad": (4 * h, h, M, 1, 1, N.EPI_STORE_F32),
     "fc1_wgrad_acc": (4 * h, h, M, 1, 1, N.EPI_ACCUM_F32),
+    "proj_fwd": (M, h, h, 0, 0, N.EPI_STORE_BF16),
+    # MT-NLG h=20480 at TP=8 (per-GPU shard shapes)
+    "mt_qkv_fwd": (M, 7680, 20480, 0, 0, N.EPI_STORE_BF16),
+    "mt_proj_fwd": (M, 20480, 2560, 0, 0, N.EPI_STORE_BF16),
+    "mt_fc1_fwd": (M, 10240, 20480, 0, 0, N.EPI_STORE_BF16),
+    "mt_fc2_fwd": (M, 20480, 10240, 0, 0, N.EPI_STORE_BF16),
+    "mt_fc1_wgrad": (10240, 20480, M, 1, 1, N.EPI_STORE_F32),
 }
 name = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
@@ -31,6 +38,7 @@ a.a, a.b, a.d = A.data_ptr(), B.data_ptr(), D.data_ptr()
 a.lda, a.ldb, a.ldd = (m if amn else k), (n if bmn else k), n
 a.a_mn_major, a.b_mn_major = amn, bmn
 a.m, a.n, a.k, a.batch, a.alpha, a.epilogue = m, n, k, 1, 1.0, epi
+a.block_n = int(os.environ.get("MT_BN", "0"))
 s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for i in range(reps):
