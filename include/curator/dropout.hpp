@@ -4,10 +4,12 @@
 // (proj/include/curator/hashing.hpp:45-63) and its seed-derivation pattern
 // `mix64(seed, fnv1a64(name))` (proj/src/pipeline.cpp:708-711).
 //
-// Mask definition (one mix64 per group of 4 consecutive elements, 16 uniform bits each):
-//   bits = mix64(site_seed, idx >> 2)
+// Mask definition (one SplitMix64 output per group of 4 consecutive elements, 16 uniform bits each):
+//   bits = splitmix64(site_seed + (idx >> 2) * 0x9e3779b97f4a7c15)   i.e. output (idx>>2)+1 of the
+//          SplitMix64 generator seeded with site_seed (reference hashing.hpp:45-50)
 //   u16  = (bits >> (16 * (idx & 3))) & 0xffff
 //   keep = u16 >= dropout_threshold16(p)          kept values are scaled by 1 / (1 - p)
+// site_seed itself is derived with the reference's mix64 pattern (see site_seed() below).
 
 #include <cmath>
 #include <cstdint>
@@ -24,8 +26,15 @@ inline std::uint32_t dropout_threshold16(double p) {
   return static_cast<std::uint32_t>(std::llround(p * 65536.0));
 }
 
+inline constexpr std::uint64_t kSplitMixGamma = 0x9e3779b97f4a7c15ull;
+
+/// 64 random bits for the group of 4 elements containing idx.
+CURATOR_HD inline constexpr std::uint64_t dropout_bits(std::uint64_t site_seed, std::uint64_t group) {
+  return splitmix64(site_seed + group * kSplitMixGamma);
+}
+
 CURATOR_HD inline constexpr bool dropout_keep(std::uint64_t site_seed, std::uint64_t idx, std::uint32_t thresh16) {
-  const std::uint64_t bits = mix64(site_seed, idx >> 2);
+  const std::uint64_t bits = dropout_bits(site_seed, idx >> 2);
   const std::uint32_t u16 = static_cast<std::uint32_t>((bits >> (16u * static_cast<unsigned>(idx & 3u))) & 0xffffu);
   return u16 >= thresh16;
 }

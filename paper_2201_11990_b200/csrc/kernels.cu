@@ -30,6 +30,19 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
     f[2 * j + 1] = p.y;
   }
 }
+// bf16x8 unpack the compiler may not CSE across passes (re-unpacking costs 8 ALU ops; keeping the
+// floats costs 8 registers per vector).
+__device__ __forceinline__ void unpack8_v(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t lo, hi;
+    asm volatile("shl.b32 %0, %2, 16; and.b32 %1, %2, 0xffff0000;" : "=r"(lo), "=r"(hi) : "r"(w[j]));
+    f[2 * j] = __uint_as_float(lo);
+    f[2 * j + 1] = __uint_as_float(hi);
+  }
+}
+
 __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   uint32_t w[4];
 #pragma unroll
@@ -62,13 +75,14 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return warp_sum(t);
 }
 
-// Drop mask for 8 consecutive elements starting at idx (idx % 4 == 0): two mix64 groups.
+// Drop mask for 8 consecutive elements starting at idx (idx % 4 == 0): two SplitMix64 groups
+// (include/curator/dropout.hpp).
 __device__ __forceinline__ uint32_t keep_mask8(uint64_t seed, uint64_t idx, uint32_t thresh16) {
   if (thresh16 == 0) return 0xffu;
   uint32_t m = 0;
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
-    const uint64_t bits = curator::mix64(seed, (idx >> 2) + g);
+    const uint64_t bits = curator::dropout_bits(seed, (idx >> 2) + g);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (((bits >> (16 * q)) & 0xffffu) >= thresh16) m |= 1u << (4 * g + q);
@@ -77,24 +91,29 @@ __device__ __forceinline__ uint32_t keep_mask8(uint64_t seed, uint64_t idx, uint
 }
 
 // ------------------------------------------------------------------ LayerNorm
+// One CTA per row; the row stays in registers as packed bf16 (4 regs per 8 elements) and is
+// re-unpacked in each pass (unpack8_v), keeping ~half the registers of an fp32 copy.
 template <int VPT>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const uint4* __restrict__ x, const uint4* __restrict__ gamma,
+__global__ void __launch_bounds__(1024) ln_fwd_kernel(const uint4* __restrict__ x, const uint4* __restrict__ gamma,
                                                      const uint4* __restrict__ beta, uint4* __restrict__ y,
                                                      float* __restrict__ mean, float* __restrict__ rstd, int nvec,
                                                      float inv_h, float eps) {
   __shared__ float red[32];
   const size_t row = blockIdx.x;
   const uint4* xr = x + row * nvec;
-  float v[VPT][8];
-  float s = 0.f;
+  uint4 raw[VPT];
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int idx = i * blockDim.x + threadIdx.x;
-    if (idx < nvec) {
-      unpack8(xr[idx], v[i]);
+    raw[i] = idx < nvec ? xr[idx] : make_uint4(0, 0, 0, 0);  // zero bf16 = 0.0: neutral for the sum
+  }
+  float s = 0.f;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) s += v[i][j];
-    }
+  for (int i = 0; i < VPT; ++i) {
+    float v[8];
+    unpack8_v(raw[i], v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[j];
   }
   const float mu = block_sum(s, red) * inv_h;
   float sq = 0.f;
@@ -102,9 +121,11 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const uint4* __restrict__ x
   for (int i = 0; i < VPT; ++i) {
     const int idx = i * blockDim.x + threadIdx.x;
     if (idx < nvec) {
+      float v[8];
+      unpack8_v(raw[i], v);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float d = v[i][j] - mu;
+        const float d = v[j] - mu;
         sq += d * d;
       }
     }
@@ -114,11 +135,12 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const uint4* __restrict__ x
   for (int i = 0; i < VPT; ++i) {
     const int idx = i * blockDim.x + threadIdx.x;
     if (idx < nvec) {
-      float g[8], b[8], o[8];
+      float v[8], g[8], b[8], o[8];
+      unpack8_v(raw[i], v);
       unpack8(gamma[idx], g);
       unpack8(beta[idx], b);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mu) * rs * g[j] + b[j];
+      for (int j = 0; j < 8; ++j) o[j] = (v[j] - mu) * rs * g[j] + b[j];
       y[row * nvec + idx] = pack8(o);
     }
   }
@@ -129,29 +151,35 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const uint4* __restrict__ x
 }
 
 template <int VPT>
-__global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ x,
+__global__ void __launch_bounds__(1024) ln_bwd_dx_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ x,
                                                         const uint4* __restrict__ gamma, const float* __restrict__ mean,
                                                         const float* __restrict__ rstd, const uint4* __restrict__ resid,
                                                         uint4* __restrict__ dx, int nvec, float inv_h) {
   __shared__ float red[32];
   const size_t row = blockIdx.x;
   const float mu = mean[row], rs = rstd[row];
-  float g[VPT][8], xh[VPT][8];
+  uint4 rdy[VPT], rx[VPT];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int idx = i * blockDim.x + threadIdx.x;
+    const bool in = idx < nvec;
+    rdy[i] = in ? dy[row * nvec + idx] : make_uint4(0, 0, 0, 0);
+    rx[i] = in ? x[row * nvec + idx] : make_uint4(0, 0, 0, 0);
+  }
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int idx = i * blockDim.x + threadIdx.x;
     if (idx < nvec) {
       float d[8], xv[8], gm[8];
-      unpack8(dy[row * nvec + idx], d);
-      unpack8(x[row * nvec + idx], xv);
+      unpack8_v(rdy[i], d);
+      unpack8_v(rx[i], xv);
       unpack8(gamma[idx], gm);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        xh[i][j] = (xv[j] - mu) * rs;
-        g[i][j] = d[j] * gm[j];
-        s1 += g[i][j];
-        s2 += g[i][j] * xh[i][j];
+        const float g = d[j] * gm[j];
+        s1 += g;
+        s2 += g * ((xv[j] - mu) * rs);
       }
     }
   }
@@ -161,9 +189,12 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const uint4* __restrict_
   for (int i = 0; i < VPT; ++i) {
     const int idx = i * blockDim.x + threadIdx.x;
     if (idx < nvec) {
-      float o[8];
+      float d[8], xv[8], gm[8], o[8];
+      unpack8_v(rdy[i], d);
+      unpack8_v(rx[i], xv);
+      unpack8(gamma[idx], gm);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = rs * (g[i][j] - m1 - xh[i][j] * m2);
+      for (int j = 0; j < 8; ++j) o[j] = rs * (d[j] * gm[j] - m1 - (xv[j] - mu) * rs * m2);
       if (resid != nullptr) {
         float r[8];
         unpack8(resid[row * nvec + idx], r);
@@ -286,6 +317,19 @@ __global__ void bias_dropout_residual_kernel(const uint4* __restrict__ z, const 
 }
 
 // ------------------------------------------------------------------ causal softmax
+// One warp per score row; the row's bf16 vectors stay packed in registers (4 regs per 8 scores)
+// and are unpacked on the fly in each pass, which keeps the backward at ~half the registers of an
+// fp32 copy and lets 3-4 CTAs share an SM. exp is exp2 of log2e-prescaled values (one FFMA + MUFU).
+constexpr float kLog2e = 1.4426950408889634f;
+
+// exp2 that the compiler may not CSE across passes (volatile): recomputing it in the second pass is
+// cheaper than keeping a row's worth of fp32 probabilities live in registers.
+__device__ __forceinline__ float ex2_recompute(float x) {
+  float y;
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 template <int VPL>
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(const uint4* __restrict__ S, uint4* __restrict__ P,
                                                           float* __restrict__ lse, int rows_total, int seq,
@@ -299,50 +343,59 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const uint4* __restric
   const uint4* srow = S + (size_t)warp * nvec_row;
   uint4* prow = P + (size_t)warp * nvec_row;
   const int nvalid = i + 1, nvec = (nvalid + 7) >> 3;
-  float x[VPL][8];
+  uint4 raw[VPL];
   float mx = -INFINITY;
 #pragma unroll
   for (int t = 0; t < VPL; ++t) {
     const int v = lane + 32 * t;
-    if (v < nvec) {
-      unpack8(srow[v], x[t]);
+    raw[t] = v < nvec ? srow[v] : make_uint4(0, 0, 0, 0);
+  }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (v * 8 + j >= nvalid) x[t][j] = -INFINITY;
-        mx = fmaxf(mx, x[t][j]);
-      }
+  for (int t = 0; t < VPL; ++t) {
+    const int v = lane + 32 * t;
+    if (v < nvec) {
+      float x[8];
+      unpack8_v(raw[t], x);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (v * 8 + j < nvalid) mx = fmaxf(mx, x[j]);
     }
   }
   mx = warp_max(mx);
+  const float mx2 = mx * kLog2e;
   float sum = 0.f;
 #pragma unroll
   for (int t = 0; t < VPL; ++t) {
     const int v = lane + 32 * t;
     if (v < nvec) {
+      float x[8];
+      unpack8_v(raw[t], x);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        x[t][j] = __expf(x[t][j] - mx);
-        sum += x[t][j];
-      }
+      for (int j = 0; j < 8; ++j) sum += (v * 8 + j < nvalid) ? ex2_recompute(fmaf(x[j], kLog2e, -mx2)) : 0.f;
     }
   }
   sum = warp_sum(sum);
-  const float inv = 1.f / sum;
+  const float l = mx + logf(sum);
+  const float l2 = l * kLog2e;
   const uint64_t base_idx = ((uint64_t)(head_base + bh) * seq + i) * (uint64_t)seq;
 #pragma unroll
   for (int t = 0; t < VPL; ++t) {
     const int v = lane + 32 * t;
     if (v < nvec) {
       const uint32_t keep = keep_mask8(seed, base_idx + v * 8, thresh16);
-      float o[8];
+      float x[8], o[8];
+      unpack8_v(raw[t], x);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = ((keep >> j) & 1u) ? x[t][j] * inv * scale : 0.f;
+      for (int j = 0; j < 8; ++j) {
+        const bool ok = (v * 8 + j < nvalid) && ((keep >> j) & 1u);
+        o[j] = ok ? ex2_recompute(fmaf(x[j], kLog2e, -l2)) * scale : 0.f;
+      }
       prow[v] = pack8(o);
     }
   }
   const int zend = min(seq, (i / 256 + 1) * 256) >> 3;
   for (int v = nvec + lane; v < zend; v += 32) prow[v] = make_uint4(0, 0, 0, 0);
-  if (lane == 0) lse[warp] = mx + logf(sum);
+  if (lane == 0) lse[warp] = l;
 }
 
 template <int VPL>
@@ -358,35 +411,49 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const uint4* __restric
   const uint4* srow = S + (size_t)warp * nvec_row;
   uint4* drow = dP + (size_t)warp * nvec_row;
   const int nvalid = i + 1, nvec = (nvalid + 7) >> 3;
-  const float l = lse[warp];
+  const float l2 = lse[warp] * kLog2e;
   const uint64_t base_idx = ((uint64_t)(head_base + bh) * seq + i) * (uint64_t)seq;
-  float y[VPL][8], g[VPL][8];
+  uint4 rs[VPL], rg[VPL];
+  uint32_t keep[VPL];
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    const int v = lane + 32 * t;
+    const bool in = v < nvec;
+    rs[t] = in ? srow[v] : make_uint4(0, 0, 0, 0);
+    rg[t] = in ? drow[v] : make_uint4(0, 0, 0, 0);
+  }
   float dot = 0.f;
 #pragma unroll
   for (int t = 0; t < VPL; ++t) {
     const int v = lane + 32 * t;
+    keep[t] = 0;
     if (v < nvec) {
-      float sv[8];
-      unpack8(srow[v], sv);
-      unpack8(drow[v], g[t]);
-      const uint32_t keep = keep_mask8(seed, base_idx + v * 8, thresh16);
+      uint32_t k = keep_mask8(seed, base_idx + v * 8, thresh16);
+      if (v * 8 + 8 > nvalid) k &= (1u << (nvalid - v * 8)) - 1u;  // causal tail of the row
+      keep[t] = k;
+      float sv[8], g[8];
+      unpack8_v(rs[t], sv);
+      unpack8_v(rg[t], g);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const bool valid = v * 8 + j < nvalid;
-        y[t][j] = valid ? __expf(sv[j] - l) : 0.f;
-        g[t][j] = (valid && ((keep >> j) & 1u)) ? g[t][j] * scale : 0.f;
-        dot += y[t][j] * g[t][j];
-      }
+      for (int j = 0; j < 8; ++j)
+        if ((k >> j) & 1u) dot += ex2_recompute(fmaf(sv[j], kLog2e, -l2)) * g[j];
     }
   }
-  dot = warp_sum(dot);
+  dot = warp_sum(dot) * scale;
 #pragma unroll
   for (int t = 0; t < VPL; ++t) {
     const int v = lane + 32 * t;
     if (v < nvec) {
-      float o[8];
+      float sv[8], g[8], o[8];
+      unpack8_v(rs[t], sv);
+      unpack8_v(rg[t], g);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = alpha * y[t][j] * (g[t][j] - dot);
+      for (int j = 0; j < 8; ++j) {
+        const bool valid = v * 8 + j < nvalid;
+        const float y = valid ? ex2_recompute(fmaf(sv[j], kLog2e, -l2)) : 0.f;
+        const float gj = ((keep[t] >> j) & 1u) ? g[j] * scale : 0.f;
+        o[j] = alpha * y * (gj - dot);
+      }
       drow[v] = pack8(o);
     }
   }
@@ -458,10 +525,12 @@ int grid_for(long long work, int block) {
     }                                       \
   } while (0)
 
+// Threads per row: enough that each holds <= 2 vectors (16 elements) up to h = 16384 (<= 1024
+// threads), so the row fits in a few registers per thread.
 static void row_launch_shape(int h, int& threads, int& vpt) {
   const int nvec = h / 8;
-  threads = ((nvec + 31) / 32) * 32;
-  if (threads > 256) threads = 256;
+  threads = (((nvec + 1) / 2 + 31) / 32) * 32;
+  if (threads > 1024) threads = 1024;
   vpt = (nvec + threads - 1) / threads;
 }
 

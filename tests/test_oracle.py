@@ -24,11 +24,11 @@ def splitmix64(z):
 
 
 def keep_mask(site, n, p):
-    """Vectorised restatement of include/curator/dropout.hpp (16-bit uniforms, 4 per mix64)."""
+    """Vectorised restatement of include/curator/dropout.hpp (16-bit uniforms, 4 per SplitMix64 output)."""
     th = 0 if p <= 0 else int(round(p * 65536))
     idx = np.arange(n, dtype=np.uint64)
     with np.errstate(over="ignore"):
-        bits = splitmix64(np.uint64(site) ^ splitmix64(idx >> np.uint64(2)))
+        bits = splitmix64((np.uint64(site) + (idx >> np.uint64(2)) * np.uint64(0x9E3779B97F4A7C15)) & M64)
     u16 = (bits >> (np.uint64(16) * (idx & np.uint64(3)))) & np.uint64(0xFFFF)
     return u16 >= np.uint64(th)
 
