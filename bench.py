@@ -274,6 +274,23 @@ def run_ours(args, L: dict) -> None:
         dist.all_reduce(tot)
     h2d_all, d2h_all = int(tot[0].item()), int(tot[1].item())
 
+    op_breakdown = None
+    if args.op_timing:
+        lib().mt_ctx_op_timing(ctx._h, 1)
+        for _ in range(args.steps):
+            step_dev()
+        buf = C.create_string_buffer(1 << 16)
+        n = C.c_int64()
+        lib().mt_ctx_op_timing_read(ctx._h, buf, len(buf), C.byref(n))
+        lib().mt_ctx_op_timing(ctx._h, 0)
+        op_breakdown = {}
+        for line in buf.value.decode().splitlines():
+            name, tot, cnt = line.split()
+            op_breakdown[name] = round(float(tot) / args.steps, 4)
+        if world > 1:
+            allb = [None] * world
+            dist.all_gather_object(allb, op_breakdown)
+            op_breakdown = {f"rank{r}": b for r, b in enumerate(allb)}
     clocks = clk.summary()
     pk = peaks()
     tokens = L["b"] * L["seq"] * MB * L["dp"]
@@ -323,6 +340,7 @@ def run_ours(args, L: dict) -> None:
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,
+            **({"op_breakdown_ms": op_breakdown} if op_breakdown is not None else {}),
         }
         print(json.dumps(line), flush=True)
     stage.close()
@@ -339,6 +357,9 @@ def main() -> None:
     ap.add_argument("--config", default="gpt3", choices=["gpt3", "mtnlg", "pp", "3d", "tiny"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
+    ap.add_argument("--op-timing", action="store_true",
+                    help="after the timed region, run the steps again with per-op event marks and report the "
+                         "per-op breakdown (ms per step) in the JSON line as op_breakdown_ms")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     L = layout_for(args.config, args.gpus)

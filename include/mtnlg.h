@@ -122,6 +122,10 @@ int mt_ctx_placement(const mt_ctx* ctx, mt_rank_placement* out);
  * events around each launch). _read synchronises, returns the summed kernel time, summed
  * algorithmic FLOPs and launch count since enabling / the last read, and resets. */
 int mt_ctx_gemm_timing(mt_ctx* ctx, int32_t enable);
+/* Per-op timing of the layers' forward/backward (stream-ordered event marks between ops; adds
+ * ~40 event records per layer call). _read renders "op total_ms count" lines (NUL-terminated). */
+int mt_ctx_op_timing(mt_ctx* ctx, int32_t enable);
+int mt_ctx_op_timing_read(mt_ctx* ctx, char* out, int64_t cap, int64_t* len);
 int mt_ctx_gemm_timing_read(mt_ctx* ctx, double* total_ms, double* total_flops, int64_t* launches);
 
 int mt_layer_create(mt_ctx* ctx, const mt_layer_desc* d, mt_layer** out);

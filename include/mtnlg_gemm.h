@@ -54,7 +54,8 @@ typedef struct mt_gemm_args {
   const void* bias; /* bf16[n] or NULL */
   void* aux;        /* bf16, ld = ld_aux (pre-activation for the GeLU epilogues) */
   int64_t ld_aux;
-  int32_t block_n;  /* 0 = auto; else 64/128/160/256 */
+  int32_t block_n;  /* 0 = auto; else 64/128/160/192/256 */
+  int32_t max_ctas; /* 0 = one CTA per SM; else cap (leaves SMs free for a concurrent collective) */
 } mt_gemm_args;
 
 /* Launches on `stream` (a cudaStream_t). Returns 0 on success, 1 on bad arguments, 2 on CUDA error. */

@@ -21,6 +21,7 @@ class GemmArgs(C.Structure):
         ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64), ("batch", C.c_int64),
         ("alpha", C.c_float), ("epilogue", C.c_int32), ("causal", C.c_int32),
         ("bias", C.c_void_p), ("aux", C.c_void_p), ("ld_aux", C.c_int64), ("block_n", C.c_int32),
+        ("max_ctas", C.c_int32),
     ]
 
 
@@ -95,6 +96,8 @@ _SIGS = {
     "mt_ctx_placement": (C.c_int, [P, C.POINTER(RankPlacement)]),
     "mt_ctx_gemm_timing": (C.c_int, [P, I32]),
     "mt_ctx_gemm_timing_read": (C.c_int, [P, PF64, PF64, PI64]),
+    "mt_ctx_op_timing": (C.c_int, [P, I32]),
+    "mt_ctx_op_timing_read": (C.c_int, [P, C.c_char_p, I64, PI64]),
     "mt_layer_create": (C.c_int, [P, C.POINTER(LayerDesc), C.POINTER(P)]),
     "mt_layer_destroy": (C.c_int, [P]),
     "mt_layer_init_params": (C.c_int, [P, P]),

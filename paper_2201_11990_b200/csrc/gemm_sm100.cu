@@ -514,11 +514,13 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
     attr_set = true;
   }
   if (!kPair) {
-    const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
+    const int cap = a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms();
+    const int grid = p.total_tiles < cap ? p.total_tiles : cap;
     kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, md, maux, p);
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
   }
-  const int pairs = std::min(p.total_tiles, num_sms() / 2);
+  const int cap = a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms();
+  const int pairs = std::max(1, std::min(p.total_tiles, cap / 2));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(kThreads);

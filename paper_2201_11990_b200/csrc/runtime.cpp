@@ -11,7 +11,9 @@
 //             sums, and the TP all-reduce of the LN inputs' gradients ("f" operator).
 #include "runtime.hpp"
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -116,6 +118,10 @@ struct Gemm {
   }
   Gemm& causal(int c) {
     a.causal = c;
+    return *this;
+  }
+  Gemm& max_ctas(int n) {
+    a.max_ctas = n;
     return *this;
   }
   // Algorithmic FLOPs of this call (causal contractions count the lower triangle only).
@@ -228,9 +234,13 @@ extern "C" int mt_ctx_create(int32_t device, mt_ctx** out) {
 extern "C" int mt_ctx_destroy(mt_ctx* c) {
   return guarded([&] {
     if (!c) return;
-    for (ncclComm_t* cm : {&c->tp, &c->pp, &c->dp, &c->world})
+    for (ncclComm_t* cm : {&c->tp_side, &c->tp, &c->pp, &c->dp, &c->world})
       if (*cm) ncclCommDestroy(*cm);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (auto& m : c->marks) cudaEventDestroy(m.second);
+    if (c->comm) cudaStreamDestroy(c->comm);
+    if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+    if (c->ev_done) cudaEventDestroy(c->ev_done);
     delete c;
   });
 }
@@ -273,9 +283,24 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
     const int tp_color = me.pipeline * p.data + me.data;
     const int pp_color = me.data * p.tensor + me.tensor;
     const int dp_color = me.pipeline * p.tensor + me.tensor;
+    // Two communicators over the TP group: `tp` (all channels) for the critical-path forward
+    // all-reduces, `tp_side` capped at comm_sms CTAs for the backward all-reduces that run beside a
+    // wgrad GEMM launched on the remaining SMs.
     check_nccl(ncclCommSplit(c->world, tp_color, me.tensor, &c->tp, nullptr), "ncclCommSplit(tp)");
+    if (const char* e = getenv("MT_COMM_SMS")) c->comm_sms = atoi(e);
+    ncclConfig_t side_cfg = NCCL_CONFIG_INITIALIZER;
+    side_cfg.maxCTAs = std::max(1, c->comm_sms);
+    side_cfg.minCTAs = std::min(side_cfg.maxCTAs, 4);
+    check_nccl(ncclCommSplit(c->world, tp_color, me.tensor, &c->tp_side, &side_cfg), "ncclCommSplit(tp_side)");
     check_nccl(ncclCommSplit(c->world, pp_color, me.pipeline, &c->pp, nullptr), "ncclCommSplit(pp)");
     check_nccl(ncclCommSplit(c->world, dp_color, me.data, &c->dp, nullptr), "ncclCommSplit(dp)");
+    if (p.tensor > 1) {
+      int lo = 0, hi = 0;
+      check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+      check_cuda(cudaStreamCreateWithPriority(&c->comm, cudaStreamNonBlocking, hi), "comm stream");
+      check_cuda(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming), "event");
+      check_cuda(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming), "event");
+    }
   });
 }
 
@@ -304,6 +329,41 @@ extern "C" int mt_ctx_gemm_timing_read(mt_ctx* c, double* total_ms, double* tota
     if (launches) *launches = static_cast<int64_t>(c->ev_flops.size());
     c->ev_used = 0;
     c->ev_flops.clear();
+  });
+}
+
+extern "C" int mt_ctx_op_timing(mt_ctx* c, int32_t enable) {
+  return guarded([&] {
+    if (!c) throw std::invalid_argument("null ctx");
+    c->op_timing = enable != 0;
+    c->marks_used = 0;
+    c->op_acc.clear();
+  });
+}
+
+// Accumulates the marks recorded so far into per-op totals, then renders "label total_ms count" lines.
+extern "C" int mt_ctx_op_timing_read(mt_ctx* c, char* out, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    if (!c) throw std::invalid_argument("null ctx");
+    check_cuda(cudaDeviceSynchronize(), "sync");
+    for (size_t i = 1; i < c->marks_used; ++i) {
+      if (std::string(c->marks[i].first) == "begin") continue;
+      float t = 0;
+      check_cuda(cudaEventElapsedTime(&t, c->marks[i - 1].second, c->marks[i].second), "elapsed");
+      auto& a = c->op_acc[c->marks[i].first];
+      a.first += t;
+      a.second += 1;
+    }
+    c->marks_used = 0;
+    std::string text;
+    for (const auto& [k, v] : c->op_acc)
+      text += k + " " + std::to_string(v.first) + " " + std::to_string(v.second) + "\n";
+    *len = static_cast<int64_t>(text.size());
+    if (out && cap > 0) {
+      const int64_t k = std::min<int64_t>(cap - 1, *len);
+      std::memcpy(out, text.data(), static_cast<size_t>(k));
+      out[k] = '\0';
+    }
   });
 }
 
@@ -482,6 +542,35 @@ extern "C" int mt_layer_launch_counts(const mt_layer* l, int32_t* f, int32_t* b)
 // =========================================================================== forward
 namespace {
 
+// TP all-reduce of `buf` on the context's comm stream, ordered after the work already queued on
+// `st`; returns the CTA cap for GEMMs that overlap it (0 when there is nothing to overlap).
+int tp_allreduce_async(mt_ctx* c, void* buf, int64_t n, cudaStream_t st, const char* what) {
+  check_cuda(cudaEventRecord(c->ev_ready, st), "cudaEventRecord");
+  check_cuda(cudaStreamWaitEvent(c->comm, c->ev_ready, 0), "cudaStreamWaitEvent");
+  check_nccl(ncclAllReduce(buf, buf, n, ncclBfloat16, ncclSum, c->tp_side, c->comm), what);
+  check_cuda(cudaEventRecord(c->ev_done, c->comm), "cudaEventRecord");
+  int sms = 0;
+  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device), "attr");
+  return std::max(2, sms - c->comm_sms);
+}
+void tp_allreduce_join(mt_ctx* c, cudaStream_t st) {
+  check_cuda(cudaStreamWaitEvent(st, c->ev_done, 0), "cudaStreamWaitEvent");
+}
+
+// Stream-ordered mark for per-op timing; the time between consecutive marks is attributed to the
+// op named by the later mark. No-op unless the context has op timing enabled.
+void mark(mt_ctx* c, cudaStream_t st, const char* label) {
+  if (!c->op_timing) return;
+  if (c->marks_used == c->marks.size()) {
+    cudaEvent_t e;
+    check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+    c->marks.push_back({label, e});
+  }
+  c->marks[c->marks_used].first = label;
+  check_cuda(cudaEventRecord(c->marks[c->marks_used].second, st), "cudaEventRecord");
+  ++c->marks_used;
+}
+
 mt_layer::Saved& acquire_slot(mt_layer* l, uint32_t mb) {
   if (l->saved.count(mb)) throw std::invalid_argument("microbatch already has saved activations");
   std::unique_ptr<mt_layer::Saved> sv;
@@ -528,13 +617,16 @@ void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_
   const uint64_t site_out1 = key_of(d.seed, "attn.out", d.layer_index, mb);
   const uint64_t site_out2 = key_of(d.seed, "mlp.out", d.layer_index, mb);
   void* z = c->scratch_h[0].ptr;
+  mark(c, st, "begin");
 
   ln_fwd(x, l->param_ptr(MT_P_LN1_GAMMA), l->param_ptr(MT_P_LN1_BETA), sv.ln1.ptr, mean1, rstd1, (int)M, (int)h,
          d.ln_eps, st);
   ++n;
+  mark(c, st, "fwd.ln1");
   Gemm(sv.ln1.ptr, h, false, l->param_ptr(MT_P_QKV_W), h, false, sv.qkv.ptr, ld3, M, ld3, h)
       .bias(l->param_ptr(MT_P_QKV_B))
       .run(st, n);
+  mark(c, st, "fwd.qkv_gemm");
   const float alpha = 1.f / std::sqrt((float)hd);
   for (int64_t bb = 0; bb < d.micro_batch; ++bb) {
     const uint16_t* q = sv.qkv.as<uint16_t>() + bb * s * ld3;
@@ -546,36 +638,47 @@ void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_
         .alpha(alpha)
         .causal(MT_CAUSAL_SKIP_UPPER_TILES)
         .run(st, n);
+    mark(c, st, "fwd.attn_s_gemm");
     const long long head_base = bb * d.heads + int64_t{d.tp_rank} * Hl;
     softmax_fwd(S, P, lse, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, st);
     ++n;
+    mark(c, st, "fwd.softmax");
     Gemm(P, s, false, q + 2 * hd, ld3, true, sv.ctx.as<uint16_t>() + bb * s * hl, hl, s, hd, s)
         .batched(Hl, s * s, 3 * hd, hd)
         .causal(MT_CAUSAL_K_LE_M)
         .run(st, n);
+    mark(c, st, "fwd.attn_pv_gemm");
   }
   Gemm(sv.ctx.ptr, hl, false, l->param_ptr(MT_P_PROJ_W), hl, false, z, h, M, h, hl).run(st, n);
+  mark(c, st, "fwd.proj_gemm");
   if (d.tp_size > 1) {
     check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(attn.out)");
     ++n;
+    mark(c, st, "fwd.tp_allreduce");
   }
   bias_dropout_residual(z, l->param_ptr(MT_P_PROJ_B), x, sv.x1.ptr, (int)M, (int)h, site_out1, th_h, scale_h, st);
   ++n;
+  mark(c, st, "fwd.bias_dropout_residual");
   ln_fwd(sv.x1.ptr, l->param_ptr(MT_P_LN2_GAMMA), l->param_ptr(MT_P_LN2_BETA), sv.ln2.ptr, mean2, rstd2, (int)M,
          (int)h, d.ln_eps, st);
   ++n;
+  mark(c, st, "fwd.ln2");
   Gemm(sv.ln2.ptr, h, false, l->param_ptr(MT_P_FC1_W), h, false, sv.act.ptr, ffl, M, ffl, h)
       .epi(MT_EPI_BIAS_GELU)
       .bias(l->param_ptr(MT_P_FC1_B))
       .aux(sv.pre.ptr, ffl)
       .run(st, n);
+  mark(c, st, "fwd.fc1_gemm");
   Gemm(sv.act.ptr, ffl, false, l->param_ptr(MT_P_FC2_W), ffl, false, z, h, M, h, ffl).run(st, n);
+  mark(c, st, "fwd.fc2_gemm");
   if (d.tp_size > 1) {
     check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(mlp.out)");
     ++n;
+    mark(c, st, "fwd.tp_allreduce");
   }
   bias_dropout_residual(z, l->param_ptr(MT_P_FC2_B), sv.x1.ptr, y, (int)M, (int)h, site_out2, th_h, scale_h, st);
   ++n;
+  mark(c, st, "fwd.bias_dropout_residual");
   check_cuda(cudaGetLastError(), "layer forward launch");
   l->fwd_launches = n;
 }
@@ -612,32 +715,47 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
   l->grads_fresh = false;
   const int wg_epi = acc ? MT_EPI_ACCUM_F32 : MT_EPI_STORE_F32;
 
+  mark(c, st, "begin");
   // ---- MLP block
   dropout_bwd_bias_grad(dy, dm, l->grad_ptr(MT_P_FC2_B), (int)M, (int)h, site_out2, th_h, scale_h, ws, acc, st);
   n += 2;
+  mark(c, st, "bwd.dropout_bias_grad");
   Gemm(dm, h, false, l->param_ptr(MT_P_FC2_W), ffl, true, dpre, ffl, M, ffl, h)
       .epi(MT_EPI_GELU_BWD)
       .aux(sv.pre.ptr, ffl)
       .run(st, n);
+  mark(c, st, "bwd.fc2_dgrad_gelu");
   Gemm(dm, h, true, sv.act.ptr, ffl, true, l->grad_ptr(MT_P_FC2_W), ffl, h, ffl, M).epi(wg_epi).run(st, n);
-  bias_grad(dpre, l->grad_ptr(MT_P_FC1_B), (int)M, (int)ffl, ffl, ws, acc, st);
-  n += 2;
-  Gemm(dpre, ffl, true, sv.ln2.ptr, h, true, l->grad_ptr(MT_P_FC1_W), h, ffl, h, M).epi(wg_epi).run(st, n);
+  mark(c, st, "bwd.fc2_wgrad");
+  // dgrad first so its TP all-reduce ("f") overlaps the independent wgrad and bias-grad work
   Gemm(dpre, ffl, false, l->param_ptr(MT_P_FC1_W), h, true, dln, h, M, h, ffl).run(st, n);
+  mark(c, st, "bwd.fc1_dgrad");
+  int cap = 0;
   if (d.tp_size > 1) {
-    check_nccl(ncclAllReduce(dln, dln, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(ln2.grad)");
+    cap = tp_allreduce_async(c, dln, M * h, st, "ncclAllReduce(ln2.grad)");
     ++n;
   }
+  bias_grad(dpre, l->grad_ptr(MT_P_FC1_B), (int)M, (int)ffl, ffl, ws, acc, st);
+  n += 2;
+  mark(c, st, "bwd.bias_grad");
+  Gemm(dpre, ffl, true, sv.ln2.ptr, h, true, l->grad_ptr(MT_P_FC1_W), h, ffl, h, M).epi(wg_epi).max_ctas(cap).run(st, n);
+  mark(c, st, "bwd.fc1_wgrad");
+  if (d.tp_size > 1) tp_allreduce_join(c, st);
+  mark(c, st, "bwd.tp_allreduce_wait");
   ln_bwd_dx(dln, sv.x1.ptr, l->param_ptr(MT_P_LN2_GAMMA), mean2, rstd2, dy, dx1, (int)M, (int)h, st);
   ln_bwd_params(dln, sv.x1.ptr, mean2, rstd2, l->grad_ptr(MT_P_LN2_GAMMA), l->grad_ptr(MT_P_LN2_BETA), (int)M, (int)h,
                 ws, acc, st);
   n += 3;
+  mark(c, st, "bwd.ln_bwd");
   // ---- attention block
   void* dz = dm;
   dropout_bwd_bias_grad(dx1, dz, l->grad_ptr(MT_P_PROJ_B), (int)M, (int)h, site_out1, th_h, scale_h, ws, acc, st);
   n += 2;
+  mark(c, st, "bwd.dropout_bias_grad");
   Gemm(dz, h, false, l->param_ptr(MT_P_PROJ_W), hl, true, dctx, hl, M, hl, h).run(st, n);
+  mark(c, st, "bwd.proj_dgrad");
   Gemm(dz, h, true, sv.ctx.ptr, hl, true, l->grad_ptr(MT_P_PROJ_W), hl, h, hl, M).epi(wg_epi).run(st, n);
+  mark(c, st, "bwd.proj_wgrad");
   const float alpha = 1.f / std::sqrt((float)hd);
   for (int64_t bb = 0; bb < d.micro_batch; ++bb) {
     const uint16_t* q = sv.qkv.as<uint16_t>() + bb * s * ld3;
@@ -651,14 +769,17 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
         .batched(Hl, hd, 3 * hd, s * s)
         .causal(MT_CAUSAL_SKIP_UPPER_TILES)
         .run(st, n);
+    mark(c, st, "bwd.attn_dp_gemm");
     // dV_h = P_h^T dctx_h
     Gemm(P, s, true, dc, hl, true, dq + 2 * hd, ld3, s, hd, s)
         .batched(Hl, s * s, hd, 3 * hd)
         .causal(MT_CAUSAL_K_GE_M)
         .run(st, n);
+    mark(c, st, "bwd.attn_dv_gemm");
     const long long head_base = bb * d.heads + int64_t{d.tp_rank} * Hl;
     softmax_bwd(S, lse, dP, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, alpha, st);
     ++n;
+    mark(c, st, "bwd.softmax");
     // dQ_h = dS_h K_h ; dK_h = dS_h^T Q_h   (dS already carries the 1/sqrt(d) factor)
     Gemm(dP, s, false, q + hd, ld3, true, dq, ld3, s, hd, s)
         .batched(Hl, s * s, 3 * hd, 3 * hd)
@@ -668,19 +789,27 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
         .batched(Hl, s * s, 3 * hd, 3 * hd)
         .causal(MT_CAUSAL_K_GE_M)
         .run(st, n);
+    mark(c, st, "bwd.attn_dq_dk_gemm");
+  }
+  Gemm(dqkv, ld3, false, l->param_ptr(MT_P_QKV_W), h, true, dln, h, M, h, ld3).run(st, n);
+  mark(c, st, "bwd.qkv_dgrad");
+  cap = 0;
+  if (d.tp_size > 1) {
+    cap = tp_allreduce_async(c, dln, M * h, st, "ncclAllReduce(ln1.grad)");
+    ++n;
   }
   bias_grad(dqkv, l->grad_ptr(MT_P_QKV_B), (int)M, (int)ld3, ld3, ws, acc, st);
   n += 2;
-  Gemm(dqkv, ld3, true, sv.ln1.ptr, h, true, l->grad_ptr(MT_P_QKV_W), h, ld3, h, M).epi(wg_epi).run(st, n);
-  Gemm(dqkv, ld3, false, l->param_ptr(MT_P_QKV_W), h, true, dln, h, M, h, ld3).run(st, n);
-  if (d.tp_size > 1) {
-    check_nccl(ncclAllReduce(dln, dln, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(ln1.grad)");
-    ++n;
-  }
+  mark(c, st, "bwd.bias_grad");
+  Gemm(dqkv, ld3, true, sv.ln1.ptr, h, true, l->grad_ptr(MT_P_QKV_W), h, ld3, h, M).epi(wg_epi).max_ctas(cap).run(st, n);
+  mark(c, st, "bwd.qkv_wgrad");
+  if (d.tp_size > 1) tp_allreduce_join(c, st);
+  mark(c, st, "bwd.tp_allreduce_wait");
   ln_bwd_dx(dln, sv.x, l->param_ptr(MT_P_LN1_GAMMA), mean1, rstd1, dx1, dx, (int)M, (int)h, st);
   ln_bwd_params(dln, sv.x, mean1, rstd1, l->grad_ptr(MT_P_LN1_GAMMA), l->grad_ptr(MT_P_LN1_BETA), (int)M, (int)h, ws,
                 acc, st);
   n += 3;
+  mark(c, st, "bwd.ln_bwd");
   check_cuda(cudaGetLastError(), "layer backward launch");
   l->bwd_launches = n;
   l->free_slots.push_back(std::move(it->second));

@@ -53,6 +53,7 @@ struct mt_ctx {
   curator::ParallelConfig par;
   curator::RankPlacement place;
   ncclComm_t world = nullptr, tp = nullptr, pp = nullptr, dp = nullptr;
+  ncclComm_t tp_side = nullptr;  // same TP group, CTA-capped: collectives overlapped with GEMMs
   // scratch shared by all layers of this context (sized to the largest layer)
   mt::DeviceBuffer scratch_h[4];   // [M, h] bf16 temporaries
   mt::DeviceBuffer scratch_ffn;    // [M, ffn/t] bf16
@@ -60,6 +61,16 @@ struct mt_ctx {
   mt::DeviceBuffer scratch_qkv;    // [M, 3h/t] bf16
   mt::DeviceBuffer scratch_attn;   // [heads/t, s, s] bf16
   mt::DeviceBuffer scratch_ws;     // fp32 column-reduction workspace
+  // side stream for TP collectives overlapped with independent GEMMs (backward: the all-reduce of
+  // an LN-input gradient runs while the matching wgrad GEMM executes on SMs left free for NCCL)
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+  int comm_sms = 16;  // SMs kept free for the collective during an overlapped GEMM
+  // optional per-op timing (MT_OP_TIMING=1): stream-ordered marks between consecutive layer ops
+  bool op_timing = false;
+  std::vector<std::pair<const char*, cudaEvent_t>> marks;
+  size_t marks_used = 0;
+  std::map<std::string, std::pair<double, int>> op_acc;
   // optional per-GEMM CUDA-event timing (bench.py's live roofline measurement)
   bool gemm_timing = false;
   std::vector<cudaEvent_t> ev_pool;
