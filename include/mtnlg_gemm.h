@@ -56,7 +56,14 @@ typedef struct mt_gemm_args {
   int64_t ld_aux;
   int32_t block_n;  /* 0 = auto; else 64/128/160/192/256 */
   int32_t max_ctas; /* 0 = one CTA per SM; else cap (leaves SMs free for a concurrent collective) */
+  /* Optional zero-initialised device workspace enabling the split-K tail (the last, partial wave of
+   * tiles is split over k and reduced by the last-arriving split). The first 64 KB hold arrival
+   * counters, which the kernel leaves zeroed. NULL disables. MT_GEMM_WORKSPACE_BYTES suggests a size. */
+  void* workspace;
+  int64_t workspace_bytes;
 } mt_gemm_args;
+
+#define MT_GEMM_WORKSPACE_BYTES (64ll << 20)
 
 /* Launches on `stream` (a cudaStream_t). Returns 0 on success, 1 on bad arguments, 2 on CUDA error. */
 int mt_gemm(const mt_gemm_args* args, void* stream);

@@ -21,7 +21,7 @@ class GemmArgs(C.Structure):
         ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64), ("batch", C.c_int64),
         ("alpha", C.c_float), ("epilogue", C.c_int32), ("causal", C.c_int32),
         ("bias", C.c_void_p), ("aux", C.c_void_p), ("ld_aux", C.c_int64), ("block_n", C.c_int32),
-        ("max_ctas", C.c_int32),
+        ("max_ctas", C.c_int32), ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64),
     ]
 
 

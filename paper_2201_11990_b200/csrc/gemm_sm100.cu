@@ -42,6 +42,11 @@ struct GemmParams {
   const __nv_bfloat16* bias;
   __nv_bfloat16* aux;
   long long ld_aux;
+  // split-K tail: work items [0, full_tiles) are whole tiles; the remaining total_tiles - full_tiles
+  // tiles (fewer than one wave) are each split over `splits` k-ranges run by otherwise idle CTAs.
+  int full_tiles, splits, work_items;
+  float* split_ws;  // fp32 partial tiles [tail][split][rank][128 x BN]
+  int* split_cnt;   // arrival counters [tail][rank], self-resetting
 };
 
 // kPair: 2-CTA (cta_group::2) tiles of 256 x BN — each CTA of the pair holds 128 rows of A and
@@ -92,6 +97,37 @@ __device__ __forceinline__ void k_range(const GemmParams& p, int mb, int& kb0, i
     kb0 = (mb * BMT) / kBK;
   }
 }
+
+struct Work {
+  int b, mb, nb, kb0, kb1;
+  int split;  // -1: whole tile; else the split index of a tail tile
+  int tail;   // tail tile index (split items)
+};
+
+// Decodes work item w (identically in every role) into tile coordinates and its k-block range.
+template <int BN, int BMT>
+__device__ __forceinline__ bool get_work(const GemmParams& p, int w, Work& o) {
+  int t = w;
+  o.split = -1;
+  o.tail = 0;
+  if (w >= p.full_tiles) {
+    const int j = w - p.full_tiles;
+    o.tail = j / p.splits;
+    o.split = j - o.tail * p.splits;
+    t = p.full_tiles + o.tail;
+  }
+  tile_coords(p, t, o.b, o.mb, o.nb);
+  if (!tile_valid<BN, BMT>(p, o.mb, o.nb)) return false;
+  k_range<BMT>(p, o.mb, o.kb0, o.kb1);
+  if (o.split >= 0) {
+    const int a = o.kb0, len = o.kb1 - o.kb0;
+    o.kb0 = a + (len * o.split) / p.splits;
+    o.kb1 = a + (len * (o.split + 1)) / p.splits;
+  }
+  return true;
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // Epilogue of one 32-row x 32-column piece held by one warp (thread t = row t, r[j] = column j):
 // apply the fused epilogue, write the piece into a swizzled staging buffer and hand it to the TMA
@@ -153,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + C::kEpiBytes);
   // bars[0..S) full, bars[S..2S) empty, bars[2S..2S+2) tmem_full, bars[2S+2..2S+4) tmem_empty
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4);
+  volatile int* split_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -200,13 +237,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_a = !p.hints ? kEvictNormal : (p.n_fastest ? kEvictFirst : kEvictLast);
       const uint64_t pol_b = !p.hints ? kEvictNormal : (p.n_fastest ? kEvictLast : kEvictFirst);
       uint32_t stage = 0, phase = 0;
-      for (int t = t_first; t < p.total_tiles; t += t_stride) {
-        int b, mb, nb;
-        tile_coords(p, t, b, mb, nb);
-        if (!tile_valid<BN, BMT>(p, mb, nb)) continue;
-        int kb0, kb1;
-        k_range<BMT>(p, mb, kb0, kb1);
-        for (int kb = kb0; kb < kb1; ++kb) {
+      for (int w = t_first; w < p.work_items; w += t_stride) {
+        Work wk;
+        if (!get_work<BN, BMT>(p, w, wk)) continue;
+        const int b = wk.b, mb = wk.mb, nb = wk.nb;
+        for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
           mbar_wait(smem_u32(&bars[C::kStages + stage]), phase ^ 1);
           const uint32_t full = smem_u32(&bars[stage]);
           if (leader) mbar_arrive_expect_tx(full, kTx);
@@ -244,12 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------------------------------ MMA issuer (pair leader only)
       constexpr uint32_t idesc = umma_idesc_bf16(BMT, BN, kAMN ? 1 : 0, kBMN ? 1 : 0);
       uint32_t stage = 0, phase = 0, it = 0;
-      for (int t = t_first; t < p.total_tiles; t += t_stride) {
-        int b, mb, nb;
-        tile_coords(p, t, b, mb, nb);
-        if (!tile_valid<BN, BMT>(p, mb, nb)) continue;
-        int kb0, kb1;
-        k_range<BMT>(p, mb, kb0, kb1);
+      for (int w = t_first; w < p.work_items; w += t_stride) {
+        Work wk;
+        if (!get_work<BN, BMT>(p, w, wk)) continue;
+        const int kb0 = wk.kb0, kb1 = wk.kb1;
         const uint32_t acc = it & 1, acc_phase = (it >> 1) & 1;
         mbar_wait(smem_u32(&bars[2 * C::kStages + 2 + acc]), acc_phase ^ 1);
         tc_fence_after();
@@ -293,25 +326,83 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool f32 = ep == MT_EPI_STORE_F32 || ep == MT_EPI_ACCUM_F32;
     const float alpha = p.alpha;
     uint32_t it = 0;
-    for (int t = t_first; t < p.total_tiles; t += t_stride) {
-      int b, mb, nb;
-      tile_coords(p, t, b, mb, nb);
-      if (!tile_valid<BN, BMT>(p, mb, nb)) continue;
+    for (int w = t_first; w < p.work_items; w += t_stride) {
+      Work wk;
+      if (!get_work<BN, BMT>(p, w, wk)) continue;
+      const int b = wk.b, mb = wk.mb, nb = wk.nb;
       const uint32_t acc = it & 1, acc_phase = (it >> 1) & 1;
       mbar_wait(smem_u32(&bars[2 * C::kStages + acc]), acc_phase);
       tc_fence_after();
       const int row0 = mb * BMT + (int)rank * kBM + quad * 32;
       const int row = row0 + lane;
+      const uint32_t tmem_row = tmem_base + ((quad * 32) << 16) + acc * C::kAccStride;
+      const float* parts = nullptr;  // split-K: this CTA's partial tiles of the tail tile
+      if (wk.split >= 0) {
+        // Publish this split's raw partial (rows of this thread), then count arrivals; the last
+        // arriving split reduces the others' partials into its accumulator and runs the epilogue.
+        float* base = p.split_ws + (size_t)(wk.tail * p.splits) * 2 * (128 * BN);
+        float* mine = base + ((size_t)wk.split * 2 + rank) * (128 * BN) + (size_t)(quad * 32 + lane) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_row + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            __stcg(reinterpret_cast<float4*>(mine + c * 32 + 4 * j),
+                   make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                               __uint_as_float(r[4 * j + 3])));
+        }
+        __threadfence();
+        epi_bar();
+        if (threadIdx.x == 128) {
+          const int old = atomicAdd(&p.split_cnt[wk.tail * 2 + rank], 1);
+          *split_flag = (old == p.splits - 1) ? 1 : 0;
+          if (old == p.splits - 1) p.split_cnt[wk.tail * 2 + rank] = 0;  // reset for the next launch
+        }
+        epi_bar();
+        const bool last = *split_flag != 0;
+        if (!last) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (kPair)
+              mbar_arrive_cluster(smem_u32(&bars[2 * C::kStages + 2 + acc]), 0);
+            else
+              mbar_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
+          }
+          ++it;
+          continue;
+        }
+        __threadfence();
+        parts = base + (size_t)rank * (128 * BN) + (size_t)(quad * 32 + lane) * BN;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         const int col0 = nb * BN + c * 32;
         if (col0 >= p.n) break;
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((quad * 32) << 16) + acc * C::kAccStride + c * 32, r);
+        tmem_ld_32x32b_x32(tmem_row + c * 32, r);
         tmem_ld_wait();
         float x[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) x[j] = alpha * __uint_as_float(r[j]);
+        for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
+        if (parts != nullptr) {
+          for (int sp = 0; sp < p.splits; ++sp) {
+            if (sp == wk.split) continue;
+            const float* q = parts + (size_t)sp * 2 * (128 * BN) + c * 32;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 v = __ldcg(reinterpret_cast<const float4*>(q + 4 * j));
+              x[4 * j] += v.x;
+              x[4 * j + 1] += v.y;
+              x[4 * j + 2] += v.z;
+              x[4 * j + 3] += v.w;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] *= alpha;
         if (f32) {
           reuse_wait(lane);
           stage_f32(stg + bi * 4096, lane, x);
@@ -449,6 +540,17 @@ bool make_store_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t m, 
                      f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
+constexpr size_t kSplitCounterBytes = 64 * 1024;  // arrival counters at the head of the workspace
+
+bool split_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MT_GEMM_SPLITK");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -486,6 +588,26 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   p.nblocks = (n + BN - 1) / BN;
   p.kblocks = (k + kBK - 1) / kBK;
   p.total_tiles = p.mblocks * p.nblocks * batch;
+  // split-K tail (whole-tile work first; the last partial wave's tiles split over idle units)
+  const int cap_units = (a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms()) / (kPair ? 2 : 1);
+  p.full_tiles = p.total_tiles;
+  p.splits = 1;
+  p.work_items = p.total_tiles;
+  if (a.causal == MT_CAUSAL_NONE && a.workspace != nullptr && split_enabled()) {
+    const int units = std::max(1, cap_units);
+    const int full = (p.total_tiles / units) * units, tail = p.total_tiles - full;
+    if (full > 0 && tail > 0 && tail * 2 <= units) {
+      const int splits = std::min({units / tail, p.kblocks / 4, 8});
+      const size_t need = kSplitCounterBytes + (size_t)tail * splits * 2 * 128 * BN * sizeof(float);
+      if (splits >= 2 && (size_t)a.workspace_bytes >= need && tail * 2 * (int)sizeof(int) <= kSplitCounterBytes) {
+        p.full_tiles = full;
+        p.splits = splits;
+        p.work_items = full + tail * splits;
+        p.split_cnt = static_cast<int*>(a.workspace);
+        p.split_ws = reinterpret_cast<float*>(static_cast<char*>(a.workspace) + kSplitCounterBytes);
+      }
+    }
+  }
   p.alpha = a.alpha;
   p.epilogue = a.epilogue;
   p.causal = a.causal;
@@ -515,12 +637,12 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   }
   if (!kPair) {
     const int cap = a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms();
-    const int grid = p.total_tiles < cap ? p.total_tiles : cap;
+    const int grid = p.work_items < cap ? p.work_items : cap;
     kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, md, maux, p);
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
   }
   const int cap = a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms();
-  const int pairs = std::max(1, std::min(p.total_tiles, cap / 2));
+  const int pairs = std::max(1, std::min(p.work_items, cap / 2));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(kThreads);

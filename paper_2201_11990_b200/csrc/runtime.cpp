@@ -141,6 +141,10 @@ struct Gemm {
       }
       check_cuda(cudaEventRecord(c->ev_pool[c->ev_used], s), "cudaEventRecord");
     }
+    if (c && c->gemm_ws.ptr) {
+      a.workspace = c->gemm_ws.ptr;
+      a.workspace_bytes = static_cast<int64_t>(c->gemm_ws.bytes);
+    }
     const int rc = mt_gemm(&a, s);
     if (rc == 1) throw std::invalid_argument("mt_gemm: invalid arguments");
     if (rc != 0) throw RuntimeFailure(std::string("mt_gemm: ") + cudaGetErrorString(cudaGetLastError()));
@@ -227,6 +231,8 @@ extern "C" int mt_ctx_create(int32_t device, mt_ctx** out) {
     check_cuda(cudaSetDevice(device), "cudaSetDevice");
     auto* c = new mt_ctx();
     c->device = device;
+    c->gemm_ws.ensure(MT_GEMM_WORKSPACE_BYTES);
+    check_cuda(cudaMemset(c->gemm_ws.ptr, 0, MT_GEMM_WORKSPACE_BYTES), "cudaMemset(gemm workspace)");
     *out = c;
   });
 }

@@ -61,6 +61,7 @@ struct mt_ctx {
   mt::DeviceBuffer scratch_qkv;    // [M, 3h/t] bf16
   mt::DeviceBuffer scratch_attn;   // [heads/t, s, s] bf16
   mt::DeviceBuffer scratch_ws;     // fp32 column-reduction workspace
+  mt::DeviceBuffer gemm_ws;        // split-K tail workspace (zeroed counters + partial tiles)
   // side stream for TP collectives overlapped with independent GEMMs (backward: the all-reduce of
   // an LN-input gradient runs while the matching wgrad GEMM executes on SMs left free for NCCL)
   cudaStream_t comm = nullptr;

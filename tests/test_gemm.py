@@ -15,7 +15,8 @@ pytestmark = pytest.mark.gpu
 
 
 def _gemm(a, b, d, m, n, k, *, a_mn=False, b_mn=False, batch=1, lda=None, ldb=None, ldd=None,
-          abs_=0, bbs=0, dbs=0, alpha=1.0, epi=N.EPI_STORE_BF16, causal=0, bias=None, aux=None, ld_aux=0, bn=0):
+          abs_=0, bbs=0, dbs=0, alpha=1.0, epi=N.EPI_STORE_BF16, causal=0, bias=None, aux=None, ld_aux=0, bn=0,
+          ws=None, max_ctas=0):
     args = N.GemmArgs()
     args.a, args.b, args.d = a.data_ptr(), b.data_ptr(), d.data_ptr()
     args.lda = lda if lda is not None else (m if a_mn else k)
@@ -27,7 +28,9 @@ def _gemm(a, b, d, m, n, k, *, a_mn=False, b_mn=False, batch=1, lda=None, ldb=No
     args.alpha, args.epilogue, args.causal = alpha, epi, causal
     args.bias = bias.data_ptr() if bias is not None else None
     args.aux = aux.data_ptr() if aux is not None else None
-    args.ld_aux, args.block_n = ld_aux, bn
+    args.ld_aux, args.block_n, args.max_ctas = ld_aux, bn, max_ctas
+    if ws is not None:
+        args.workspace, args.workspace_bytes = ws.data_ptr(), ws.numel()
     rc = N.lib().mt_gemm(C.byref(args), C.c_void_p(torch.cuda.current_stream().cuda_stream))
     assert rc == 0, rc
     torch.cuda.synchronize()
@@ -119,3 +122,31 @@ def test_gemm_causal_modes(causal):
     D = torch.empty(s, k, device="cuda", dtype=torch.bfloat16)
     _gemm(P, V, D, s, k, s, b_mn=True, causal=causal)
     _close(D, P.float() @ V.float())
+
+
+@pytest.mark.parametrize("epi", [N.EPI_STORE_BF16, N.EPI_ACCUM_F32, N.EPI_BIAS_GELU])
+@pytest.mark.parametrize("max_ctas", [0, 132, 40])
+def test_gemm_split_k_tail(epi, max_ctas):
+    """Shapes whose last wave is partial take the split-K tail path (partials + last-arriver reduce)."""
+    m, n, k = 2048, 12288, 1024
+    A = torch.randn(m, k, device="cuda").bfloat16()
+    B = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    bias = torch.randn(n, device="cuda").bfloat16()
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    ref = A.float() @ B.float().t()
+    for _ in range(2):  # second launch checks the counters were reset
+        if epi == N.EPI_ACCUM_F32:
+            D = torch.ones(m, n, device="cuda")
+            _gemm(A, B, D, m, n, k, epi=epi, ws=ws, max_ctas=max_ctas)
+            _close(D, ref + 1.0, 1e-4)
+        elif epi == N.EPI_BIAS_GELU:
+            D = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+            pre = torch.empty_like(D)
+            _gemm(A, B, D, m, n, k, epi=epi, bias=bias, aux=pre, ld_aux=n, ws=ws, max_ctas=max_ctas)
+            _close(pre, ref + bias.float())
+            _close(D, torch.nn.functional.gelu(pre.float(), approximate="tanh"))
+        else:
+            D = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+            _gemm(A, B, D, m, n, k, ws=ws, max_ctas=max_ctas)
+            _close(D, ref)
+    assert int(ws[: 64 * 1024].sum()) == 0  # counters left zeroed

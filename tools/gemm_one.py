@@ -39,6 +39,9 @@ a.lda, a.ldb, a.ldd = (m if amn else k), (n if bmn else k), n
 a.a_mn_major, a.b_mn_major = amn, bmn
 a.m, a.n, a.k, a.batch, a.alpha, a.epilogue = m, n, k, 1, 1.0, epi
 a.block_n = int(os.environ.get("MT_BN", "0"))
+WS = \
+    torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+a.workspace, a.workspace_bytes = WS.data_ptr(), WS.numel()
 s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for i in range(reps):
