@@ -30,6 +30,12 @@ struct mt_stage {
   mt::DeviceBuffer target;                         // [M, h]
   mt::DeviceBuffer loss;                           // fp32 scalar
   int64_t launches = 0;
+  // host-input path: all microbatches' H2D copies are queued up front on a copy stream and
+  // overlap compute; each microbatch's first use waits on its own event
+  cudaStream_t copy = nullptr;
+  cudaEvent_t iter_start = nullptr;
+  std::vector<cudaEvent_t> in_ev, tgt_ev;
+  std::vector<mt::DeviceBuffer> targets;           // [MB][M, h] (host-target path)
 };
 
 namespace {
@@ -75,11 +81,32 @@ struct Step {
   const void* input(int mb) const {
     return (in_dev && first()) ? static_cast<const void*>(in_dev + mb * elems()) : st->act[mb][0].ptr;
   }
+  // Queue every microbatch's host->device copies on the copy stream (after the previous
+  // iteration's compute released the buffers).
+  void prefetch_host() {
+    if (!in_host && !tgt_host) return;
+    mt::check_cuda(cudaEventRecord(st->iter_start, s), "cudaEventRecord");
+    mt::check_cuda(cudaStreamWaitEvent(st->copy, st->iter_start, 0), "cudaStreamWaitEvent");
+    for (int mb = 0; mb < st->d.micro_batches; ++mb) {
+      if (in_host && first()) {
+        mt::check_cuda(cudaMemcpyAsync(st->act[mb][0].ptr, in_host + mb * elems(), bytes(), cudaMemcpyHostToDevice,
+                                       st->copy),
+                       "H2D input");
+        mt::check_cuda(cudaEventRecord(st->in_ev[mb], st->copy), "cudaEventRecord");
+      }
+      if (tgt_host && last()) {
+        mt::check_cuda(cudaMemcpyAsync(st->targets[mb].ptr, tgt_host + mb * elems(), bytes(), cudaMemcpyHostToDevice,
+                                       st->copy),
+                       "H2D target");
+        mt::check_cuda(cudaEventRecord(st->tgt_ev[mb], st->copy), "cudaEventRecord");
+      }
+    }
+  }
   void load_input(int mb) {
     if (in_dev) return;  // read in place by layer 0
     void* dst = st->act[mb][0].ptr;
     if (in_host) {
-      mt::check_cuda(cudaMemcpyAsync(dst, in_host + mb * elems(), bytes(), cudaMemcpyHostToDevice, s), "H2D input");
+      mt::check_cuda(cudaStreamWaitEvent(s, st->in_ev[mb], 0), "cudaStreamWaitEvent");
     } else {
       const uint64_t key = mt_stream_key(st->d.layer.seed, "input", 0, gid(mb));
       mt::fill_normal(dst, 1, elems(), elems(), 0, 0, key, 0.f, 1.f, s);
@@ -100,8 +127,8 @@ struct Step {
       if (tgt_dev) {
         tgt = tgt_dev + mb * elems();
       } else if (tgt_host) {
-        mt::check_cuda(cudaMemcpyAsync(st->target.ptr, tgt_host + mb * elems(), bytes(), cudaMemcpyHostToDevice, s),
-                       "H2D target");
+        mt::check_cuda(cudaStreamWaitEvent(s, st->tgt_ev[mb], 0), "cudaStreamWaitEvent");
+        tgt = st->targets[mb].ptr;
       } else {
         const uint64_t key = mt_stream_key(st->d.layer.seed, "target", 0, gid(mb));
         mt::fill_normal(st->target.ptr, 1, elems(), elems(), 0, 0, key, 0.f, 1.f, s);
@@ -172,6 +199,16 @@ extern "C" int mt_stage_create(mt_ctx* c, const mt_stage_desc* d, mt_stage** out
     for (auto& g : st->grad) g.ensure(bytes);
     st->target.ensure(bytes);
     st->loss.ensure(4);
+    mt::check_cuda(cudaStreamCreateWithFlags(&st->copy, cudaStreamNonBlocking), "copy stream");
+    mt::check_cuda(cudaEventCreateWithFlags(&st->iter_start, cudaEventDisableTiming), "event");
+    st->in_ev.resize(d->micro_batches);
+    st->tgt_ev.resize(d->micro_batches);
+    for (auto& e : st->in_ev) mt::check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (auto& e : st->tgt_ev) mt::check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    if (st->stage == st->stages - 1) {
+      st->targets.resize(d->micro_batches);
+      for (auto& b : st->targets) b.ensure(bytes);
+    }
     *out = st;
   });
 }
@@ -180,6 +217,10 @@ extern "C" int mt_stage_destroy(mt_stage* st) {
   return call([&] {
     if (!st) return;
     for (auto* l : st->layers) mt_layer_destroy(l);
+    for (auto e : st->in_ev) cudaEventDestroy(e);
+    for (auto e : st->tgt_ev) cudaEventDestroy(e);
+    if (st->iter_start) cudaEventDestroy(st->iter_start);
+    if (st->copy) cudaStreamDestroy(st->copy);
     delete st;
   });
 }
@@ -199,6 +240,7 @@ namespace {
 
 void run_iteration(Step& k, mt_stage* st, void* stream) {
   const int MB = st->d.micro_batches;
+  k.prefetch_host();
   for (auto* l : st->layers) ok(mt_layer_zero_grads(l, stream));
   mt::check_cuda(cudaMemsetAsync(st->loss.ptr, 0, 4, k.s), "memset loss");
   const int warmup = std::min(st->stages - st->stage - 1, MB);
