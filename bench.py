@@ -189,7 +189,8 @@ def run_ours(args, L: dict) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != L["tp"] * L["pp"] * L["dp"]:
+    shard_only = L.get("shard_only", False)
+    if not shard_only and world != L["tp"] * L["pp"] * L["dp"]:
         raise SystemExit(f"layout {L['note']} needs {L['tp'] * L['pp'] * L['dp']} ranks, got {world}")
     torch.cuda.set_device(local)
     if world > 1:
@@ -201,10 +202,12 @@ def run_ours(args, L: dict) -> None:
         ctx.init_comm(obj[0], world, rank, L["tp"], L["pp"], L["dp"], L["b"] * L["mb"] * L["dp"], L["mb"])
     else:
         ctx.init_comm(bytes(128), 1, 0, 1, 1, 1, L["b"] * L["mb"], L["mb"])
+    if shard_only:
+        lib().mt_ctx_shard_only(ctx._h, 1)
     place = ctx.placement()
     first, last = place.pipeline == 0, place.pipeline == L["pp"] - 1
     desc = PL.layer_desc(L["hidden"], L["heads"], L["seq"], L["b"], dropout_hidden=0.1, dropout_attn=0.1,
-                         seed=SEED)
+                         seed=SEED, tp_size=L["tp"] if shard_only else 1)
     stage = Stage(ctx, desc, L["layers"], L["mb"])
     stream = torch.cuda.current_stream()
     stage.init_params(L["layers"] // L["pp"], stream)
@@ -340,6 +343,7 @@ def run_ours(args, L: dict) -> None:
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,
+            **({"shard_only": True} if shard_only else {}),
             **({"op_breakdown_ms": op_breakdown} if op_breakdown is not None else {}),
         }
         print(json.dumps(line), flush=True)
@@ -357,12 +361,20 @@ def main() -> None:
     ap.add_argument("--config", default="gpt3", choices=["gpt3", "mtnlg", "pp", "3d", "tiny"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="single GPU: run ONE rank's tensor-parallel shard of the config at TP=SHARD_OF with the "
+                         "TP all-reduces skipped (compute-only per-GPU measurement, flagged in the JSON)")
     ap.add_argument("--op-timing", action="store_true",
                     help="after the timed region, run the steps again with per-op event marks and report the "
                          "per-op breakdown (ms per step) in the JSON line as op_breakdown_ms")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     L = layout_for(args.config, args.gpus)
+    if args.shard_of > 1:
+        if args.gpus != 1 or int(os.environ.get("WORLD_SIZE", "1")) != 1:
+            raise SystemExit("--shard-of is a single-GPU measurement")
+        L = dict(L, tp=args.shard_of, shard_only=True,
+                 note=f"ONE TP={args.shard_of} shard on 1 GPU, compute only (TP all-reduces excluded)")
     if args.impl == "reference":
         run_reference(args, L)
     else:

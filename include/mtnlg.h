@@ -118,6 +118,10 @@ int mt_nccl_unique_id(unsigned char out[128]);
 int mt_ctx_init_comm(mt_ctx* ctx, const unsigned char id[128], int32_t world_size, int32_t rank,
                      const mt_parallel_config* par);
 int mt_ctx_placement(const mt_ctx* ctx, mt_rank_placement* out);
+/* Single-process measurement of ONE tensor-parallel shard (layers created with tp_size > 1): the
+ * layers run their shard's kernels and skip the TP all-reduces. Compute-only numbers; the
+ * collectives are measured in real multi-GPU runs. Rejected when the context has a world > 1. */
+int mt_ctx_shard_only(mt_ctx* ctx, int32_t enable);
 /* Per-GEMM CUDA-event timing of every tcgen05 GEMM the context's layers launch (stream-ordered
  * events around each launch). _read synchronises, returns the summed kernel time, summed
  * algorithmic FLOPs and launch count since enabling / the last read, and resets. */

@@ -94,6 +94,7 @@ _SIGS = {
     "mt_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "mt_ctx_init_comm": (C.c_int, [P, C.c_char_p, I32, I32, C.POINTER(ParallelConfig)]),
     "mt_ctx_placement": (C.c_int, [P, C.POINTER(RankPlacement)]),
+    "mt_ctx_shard_only": (C.c_int, [P, I32]),
     "mt_ctx_gemm_timing": (C.c_int, [P, I32]),
     "mt_ctx_gemm_timing_read": (C.c_int, [P, PF64, PF64, PI64]),
     "mt_ctx_op_timing": (C.c_int, [P, I32]),

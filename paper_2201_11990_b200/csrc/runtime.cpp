@@ -373,6 +373,14 @@ extern "C" int mt_ctx_op_timing_read(mt_ctx* c, char* out, int64_t cap, int64_t*
   });
 }
 
+extern "C" int mt_ctx_shard_only(mt_ctx* c, int32_t enable) {
+  return guarded([&] {
+    if (!c) throw std::invalid_argument("null ctx");
+    if (enable && c->world_size > 1) throw std::invalid_argument("shard-only mode is for single-process runs");
+    c->shard_only = enable != 0;
+  });
+}
+
 extern "C" int mt_ctx_placement(const mt_ctx* c, mt_rank_placement* out) {
   return guarded([&] {
     if (!c || !out) throw std::invalid_argument("null argument");
@@ -577,6 +585,15 @@ void mark(mt_ctx* c, cudaStream_t st, const char* label) {
   ++c->marks_used;
 }
 
+// Whether the layer performs its TP collectives (TP > 1 with a communicator); TP > 1 without one
+// is only legal in shard-only (compute-only measurement) mode.
+bool tp_collectives(const mt_ctx* c, const mt_layer_desc& d) {
+  if (d.tp_size <= 1) return false;
+  if (c->tp) return true;
+  if (c->shard_only) return false;
+  throw std::invalid_argument("TP > 1 needs mt_ctx_init_comm (or mt_ctx_shard_only for a compute-only shard run)");
+}
+
 mt_layer::Saved& acquire_slot(mt_layer* l, uint32_t mb) {
   if (l->saved.count(mb)) throw std::invalid_argument("microbatch already has saved activations");
   std::unique_ptr<mt_layer::Saved> sv;
@@ -609,6 +626,7 @@ void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_
   const mt_layer_desc& d = l->d;
   const int64_t M = l->M, h = l->h, hl = l->hl, ffl = l->ffl, ld3 = l->qkvl, s = d.seq, Hl = l->heads_local,
                 hd = l->head_dim;
+  const bool tpc = tp_collectives(c, d);
   auto& sv = acquire_slot(l, mb);
   sv.x = x;
   float* mean1 = sv.stats.as<float>();
@@ -657,7 +675,7 @@ void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_
   }
   Gemm(sv.ctx.ptr, hl, false, l->param_ptr(MT_P_PROJ_W), hl, false, z, h, M, h, hl).run(st, n);
   mark(c, st, "fwd.proj_gemm");
-  if (d.tp_size > 1) {
+  if (tpc) {
     check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(attn.out)");
     ++n;
     mark(c, st, "fwd.tp_allreduce");
@@ -677,7 +695,7 @@ void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_
   mark(c, st, "fwd.fc1_gemm");
   Gemm(sv.act.ptr, ffl, false, l->param_ptr(MT_P_FC2_W), ffl, false, z, h, M, h, ffl).run(st, n);
   mark(c, st, "fwd.fc2_gemm");
-  if (d.tp_size > 1) {
+  if (tpc) {
     check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(mlp.out)");
     ++n;
     mark(c, st, "fwd.tp_allreduce");
@@ -696,6 +714,7 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
   auto it = l->saved.find(mb);
   if (it == l->saved.end()) throw std::invalid_argument("backward without a saved forward for this microbatch");
   auto& sv = *it->second;
+  const bool tpc = tp_collectives(c, d);
   const int64_t M = l->M, h = l->h, hl = l->hl, ffl = l->ffl, ld3 = l->qkvl, s = d.seq, Hl = l->heads_local,
                 hd = l->head_dim;
   float* mean1 = sv.stats.as<float>();
@@ -737,7 +756,7 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
   Gemm(dpre, ffl, false, l->param_ptr(MT_P_FC1_W), h, true, dln, h, M, h, ffl).run(st, n);
   mark(c, st, "bwd.fc1_dgrad");
   int cap = 0;
-  if (d.tp_size > 1) {
+  if (tpc) {
     cap = tp_allreduce_async(c, dln, M * h, st, "ncclAllReduce(ln2.grad)");
     ++n;
   }
@@ -746,7 +765,7 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
   mark(c, st, "bwd.bias_grad");
   Gemm(dpre, ffl, true, sv.ln2.ptr, h, true, l->grad_ptr(MT_P_FC1_W), h, ffl, h, M).epi(wg_epi).max_ctas(cap).run(st, n);
   mark(c, st, "bwd.fc1_wgrad");
-  if (d.tp_size > 1) tp_allreduce_join(c, st);
+  if (tpc) tp_allreduce_join(c, st);
   mark(c, st, "bwd.tp_allreduce_wait");
   ln_bwd_dx(dln, sv.x1.ptr, l->param_ptr(MT_P_LN2_GAMMA), mean2, rstd2, dy, dx1, (int)M, (int)h, st);
   ln_bwd_params(dln, sv.x1.ptr, mean2, rstd2, l->grad_ptr(MT_P_LN2_GAMMA), l->grad_ptr(MT_P_LN2_BETA), (int)M, (int)h,
@@ -800,7 +819,7 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
   Gemm(dqkv, ld3, false, l->param_ptr(MT_P_QKV_W), h, true, dln, h, M, h, ld3).run(st, n);
   mark(c, st, "bwd.qkv_dgrad");
   cap = 0;
-  if (d.tp_size > 1) {
+  if (tpc) {
     cap = tp_allreduce_async(c, dln, M * h, st, "ncclAllReduce(ln1.grad)");
     ++n;
   }
@@ -809,7 +828,7 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
   mark(c, st, "bwd.bias_grad");
   Gemm(dqkv, ld3, true, sv.ln1.ptr, h, true, l->grad_ptr(MT_P_QKV_W), h, ld3, h, M).epi(wg_epi).max_ctas(cap).run(st, n);
   mark(c, st, "bwd.qkv_wgrad");
-  if (d.tp_size > 1) tp_allreduce_join(c, st);
+  if (tpc) tp_allreduce_join(c, st);
   mark(c, st, "bwd.tp_allreduce_wait");
   ln_bwd_dx(dln, sv.x, l->param_ptr(MT_P_LN1_GAMMA), mean1, rstd1, dx1, dx, (int)M, (int)h, st);
   ln_bwd_params(dln, sv.x, mean1, rstd1, l->grad_ptr(MT_P_LN1_GAMMA), l->grad_ptr(MT_P_LN1_BETA), (int)M, (int)h, ws,

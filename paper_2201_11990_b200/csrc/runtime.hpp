@@ -53,7 +53,10 @@ struct mt_ctx {
   curator::ParallelConfig par;
   curator::RankPlacement place;
   ncclComm_t world = nullptr, tp = nullptr, pp = nullptr, dp = nullptr;
-  ncclComm_t tp_side = nullptr;  // same TP group, CTA-capped: collectives overlapped with GEMMs
+  ncclComm_t tp_side = nullptr;
+  // compute-only measurement of one TP shard on a single GPU: the layer skips its TP collectives
+  // (mt_ctx_shard_only); never set in a real multi-GPU run
+  bool shard_only = false;  // same TP group, CTA-capped: collectives overlapped with GEMMs
   // scratch shared by all layers of this context (sized to the largest layer)
   mt::DeviceBuffer scratch_h[4];   // [M, h] bf16 temporaries
   mt::DeviceBuffer scratch_ffn;    // [M, ffn/t] bf16

@@ -175,8 +175,10 @@ extern "C" int mt_stage_create(mt_ctx* c, const mt_stage_desc* d, mt_stage** out
     st->stages = c->par.pipeline;
     const curator::Range own = curator::stage_layers(d->layers, st->stages, st->stage);
     mt_layer_desc ld = d->layer;
-    ld.tp_size = c->par.tensor;
-    ld.tp_rank = c->place.tensor;
+    if (!(c->shard_only && ld.tp_size > 1)) {  // shard-only runs keep the descriptor's TP shard
+      ld.tp_size = c->par.tensor;
+      ld.tp_rank = c->place.tensor;
+    }
     for (int64_t li = own.begin; li < own.end; ++li) {
       ld.layer_index = static_cast<uint32_t>(li);
       mt_layer* l = nullptr;
