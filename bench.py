@@ -277,6 +277,18 @@ def run_ours(args, L: dict) -> None:
         dist.all_reduce(tot)
     h2d_all, d2h_all = int(tot[0].item()), int(tot[1].item())
 
+    # optimizer step, timed separately: the metric is the layer fwd+bwd
+    from paper_2201_11990_b200.runtime import adam_defaults
+    adam = adam_defaults(tokens_seen=1e10, step=1)
+    stage.optimizer_step(adam, stream, want_norm=False)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for i in range(args.steps):
+        adam.step = 2 + i
+        stage.optimizer_step(adam, stream, want_norm=False)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    opt_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     op_breakdown = None
     if args.op_timing:
         lib().mt_ctx_op_timing(ctx._h, 1)
@@ -330,6 +342,7 @@ def run_ours(args, L: dict) -> None:
             "peak_fraction_datasheet": tflops_gpu / 2250.0,
             "tokens_per_s_per_gpu": tokens / (ms * 1e-3) / world,
             "loss": loss_value,
+            "optimizer_ms_per_step": opt_ms,
             "roofline": {"bound": "tensor", "kernel": "gemm_sm100_kernel (tcgen05, all GEMM launches of the step)",
                          "achieved": gemm_tflops, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
                          "frac": (gemm_tflops / pk["bf16_sustained"]) if gemm_tflops else None,

@@ -167,6 +167,21 @@ int mt_dp_allreduce_f32(mt_ctx* ctx, float* buf, int64_t n, int32_t average, voi
 int mt_pp_send_bf16(mt_ctx* ctx, const void* buf, int64_t n, int32_t peer_stage, void* stream);
 int mt_pp_recv_bf16(mt_ctx* ctx, void* buf, int64_t n, int32_t peer_stage, void* stream);
 
+/* ------------------------------------------------------------------ optimizer */
+/* AdamW + global gradient-norm clipping with the reference recipe (curator::TrainingRecipe,
+ * planner.hpp:39-53) and learning rate curator::lr_at(tokens_seen) (planner.cpp:59-70) when lr < 0. */
+typedef struct mt_adam_desc {
+  float lr;              /* < 0: lr_at(tokens_seen) */
+  double tokens_seen;
+  float beta1, beta2, eps, weight_decay, grad_clip;  /* grad_clip <= 0 disables clipping */
+  int64_t step;          /* 1-based step count (bias correction) */
+} mt_adam_desc;
+int mt_adam_defaults(mt_adam_desc* out);  /* recipe constants, lr = -1, step = 1 */
+/* One layer on its own (no collectives): norm over this layer's gradients only. */
+int mt_layer_adam_step(mt_layer* l, const mt_adam_desc* d, float* grad_norm_out, void* stream);
+/* Read back the optimizer state of a parameter shard (fp32, shard_shape elements each; NULL skips). */
+int mt_layer_get_optimizer_state(mt_layer* l, int32_t param, float* master, float* m, float* v);
+
 /* ------------------------------------------------------------------ pipeline stage (1F1B driver) */
 typedef struct mt_stage mt_stage;
 typedef struct mt_stage_desc {
@@ -192,6 +207,10 @@ int mt_stage_train_step(mt_stage* st, const void* inputs_host, const void* targe
 int mt_stage_train_step_dev(mt_stage* st, const void* inputs_dev, const void* targets_dev, float* loss_dev,
                             void* stream);
 int mt_stage_launch_count(const mt_stage* st, int64_t* launches_per_step);
+/* Optimizer step of this rank's layers after mt_stage_train_step: the squared gradient norm is
+ * summed over the model-parallel group (TP and PP; TP-replicated parameters counted once; DP
+ * replicas already hold the averaged gradient), clipped to grad_clip, then fused AdamW. */
+int mt_stage_optimizer_step(mt_stage* st, const mt_adam_desc* d, float* grad_norm_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -60,6 +60,11 @@ class LayerDesc(C.Structure):
                 ("seed", C.c_uint64), ("layer_index", C.c_uint32)]
 
 
+class AdamDesc(C.Structure):
+    _fields_ = [("lr", C.c_float), ("tokens_seen", C.c_double), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("eps", C.c_float), ("weight_decay", C.c_float), ("grad_clip", C.c_float), ("step", C.c_int64)]
+
+
 class StageDesc(C.Structure):
     _fields_ = [("layer", LayerDesc), ("layers", C.c_int32), ("micro_batches", C.c_int32)]
 
@@ -122,6 +127,10 @@ _SIGS = {
     "mt_stage_train_step": (C.c_int, [P, P, P, PF32, P]),
     "mt_stage_train_step_dev": (C.c_int, [P, P, P, P, P]),
     "mt_stage_launch_count": (C.c_int, [P, PI64]),
+    "mt_stage_optimizer_step": (C.c_int, [P, C.POINTER(AdamDesc), PF32, P]),
+    "mt_adam_defaults": (C.c_int, [C.POINTER(AdamDesc)]),
+    "mt_layer_adam_step": (C.c_int, [P, C.POINTER(AdamDesc), PF32, P]),
+    "mt_layer_get_optimizer_state": (C.c_int, [P, I32, PF32, PF32, PF32]),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -871,3 +871,56 @@ extern "C" int mt_fill_normal(void* out, int64_t n, uint64_t key, float mean, fl
     check_cuda(cudaGetLastError(), "fill_normal");
   });
 }
+
+// =========================================================================== optimizer (N1)
+extern "C" int mt_adam_defaults(mt_adam_desc* o) {
+  return guarded([&] {
+    if (!o) throw std::invalid_argument("null out");
+    const curator::TrainingRecipe r;
+    o->lr = -1.f;
+    o->tokens_seen = 0.0;
+    o->beta1 = static_cast<float>(r.adam_beta1);
+    o->beta2 = static_cast<float>(r.adam_beta2);
+    o->eps = static_cast<float>(r.adam_eps);
+    o->weight_decay = static_cast<float>(r.weight_decay);
+    o->grad_clip = static_cast<float>(r.grad_clip);
+    o->step = 1;
+  });
+}
+
+float resolve_lr(const mt_adam_desc& d) {
+  return d.lr >= 0.f ? d.lr : static_cast<float>(curator::lr_at(d.tokens_seen));
+}
+
+extern "C" int mt_layer_adam_step(mt_layer* l, const mt_adam_desc* d, float* grad_norm_out, void* stream) {
+  return guarded([&] {
+    if (!l || !d) throw std::invalid_argument("null argument");
+    if (d->step < 1) throw std::invalid_argument("step must be >= 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    settle_fresh_grads(l, s);
+    mt::DeviceBuffer& buf = l->ctx->opt_scratch;
+    buf.ensure(4 * sizeof(float));
+    float* sq = buf.as<float>();
+    check_cuda(cudaMemsetAsync(sq, 0, 2 * sizeof(float), s), "memset");
+    mt::layer_grad_sq(l, sq, s);
+    mt::clip_coefficient(sq, d->grad_clip, sq + 2, s);
+    mt::layer_adamw(l, *d, resolve_lr(*d), sq + 3, s);
+    if (grad_norm_out) {
+      check_cuda(cudaMemcpyAsync(grad_norm_out, sq + 2, sizeof(float), cudaMemcpyDeviceToHost, s), "D2H norm");
+      check_cuda(cudaStreamSynchronize(s), "sync");
+    }
+  });
+}
+
+extern "C" int mt_layer_get_optimizer_state(mt_layer* l, int32_t p, float* master, float* m, float* v) {
+  return guarded([&] {
+    if (p < 0 || p >= MT_P_COUNT) throw std::invalid_argument("unknown parameter id");
+    if (!l->opt_master.ptr) throw std::invalid_argument("no optimizer step has run");
+    check_cuda(cudaDeviceSynchronize(), "sync");
+    const size_t n = static_cast<size_t>(l->param_rows[p] * l->param_cols[p]) * 4;
+    const size_t off = static_cast<size_t>(l->param_off[p]) * 4;
+    if (master) check_cuda(cudaMemcpy(master, l->opt_master.as<char>() + off, n, cudaMemcpyDeviceToHost), "D2H");
+    if (m) check_cuda(cudaMemcpy(m, l->opt_m.as<char>() + off, n, cudaMemcpyDeviceToHost), "D2H");
+    if (v) check_cuda(cudaMemcpy(v, l->opt_v.as<char>() + off, n, cudaMemcpyDeviceToHost), "D2H");
+  });
+}

@@ -15,6 +15,8 @@
 #include "curator/schedule.hpp"
 #include "mtnlg.h"
 
+struct mt_layer;
+
 namespace mt {
 
 // Failed CUDA / NCCL call -> DataError-class status 2.
@@ -45,6 +47,11 @@ struct DeviceBuffer {
   void ensure(size_t n);  // grow (contents discarded)
 };
 
+void ensure_optimizer_state(mt_layer* l, cudaStream_t s);
+void layer_grad_sq(mt_layer* l, float* sq, cudaStream_t s);
+void layer_adamw(mt_layer* l, const mt_adam_desc& d, float lr, const float* clip_coef, cudaStream_t s);
+void clip_coefficient(const float* sq, float max_norm, float* out, cudaStream_t s);
+
 }  // namespace mt
 
 struct mt_ctx {
@@ -65,6 +72,7 @@ struct mt_ctx {
   mt::DeviceBuffer scratch_attn;   // [heads/t, s, s] bf16
   mt::DeviceBuffer scratch_ws;     // fp32 column-reduction workspace
   mt::DeviceBuffer gemm_ws;        // split-K tail workspace (zeroed counters + partial tiles)
+  mt::DeviceBuffer opt_scratch;    // optimizer: squared norms + {norm, clip coefficient}
   // side stream for TP collectives overlapped with independent GEMMs (backward: the all-reduce of
   // an LN-input gradient runs while the matching wgrad GEMM executes on SMs left free for NCCL)
   cudaStream_t comm = nullptr;
@@ -102,6 +110,8 @@ struct mt_layer {
   // Logically zero gradients: the next backward writes (=) instead of accumulating (+=), which
   // saves both the memset and the read half of the fp32 read-modify-write in the wgrad epilogues.
   bool grads_fresh = false;
+  // optimizer state (created on the first optimizer step): fp32 master weights, Adam moments
+  mt::DeviceBuffer opt_master, opt_m, opt_v;
   void* param_ptr(int p) const { return static_cast<uint16_t*>(params.ptr) + param_off[p]; }
   float* grad_ptr(int p) const { return grads.as<float>() + param_off[p]; }
 };

@@ -343,3 +343,36 @@ extern "C" int mt_stage_train_step_dev(mt_stage* st, const void* inputs_dev, con
     st->launches = k.launches;
   });
 }
+
+float resolve_lr(const mt_adam_desc& d);  // runtime.cpp
+
+extern "C" int mt_stage_optimizer_step(mt_stage* st, const mt_adam_desc* d, float* grad_norm_out, void* stream) {
+  return call([&] {
+    if (!st || !d) throw std::invalid_argument("null argument");
+    if (d->step < 1) throw std::invalid_argument("step must be >= 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    mt_ctx* c = st->ctx;
+    c->opt_scratch.ensure(4 * sizeof(float));
+    float* sq = c->opt_scratch.as<float>();
+    mt::check_cuda(cudaMemsetAsync(sq, 0, 2 * sizeof(float), s), "memset");
+    for (auto* l : st->layers) {
+      float* g;
+      int64_t n;
+      ok(mt_layer_grad_buffer(l, &g, &n));  // materialises logically-zero grads if needed
+      mt::layer_grad_sq(l, sq, s);
+    }
+    // TP-replicated parameters (LayerNorm, row-parallel biases) count once per TP group
+    if (c->place.tensor != 0) mt::check_cuda(cudaMemsetAsync(sq + 1, 0, sizeof(float), s), "memset");
+    if (c->par.tensor > 1 && c->tp)
+      mt::check_nccl(ncclAllReduce(sq, sq, 2, ncclFloat32, ncclSum, c->tp, s), "ncclAllReduce(grad norm, tp)");
+    if (c->par.pipeline > 1 && c->pp)
+      mt::check_nccl(ncclAllReduce(sq, sq, 2, ncclFloat32, ncclSum, c->pp, s), "ncclAllReduce(grad norm, pp)");
+    mt::clip_coefficient(sq, d->grad_clip, sq + 2, s);
+    const float lr = resolve_lr(*d);
+    for (auto* l : st->layers) mt::layer_adamw(l, *d, lr, sq + 3, s);
+    if (grad_norm_out) {
+      mt::check_cuda(cudaMemcpyAsync(grad_norm_out, sq + 2, sizeof(float), cudaMemcpyDeviceToHost, s), "D2H norm");
+      mt::check_cuda(cudaStreamSynchronize(s), "sync");
+    }
+  });
+}

@@ -8,7 +8,16 @@ from __future__ import annotations
 
 import ctypes as C
 
-from ._native import LayerDesc, ParallelConfig, RankPlacement, StageDesc, check, lib
+from ._native import AdamDesc, LayerDesc, ParallelConfig, RankPlacement, StageDesc, check, lib
+
+
+def adam_defaults(**overrides) -> AdamDesc:
+    """curator::TrainingRecipe optimizer constants (lr < 0 => curator::lr_at(tokens_seen))."""
+    d = AdamDesc()
+    check(lib().mt_adam_defaults(C.byref(d)))
+    for k, v in overrides.items():
+        setattr(d, k, v)
+    return d
 from .planner import layer_desc  # noqa: F401  (re-export)
 
 
@@ -75,6 +84,16 @@ class Layer:
     def backward(self, dy_ptr: int, dx_ptr: int, micro_batch: int = 0, stream=None) -> None:
         check(lib().mt_layer_backward(self._h, C.c_void_p(dy_ptr), C.c_void_p(dx_ptr), micro_batch, _stream(stream)))
 
+    def adam_step(self, desc: AdamDesc, stream=None) -> float:
+        norm = C.c_float()
+        check(lib().mt_layer_adam_step(self._h, C.byref(desc), C.byref(norm), _stream(stream)))
+        return norm.value
+
+    def optimizer_state(self, param: int, master_ptr: int, m_ptr: int, v_ptr: int) -> None:
+        f = C.POINTER(C.c_float)
+        check(lib().mt_layer_get_optimizer_state(self._h, param, C.cast(C.c_void_p(master_ptr), f),
+                                                 C.cast(C.c_void_p(m_ptr), f), C.cast(C.c_void_p(v_ptr), f)))
+
     def launch_counts(self) -> tuple[int, int]:
         f, b = C.c_int32(), C.c_int32()
         check(lib().mt_layer_launch_counts(self._h, C.byref(f), C.byref(b)))
@@ -118,6 +137,12 @@ class Stage:
         """Iteration with device-resident inputs / targets ([MB][b*s*h] bf16); asynchronous."""
         check(lib().mt_stage_train_step_dev(self._h, C.c_void_p(inputs_dev_ptr or 0), C.c_void_p(targets_dev_ptr or 0),
                                             C.c_void_p(loss_dev_ptr or 0), _stream(stream)))
+
+    def optimizer_step(self, desc: AdamDesc, stream=None, want_norm: bool = True) -> float:
+        norm = C.c_float()
+        check(lib().mt_stage_optimizer_step(self._h, C.byref(desc), C.byref(norm) if want_norm else None,
+                                            _stream(stream)))
+        return norm.value
 
     def launch_count(self) -> int:
         n = C.c_int64()

@@ -96,6 +96,8 @@ def _worker(rank, world, port, mode, q):
             for _ in range(2):  # the second iteration must reproduce the first (grads re-zeroed)
                 loss = st.train_step(xh.data_ptr(), th.data_ptr(), s)
             out["loss"], out["place"] = loss, (place.data, place.pipeline, place.tensor)
+            from paper_2201_11990_b200.runtime import adam_defaults
+            out["grad_norm"] = None
             out["grads"] = []
             for li in range(per):
                 gl = []
@@ -104,6 +106,8 @@ def _worker(rank, world, port, mode, q):
                     st.layer(li).get_grad(i, a.ctypes.data)
                     gl.append(a.reshape(p))
                 out["grads"].append(gl)
+            # optimizer step: the clip norm is summed over the model-parallel group (PP here)
+            out["grad_norm"] = st.optimizer_step(adam_defaults(tokens_seen=2e9, step=1), s)
             st.close()
         ctx.close()
         q.put((rank, out))
@@ -179,6 +183,9 @@ def test_pipeline_parallel_1f1b_two_gpus():
     res = _run("pp")
     loss, grads = _oracle_step([0, 1, 2, 3], range(4))
     assert abs(res[1]["loss"] - loss) / loss < 5e-3, (res[1]["loss"], loss)
+    norm = np.sqrt(sum(float((g.astype(np.float64) ** 2).sum()) for lg in grads for g in lg))
+    for r in (0, 1):
+        assert abs(res[r]["grad_norm"] - norm) / norm < 2e-2, (res[r]["grad_norm"], norm)
     for r in (0, 1):
         for li in range(2):
             for i in range(12):
@@ -192,5 +199,7 @@ def test_data_parallel_gradient_allreduce_two_gpus():
     loss, grads = _oracle_step([0], range(4))
     for r in (0, 1):
         assert abs(res[r]["loss"] - loss / 2) / loss < 5e-3
+        norm = np.sqrt(sum(float(((g / 2).astype(np.float64) ** 2).sum()) for g in grads[0]))
+        assert abs(res[r]["grad_norm"] - norm) / norm < 2e-2
         for i in range(12):
             assert rel(res[r]["grads"][0][i], grads[0][i] / 2) < 2e-2, (r, i)
