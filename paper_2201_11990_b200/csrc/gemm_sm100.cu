@@ -621,6 +621,7 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
     return (e && e[0] == '1') ? 1 : 0;
   }();
   p.hints = hints;
+  // (direct register->global fp32 stores were measured 8% slower than smem staging + TMA store)
   p.d_bf16 = static_cast<__nv_bfloat16*>(a.d);
   p.d_f32 = static_cast<float*>(a.d);
   p.ldd = a.ldd;

@@ -300,20 +300,23 @@ int col_splits(int rows) {
 }
 
 // ------------------------------------------------------------------ bias + dropout + residual
-__global__ void bias_dropout_residual_kernel(const uint4* __restrict__ z, const uint4* __restrict__ bias,
-                                             const uint4* __restrict__ resid, uint4* __restrict__ out, long long nvec_total,
-                                             int nvec_row, uint64_t seed, uint32_t thresh16, float scale) {
-  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvec_total;
-       v += (long long)gridDim.x * blockDim.x) {
-    float a[8], b[8], r[8], o[8];
-    unpack8(z[v], a);
-    unpack8(bias[v % nvec_row], b);
-    unpack8(resid[v], r);
-    const uint32_t keep = keep_mask8(seed, (uint64_t)v * 8, thresh16);
+// 2-D grid: blockIdx.y = row, x covers the row's 8-element vectors (no 64-bit div/mod per element).
+__global__ void __launch_bounds__(256) bias_dropout_residual_kernel(const uint4* __restrict__ z,
+                                                                    const uint4* __restrict__ bias,
+                                                                    const uint4* __restrict__ resid,
+                                                                    uint4* __restrict__ out, int nvec_row,
+                                                                    uint64_t seed, uint32_t thresh16, float scale) {
+  const int cv = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cv >= nvec_row) return;
+  const size_t v = (size_t)blockIdx.y * nvec_row + cv;
+  float a[8], b[8], r[8], o[8];
+  unpack8(z[v], a);
+  unpack8(bias[cv], b);
+  unpack8(resid[v], r);
+  const uint32_t keep = keep_mask8(seed, (uint64_t)v * 8, thresh16);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = r[j] + (((keep >> j) & 1u) ? (a[j] + b[j]) * scale : 0.f);
-    out[v] = pack8(o);
-  }
+  for (int j = 0; j < 8; ++j) o[j] = r[j] + (((keep >> j) & 1u) ? (a[j] + b[j]) * scale : 0.f);
+  out[v] = pack8(o);
 }
 
 // ------------------------------------------------------------------ causal softmax
@@ -587,10 +590,10 @@ void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int
 
 void bias_dropout_residual(const void* z, const void* bias, const void* resid, void* out, int rows, int h,
                            uint64_t seed, uint32_t thresh16, float scale, cudaStream_t s) {
-  const long long nvec = (long long)rows * h / 8;
-  bias_dropout_residual_kernel<<<grid_for(nvec, 256), 256, 0, s>>>((const uint4*)z, (const uint4*)bias,
-                                                                   (const uint4*)resid, (uint4*)out, nvec, h / 8, seed,
-                                                                   thresh16, scale);
+  const int nvec_row = h / 8;
+  dim3 grid((nvec_row + 255) / 256, rows);
+  bias_dropout_residual_kernel<<<grid, 256, 0, s>>>((const uint4*)z, (const uint4*)bias, (const uint4*)resid,
+                                                    (uint4*)out, nvec_row, seed, thresh16, scale);
 }
 
 #define MT_VPL_DISPATCH(SEQ, LAUNCH) \

@@ -20,6 +20,11 @@ SHAPES = {  # name: (m, n, k, a_mn, b_mn, epilogue)
     "fc1_wgrad": (4 * h, h, M, 1, 1, N.EPI_STORE_F32),
     "fc1_wgrad_acc": (4 * h, h, M, 1, 1, N.EPI_ACCUM_F32),
     "proj_fwd": (M, h, h, 0, 0, N.EPI_STORE_BF16),
+    # wgrad shape with the four operand-major combinations (K = tokens)
+    "wg_kk_f32": (4 * h, h, M, 0, 0, N.EPI_STORE_F32),
+    "wg_mm_f32": (4 * h, h, M, 1, 1, N.EPI_STORE_F32),
+    "wg_mm_bf16": (4 * h, h, M, 1, 1, N.EPI_STORE_BF16),
+    "wg_kk_bf16": (4 * h, h, M, 0, 0, N.EPI_STORE_BF16),
     # MT-NLG h=20480 at TP=8 (per-GPU shard shapes)
     "mt_qkv_fwd": (M, 7680, 20480, 0, 0, N.EPI_STORE_BF16),
     "mt_proj_fwd": (M, 20480, 2560, 0, 0, N.EPI_STORE_BF16),
