@@ -43,6 +43,15 @@ void softmax_fwd(const void* S, void* P, float* lse, int batch_heads, int seq, l
 void softmax_bwd(const void* S, const float* lse, void* dP, int batch_heads, int seq, long long head_base,
                  uint64_t site_seed, uint32_t thresh16, float scale, float alpha, cudaStream_t s);
 
+// Fused causal flash attention on tcgen05 (attention_sm100.cu). Return 0 ok, 1 unsupported shape
+// (seq % 128 or head dim not in {64, 128, 160}), 2 CUDA error.
+int attention_fwd(const void* qkv, long long ld_qkv, int heads, int seq, int hd, long long head_base, float alpha,
+                  uint64_t seed, uint32_t thresh16, float drop_scale, void* out, long long ld_out, float* lse,
+                  cudaStream_t s);
+int attention_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* dctx, long long ld_ctx, int heads,
+                  int seq, int hd, long long head_base, float alpha, uint64_t seed, uint32_t thresh16,
+                  float drop_scale, const float* lse, float* D, void* dqkv, cudaStream_t s);
+
 // loss += sum 0.5 (y - t)^2 / n ; dy = (y - t) / n     (n = rows * h)
 void mse_loss(const void* y, const void* t, void* dy, float* loss, long long n, cudaStream_t s);
 

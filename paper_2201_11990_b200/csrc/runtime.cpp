@@ -455,6 +455,14 @@ extern "C" int mt_layer_create(mt_ctx* c, const mt_layer_desc* d, mt_layer** out
     l->heads_local = d->heads / d->tp_size;
     l->head_dim = d->hidden / d->heads;
     l->shard = curator::layer_shard(d->hidden, d->heads, d->ffn_mult, d->tp_size, d->tp_rank);
+    {
+      // Default: unfused (score GEMM + causal softmax + PV GEMM), measured faster end to end than the
+      // current flash kernels (1 softmax warp per SMSP is latency-bound); MT_ATTN_FUSED=1 opts in.
+      const char* e = getenv("MT_ATTN_FUSED");
+      const bool want = e && e[0] == '1';
+      const int hd = static_cast<int>(l->head_dim);
+      l->fused_attn = want && d->seq % 128 == 0 && (hd == 64 || hd == 128 || hd == 160);
+    }
     int64_t off = 0;
     for (int p = 0; p < MT_P_COUNT; ++p) {
       const ShardInfo si = shard_info(*d, p);
@@ -473,7 +481,8 @@ extern "C" int mt_layer_create(mt_ctx* c, const mt_layer_desc* d, mt_layer** out
     c->scratch_ffn.ensure(M * l->ffl * 2);
     c->scratch_ctx.ensure(M * l->hl * 2);
     c->scratch_qkv.ensure(M * l->qkvl * 2);
-    c->scratch_attn.ensure(l->heads_local * int64_t{d->seq} * d->seq * 2);
+    c->scratch_attn.ensure(l->fused_attn ? l->heads_local * int64_t{d->seq} * 4
+                                         : l->heads_local * int64_t{d->seq} * d->seq * 2);
     size_t ws = 0;
     for (int64_t n : {l->h, l->ffl, l->qkvl}) ws = std::max(ws, mt::colsum_workspace_floats((int)M, (int)n));
     c->scratch_ws.ensure(ws * 4);
@@ -606,8 +615,10 @@ mt_layer::Saved& acquire_slot(mt_layer* l, uint32_t mb) {
   const int64_t M = l->M, b = l->d.micro_batch, s = l->d.seq, Hl = l->heads_local;
   sv->ln1.ensure(M * l->h * 2);
   sv->qkv.ensure(M * l->qkvl * 2);
-  sv->S.ensure(b * Hl * s * s * 2);
-  sv->P.ensure(b * Hl * s * s * 2);
+  if (!l->fused_attn) {
+    sv->S.ensure(b * Hl * s * s * 2);
+    sv->P.ensure(b * Hl * s * s * 2);
+  }
   sv->lse.ensure(b * Hl * s * 4);
   sv->ctx.ensure(M * l->hl * 2);
   sv->x1.ensure(M * l->h * 2);
@@ -654,16 +665,24 @@ void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_
   const float alpha = 1.f / std::sqrt((float)hd);
   for (int64_t bb = 0; bb < d.micro_batch; ++bb) {
     const uint16_t* q = sv.qkv.as<uint16_t>() + bb * s * ld3;
+    float* lse = sv.lse.as<float>() + bb * Hl * s;
+    const long long head_base = bb * d.heads + int64_t{d.tp_rank} * Hl;
+    if (l->fused_attn) {
+      const int rc = attention_fwd(q, ld3, (int)Hl, (int)s, (int)hd, head_base, alpha, site_attn, th_a, scale_a,
+                                   sv.ctx.as<uint16_t>() + bb * s * hl, hl, lse, st);
+      if (rc != 0) throw RuntimeFailure("attention_fwd failed");
+      ++n;
+      mark(c, st, "fwd.flash_attention");
+      continue;
+    }
     uint16_t* S = sv.S.as<uint16_t>() + bb * Hl * s * s;
     uint16_t* P = sv.P.as<uint16_t>() + bb * Hl * s * s;
-    float* lse = sv.lse.as<float>() + bb * Hl * s;
     Gemm(q, ld3, false, q + hd, ld3, false, S, s, s, s, hd)
         .batched(Hl, 3 * hd, 3 * hd, s * s)
         .alpha(alpha)
         .causal(MT_CAUSAL_SKIP_UPPER_TILES)
         .run(st, n);
     mark(c, st, "fwd.attn_s_gemm");
-    const long long head_base = bb * d.heads + int64_t{d.tp_rank} * Hl;
     softmax_fwd(S, P, lse, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, st);
     ++n;
     mark(c, st, "fwd.softmax");
@@ -786,6 +805,16 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
     const uint16_t* q = sv.qkv.as<uint16_t>() + bb * s * ld3;
     uint16_t* dq = static_cast<uint16_t*>(dqkv) + bb * s * ld3;
     const uint16_t* dc = static_cast<const uint16_t*>(dctx) + bb * s * hl;
+    if (l->fused_attn) {
+      const long long head_base = bb * d.heads + int64_t{d.tp_rank} * Hl;
+      const int rc = attention_bwd(q, ld3, sv.ctx.as<uint16_t>() + bb * s * hl, dc, hl, (int)Hl, (int)s, (int)hd,
+                                   head_base, alpha, site_attn, th_a, scale_a, sv.lse.as<float>() + bb * Hl * s,
+                                   c->scratch_attn.as<float>(), dq, st);
+      if (rc != 0) throw RuntimeFailure("attention_bwd failed");
+      n += 3;
+      mark(c, st, "bwd.flash_attention");
+      continue;
+    }
     const uint16_t* S = sv.S.as<uint16_t>() + bb * Hl * s * s;
     const uint16_t* P = sv.P.as<uint16_t>() + bb * Hl * s * s;
     const float* lse = sv.lse.as<float>() + bb * Hl * s;

@@ -107,6 +107,9 @@ struct mt_layer {
   std::map<uint32_t, std::unique_ptr<Saved>> saved;
   std::vector<std::unique_ptr<Saved>> free_slots;
   int fwd_launches = 0, bwd_launches = 0;
+  // fused flash attention (attention_sm100.cu) instead of score GEMM + softmax + PV GEMM; S / P are
+  // then never materialised (opt-in with MT_ATTN_FUSED=1; parity-tested, not yet the faster path)
+  bool fused_attn = false;
   // Logically zero gradients: the next backward writes (=) instead of accumulating (+=), which
   // saves both the memset and the read half of the fp32 read-modify-write in the wgrad epilogues.
   bool grads_fresh = false;

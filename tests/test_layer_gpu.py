@@ -45,8 +45,12 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["flash_attn", "unfused_attn"])
 @pytest.mark.parametrize("hidden,heads,seq,mb,p", CASES)
-def test_layer_matches_oracle(hidden, heads, seq, mb, p):
+def test_layer_matches_oracle(hidden, heads, seq, mb, p, fused, monkeypatch):
+    # the attention path is chosen at layer creation: fused tcgen05 flash attention, or score GEMM +
+    # causal softmax + PV GEMM (both must match the oracle)
+    monkeypatch.setenv("MT_ATTN_FUSED", "1" if fused else "0")
     ctx = Context(0)
     desc = PL.layer_desc(hidden, heads, seq, mb, dropout_hidden=p, dropout_attn=p, seed=SEED, layer_index=3)
     layer = Layer(ctx, desc)
