@@ -209,6 +209,8 @@ def run_ours(args, L: dict) -> None:
     desc = PL.layer_desc(L["hidden"], L["heads"], L["seq"], L["b"], dropout_hidden=0.1, dropout_attn=0.1,
                          seed=SEED, tp_size=L["tp"] if shard_only else 1)
     stage = Stage(ctx, desc, L["layers"], L["mb"])
+    if args.recompute:
+        stage.set_recompute(True)
     stream = torch.cuda.current_stream()
     stage.init_params(L["layers"] // L["pp"], stream)
     M, h, MB = L["b"] * L["seq"], L["hidden"], L["mb"]
@@ -337,6 +339,7 @@ def run_ours(args, L: dict) -> None:
                        "global_batch": L["b"] * MB * L["dp"], "parallelism": f"tp{L['tp']}pp{L['pp']}dp{L['dp']}",
                        "dropout": 0.1, "l2": "working set > L2 (weights alone exceed 126 MB); no flush"},
             "tflops_per_gpu": tflops_gpu,
+            **({"recompute": True, "hardware_tflops_per_gpu": tflops_gpu * 96.0 / 72.0} if args.recompute else {}),
             "peak_fraction": tflops_gpu / pk["bf16"],
             "peak_fraction_sustained": tflops_gpu / pk["bf16_sustained"],
             "peak_fraction_datasheet": tflops_gpu / 2250.0,
@@ -377,6 +380,9 @@ def main() -> None:
     ap.add_argument("--shard-of", type=int, default=0,
                     help="single GPU: run ONE rank's tensor-parallel shard of the config at TP=SHARD_OF with the "
                          "TP all-reduces skipped (compute-only per-GPU measurement, flagged in the JSON)")
+    ap.add_argument("--recompute", action="store_true",
+                    help="activation recompute (SURVEY.md §8f N2): the backward re-runs each layer's forward; "
+                         "tflops_per_gpu stays model FLOPs (72 coeff.), hardware_tflops_per_gpu counts the re-run (96)")
     ap.add_argument("--op-timing", action="store_true",
                     help="after the timed region, run the steps again with per-op event marks and report the "
                          "per-op breakdown (ms per step) in the JSON line as op_breakdown_ms")

@@ -151,6 +151,11 @@ int mt_layer_forward(mt_layer* l, const void* x, void* y, uint32_t micro_batch, 
 /* Backward of one microbatch (frees its saved activations): dy -> dx (device bf16 [b*s, h]);
  * parameter gradients accumulate in fp32. */
 int mt_layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t micro_batch, void* stream);
+/* Activation recompute (full-layer checkpointing): the forward keeps only the layer
+ * input; the backward re-runs the forward (identical dropout masks) before differentiating, so the
+ * executed FLOPs follow the reference cost model's recompute-inclusive 96 coefficient
+ * (proj/src/planner.cpp:52-54). Only while no microbatch is in flight. */
+int mt_layer_set_recompute(mt_layer* l, int32_t enable);
 /* Kernel launches one forward / backward issues (for the bench's gpu_launches claim). */
 int mt_layer_launch_counts(const mt_layer* l, int32_t* fwd, int32_t* bwd);
 /* Device pointer to the flat fp32 gradient buffer of the layer and its element count. */
@@ -207,6 +212,7 @@ int mt_stage_train_step(mt_stage* st, const void* inputs_host, const void* targe
 int mt_stage_train_step_dev(mt_stage* st, const void* inputs_dev, const void* targets_dev, float* loss_dev,
                             void* stream);
 int mt_stage_launch_count(const mt_stage* st, int64_t* launches_per_step);
+int mt_stage_set_recompute(mt_stage* st, int32_t enable);
 /* Optimizer step of this rank's layers after mt_stage_train_step: the squared gradient norm is
  * summed over the model-parallel group (TP and PP; TP-replicated parameters counted once; DP
  * replicas already hold the averaged gradient), clipped to grad_clip, then fused AdamW. */

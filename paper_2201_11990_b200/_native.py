@@ -114,6 +114,8 @@ _SIGS = {
     "mt_layer_forward": (C.c_int, [P, P, P, U32, P]),
     "mt_layer_backward": (C.c_int, [P, P, P, U32, P]),
     "mt_layer_launch_counts": (C.c_int, [P, PI32, PI32]),
+    "mt_layer_set_recompute": (C.c_int, [P, I32]),
+    "mt_stage_set_recompute": (C.c_int, [P, I32]),
     "mt_layer_grad_buffer": (C.c_int, [P, C.POINTER(PF32), PI64]),
     "mt_mse_loss": (C.c_int, [P, P, P, P, I64, P]),
     "mt_fill_normal": (C.c_int, [P, I64, U64, F32, F32, P]),

@@ -555,6 +555,15 @@ extern "C" int mt_layer_grad_buffer(mt_layer* l, float** ptr, int64_t* n) {
   });
 }
 
+extern "C" int mt_layer_set_recompute(mt_layer* l, int32_t enable) {
+  return guarded([&] {
+    if (!l) throw std::invalid_argument("null layer");
+    if (!l->saved.empty()) throw std::invalid_argument("cannot switch recompute with activations in flight");
+    l->recompute = enable != 0;
+    for (auto& f : l->free_slots) f.reset(new mt_layer::Saved());  // drop full-size slots
+  });
+}
+
 extern "C" int mt_layer_launch_counts(const mt_layer* l, int32_t* f, int32_t* b) {
   return guarded([&] {
     *f = l->fwd_launches;
@@ -603,6 +612,26 @@ bool tp_collectives(const mt_ctx* c, const mt_layer_desc& d) {
   throw std::invalid_argument("TP > 1 needs mt_ctx_init_comm (or mt_ctx_shard_only for a compute-only shard run)");
 }
 
+void ensure_slot_buffers(mt_layer* l, mt_layer::Saved& sv) {
+  const int64_t M = l->M, b = l->d.micro_batch, s = l->d.seq, Hl = l->heads_local;
+  sv.ln1.ensure(M * l->h * 2);
+  sv.qkv.ensure(M * l->qkvl * 2);
+  if (!l->fused_attn) {
+    sv.S.ensure(b * Hl * s * s * 2);
+    sv.P.ensure(b * Hl * s * s * 2);
+  }
+  sv.lse.ensure(b * Hl * s * 4);
+  sv.ctx.ensure(M * l->hl * 2);
+  sv.x1.ensure(M * l->h * 2);
+  sv.ln2.ensure(M * l->h * 2);
+  sv.pre.ensure(M * l->ffl * 2);
+  sv.act.ensure(M * l->ffl * 2);
+  sv.stats.ensure(4 * M * 4);
+}
+
+// Per-microbatch slot. With activation recompute the slot keeps only the layer
+// input; the intermediate tensors live in one per-layer work slot that the backward refills by
+// re-running the forward (same microbatch id -> identical dropout masks).
 mt_layer::Saved& acquire_slot(mt_layer* l, uint32_t mb) {
   if (l->saved.count(mb)) throw std::invalid_argument("microbatch already has saved activations");
   std::unique_ptr<mt_layer::Saved> sv;
@@ -612,33 +641,33 @@ mt_layer::Saved& acquire_slot(mt_layer* l, uint32_t mb) {
   } else {
     sv = std::make_unique<mt_layer::Saved>();
   }
-  const int64_t M = l->M, b = l->d.micro_batch, s = l->d.seq, Hl = l->heads_local;
-  sv->ln1.ensure(M * l->h * 2);
-  sv->qkv.ensure(M * l->qkvl * 2);
-  if (!l->fused_attn) {
-    sv->S.ensure(b * Hl * s * s * 2);
-    sv->P.ensure(b * Hl * s * s * 2);
-  }
-  sv->lse.ensure(b * Hl * s * 4);
-  sv->ctx.ensure(M * l->hl * 2);
-  sv->x1.ensure(M * l->h * 2);
-  sv->ln2.ensure(M * l->h * 2);
-  sv->pre.ensure(M * l->ffl * 2);
-  sv->act.ensure(M * l->ffl * 2);
-  sv->stats.ensure(4 * M * 4);
+  if (!l->recompute) ensure_slot_buffers(l, *sv);
   auto& ref = *sv;
   l->saved[mb] = std::move(sv);
   return ref;
 }
 
+mt_layer::Saved& work_slot(mt_layer* l) {
+  if (!l->work) l->work = std::make_unique<mt_layer::Saved>();
+  ensure_slot_buffers(l, *l->work);
+  return *l->work;
+}
+
+void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t st, mt_layer::Saved& sv);
+
 void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t st) {
+  auto& slot = acquire_slot(l, mb);
+  slot.x = x;
+  forward_into(l, x, y, mb, st, l->recompute ? work_slot(l) : slot);
+}
+
+void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t st, mt_layer::Saved& sv) {
   mt_ctx* c = l->ctx;
   tl_ctx = c;
   const mt_layer_desc& d = l->d;
   const int64_t M = l->M, h = l->h, hl = l->hl, ffl = l->ffl, ld3 = l->qkvl, s = d.seq, Hl = l->heads_local,
                 hd = l->head_dim;
   const bool tpc = tp_collectives(c, d);
-  auto& sv = acquire_slot(l, mb);
   sv.x = x;
   float* mean1 = sv.stats.as<float>();
   float* rstd1 = mean1 + M;
@@ -726,13 +755,30 @@ void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_
   l->fwd_launches = n;
 }
 
+void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStream_t st, mt_layer::Saved& sv);
+
 void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStream_t st) {
+  auto it = l->saved.find(mb);
+  if (it == l->saved.end()) throw std::invalid_argument("backward without a saved forward for this microbatch");
+  if (l->recompute) {
+    mt_layer::Saved& w = work_slot(l);
+    const int fwd_n = l->fwd_launches;
+    forward_into(l, it->second->x, l->ctx->scratch_h[3].ptr, mb, st, w);  // regenerate the activations
+    const int refwd = l->fwd_launches;
+    l->fwd_launches = fwd_n;
+    backward_from(l, dy, dx, mb, st, w);
+    l->bwd_launches += refwd;
+  } else {
+    backward_from(l, dy, dx, mb, st, *it->second);
+  }
+  l->free_slots.push_back(std::move(it->second));
+  l->saved.erase(it);
+}
+
+void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStream_t st, mt_layer::Saved& sv) {
   mt_ctx* c = l->ctx;
   tl_ctx = c;
   const mt_layer_desc& d = l->d;
-  auto it = l->saved.find(mb);
-  if (it == l->saved.end()) throw std::invalid_argument("backward without a saved forward for this microbatch");
-  auto& sv = *it->second;
   const bool tpc = tp_collectives(c, d);
   const int64_t M = l->M, h = l->h, hl = l->hl, ffl = l->ffl, ld3 = l->qkvl, s = d.seq, Hl = l->heads_local,
                 hd = l->head_dim;
@@ -866,8 +912,6 @@ void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStre
   mark(c, st, "bwd.ln_bwd");
   check_cuda(cudaGetLastError(), "layer backward launch");
   l->bwd_launches = n;
-  l->free_slots.push_back(std::move(it->second));
-  l->saved.erase(it);
 }
 
 }  // namespace

@@ -105,6 +105,8 @@ struct mt_layer {
     mt::DeviceBuffer ln1, qkv, S, P, lse, ctx, x1, ln2, pre, act, stats;  // stats: mean1,rstd1,mean2,rstd2
   };
   std::map<uint32_t, std::unique_ptr<Saved>> saved;
+  bool recompute = false;           // activation recompute (full-layer checkpointing)
+  std::unique_ptr<Saved> work;      // recompute: the one set of intermediate buffers
   std::vector<std::unique_ptr<Saved>> free_slots;
   int fwd_launches = 0, bwd_launches = 0;
   // fused flash attention (attention_sm100.cu) instead of score GEMM + softmax + PV GEMM; S / P are

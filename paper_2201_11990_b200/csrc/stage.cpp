@@ -376,3 +376,10 @@ extern "C" int mt_stage_optimizer_step(mt_stage* st, const mt_adam_desc* d, floa
     }
   });
 }
+
+extern "C" int mt_stage_set_recompute(mt_stage* st, int32_t enable) {
+  return call([&] {
+    if (!st) throw std::invalid_argument("null stage");
+    for (auto* l : st->layers) ok(mt_layer_set_recompute(l, enable));
+  });
+}

@@ -94,6 +94,9 @@ class Layer:
         check(lib().mt_layer_get_optimizer_state(self._h, param, C.cast(C.c_void_p(master_ptr), f),
                                                  C.cast(C.c_void_p(m_ptr), f), C.cast(C.c_void_p(v_ptr), f)))
 
+    def set_recompute(self, enable: bool = True) -> None:
+        check(lib().mt_layer_set_recompute(self._h, int(enable)))
+
     def launch_counts(self) -> tuple[int, int]:
         f, b = C.c_int32(), C.c_int32()
         check(lib().mt_layer_launch_counts(self._h, C.byref(f), C.byref(b)))
@@ -143,6 +146,9 @@ class Stage:
         check(lib().mt_stage_optimizer_step(self._h, C.byref(desc), C.byref(norm) if want_norm else None,
                                             _stream(stream)))
         return norm.value
+
+    def set_recompute(self, enable: bool = True) -> None:
+        check(lib().mt_stage_set_recompute(self._h, int(enable)))
 
     def launch_count(self) -> int:
         n = C.c_int64()

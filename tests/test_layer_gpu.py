@@ -122,3 +122,42 @@ def test_layer_rejects_bad_config():
     with pytest.raises(PL.ConfigError):
         Layer(ctx, PL.layer_desc(256, 4, 128, 1, tp_size=8, tp_rank=0))  # heads % TP
     ctx.close()
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["unfused_attn", "flash_attn"])
+def test_activation_recompute_is_bit_identical(fused, monkeypatch):
+    """with recompute the backward re-runs the forward (same dropout masks) — the
+    outputs, input gradients and parameter gradients must be bit-identical to the stored path."""
+    monkeypatch.setenv("MT_ATTN_FUSED", "1" if fused else "0")
+    hidden, heads, seq, mb = 1024, 8, 256, 2
+    out = []
+    for rc in (False, True):
+        ctx = Context(0)
+        lay = Layer(ctx, PL.layer_desc(hidden, heads, seq, mb, seed=SEED, layer_index=1))
+        lay.set_recompute(rc)
+        params = O.init_params(hidden, SEED, 1)
+        for i, p in enumerate(params):
+            b = np.ascontiguousarray(O.to_bf16_bits(p))
+            lay.set_param(i, b.ctypes.data)
+        x = bf16_tensor(O.normal(O.site_seed(SEED, "input", 0, 0), mb * seq, hidden))
+        g = bf16_tensor(O.normal(O.site_seed(SEED, "grad", 0, 0), mb * seq, hidden, std=1e-2))
+        y, dx = torch.empty_like(x), torch.empty_like(x)
+        s = torch.cuda.current_stream()
+        lay.zero_grads(s)
+        for m in range(2):  # two microbatches in flight, like a pipeline stage
+            lay.forward(x.data_ptr(), y.data_ptr(), m, s)
+        for m in range(2):
+            lay.backward(g.data_ptr(), dx.data_ptr(), m, s)
+        torch.cuda.synchronize()
+        grads = []
+        for i, p in enumerate(params):
+            a = np.empty(p.size, np.float32)
+            lay.get_grad(i, a.ctypes.data)
+            grads.append(a)
+        out.append((y.cpu().view(torch.int16).numpy(), dx.cpu().view(torch.int16).numpy(), grads))
+        lay.close()
+        ctx.close()
+    (y0, dx0, g0), (y1, dx1, g1) = out
+    assert (y0 == y1).all() and (dx0 == dx1).all()
+    for a, b in zip(g0, g1):
+        assert (a == b).all()
