@@ -305,7 +305,8 @@ __global__ void __launch_bounds__(256) bias_dropout_residual_kernel(const uint4*
                                                                     const uint4* __restrict__ bias,
                                                                     const uint4* __restrict__ resid,
                                                                     uint4* __restrict__ out, int nvec_row,
-                                                                    uint64_t seed, uint32_t thresh16, float scale) {
+                                                                    uint64_t seed, uint32_t thresh16, float scale,
+                                                                    uint64_t elem_offset) {
   const int cv = blockIdx.x * blockDim.x + threadIdx.x;
   if (cv >= nvec_row) return;
   const size_t v = (size_t)blockIdx.y * nvec_row + cv;
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(256) bias_dropout_residual_kernel(const uint4*
   unpack8(z[v], a);
   unpack8(bias[cv], b);
   unpack8(resid[v], r);
-  const uint32_t keep = keep_mask8(seed, (uint64_t)v * 8, thresh16);
+  const uint32_t keep = keep_mask8(seed, elem_offset + (uint64_t)v * 8, thresh16);
 #pragma unroll
   for (int j = 0; j < 8; ++j) o[j] = r[j] + (((keep >> j) & 1u) ? (a[j] + b[j]) * scale : 0.f);
   out[v] = pack8(o);
@@ -589,11 +590,11 @@ void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int
 }
 
 void bias_dropout_residual(const void* z, const void* bias, const void* resid, void* out, int rows, int h,
-                           uint64_t seed, uint32_t thresh16, float scale, cudaStream_t s) {
+                           uint64_t seed, uint32_t thresh16, float scale, cudaStream_t s, uint64_t elem_offset) {
   const int nvec_row = h / 8;
   dim3 grid((nvec_row + 255) / 256, rows);
   bias_dropout_residual_kernel<<<grid, 256, 0, s>>>((const uint4*)z, (const uint4*)bias, (const uint4*)resid,
-                                                    (uint4*)out, nvec_row, seed, thresh16, scale);
+                                                    (uint4*)out, nvec_row, seed, thresh16, scale, elem_offset);
 }
 
 #define MT_VPL_DISPATCH(SEQ, LAUNCH) \

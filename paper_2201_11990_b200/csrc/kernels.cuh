@@ -21,9 +21,10 @@ void ln_bwd_dx(const void* dy, const void* x, const void* gamma, const float* me
 void ln_bwd_params(const void* dy, const void* x, const float* mean, const float* rstd, float* dgamma, float* dbeta,
                    int rows, int h, float* workspace, bool accumulate, cudaStream_t s);
 
-// out = resid + dropout(z + bias)
+// out = resid + dropout(z + bias); mask index = elem_offset + (row * h + col) of the rows passed
 void bias_dropout_residual(const void* z, const void* bias, const void* resid, void* out, int rows, int h,
-                           uint64_t site_seed, uint32_t thresh16, float scale, cudaStream_t s);
+                           uint64_t site_seed, uint32_t thresh16, float scale, cudaStream_t s,
+                           uint64_t elem_offset = 0);
 // dz = dropout'(dy) ; dbias (+)= sum_rows dz
 void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int h, uint64_t site_seed,
                            uint32_t thresh16, float scale, float* workspace, bool accumulate, cudaStream_t s);

@@ -247,6 +247,10 @@ extern "C" int mt_ctx_destroy(mt_ctx* c) {
     if (c->comm) cudaStreamDestroy(c->comm);
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
     if (c->ev_done) cudaEventDestroy(c->ev_done);
+    for (int i = 0; i < 4; ++i) {
+      if (c->ev_chunk_ready[i]) cudaEventDestroy(c->ev_chunk_ready[i]);
+      if (c->ev_chunk_done[i]) cudaEventDestroy(c->ev_chunk_done[i]);
+    }
     delete c;
   });
 }
@@ -306,6 +310,11 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
       check_cuda(cudaStreamCreateWithPriority(&c->comm, cudaStreamNonBlocking, hi), "comm stream");
       check_cuda(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming), "event");
       check_cuda(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming), "event");
+      for (int i = 0; i < 4; ++i) {
+        check_cuda(cudaEventCreateWithFlags(&c->ev_chunk_ready[i], cudaEventDisableTiming), "event");
+        check_cuda(cudaEventCreateWithFlags(&c->ev_chunk_done[i], cudaEventDisableTiming), "event");
+      }
+      if (const char* e = getenv("MT_TP_CHUNKS")) c->tp_chunks = std::max(1, std::min(4, atoi(e)));
     }
   });
 }
@@ -612,6 +621,78 @@ bool tp_collectives(const mt_ctx* c, const mt_layer_desc& d) {
   throw std::invalid_argument("TP > 1 needs mt_ctx_init_comm (or mt_ctx_shard_only for a compute-only shard run)");
 }
 
+// Row-parallel output block of the forward: z = in W^T (partial sums), TP all-reduce ("g"), then
+// out = resid + dropout(z + bias) and optionally LayerNorm(out). With TP > 1 the rows are split into
+// c->tp_chunks chunks: the all-reduce of chunk k runs on the comm stream while the GEMM of chunk k+1
+// runs on the SMs left free for it, and the bias/dropout/LayerNorm of chunk k overlaps the
+// all-reduce of chunk k+1. Row chunks keep their global dropout element indices.
+struct LnOut {
+  const void* gamma;
+  const void* beta;
+  void* y;
+  float* mean;
+  float* rstd;
+  float eps;
+};
+
+template <class GemmFor>
+void row_parallel_block(mt_ctx* c, bool tpc, int64_t M, int64_t h, GemmFor gemm_rows, void* z, const void* bias,
+                        const void* resid, void* out, uint64_t site, uint32_t th, float scale, const LnOut* ln,
+                        cudaStream_t st, int& n, const char* gemm_label) {
+  const int chunks = (tpc && M % (c->tp_chunks * 128) == 0) ? c->tp_chunks : 1;
+  const int64_t rows = M / chunks;
+  auto row_ptr = [&](const void* p, int64_t r) {
+    return static_cast<void*>(const_cast<uint16_t*>(static_cast<const uint16_t*>(p)) + r * h);
+  };
+  auto epilogue = [&](int64_t r0, int64_t nr) {
+    bias_dropout_residual(row_ptr(z, r0), bias, row_ptr(resid, r0), row_ptr(out, r0), (int)nr, (int)h, site, th, scale,
+                          st, static_cast<uint64_t>(r0 * h));
+    ++n;
+    if (ln) {
+      ln_fwd(row_ptr(out, r0), ln->gamma, ln->beta, row_ptr(ln->y, r0), ln->mean + r0, ln->rstd + r0, (int)nr, (int)h,
+             ln->eps, st);
+      ++n;
+    }
+  };
+  if (!tpc) {
+    gemm_rows(0, M, 0);
+    mark(c, st, gemm_label);
+    epilogue(0, M);
+    mark(c, st, "fwd.bias_dropout_residual_ln");
+    return;
+  }
+  if (chunks == 1) {
+    gemm_rows(0, M, 0);
+    mark(c, st, gemm_label);
+    check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(row-parallel out)");
+    ++n;
+    mark(c, st, "fwd.tp_allreduce");
+    epilogue(0, M);
+    mark(c, st, "fwd.bias_dropout_residual_ln");
+    return;
+  }
+  int sms = 0;
+  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device), "attr");
+  const int cap = std::max(2, sms - c->comm_sms);
+  for (int k = 0; k < chunks; ++k) {
+    gemm_rows(k * rows, rows, k == 0 ? 0 : cap);  // later chunks share the SMs with the chunk all-reduces
+    check_cuda(cudaEventRecord(c->ev_chunk_ready[k], st), "cudaEventRecord");
+    check_cuda(cudaStreamWaitEvent(c->comm, c->ev_chunk_ready[k], 0), "cudaStreamWaitEvent");
+    ncclComm_t comm = (k + 1 < chunks) ? c->tp_side : c->tp;  // the last chunk overlaps only small kernels
+    check_nccl(ncclAllReduce(row_ptr(z, k * rows), row_ptr(z, k * rows), rows * h, ncclBfloat16, ncclSum, comm,
+                             c->comm),
+               "ncclAllReduce(row-parallel chunk)");
+    ++n;
+    check_cuda(cudaEventRecord(c->ev_chunk_done[k], c->comm), "cudaEventRecord");
+  }
+  mark(c, st, gemm_label);
+  for (int k = 0; k < chunks; ++k) {
+    check_cuda(cudaStreamWaitEvent(st, c->ev_chunk_done[k], 0), "cudaStreamWaitEvent");
+    epilogue(k * rows, rows);
+  }
+  mark(c, st, "fwd.tp_allreduce+bias_dropout_residual_ln");
+}
+
 void ensure_slot_buffers(mt_layer* l, mt_layer::Saved& sv) {
   const int64_t M = l->M, b = l->d.micro_batch, s = l->d.seq, Hl = l->heads_local;
   sv.ln1.ensure(M * l->h * 2);
@@ -721,36 +802,33 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
         .run(st, n);
     mark(c, st, "fwd.attn_pv_gemm");
   }
-  Gemm(sv.ctx.ptr, hl, false, l->param_ptr(MT_P_PROJ_W), hl, false, z, h, M, h, hl).run(st, n);
-  mark(c, st, "fwd.proj_gemm");
-  if (tpc) {
-    check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(attn.out)");
-    ++n;
-    mark(c, st, "fwd.tp_allreduce");
+  {
+    const LnOut ln2{l->param_ptr(MT_P_LN2_GAMMA), l->param_ptr(MT_P_LN2_BETA), sv.ln2.ptr, mean2, rstd2, d.ln_eps};
+    row_parallel_block(
+        c, tpc, M, h,
+        [&](int64_t r0, int64_t nr, int cap) {
+          Gemm(sv.ctx.as<uint16_t>() + r0 * hl, hl, false, l->param_ptr(MT_P_PROJ_W), hl, false,
+               static_cast<uint16_t*>(z) + r0 * h, h, nr, h, hl)
+              .max_ctas(cap)
+              .run(st, n);
+        },
+        z, l->param_ptr(MT_P_PROJ_B), x, sv.x1.ptr, site_out1, th_h, scale_h, &ln2, st, n, "fwd.proj_gemm");
   }
-  bias_dropout_residual(z, l->param_ptr(MT_P_PROJ_B), x, sv.x1.ptr, (int)M, (int)h, site_out1, th_h, scale_h, st);
-  ++n;
-  mark(c, st, "fwd.bias_dropout_residual");
-  ln_fwd(sv.x1.ptr, l->param_ptr(MT_P_LN2_GAMMA), l->param_ptr(MT_P_LN2_BETA), sv.ln2.ptr, mean2, rstd2, (int)M,
-         (int)h, d.ln_eps, st);
-  ++n;
-  mark(c, st, "fwd.ln2");
   Gemm(sv.ln2.ptr, h, false, l->param_ptr(MT_P_FC1_W), h, false, sv.act.ptr, ffl, M, ffl, h)
       .epi(MT_EPI_BIAS_GELU)
       .bias(l->param_ptr(MT_P_FC1_B))
       .aux(sv.pre.ptr, ffl)
       .run(st, n);
   mark(c, st, "fwd.fc1_gemm");
-  Gemm(sv.act.ptr, ffl, false, l->param_ptr(MT_P_FC2_W), ffl, false, z, h, M, h, ffl).run(st, n);
-  mark(c, st, "fwd.fc2_gemm");
-  if (tpc) {
-    check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(mlp.out)");
-    ++n;
-    mark(c, st, "fwd.tp_allreduce");
-  }
-  bias_dropout_residual(z, l->param_ptr(MT_P_FC2_B), sv.x1.ptr, y, (int)M, (int)h, site_out2, th_h, scale_h, st);
-  ++n;
-  mark(c, st, "fwd.bias_dropout_residual");
+  row_parallel_block(
+      c, tpc, M, h,
+      [&](int64_t r0, int64_t nr, int cap) {
+        Gemm(sv.act.as<uint16_t>() + r0 * ffl, ffl, false, l->param_ptr(MT_P_FC2_W), ffl, false,
+             static_cast<uint16_t*>(z) + r0 * h, h, nr, h, ffl)
+            .max_ctas(cap)
+            .run(st, n);
+      },
+      z, l->param_ptr(MT_P_FC2_B), sv.x1.ptr, y, site_out2, th_h, scale_h, nullptr, st, n, "fwd.fc2_gemm");
   check_cuda(cudaGetLastError(), "layer forward launch");
   l->fwd_launches = n;
 }

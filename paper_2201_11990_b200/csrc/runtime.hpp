@@ -78,6 +78,9 @@ struct mt_ctx {
   cudaStream_t comm = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
   int comm_sms = 16;  // SMs kept free for the collective during an overlapped GEMM
+  int tp_chunks = 1;  // >1: forward row-parallel GEMM + all-reduce pipelined over row chunks (MT_TP_CHUNKS;
+                      // measured slower at TP=4 so far, kept opt-in)
+  cudaEvent_t ev_chunk_ready[4] = {}, ev_chunk_done[4] = {};
   // optional per-op timing (MT_OP_TIMING=1): stream-ordered marks between consecutive layer ops
   bool op_timing = false;
   std::vector<std::pair<const char*, cudaEvent_t>> marks;
