@@ -187,6 +187,31 @@ int mt_layer_adam_step(mt_layer* l, const mt_adam_desc* d, float* grad_norm_out,
 /* Read back the optimizer state of a parameter shard (fp32, shard_shape elements each; NULL skips). */
 int mt_layer_get_optimizer_state(mt_layer* l, int32_t param, float* master, float* m, float* v);
 
+/* ------------------------------------------------------------------ vocab */
+/* Vocab-parallel word embedding (+ replicated learned position embedding, embedding dropout), final
+ * LayerNorm and tied LM head with vocab-parallel cross-entropy (Megatron). The table is padded to a
+ * multiple of 128 * TP rows; rank r owns rows [r * V_pad / TP, (r + 1) * V_pad / TP). */
+typedef struct mt_vocab mt_vocab;
+typedef struct mt_vocab_desc {
+  int32_t vocab, hidden, seq, micro_batch, tp_size, tp_rank;
+  float dropout, ln_eps;
+  uint64_t seed;
+} mt_vocab_desc;
+int mt_vocab_create(mt_ctx* ctx, const mt_vocab_desc* d, mt_vocab** out);
+int mt_vocab_destroy(mt_vocab* v);
+int mt_vocab_padded(const mt_vocab* v, int64_t* vocab_padded, int64_t* slice_begin, int64_t* slice_rows);
+/* param 0: word embedding [V_pad, h] (global bf16, this rank's rows are copied), 1: position [seq, h],
+ * 2: final-LN gamma [h], 3: final-LN beta [h]. Gradients are fp32 of this rank's shard. */
+int mt_vocab_set_param(mt_vocab* v, int32_t param, const void* host_global_bf16);
+int mt_vocab_get_grad(mt_vocab* v, int32_t param, float* host);
+int mt_vocab_zero_grads(mt_vocab* v, void* stream);
+/* x (device bf16 [b*s, h]) = dropout(E[tokens] + P[pos]); tokens device int32 [b*s]. */
+int mt_vocab_embed_forward(mt_vocab* v, const int32_t* tokens, void* x, uint32_t micro_batch, void* stream);
+/* scatter-add of the embedding gradient (dx = gradient w.r.t. the embedding output). */
+int mt_vocab_embed_backward(mt_vocab* v, const int32_t* tokens, const void* dx, uint32_t micro_batch, void* stream);
+/* loss_dev += mean cross-entropy of LN_f(y) E^T against targets; dy = d loss / d y (forward+backward). */
+int mt_vocab_head_loss(mt_vocab* v, const void* y, const int32_t* targets, void* dy, float* loss_dev, void* stream);
+
 /* ------------------------------------------------------------------ pipeline stage (1F1B driver) */
 typedef struct mt_stage mt_stage;
 typedef struct mt_stage_desc {

@@ -65,6 +65,12 @@ class AdamDesc(C.Structure):
                 ("eps", C.c_float), ("weight_decay", C.c_float), ("grad_clip", C.c_float), ("step", C.c_int64)]
 
 
+class VocabDesc(C.Structure):
+    _fields_ = [("vocab", C.c_int32), ("hidden", C.c_int32), ("seq", C.c_int32), ("micro_batch", C.c_int32),
+                ("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("dropout", C.c_float), ("ln_eps", C.c_float),
+                ("seed", C.c_uint64)]
+
+
 class StageDesc(C.Structure):
     _fields_ = [("layer", LayerDesc), ("layers", C.c_int32), ("micro_batches", C.c_int32)]
 
@@ -116,6 +122,15 @@ _SIGS = {
     "mt_layer_launch_counts": (C.c_int, [P, PI32, PI32]),
     "mt_layer_set_recompute": (C.c_int, [P, I32]),
     "mt_stage_set_recompute": (C.c_int, [P, I32]),
+    "mt_vocab_create": (C.c_int, [P, C.POINTER(VocabDesc), C.POINTER(P)]),
+    "mt_vocab_destroy": (C.c_int, [P]),
+    "mt_vocab_padded": (C.c_int, [P, PI64, PI64, PI64]),
+    "mt_vocab_set_param": (C.c_int, [P, I32, P]),
+    "mt_vocab_get_grad": (C.c_int, [P, I32, PF32]),
+    "mt_vocab_zero_grads": (C.c_int, [P, P]),
+    "mt_vocab_embed_forward": (C.c_int, [P, P, P, U32, P]),
+    "mt_vocab_embed_backward": (C.c_int, [P, P, P, U32, P]),
+    "mt_vocab_head_loss": (C.c_int, [P, P, P, P, P, P]),
     "mt_layer_grad_buffer": (C.c_int, [P, C.POINTER(PF32), PI64]),
     "mt_mse_loss": (C.c_int, [P, P, P, P, I64, P]),
     "mt_fill_normal": (C.c_int, [P, I64, U64, F32, F32, P]),

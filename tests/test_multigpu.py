@@ -50,7 +50,45 @@ def _worker(rank, world, port, mode, q):
         ctx = Context(rank)
         s = torch.cuda.current_stream()
         out = {}
-        if mode == "tp":
+        if mode == "vocab":
+            import ctypes as C
+            from paper_2201_11990_b200._native import VocabDesc, check, lib
+            ctx.init_comm(obj[0], world, rank, tensor=world)
+            V, h, s_, b = 1000, 256, 128, 2
+            M = s_ * b
+            hv = C.c_void_p()
+            check(lib().mt_vocab_create(ctx._h, C.byref(VocabDesc(V, h, s_, b, world, rank, 0.1, 1e-5, SEED)),
+                                        C.byref(hv)))
+            vpad, v0, vp = C.c_int64(), C.c_int64(), C.c_int64()
+            check(lib().mt_vocab_padded(hv, C.byref(vpad), C.byref(v0), C.byref(vp)))
+            rng = np.random.default_rng(0)
+            bfr = lambda a: O.from_bf16_bits(O.to_bf16_bits(a))  # noqa
+            word = bfr(rng.standard_normal((vpad.value, h)).astype(np.float32) * 0.05)
+            pos = bfr(rng.standard_normal((s_, h)).astype(np.float32) * 0.02)
+            g = bfr(1 + rng.standard_normal(h).astype(np.float32) * 0.02)
+            be = bfr(rng.standard_normal(h).astype(np.float32) * 0.02)
+            for i, a in enumerate((word, pos, g, be)):
+                bits = np.ascontiguousarray(O.to_bf16_bits(a))
+                check(lib().mt_vocab_set_param(hv, i, bits.ctypes.data))
+            tokens = rng.integers(0, V, M).astype(np.int32)
+            targets = rng.integers(0, V, M).astype(np.int32)
+            y = bfr(rng.standard_normal((M, h)).astype(np.float32))
+            dev = lambda a: torch.from_numpy(O.to_bf16_bits(a).view(np.int16)).view(torch.bfloat16).cuda()  # noqa
+            tok_d, tgt_d = torch.from_numpy(tokens).cuda(), torch.from_numpy(targets).cuda()
+            x_d, y_d = torch.empty(M, h, dtype=torch.bfloat16, device="cuda"), dev(y)
+            dy_d, loss_d = torch.empty_like(y_d), torch.zeros(1, device="cuda")
+            sp = C.c_void_p(s.cuda_stream)
+            check(lib().mt_vocab_embed_forward(hv, C.c_void_p(tok_d.data_ptr()), C.c_void_p(x_d.data_ptr()), 0, sp))
+            check(lib().mt_vocab_head_loss(hv, C.c_void_p(y_d.data_ptr()), C.c_void_p(tgt_d.data_ptr()),
+                                           C.c_void_p(dy_d.data_ptr()), C.c_void_p(loss_d.data_ptr()), sp))
+            torch.cuda.synchronize()
+            gw = np.empty(vp.value * h, np.float32)
+            check(lib().mt_vocab_get_grad(hv, 0, gw.ctypes.data_as(C.POINTER(C.c_float))))
+            out.update(x=x_d.float().cpu().numpy(), loss=float(loss_d.item()), dy=dy_d.float().cpu().numpy(),
+                       gword=gw.reshape(vp.value, h), v0=v0.value, vp=vp.value,
+                       args=(V, h, s_, b, word, pos, g, be, tokens, targets, y))
+            lib().mt_vocab_destroy(hv)
+        elif mode == "tp":
             ctx.init_comm(obj[0], world, rank, tensor=world)
             d = PL.layer_desc(H, HEADS, S, B, tp_size=world, tp_rank=rank, seed=SEED, layer_index=0)
             lay = Layer(ctx, d)
@@ -203,3 +241,23 @@ def test_data_parallel_gradient_allreduce_two_gpus():
         assert abs(res[r]["grad_norm"] - norm) / norm < 2e-2
         for i in range(12):
             assert rel(res[r]["grads"][0][i], grads[0][i] / 2) < 2e-2, (r, i)
+
+
+@pytest.mark.timeout(900)
+def test_vocab_parallel_head_two_gpus():
+    """N3 at TP=2: each rank holds half of the (padded) vocabulary; the loss, the embedding output
+    and dL/dy agree with the unsharded numpy reference on both ranks; the word-embedding gradient
+    shards tile the full gradient."""
+    _need(2)
+    from tests.test_vocab_gpu import reference
+    res = _run("vocab")
+    V, h, s_, b, word, pos, g, be, tokens, targets, y = res[0]["args"]
+    x_ref, loss_ref, dy_ref, dword_ref, _, _, _ = reference(V, h, s_, b, 0.1, word, pos, g, be, tokens, targets, y,
+                                                            np.zeros((s_ * b, h), np.float32))
+    full = np.zeros_like(dword_ref)
+    for r in (0, 1):
+        assert rel(res[r]["x"], x_ref) < 5e-3
+        assert abs(res[r]["loss"] - loss_ref) / loss_ref < 2e-3
+        assert rel(res[r]["dy"], dy_ref) < 2e-2
+        full[res[r]["v0"]:res[r]["v0"] + res[r]["vp"]] = res[r]["gword"]
+    assert rel(full, dword_ref) < 2e-2
