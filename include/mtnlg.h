@@ -204,6 +204,8 @@ int mt_vocab_padded(const mt_vocab* v, int64_t* vocab_padded, int64_t* slice_beg
  * 2: final-LN gamma [h], 3: final-LN beta [h]. Gradients are fp32 of this rank's shard. */
 int mt_vocab_set_param(mt_vocab* v, int32_t param, const void* host_global_bf16);
 int mt_vocab_get_grad(mt_vocab* v, int32_t param, float* host);
+/* This rank's shard of a parameter (bf16; word: [slice_rows, h]). */
+int mt_vocab_get_param(mt_vocab* v, int32_t param, void* host_bf16);
 int mt_vocab_zero_grads(mt_vocab* v, void* stream);
 /* x (device bf16 [b*s, h]) = dropout(E[tokens] + P[pos]); tokens device int32 [b*s]. */
 int mt_vocab_embed_forward(mt_vocab* v, const int32_t* tokens, void* x, uint32_t micro_batch, void* stream);
@@ -242,6 +244,13 @@ int mt_stage_set_recompute(mt_stage* st, int32_t enable);
  * summed over the model-parallel group (TP and PP; TP-replicated parameters counted once; DP
  * replicas already hold the averaged gradient), clipped to grad_clip, then fused AdamW. */
 int mt_stage_optimizer_step(mt_stage* st, const mt_adam_desc* d, float* grad_norm_out, void* stream);
+/* Attach the vocab module (not owned; must outlive the stage) so the stage trains a language model:
+ * the first stage embeds int32 token ids, the last stage runs the tied LM head + cross-entropy
+ * against int32 target ids. Inputs/targets of mt_stage_train_step(_dev) then become int32
+ * [MB][b*s] token arrays. With PP > 1 the word-embedding gradient is all-reduced between the first
+ * and the last stage (tied weights, Megatron); DP averages all vocab gradients; the optimizer step
+ * covers the vocab parameters (word embedding counted once in the gradient norm). */
+int mt_stage_attach_vocab(mt_stage* st, mt_vocab* v);
 
 #ifdef __cplusplus
 }

@@ -127,6 +127,7 @@ _SIGS = {
     "mt_vocab_padded": (C.c_int, [P, PI64, PI64, PI64]),
     "mt_vocab_set_param": (C.c_int, [P, I32, P]),
     "mt_vocab_get_grad": (C.c_int, [P, I32, PF32]),
+    "mt_vocab_get_param": (C.c_int, [P, I32, P]),
     "mt_vocab_zero_grads": (C.c_int, [P, P]),
     "mt_vocab_embed_forward": (C.c_int, [P, P, P, U32, P]),
     "mt_vocab_embed_backward": (C.c_int, [P, P, P, U32, P]),
@@ -145,6 +146,7 @@ _SIGS = {
     "mt_stage_train_step_dev": (C.c_int, [P, P, P, P, P]),
     "mt_stage_launch_count": (C.c_int, [P, PI64]),
     "mt_stage_optimizer_step": (C.c_int, [P, C.POINTER(AdamDesc), PF32, P]),
+    "mt_stage_attach_vocab": (C.c_int, [P, P]),
     "mt_adam_defaults": (C.c_int, [C.POINTER(AdamDesc)]),
     "mt_layer_adam_step": (C.c_int, [P, C.POINTER(AdamDesc), PF32, P]),
     "mt_layer_get_optimizer_state": (C.c_int, [P, I32, PF32, PF32, PF32]),

@@ -169,6 +169,33 @@ void layer_adamw(mt_layer* l, const mt_adam_desc& d, float lr, const float* clip
   check_cuda(cudaGetLastError(), "adamw");
 }
 
+// Generic parameter slices (used by the vocab module): n must be a multiple of 4.
+void grad_sq_segment(const float* g, int64_t n, float* out, cudaStream_t s) {
+  grad_sq_kernel<<<grid_for(n / 4), 256, 0, s>>>(reinterpret_cast<const float4*>(g), n / 4, out);
+  check_cuda(cudaGetLastError(), "grad_sq");
+}
+
+void adamw_segment(const float* g, float* m, float* v, float* master, void* w_bf16, int64_t n, const mt_adam_desc& d,
+                   float lr, int decay, const float* clip, cudaStream_t s) {
+  AdamScalars a;
+  a.lr = lr;
+  a.beta1 = d.beta1;
+  a.beta2 = d.beta2;
+  a.eps = d.eps;
+  a.weight_decay = d.weight_decay;
+  a.bc1 = 1.f - std::pow(d.beta1, (float)d.step);
+  a.bc2 = 1.f - std::pow(d.beta2, (float)d.step);
+  adamw_kernel<<<grid_for(n / 4), 256, 0, s>>>(reinterpret_cast<const float4*>(g), reinterpret_cast<float4*>(m),
+                                               reinterpret_cast<float4*>(v), reinterpret_cast<float4*>(master),
+                                               reinterpret_cast<uint2*>(w_bf16), n / 4, a, decay, clip);
+  check_cuda(cudaGetLastError(), "adamw");
+}
+
+void bf16_to_f32(const void* w, float* out, int64_t n, cudaStream_t s) {
+  bf16_to_f32_kernel<<<grid_for(n), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(w), out, n);
+  check_cuda(cudaGetLastError(), "bf16_to_f32");
+}
+
 void clip_coefficient(const float* sq, float max_norm, float* out, cudaStream_t s) {
   clip_coef_kernel<<<1, 1, 0, s>>>(sq, max_norm, out);
   check_cuda(cudaGetLastError(), "clip_coef");

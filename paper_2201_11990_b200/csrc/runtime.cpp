@@ -240,7 +240,7 @@ extern "C" int mt_ctx_create(int32_t device, mt_ctx** out) {
 extern "C" int mt_ctx_destroy(mt_ctx* c) {
   return guarded([&] {
     if (!c) return;
-    for (ncclComm_t* cm : {&c->tp_side, &c->tp, &c->pp, &c->dp, &c->world})
+    for (ncclComm_t* cm : {&c->emb, &c->tp_side, &c->tp, &c->pp, &c->dp, &c->world})
       if (*cm) ncclCommDestroy(*cm);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (auto& m : c->marks) cudaEventDestroy(m.second);
@@ -304,6 +304,11 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
     check_nccl(ncclCommSplit(c->world, tp_color, me.tensor, &c->tp_side, &side_cfg), "ncclCommSplit(tp_side)");
     check_nccl(ncclCommSplit(c->world, pp_color, me.pipeline, &c->pp, nullptr), "ncclCommSplit(pp)");
     check_nccl(ncclCommSplit(c->world, dp_color, me.data, &c->dp, nullptr), "ncclCommSplit(dp)");
+    if (p.pipeline > 1) {  // tied word embeddings live on the first and the last stage
+      const bool ends = me.pipeline == 0 || me.pipeline == p.pipeline - 1;
+      check_nccl(ncclCommSplit(c->world, ends ? pp_color : NCCL_SPLIT_NOCOLOR, me.pipeline, &c->emb, nullptr),
+                 "ncclCommSplit(emb)");
+    }
     if (p.tensor > 1) {
       int lo = 0, hi = 0;
       check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");

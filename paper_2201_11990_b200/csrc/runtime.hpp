@@ -51,6 +51,20 @@ void ensure_optimizer_state(mt_layer* l, cudaStream_t s);
 void layer_grad_sq(mt_layer* l, float* sq, cudaStream_t s);
 void layer_adamw(mt_layer* l, const mt_adam_desc& d, float lr, const float* clip_coef, cudaStream_t s);
 void clip_coefficient(const float* sq, float max_norm, float* out, cudaStream_t s);
+void grad_sq_segment(const float* g, int64_t n, float* out, cudaStream_t s);
+void adamw_segment(const float* g, float* m, float* v, float* master, void* w_bf16, int64_t n, const mt_adam_desc& d,
+                   float lr, int decay, const float* clip, cudaStream_t s);
+void bf16_to_f32(const void* w, float* out, int64_t n, cudaStream_t s);
+// vocab module hooks for the stage driver (vocab.cu)
+int64_t vocab_tokens(const mt_vocab* v);  // b*s
+int64_t vocab_hidden(const mt_vocab* v);
+int vocab_tp(const mt_vocab* v);
+void vocab_zero_grads(mt_vocab* v, cudaStream_t s);
+// first: word embedding counted in the norm (once per model-parallel group); pos/LN_f always
+// (they are zero where unused); sq[0] sharded, sq[1] TP-replicated
+void vocab_grad_sq(mt_vocab* v, bool count_word, float* sq, cudaStream_t s);
+void vocab_adamw(mt_vocab* v, const mt_adam_desc& d, float lr, const float* clip, cudaStream_t s);
+void vocab_allreduce_grads(mt_vocab* v, ncclComm_t comm, bool word_only, bool average, cudaStream_t s);
 
 }  // namespace mt
 
@@ -60,10 +74,11 @@ struct mt_ctx {
   curator::ParallelConfig par;
   curator::RankPlacement place;
   ncclComm_t world = nullptr, tp = nullptr, pp = nullptr, dp = nullptr;
-  ncclComm_t tp_side = nullptr;
+  ncclComm_t tp_side = nullptr;  // same TP group, CTA-capped: collectives overlapped with GEMMs
+  ncclComm_t emb = nullptr;  // PP > 1: first + last stage of the same (dp, tp): tied word-embedding grads
   // compute-only measurement of one TP shard on a single GPU: the layer skips its TP collectives
   // (mt_ctx_shard_only); never set in a real multi-GPU run
-  bool shard_only = false;  // same TP group, CTA-capped: collectives overlapped with GEMMs
+  bool shard_only = false;
   // scratch shared by all layers of this context (sized to the largest layer)
   mt::DeviceBuffer scratch_h[4];   // [M, h] bf16 temporaries
   mt::DeviceBuffer scratch_ffn;    // [M, ffn/t] bf16

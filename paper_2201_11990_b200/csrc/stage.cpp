@@ -36,6 +36,9 @@ struct mt_stage {
   cudaEvent_t iter_start = nullptr;
   std::vector<cudaEvent_t> in_ev, tgt_ev;
   std::vector<mt::DeviceBuffer> targets;           // [MB][M, h] (host-target path)
+  // language-model mode (mt_stage_attach_vocab): inputs/targets are int32 token ids [MB][M]
+  mt_vocab* vocab = nullptr;
+  std::vector<mt::DeviceBuffer> tokens;            // [MB][M] int32 (host-input path, first stage)
 };
 
 namespace {
@@ -62,15 +65,18 @@ void ok(int rc) {
 struct Step {
   mt_stage* st;
   cudaStream_t s;
-  const uint16_t* in_host;
-  const uint16_t* tgt_host;
-  const uint16_t* in_dev = nullptr;   // device-resident inputs (train_step_dev)
-  const uint16_t* tgt_dev = nullptr;
+  const char* in_host;
+  const char* tgt_host;
+  const char* in_dev = nullptr;   // device-resident inputs (train_step_dev)
+  const char* tgt_dev = nullptr;
   int64_t launches = 0;
   bool first() const { return st->stage == 0; }
   bool last() const { return st->stage == st->stages - 1; }
   size_t bytes() const { return static_cast<size_t>(st->M * st->h * 2); }
   int64_t elems() const { return st->M * st->h; }
+  // bytes of one microbatch's input / target: bf16 activations, or int32 token ids with a vocab
+  size_t io_bytes() const { return st->vocab ? static_cast<size_t>(st->M * 4) : bytes(); }
+  bool lm() const { return st->vocab != nullptr; }
   ncclComm_t pp() const { return st->ctx->pp; }
   // Global microbatch id (data-parallel replicas see different samples): keys the synthetic
   // inputs/targets and the dropout masks of the microbatch.
@@ -79,7 +85,7 @@ struct Step {
   }
 
   const void* input(int mb) const {
-    return (in_dev && first()) ? static_cast<const void*>(in_dev + mb * elems()) : st->act[mb][0].ptr;
+    return (in_dev && first() && !lm()) ? static_cast<const void*>(in_dev + mb * io_bytes()) : st->act[mb][0].ptr;
   }
   // Queue every microbatch's host->device copies on the copy stream (after the previous
   // iteration's compute released the buffers).
@@ -89,22 +95,31 @@ struct Step {
     mt::check_cuda(cudaStreamWaitEvent(st->copy, st->iter_start, 0), "cudaStreamWaitEvent");
     for (int mb = 0; mb < st->d.micro_batches; ++mb) {
       if (in_host && first()) {
-        mt::check_cuda(cudaMemcpyAsync(st->act[mb][0].ptr, in_host + mb * elems(), bytes(), cudaMemcpyHostToDevice,
-                                       st->copy),
+        void* dst = lm() ? st->tokens[mb].ptr : st->act[mb][0].ptr;
+        mt::check_cuda(cudaMemcpyAsync(dst, in_host + mb * io_bytes(), io_bytes(), cudaMemcpyHostToDevice, st->copy),
                        "H2D input");
         mt::check_cuda(cudaEventRecord(st->in_ev[mb], st->copy), "cudaEventRecord");
       }
       if (tgt_host && last()) {
-        mt::check_cuda(cudaMemcpyAsync(st->targets[mb].ptr, tgt_host + mb * elems(), bytes(), cudaMemcpyHostToDevice,
-                                       st->copy),
+        mt::check_cuda(cudaMemcpyAsync(st->targets[mb].ptr, tgt_host + mb * io_bytes(), io_bytes(),
+                                       cudaMemcpyHostToDevice, st->copy),
                        "H2D target");
         mt::check_cuda(cudaEventRecord(st->tgt_ev[mb], st->copy), "cudaEventRecord");
       }
     }
   }
+  const int32_t* tokens(int mb) const {
+    return in_dev ? reinterpret_cast<const int32_t*>(in_dev + mb * io_bytes()) : st->tokens[mb].as<int32_t>();
+  }
   void load_input(int mb) {
-    if (in_dev) return;  // read in place by layer 0
     void* dst = st->act[mb][0].ptr;
+    if (lm()) {  // token ids -> embeddings (+ position, dropout; TP all-reduce of the vocab-parallel gather)
+      if (in_host) mt::check_cuda(cudaStreamWaitEvent(s, st->in_ev[mb], 0), "cudaStreamWaitEvent");
+      ok(mt_vocab_embed_forward(st->vocab, tokens(mb), dst, gid(mb), s));
+      launches += 2 + (st->ctx->par.tensor > 1 ? 1 : 0);
+      return;
+    }
+    if (in_dev) return;  // read in place by layer 0
     if (in_host) {
       mt::check_cuda(cudaStreamWaitEvent(s, st->in_ev[mb], 0), "cudaStreamWaitEvent");
     } else {
@@ -123,9 +138,17 @@ struct Step {
     }
     if (last()) {
       void* y = st->act[mb][st->layers.size()].ptr;
+      if (lm()) {
+        const int32_t* tgt = tgt_dev ? reinterpret_cast<const int32_t*>(tgt_dev + mb * io_bytes())
+                                     : st->targets[mb].as<int32_t>();
+        if (!tgt_dev) mt::check_cuda(cudaStreamWaitEvent(s, st->tgt_ev[mb], 0), "cudaStreamWaitEvent");
+        ok(mt_vocab_head_loss(st->vocab, y, tgt, y, st->loss.as<float>(), s));  // dy overwrites y in place
+        launches += 10 + (st->ctx->par.tensor > 1 ? 3 : 0);
+        return;
+      }
       const void* tgt = st->target.ptr;
       if (tgt_dev) {
-        tgt = tgt_dev + mb * elems();
+        tgt = tgt_dev + mb * io_bytes();
       } else if (tgt_host) {
         mt::check_cuda(cudaStreamWaitEvent(s, st->tgt_ev[mb], 0), "cudaStreamWaitEvent");
         tgt = st->targets[mb].ptr;
@@ -148,6 +171,10 @@ struct Step {
       mt_layer_launch_counts(st->layers[i], &f, &b);
       launches += b;
       cur = out;
+    }
+    if (lm() && first()) {
+      ok(mt_vocab_embed_backward(st->vocab, tokens(mb), cur, gid(mb), s));
+      ++launches;
     }
     return cur;
   }
@@ -244,6 +271,8 @@ void run_iteration(Step& k, mt_stage* st, void* stream) {
   const int MB = st->d.micro_batches;
   k.prefetch_host();
   for (auto* l : st->layers) ok(mt_layer_zero_grads(l, stream));
+  const bool vocab_here = k.lm() && (k.first() || k.last());
+  if (vocab_here) mt::vocab_zero_grads(st->vocab, k.s);
   mt::check_cuda(cudaMemsetAsync(st->loss.ptr, 0, 4, k.s), "memset loss");
   const int warmup = std::min(st->stages - st->stage - 1, MB);
   const int steady = MB - warmup;
@@ -296,8 +325,17 @@ void run_iteration(Step& k, mt_stage* st, void* stream) {
       ++k.launches;
     }
   }
+  // tied word embedding: the first and the last stage both hold E and sum their gradients
+  if (vocab_here && st->stages > 1) {
+    mt::vocab_allreduce_grads(st->vocab, st->ctx->emb, true, false, k.s);
+    ++k.launches;
+  }
   // data-parallel gradient all-reduce (mean)
   if (st->ctx->par.data > 1) {
+    if (vocab_here) {
+      mt::vocab_allreduce_grads(st->vocab, st->ctx->dp, false, true, k.s);
+      k.launches += 4;
+    }
     for (auto* l : st->layers) {
       ok(mt_dp_allreduce_f32(st->ctx, l->grads.as<float>(), l->param_total, 1, stream));
       ++k.launches;
@@ -315,8 +353,9 @@ extern "C" int mt_stage_train_step(mt_stage* st, const void* inputs_host, const 
                                    void* stream) {
   return call([&] {
     if (!st) throw std::invalid_argument("null stage");
-    Step k{st, (cudaStream_t)stream, static_cast<const uint16_t*>(inputs_host),
-           static_cast<const uint16_t*>(targets_host)};
+    Step k{st, (cudaStream_t)stream, static_cast<const char*>(inputs_host), static_cast<const char*>(targets_host)};
+    if (k.lm() && ((k.first() && !inputs_host) || (k.last() && !targets_host)))
+      throw std::invalid_argument("a stage with a vocab needs token inputs (first stage) and targets (last stage)");
     run_iteration(k, st, stream);
     if (loss_out) {
       float host = 0.f;
@@ -333,8 +372,8 @@ extern "C" int mt_stage_train_step_dev(mt_stage* st, const void* inputs_dev, con
   return call([&] {
     if (!st) throw std::invalid_argument("null stage");
     Step k{st, (cudaStream_t)stream, nullptr, nullptr};
-    k.in_dev = static_cast<const uint16_t*>(inputs_dev);
-    k.tgt_dev = static_cast<const uint16_t*>(targets_dev);
+    k.in_dev = static_cast<const char*>(inputs_dev);
+    k.tgt_dev = static_cast<const char*>(targets_dev);
     if (k.first() && !k.in_dev) throw std::invalid_argument("first stage needs device inputs");
     if (k.last() && !k.tgt_dev) throw std::invalid_argument("last stage needs device targets");
     run_iteration(k, st, stream);
@@ -361,6 +400,9 @@ extern "C" int mt_stage_optimizer_step(mt_stage* st, const mt_adam_desc* d, floa
       ok(mt_layer_grad_buffer(l, &g, &n));  // materialises logically-zero grads if needed
       mt::layer_grad_sq(l, sq, s);
     }
+    const bool first = st->stage == 0, last = st->stage == st->stages - 1;
+    const bool vocab_here = st->vocab && (first || last);
+    if (vocab_here) mt::vocab_grad_sq(st->vocab, first, sq, s);  // tied E counted once (first stage)
     // TP-replicated parameters (LayerNorm, row-parallel biases) count once per TP group
     if (c->place.tensor != 0) mt::check_cuda(cudaMemsetAsync(sq + 1, 0, sizeof(float), s), "memset");
     if (c->par.tensor > 1 && c->tp)
@@ -370,6 +412,7 @@ extern "C" int mt_stage_optimizer_step(mt_stage* st, const mt_adam_desc* d, floa
     mt::clip_coefficient(sq, d->grad_clip, sq + 2, s);
     const float lr = resolve_lr(*d);
     for (auto* l : st->layers) mt::layer_adamw(l, *d, lr, sq + 3, s);
+    if (vocab_here) mt::vocab_adamw(st->vocab, *d, lr, sq + 3, s);
     if (grad_norm_out) {
       mt::check_cuda(cudaMemcpyAsync(grad_norm_out, sq + 2, sizeof(float), cudaMemcpyDeviceToHost, s), "D2H norm");
       mt::check_cuda(cudaStreamSynchronize(s), "sync");
@@ -381,5 +424,24 @@ extern "C" int mt_stage_set_recompute(mt_stage* st, int32_t enable) {
   return call([&] {
     if (!st) throw std::invalid_argument("null stage");
     for (auto* l : st->layers) ok(mt_layer_set_recompute(l, enable));
+  });
+}
+
+extern "C" int mt_stage_attach_vocab(mt_stage* st, mt_vocab* v) {
+  return call([&] {
+    if (!st || !v) throw std::invalid_argument("null argument");
+    if (mt::vocab_tokens(v) != st->M || mt::vocab_hidden(v) != st->h)
+      throw std::invalid_argument("vocab shape (micro_batch * seq, hidden) does not match the stage");
+    if (mt::vocab_tp(v) != st->ctx->par.tensor && !st->ctx->shard_only)
+      throw std::invalid_argument("vocab tp_size does not match the tensor-parallel degree");
+    if (st->stages > 1 && !st->ctx->emb && (st->stage == 0 || st->stage == st->stages - 1))
+      throw std::invalid_argument("pipeline-parallel vocab needs the embedding communicator (mt_ctx_init_comm)");
+    st->vocab = v;
+    const size_t tok_bytes = static_cast<size_t>(st->M * 4);
+    if (st->stage == 0) {
+      st->tokens.resize(st->d.micro_batches);
+      for (auto& b : st->tokens) b.ensure(tok_bytes);
+    }
+    // targets buffers (sized for bf16 activations) already hold M int32 ids
   });
 }

@@ -33,6 +33,11 @@ struct mt_vocab {
   mt::DeviceBuffer logits;                          // fp32 [M, vp]
   mt::DeviceBuffer dlogits;                         // bf16 [M, vp]
   mt::DeviceBuffer yn, stats, rowbuf, dyn, ws;      // LN_f out, mean/rstd, per-row CE scalars, dLN_f out
+  // optimizer state (fp32 master, Adam m, v) per parameter, created on the first optimizer step
+  mt::DeviceBuffer opt_master[4], opt_m[4], opt_v[4];
+  mt::DeviceBuffer* param(int i) { return i == 0 ? &word : i == 1 ? &pos : i == 2 ? &lnf_g : &lnf_b; }
+  mt::DeviceBuffer* grad(int i) { return i == 0 ? &g_word : i == 1 ? &g_pos : i == 2 ? &g_lnf_g : &g_lnf_b; }
+  int64_t count(int i) const { return i == 0 ? vp * h : i == 1 ? int64_t{d.seq} * h : h; }
 };
 
 namespace {
@@ -272,6 +277,14 @@ extern "C" int mt_vocab_set_param(mt_vocab* v, int32_t param, const void* host_g
   });
 }
 
+extern "C" int mt_vocab_get_param(mt_vocab* v, int32_t param, void* host) {
+  return call([&] {
+    if (param < 0 || param > 3) throw std::invalid_argument("unknown vocab parameter");
+    check_cuda(cudaDeviceSynchronize(), "sync");
+    check_cuda(cudaMemcpy(host, v->param(param)->ptr, v->count(param) * 2, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
 extern "C" int mt_vocab_get_grad(mt_vocab* v, int32_t param, float* host) {
   return call([&] {
     check_cuda(cudaDeviceSynchronize(), "sync");
@@ -284,14 +297,49 @@ extern "C" int mt_vocab_get_grad(mt_vocab* v, int32_t param, float* host) {
   });
 }
 
+namespace mt {
+int64_t vocab_tokens(const mt_vocab* v) { return v->M; }
+int64_t vocab_hidden(const mt_vocab* v) { return v->h; }
+int vocab_tp(const mt_vocab* v) { return v->d.tp_size; }
+
+void vocab_zero_grads(mt_vocab* v, cudaStream_t s) {
+  for (int i = 0; i < 4; ++i) check_cuda(cudaMemsetAsync(v->grad(i)->ptr, 0, v->count(i) * 4, s), "memset");
+}
+
+void vocab_grad_sq(mt_vocab* v, bool count_word, float* sq, cudaStream_t s) {
+  if (count_word) grad_sq_segment(v->g_word.as<float>(), v->count(0), sq, s);  // vocab-sharded
+  for (int i = 1; i < 4; ++i) grad_sq_segment(v->grad(i)->as<float>(), v->count(i), sq + 1, s);  // replicated
+}
+
+// AdamW on the four vocab parameters; weight decay on the embeddings, not on LN_f (Megatron).
+void vocab_adamw(mt_vocab* v, const mt_adam_desc& d, float lr, const float* clip, cudaStream_t s) {
+  for (int i = 0; i < 4; ++i) {
+    const int64_t n = v->count(i);
+    if (!v->opt_master[i].ptr) {
+      v->opt_master[i].ensure(n * 4);
+      v->opt_m[i].ensure(n * 4);
+      v->opt_v[i].ensure(n * 4);
+      check_cuda(cudaMemsetAsync(v->opt_m[i].ptr, 0, n * 4, s), "memset m");
+      check_cuda(cudaMemsetAsync(v->opt_v[i].ptr, 0, n * 4, s), "memset v");
+      bf16_to_f32(v->param(i)->ptr, v->opt_master[i].as<float>(), n, s);
+    }
+    adamw_segment(v->grad(i)->as<float>(), v->opt_m[i].as<float>(), v->opt_v[i].as<float>(),
+                  v->opt_master[i].as<float>(), v->param(i)->ptr, n, d, lr, i < 2 ? 1 : 0, clip, s);
+  }
+}
+
+void vocab_allreduce_grads(mt_vocab* v, ncclComm_t comm, bool word_only, bool average, cudaStream_t s) {
+  check_nccl(ncclGroupStart(), "group");
+  for (int i = 0; i < (word_only ? 1 : 4); ++i)
+    check_nccl(ncclAllReduce(v->grad(i)->ptr, v->grad(i)->ptr, v->count(i), ncclFloat32, average ? ncclAvg : ncclSum,
+                             comm, s),
+               "ncclAllReduce(vocab grads)");
+  check_nccl(ncclGroupEnd(), "group");
+}
+}  // namespace mt
+
 extern "C" int mt_vocab_zero_grads(mt_vocab* v, void* stream) {
-  return call([&] {
-    cudaStream_t s = (cudaStream_t)stream;
-    check_cuda(cudaMemsetAsync(v->g_word.ptr, 0, v->vp * v->h * 4, s), "memset");
-    check_cuda(cudaMemsetAsync(v->g_pos.ptr, 0, int64_t{v->d.seq} * v->h * 4, s), "memset");
-    check_cuda(cudaMemsetAsync(v->g_lnf_g.ptr, 0, v->h * 4, s), "memset");
-    check_cuda(cudaMemsetAsync(v->g_lnf_b.ptr, 0, v->h * 4, s), "memset");
-  });
+  return call([&] { mt::vocab_zero_grads(v, (cudaStream_t)stream); });
 }
 
 static bool tp_active(const mt_vocab* v) { return v->d.tp_size > 1 && v->ctx->tp; }

@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-from ._native import AdamDesc, LayerDesc, ParallelConfig, RankPlacement, StageDesc, check, lib
+from ._native import AdamDesc, LayerDesc, ParallelConfig, RankPlacement, StageDesc, VocabDesc, check, lib
 
 
 def adam_defaults(**overrides) -> AdamDesc:
@@ -108,6 +108,39 @@ class Layer:
             self._h = C.c_void_p()
 
 
+class Vocab:
+    """Vocab-parallel embedding + final LayerNorm + tied LM head / cross-entropy (include/mtnlg.h)."""
+
+    WORD, POS, LNF_GAMMA, LNF_BETA = 0, 1, 2, 3
+
+    def __init__(self, ctx: Context, vocab: int, hidden: int, seq: int, micro_batch: int, tp_size: int = 1,
+                 tp_rank: int = 0, dropout: float = 0.1, ln_eps: float = 1e-5, seed: int = 1234):
+        self.ctx = ctx
+        self.desc = VocabDesc(vocab, hidden, seq, micro_batch, tp_size, tp_rank, dropout, ln_eps, seed)
+        self._h = C.c_void_p()
+        check(lib().mt_vocab_create(ctx._h, C.byref(self.desc), C.byref(self._h)))
+
+    def padded(self) -> tuple[int, int, int]:
+        """(padded vocab, first row of this rank's slice, rows in the slice)."""
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().mt_vocab_padded(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def set_param(self, param: int, host_global_bf16_ptr: int) -> None:
+        check(lib().mt_vocab_set_param(self._h, param, C.c_void_p(host_global_bf16_ptr)))
+
+    def get_param(self, param: int, host_bf16_ptr: int) -> None:
+        check(lib().mt_vocab_get_param(self._h, param, C.c_void_p(host_bf16_ptr)))
+
+    def get_grad(self, param: int, host_f32_ptr: int) -> None:
+        check(lib().mt_vocab_get_grad(self._h, param, C.cast(host_f32_ptr, C.POINTER(C.c_float))))
+
+    def close(self) -> None:
+        if self._h:
+            lib().mt_vocab_destroy(self._h)
+            self._h = C.c_void_p()
+
+
 class Stage:
     """This rank's pipeline stage: layers [stage*L/PP, (stage+1)*L/PP) of the model."""
 
@@ -149,6 +182,11 @@ class Stage:
 
     def set_recompute(self, enable: bool = True) -> None:
         check(lib().mt_stage_set_recompute(self._h, int(enable)))
+
+    def attach_vocab(self, vocab: Vocab) -> None:
+        """Language-model mode: inputs / targets become int32 token ids [MB][b*s]."""
+        check(lib().mt_stage_attach_vocab(self._h, vocab._h))
+        self.vocab = vocab
 
     def launch_count(self) -> int:
         n = C.c_int64()

@@ -50,7 +50,32 @@ def _worker(rank, world, port, mode, q):
         ctx = Context(rank)
         s = torch.cuda.current_stream()
         out = {}
-        if mode == "vocab":
+        if mode == "lm_pp":
+            from tests import test_lm_gpu as LM
+            from paper_2201_11990_b200.runtime import Vocab, adam_defaults  # noqa: F401
+            MB = 4
+            ctx.init_comm(obj[0], world, rank, tensor=1, pipeline=world, data=1, batch=LM.B * MB, micro_batches=MB)
+            tok, tgt = LM.token_batch(MB)
+            tok_h, tgt_h = torch.from_numpy(tok).pin_memory(), torch.from_numpy(tgt).pin_memory()
+
+            def run(c, layers_here):
+                st = Stage(c, PL.layer_desc(LM.H, LM.HEADS, LM.S, LM.B, seed=LM.SEED), 2, MB)
+                st.init_params(layers_here, s)
+                voc = LM.make_vocab(c)
+                st.attach_vocab(voc)
+                loss = st.train_step(tok_h.data_ptr(), tgt_h.data_ptr(), s)
+                r = dict(loss=loss, layers=[LM.layer_grads(st.layer(i)) for i in range(layers_here)],
+                         vocab=LM.vocab_grads(voc))
+                r["norm"] = st.optimizer_step(adam_defaults(tokens_seen=2e9, step=1), s)
+                st.close()
+                voc.close()
+                return r
+
+            out["pp"] = run(ctx, 1)
+            solo = Context(rank)  # the same model unpartitioned on this GPU (PP = 1)
+            out["ref"] = run(solo, 2)
+            solo.close()
+        elif mode == "vocab":
             import ctypes as C
             from paper_2201_11990_b200._native import VocabDesc, check, lib
             ctx.init_comm(obj[0], world, rank, tensor=world)
@@ -261,3 +286,25 @@ def test_vocab_parallel_head_two_gpus():
         assert rel(res[r]["dy"], dy_ref) < 2e-2
         full[res[r]["v0"]:res[r]["v0"] + res[r]["vp"]] = res[r]["gword"]
     assert rel(full, dword_ref) < 2e-2
+
+
+@pytest.mark.timeout(900)
+def test_language_model_pipeline_two_gpus():
+    """Token ids -> embedding (stage 0) -> 1F1B over PP=2 -> tied head + cross-entropy (stage 1):
+    loss, every layer gradient, the tied word-embedding gradient (all-reduced between the first and
+    the last stage), the position / final-LN gradients and the clipped-norm all equal the same model
+    run unpartitioned (PP = 1) on one GPU (1e-5 relative: only float summation order differs)."""
+    _need(2)
+    res = _run("lm_pp")
+    ref = res[0]["ref"]
+    assert abs(res[1]["pp"]["loss"] - ref["loss"]) <= 1e-5 * ref["loss"], (res[1]["pp"]["loss"], ref["loss"])
+    assert res[0]["pp"]["loss"] == 0.0
+    for r in (0, 1):
+        assert abs(res[r]["ref"]["loss"] - ref["loss"]) <= 1e-6 * ref["loss"]
+        for p in range(12):
+            assert rel(res[r]["pp"]["layers"][0][p], ref["layers"][r][p]) < 1e-5, (r, p)
+        assert rel(res[r]["pp"]["vocab"][0], ref["vocab"][0]) < 1e-5, r  # tied E: both ends hold the sum
+        assert abs(res[r]["pp"]["norm"] - ref["norm"]) <= 1e-4 * ref["norm"], (res[r]["pp"]["norm"], ref["norm"])
+    assert rel(res[0]["pp"]["vocab"][1], ref["vocab"][1]) < 1e-5  # position embedding: first stage
+    for p in (2, 3):  # final LayerNorm: last stage
+        assert rel(res[1]["pp"]["vocab"][p], ref["vocab"][p]) < 1e-5
