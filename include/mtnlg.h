@@ -251,6 +251,48 @@ int mt_stage_optimizer_step(mt_stage* st, const mt_adam_desc* d, float* grad_nor
  * and the last stage (tied weights, Megatron); DP averages all vocab gradients; the optimizer step
  * covers the vocab parameters (word embedding counted once in the gradient norm). */
 int mt_stage_attach_vocab(mt_stage* st, mt_vocab* v);
+/* Microbatches of the next iterations (1 .. the micro_batches the stage was created with): a batch
+ * ramp (curator::batch_size_at) changes the global batch, hence the microbatch count, at fixed b. */
+int mt_stage_set_micro_batches(mt_stage* st, int32_t micro_batches);
+
+/* ------------------------------------------------------------------ data feed */
+/* Dataset blending: curator::next_batch_composition (include/curator/blending.hpp) over n datasets.
+ * normalize != 0 scales the weights to sum 1 first (curator::normalize_weights). */
+typedef struct mt_blend mt_blend;
+int mt_blend_create(int32_t n, const char* const* names, const double* weights, const uint64_t* available,
+                    int32_t normalize, mt_blend** out);
+int mt_blend_destroy(mt_blend* b);
+int mt_blend_weights(const mt_blend* b, double* weights);
+/* counts[n] of the next batch; credit / drawn (may be NULL) = the state after it. */
+int mt_blend_next(mt_blend* b, uint64_t batch_size, uint64_t* counts, double* credit, uint64_t* drawn);
+/* The reference blend stage (proj/src/pipeline.cpp:551-647): dataset i has doc_counts[i] documents
+ * doc_ids[i][...] in corpus order; weights are normalised; `steps` batches of batch_size samples
+ * (or batch_per_step[step] when non-NULL) are drawn and written to `path` as blend_manifest.jsonl
+ * lines {"step":t,"dataset":"name","doc_id":id}. shuffle != 0 draws each dataset in the seeded
+ * order of stage_seed (= mix64(config seed, fnv1a64("blend")) in the reference pipeline). */
+int mt_blend_manifest(int32_t n, const char* const* names, const double* weights, const uint64_t* const* doc_ids,
+                      const uint64_t* doc_counts, uint64_t steps, uint64_t batch_size,
+                      const uint64_t* batch_per_step, int32_t shuffle, uint64_t stage_seed, const char* path);
+
+/* Token feed over a blend manifest: step t's lines are its global batch G_t (file order); DP rank r
+ * takes samples [r G/DP, (r+1) G/DP), split into G/(micro_batch DP) microbatches. Tokens of a
+ * sample are the synthetic stream of its (dataset, doc_id) (mt_feed_doc_tokens): inputs = tokens
+ * [0, seq), targets = tokens [1, seq]. */
+typedef struct mt_feed mt_feed;
+typedef struct mt_feed_desc {
+  int32_t vocab, seq, micro_batch, data_parallel, dp_rank;
+  uint64_t seed;
+} mt_feed_desc;
+int mt_feed_open(const char* manifest_path, const mt_feed_desc* d, mt_feed** out);
+int mt_feed_destroy(mt_feed* f);
+int mt_feed_steps(const mt_feed* f, int64_t* steps);
+int mt_feed_dataset_name(const mt_feed* f, int32_t index, const char** name);
+/* Global batch of a step and this rank's microbatch count (status 1 unless G % (b DP) == 0). */
+int mt_feed_step_info(const mt_feed* f, int64_t step, int64_t* global_batch, int32_t* micro_batches);
+int mt_feed_sample(const mt_feed* f, int64_t step, int64_t index, int32_t* dataset, uint64_t* doc_id);
+/* This rank's inputs / targets of a step: int32 [micro_batches][micro_batch * seq] (either may be NULL). */
+int mt_feed_fill(const mt_feed* f, int64_t step, int32_t* tokens, int32_t* targets, int32_t max_micro_batches);
+int mt_feed_doc_tokens(uint64_t seed, const char* dataset, uint64_t doc_id, int32_t vocab, int64_t n, int32_t* out);
 
 #ifdef __cplusplus
 }

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "curator/errors.hpp"   // resolved to /root/reference/proj/include (first on the -I path)
+#include "curator/blending.hpp"
 #include "curator/planner.hpp"
 #include "../include/mtnlg.h"
 
@@ -91,6 +92,27 @@ int ref_plan_report(const char* path, int32_t as_json, char* out, int64_t cap, i
       const int64_t k = std::min<int64_t>(cap - 1, *len);
       std::memcpy(out, s.data(), (size_t)k);
       out[k] = '\0';
+    }
+  });
+}
+// Reference blending: `steps` batches over n datasets (weights normalised first when asked);
+// counts [steps][n], credit [steps][n] after each step.
+int ref_blend_run(int32_t n, const double* weights, int32_t normalize, uint64_t batch, int64_t steps,
+                  uint64_t* counts, double* credit) {
+  return call([&] {
+    std::vector<curator::DatasetSpec> specs(n);
+    for (int32_t i = 0; i < n; ++i) {
+      specs[i].name = "d" + std::to_string(i);
+      specs[i].weight = weights[i];
+    }
+    if (normalize) curator::normalize_weights(specs);
+    auto st = curator::BlendState::create(n);
+    for (int64_t t = 0; t < steps; ++t) {
+      const auto c = curator::next_batch_composition(st, specs, batch);
+      for (int32_t i = 0; i < n; ++i) {
+        counts[t * n + i] = c[i];
+        credit[t * n + i] = st.credit[i];
+      }
     }
   });
 }

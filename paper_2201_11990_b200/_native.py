@@ -71,6 +71,11 @@ class VocabDesc(C.Structure):
                 ("seed", C.c_uint64)]
 
 
+class FeedDesc(C.Structure):
+    _fields_ = [("vocab", C.c_int32), ("seq", C.c_int32), ("micro_batch", C.c_int32), ("data_parallel", C.c_int32),
+                ("dp_rank", C.c_int32), ("seed", C.c_uint64)]
+
+
 class StageDesc(C.Structure):
     _fields_ = [("layer", LayerDesc), ("layers", C.c_int32), ("micro_batches", C.c_int32)]
 
@@ -147,6 +152,21 @@ _SIGS = {
     "mt_stage_launch_count": (C.c_int, [P, PI64]),
     "mt_stage_optimizer_step": (C.c_int, [P, C.POINTER(AdamDesc), PF32, P]),
     "mt_stage_attach_vocab": (C.c_int, [P, P]),
+    "mt_stage_set_micro_batches": (C.c_int, [P, I32]),
+    "mt_blend_create": (C.c_int, [I32, C.POINTER(C.c_char_p), PF64, C.POINTER(U64), I32, C.POINTER(P)]),
+    "mt_blend_destroy": (C.c_int, [P]),
+    "mt_blend_weights": (C.c_int, [P, PF64]),
+    "mt_blend_next": (C.c_int, [P, U64, C.POINTER(U64), PF64, C.POINTER(U64)]),
+    "mt_blend_manifest": (C.c_int, [I32, C.POINTER(C.c_char_p), PF64, C.POINTER(C.POINTER(U64)), C.POINTER(U64), U64,
+                                    U64, C.POINTER(U64), I32, U64, C.c_char_p]),
+    "mt_feed_open": (C.c_int, [C.c_char_p, C.POINTER(FeedDesc), C.POINTER(P)]),
+    "mt_feed_destroy": (C.c_int, [P]),
+    "mt_feed_steps": (C.c_int, [P, PI64]),
+    "mt_feed_dataset_name": (C.c_int, [P, I32, C.POINTER(C.c_char_p)]),
+    "mt_feed_step_info": (C.c_int, [P, I64, PI64, PI32]),
+    "mt_feed_sample": (C.c_int, [P, I64, I64, PI32, C.POINTER(U64)]),
+    "mt_feed_fill": (C.c_int, [P, I64, PI32, PI32, I32]),
+    "mt_feed_doc_tokens": (C.c_int, [U64, C.c_char_p, U64, I32, I64, PI32]),
     "mt_adam_defaults": (C.c_int, [C.POINTER(AdamDesc)]),
     "mt_layer_adam_step": (C.c_int, [P, C.POINTER(AdamDesc), PF32, P]),
     "mt_layer_get_optimizer_state": (C.c_int, [P, I32, PF32, PF32, PF32]),

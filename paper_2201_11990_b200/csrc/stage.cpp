@@ -21,7 +21,8 @@ void set_error(const std::string& e);
 
 struct mt_stage {
   mt_ctx* ctx = nullptr;
-  mt_stage_desc d{};
+  mt_stage_desc d{};               // d.micro_batches = microbatches of the next iteration
+  int mb_capacity = 0;             // microbatch buffers allocated at creation
   int stage = 0, stages = 1;
   std::vector<mt_layer*> layers;
   int64_t M = 0, h = 0;
@@ -198,6 +199,8 @@ extern "C" int mt_stage_create(mt_ctx* c, const mt_stage_desc* d, mt_stage** out
     auto st = new mt_stage();
     st->ctx = c;
     st->d = *d;
+    if (d->micro_batches < 1 || d->layers < 1) throw std::invalid_argument("bad stage descriptor");
+    st->mb_capacity = d->micro_batches;
     st->stage = c->place.pipeline;
     st->stages = c->par.pipeline;
     const curator::Range own = curator::stage_layers(d->layers, st->stages, st->stage);
@@ -439,9 +442,18 @@ extern "C" int mt_stage_attach_vocab(mt_stage* st, mt_vocab* v) {
     st->vocab = v;
     const size_t tok_bytes = static_cast<size_t>(st->M * 4);
     if (st->stage == 0) {
-      st->tokens.resize(st->d.micro_batches);
+      st->tokens.resize(st->mb_capacity);
       for (auto& b : st->tokens) b.ensure(tok_bytes);
     }
     // targets buffers (sized for bf16 activations) already hold M int32 ids
+  });
+}
+
+extern "C" int mt_stage_set_micro_batches(mt_stage* st, int32_t micro_batches) {
+  return call([&] {
+    if (!st) throw std::invalid_argument("null stage");
+    if (micro_batches < 1 || micro_batches > st->mb_capacity)
+      throw std::invalid_argument("micro_batches must be in [1, " + std::to_string(st->mb_capacity) + "]");
+    st->d.micro_batches = micro_batches;
   });
 }

@@ -183,6 +183,10 @@ class Stage:
     def set_recompute(self, enable: bool = True) -> None:
         check(lib().mt_stage_set_recompute(self._h, int(enable)))
 
+    def set_micro_batches(self, n: int) -> None:
+        """Microbatches of the next iterations (<= the count the stage was created with)."""
+        check(lib().mt_stage_set_micro_batches(self._h, n))
+
     def attach_vocab(self, vocab: Vocab) -> None:
         """Language-model mode: inputs / targets become int32 token ids [MB][b*s]."""
         check(lib().mt_stage_attach_vocab(self._h, vocab._h))

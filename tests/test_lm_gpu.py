@@ -186,3 +186,46 @@ def test_lm_training_memorises_a_batch():
     st.close()
     voc.close()
     ctx.close()
+
+
+def test_lm_stage_consumes_blend_feed_with_batch_ramp(tmp_path):
+    """N4 end to end: a blend manifest with a growing global batch (4 then 8 samples at b=2 -> 2 then
+    4 microbatches) feeds the language-model stage through mt_feed_fill + mt_stage_set_micro_batches.
+    The 2-microbatch iteration of a stage created for 4 must equal a stage created for exactly 2
+    (to 1e-6: the per-row cross-entropy is summed with float atomics)."""
+    from paper_2201_11990_b200.feed import Feed, blend_manifest
+    m = tmp_path / "blend_manifest.jsonl"
+    blend_manifest(m, [("web", 0.6, list(range(50))), ("code", 0.4, list(range(900, 930)))], 2, 0,
+                   shuffle=True, config_seed=5, batch_per_step=[4, 8])
+    feed = Feed(m, V, S, B, 1, 0, seed=SEED)
+    ctx = Context(0)
+    s = torch.cuda.current_stream()
+    voc = make_vocab(ctx)
+    losses = {}
+    for cap in (4, 2):
+        st = Stage(ctx, PL.layer_desc(H, HEADS, S, B, seed=SEED), 1, cap)
+        st.init_params(1, s)
+        st.attach_vocab(voc)
+        G, MB = feed.step_info(0)
+        assert (G, MB) == (4, 2)
+        tok = torch.zeros(cap, B * S, dtype=torch.int32).pin_memory()
+        tgt = torch.zeros(cap, B * S, dtype=torch.int32).pin_memory()
+        feed.fill(0, tok.data_ptr(), tgt.data_ptr(), cap)
+        if cap == 4:
+            from paper_2201_11990_b200._native import ConfigError
+            with pytest.raises(ConfigError):
+                st.set_micro_batches(5)
+        st.set_micro_batches(MB)
+        losses[cap] = st.train_step(tok.data_ptr(), tgt.data_ptr(), s)
+        if cap == 4:  # the ramp's next step uses all four microbatches
+            G1, MB1 = feed.step_info(1)
+            assert (G1, MB1) == (8, 4)
+            feed.fill(1, tok.data_ptr(), tgt.data_ptr(), cap)
+            st.set_micro_batches(MB1)
+            l1 = st.train_step(tok.data_ptr(), tgt.data_ptr(), s)
+            assert np.isfinite(l1) and 0.9 * np.log(V) < l1 / MB1 < 1.1 * np.log(V)
+        st.close()
+    assert abs(losses[4] - losses[2]) <= 1e-6 * losses[2], losses  # loss sum uses float atomics
+    feed.close()
+    voc.close()
+    ctx.close()
