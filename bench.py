@@ -274,6 +274,7 @@ def run_ours(args, L: dict) -> None:
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / args.steps * 1e3
     e2e_ms = max_over_ranks(max(ev0.elapsed_time(ev1) / args.steps, wall))
+    h2d, d2h = stage.host_traffic()  # bytes actually moved (TP ranks copy 1/TP slices each)
     tot = torch.tensor([h2d, d2h], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(tot)

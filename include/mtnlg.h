@@ -254,6 +254,10 @@ int mt_stage_attach_vocab(mt_stage* st, mt_vocab* v);
 /* Microbatches of the next iterations (1 .. the micro_batches the stage was created with): a batch
  * ramp (curator::batch_size_at) changes the global batch, hence the microbatch count, at fixed b. */
 int mt_stage_set_micro_batches(mt_stage* st, int32_t micro_batches);
+/* Host<->device bytes this rank moved in its last mt_stage_train_step (with TP > 1 each rank of a
+ * TP group copies only its 1/TP slice of the inputs / targets; the slices are all-gathered over
+ * NVLink). */
+int mt_stage_host_traffic(const mt_stage* st, int64_t* h2d_bytes, int64_t* d2h_bytes);
 
 /* ------------------------------------------------------------------ data feed */
 /* Dataset blending: curator::next_batch_composition (include/curator/blending.hpp) over n datasets.

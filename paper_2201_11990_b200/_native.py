@@ -153,6 +153,7 @@ _SIGS = {
     "mt_stage_optimizer_step": (C.c_int, [P, C.POINTER(AdamDesc), PF32, P]),
     "mt_stage_attach_vocab": (C.c_int, [P, P]),
     "mt_stage_set_micro_batches": (C.c_int, [P, I32]),
+    "mt_stage_host_traffic": (C.c_int, [P, PI64, PI64]),
     "mt_blend_create": (C.c_int, [I32, C.POINTER(C.c_char_p), PF64, C.POINTER(U64), I32, C.POINTER(P)]),
     "mt_blend_destroy": (C.c_int, [P]),
     "mt_blend_weights": (C.c_int, [P, PF64]),

@@ -40,6 +40,7 @@ struct mt_stage {
   // language-model mode (mt_stage_attach_vocab): inputs/targets are int32 token ids [MB][M]
   mt_vocab* vocab = nullptr;
   std::vector<mt::DeviceBuffer> tokens;            // [MB][M] int32 (host-input path, first stage)
+  int64_t h2d_bytes = 0, d2h_bytes = 0;            // host traffic of the last mt_stage_train_step
 };
 
 namespace {
@@ -78,6 +79,22 @@ struct Step {
   // bytes of one microbatch's input / target: bf16 activations, or int32 token ids with a vocab
   size_t io_bytes() const { return st->vocab ? static_cast<size_t>(st->M * 4) : bytes(); }
   bool lm() const { return st->vocab != nullptr; }
+  // TP > 1, host inputs: the t ranks of a TP group need the same activations / targets, so each
+  // copies only its 1/t row slice over PCIe and the slices are all-gathered over NVLink (in place),
+  // instead of t full host->device copies competing for host bandwidth.
+  bool split_h2d() const {
+    const mt_ctx* c = st->ctx;
+    return !lm() && c->par.tensor > 1 && c->tp && !c->shard_only && (elems() % c->par.tensor) == 0;
+  }
+  size_t slice_bytes() const { return split_h2d() ? io_bytes() / st->ctx->par.tensor : io_bytes(); }
+  size_t slice_off() const { return split_h2d() ? slice_bytes() * st->ctx->place.tensor : 0; }
+  void gather_slices(void* buf) {
+    if (!split_h2d()) return;
+    const size_t n = elems() / st->ctx->par.tensor;
+    mt::check_nccl(ncclAllGather(static_cast<char*>(buf) + slice_off(), buf, n, ncclBfloat16, st->ctx->tp, s),
+                   "ncclAllGather(input slices)");
+    ++launches;
+  }
   ncclComm_t pp() const { return st->ctx->pp; }
   // Global microbatch id (data-parallel replicas see different samples): keys the synthetic
   // inputs/targets and the dropout masks of the microbatch.
@@ -96,15 +113,19 @@ struct Step {
     mt::check_cuda(cudaStreamWaitEvent(st->copy, st->iter_start, 0), "cudaStreamWaitEvent");
     for (int mb = 0; mb < st->d.micro_batches; ++mb) {
       if (in_host && first()) {
-        void* dst = lm() ? st->tokens[mb].ptr : st->act[mb][0].ptr;
-        mt::check_cuda(cudaMemcpyAsync(dst, in_host + mb * io_bytes(), io_bytes(), cudaMemcpyHostToDevice, st->copy),
+        char* dst = static_cast<char*>(lm() ? st->tokens[mb].ptr : st->act[mb][0].ptr) + slice_off();
+        mt::check_cuda(cudaMemcpyAsync(dst, in_host + mb * io_bytes() + slice_off(), slice_bytes(),
+                                       cudaMemcpyHostToDevice, st->copy),
                        "H2D input");
+        st->h2d_bytes += static_cast<int64_t>(slice_bytes());
         mt::check_cuda(cudaEventRecord(st->in_ev[mb], st->copy), "cudaEventRecord");
       }
       if (tgt_host && last()) {
-        mt::check_cuda(cudaMemcpyAsync(st->targets[mb].ptr, tgt_host + mb * io_bytes(), io_bytes(),
+        mt::check_cuda(cudaMemcpyAsync(static_cast<char*>(st->targets[mb].ptr) + slice_off(),
+                                       tgt_host + mb * io_bytes() + slice_off(), slice_bytes(),
                                        cudaMemcpyHostToDevice, st->copy),
                        "H2D target");
+        st->h2d_bytes += static_cast<int64_t>(slice_bytes());
         mt::check_cuda(cudaEventRecord(st->tgt_ev[mb], st->copy), "cudaEventRecord");
       }
     }
@@ -123,6 +144,7 @@ struct Step {
     if (in_dev) return;  // read in place by layer 0
     if (in_host) {
       mt::check_cuda(cudaStreamWaitEvent(s, st->in_ev[mb], 0), "cudaStreamWaitEvent");
+      gather_slices(dst);
     } else {
       const uint64_t key = mt_stream_key(st->d.layer.seed, "input", 0, gid(mb));
       mt::fill_normal(dst, 1, elems(), elems(), 0, 0, key, 0.f, 1.f, s);
@@ -152,6 +174,7 @@ struct Step {
         tgt = tgt_dev + mb * io_bytes();
       } else if (tgt_host) {
         mt::check_cuda(cudaStreamWaitEvent(s, st->tgt_ev[mb], 0), "cudaStreamWaitEvent");
+        gather_slices(st->targets[mb].ptr);
         tgt = st->targets[mb].ptr;
       } else {
         const uint64_t key = mt_stream_key(st->d.layer.seed, "target", 0, gid(mb));
@@ -357,12 +380,16 @@ extern "C" int mt_stage_train_step(mt_stage* st, const void* inputs_host, const 
   return call([&] {
     if (!st) throw std::invalid_argument("null stage");
     Step k{st, (cudaStream_t)stream, static_cast<const char*>(inputs_host), static_cast<const char*>(targets_host)};
+    st->h2d_bytes = st->d2h_bytes = 0;
     if (k.lm() && ((k.first() && !inputs_host) || (k.last() && !targets_host)))
       throw std::invalid_argument("a stage with a vocab needs token inputs (first stage) and targets (last stage)");
     run_iteration(k, st, stream);
     if (loss_out) {
       float host = 0.f;
-      if (k.last()) mt::check_cuda(cudaMemcpyAsync(&host, st->loss.ptr, 4, cudaMemcpyDeviceToHost, k.s), "D2H loss");
+      if (k.last()) {
+        mt::check_cuda(cudaMemcpyAsync(&host, st->loss.ptr, 4, cudaMemcpyDeviceToHost, k.s), "D2H loss");
+        st->d2h_bytes += 4;
+      }
       mt::check_cuda(cudaStreamSynchronize(k.s), "sync");
       *loss_out = host;
     }
@@ -455,5 +482,13 @@ extern "C" int mt_stage_set_micro_batches(mt_stage* st, int32_t micro_batches) {
     if (micro_batches < 1 || micro_batches > st->mb_capacity)
       throw std::invalid_argument("micro_batches must be in [1, " + std::to_string(st->mb_capacity) + "]");
     st->d.micro_batches = micro_batches;
+  });
+}
+
+extern "C" int mt_stage_host_traffic(const mt_stage* st, int64_t* h2d_bytes, int64_t* d2h_bytes) {
+  return call([&] {
+    if (!st) throw std::invalid_argument("null stage");
+    if (h2d_bytes) *h2d_bytes = st->h2d_bytes;
+    if (d2h_bytes) *d2h_bytes = st->d2h_bytes;
   });
 }

@@ -183,6 +183,12 @@ class Stage:
     def set_recompute(self, enable: bool = True) -> None:
         check(lib().mt_stage_set_recompute(self._h, int(enable)))
 
+    def host_traffic(self) -> tuple[int, int]:
+        """(H2D, D2H) bytes this rank moved in its last train_step."""
+        a, b = C.c_int64(), C.c_int64()
+        check(lib().mt_stage_host_traffic(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def set_micro_batches(self, n: int) -> None:
         """Microbatches of the next iterations (<= the count the stage was created with)."""
         check(lib().mt_stage_set_micro_batches(self._h, n))

@@ -139,7 +139,7 @@ def _worker(rank, world, port, mode, q):
             out["grads"] = grads
             lay.close()
         else:
-            tp, pp, dp = (1, world, 1) if mode == "pp" else (1, 1, world)
+            tp, pp, dp = {"pp": (1, world, 1), "dp": (1, 1, world), "tp_stage": (world, 1, 1)}[mode]
             layers, MB = (2 * pp, 4) if mode == "pp" else (1, 2)
             ctx.init_comm(obj[0], world, rank, tensor=tp, pipeline=pp, data=dp, batch=B * MB * dp, micro_batches=MB)
             place = ctx.placement()
@@ -159,6 +159,12 @@ def _worker(rank, world, port, mode, q):
             for _ in range(2):  # the second iteration must reproduce the first (grads re-zeroed)
                 loss = st.train_step(xh.data_ptr(), th.data_ptr(), s)
             out["loss"], out["place"] = loss, (place.data, place.pipeline, place.tensor)
+            out["h2d"] = st.host_traffic()[0]
+            if mode == "tp_stage":  # TP shards: loss + host traffic only (layer grads: test_tensor_parallel_*)
+                st.close()
+                ctx.close()
+                q.put((rank, out))
+                return
             from paper_2201_11990_b200.runtime import adam_defaults
             out["grad_norm"] = None
             out["grads"] = []
@@ -308,3 +314,16 @@ def test_language_model_pipeline_two_gpus():
     assert rel(res[0]["pp"]["vocab"][1], ref["vocab"][1]) < 1e-5  # position embedding: first stage
     for p in (2, 3):  # final LayerNorm: last stage
         assert rel(res[1]["pp"]["vocab"][p], ref["vocab"][p]) < 1e-5
+
+
+@pytest.mark.timeout(900)
+def test_tensor_parallel_stage_host_inputs_two_gpus():
+    """Stage at TP=2 fed from host buffers: each TP rank copies half of every input / target over
+    PCIe and the halves are all-gathered over NVLink; the loss equals the oracle's."""
+    _need(2)
+    res = _run("tp_stage")
+    loss, _ = _oracle_step([0], range(2))
+    full = 2 * 2 * (B * S * H * 2)  # MB=2 inputs + targets, bf16
+    for r in (0, 1):
+        assert abs(res[r]["loss"] - loss) / loss < 5e-3, (res[r]["loss"], loss)
+        assert res[r]["h2d"] == full // 2, res[r]["h2d"]
