@@ -38,6 +38,25 @@ enum mt_causal {
   MT_CAUSAL_K_GE_M = 3            /* A is upper-triangular in (m,k): contract k >= m_tile_begin only */
 };
 
+/* Fused all-reduce of the output over a tensor-parallel group (NVLink SHARP / multimem): every rank
+ * launches the same GEMM on its partial operands with d in symmetric memory; each 128-row x BN output
+ * unit is published with a flag once stored, and its owner rank (round-robin over units) sums all
+ * ranks' copies with multimem.ld_reduce (fp32 accumulation, one rounding) and writes the sum to every
+ * rank with multimem.st from its epilogue warps while the tensor cores continue with later tiles.
+ * mt_gemm_allreduce_wait(counter, target) then orders the consumers after all units of all ranks.
+ * Requirements: STORE_BF16 epilogue, batch 1, no causal mode; d is the local address of offset 0 of
+ * the symmetric buffer whose multicast address is d_multicast. */
+typedef struct mt_gemm_allreduce {
+  void* d_multicast;             /* multicast address of d */
+  uint32_t* flags_local;         /* this rank's per-unit ready flags (symmetric memory) */
+  const uint32_t* flags_peer[8]; /* each rank's flag array, load/store accessible, by rank */
+  uint32_t* counter_multicast;   /* multicast address of the per-rank completion counter */
+  int64_t flag_capacity;         /* units the flag arrays can hold */
+  uint32_t epoch;                /* larger than every epoch used before on these flags */
+  int32_t rank, ranks;
+  int64_t units;                 /* out: number of output units of this launch (counter increments) */
+} mt_gemm_allreduce;
+
 typedef struct mt_gemm_args {
   const void* a;
   int64_t lda, a_batch_stride;
@@ -61,12 +80,17 @@ typedef struct mt_gemm_args {
    * counters, which the kernel leaves zeroed. NULL disables. MT_GEMM_WORKSPACE_BYTES suggests a size. */
   void* workspace;
   int64_t workspace_bytes;
+  mt_gemm_allreduce* allreduce; /* NULL, or the fused TP all-reduce of d (see above) */
 } mt_gemm_args;
 
 #define MT_GEMM_WORKSPACE_BYTES (64ll << 20)
 
 /* Launches on `stream` (a cudaStream_t). Returns 0 on success, 1 on bad arguments, 2 on CUDA error. */
 int mt_gemm(const mt_gemm_args* args, void* stream);
+
+/* Stream-ordered wait until the local completion counter reaches `target` (all units of all ranks of
+ * the fused all-reduce launches so far); 1 launch. */
+int mt_gemm_allreduce_wait(const uint32_t* counter_local, uint32_t target, void* stream);
 
 /* Number of kernel launches mt_gemm issues per call (always 1). */
 int mt_gemm_launches_per_call(void);

@@ -22,6 +22,7 @@ class GemmArgs(C.Structure):
         ("alpha", C.c_float), ("epilogue", C.c_int32), ("causal", C.c_int32),
         ("bias", C.c_void_p), ("aux", C.c_void_p), ("ld_aux", C.c_int64), ("block_n", C.c_int32),
         ("max_ctas", C.c_int32), ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64),
+        ("allreduce", C.c_void_p),
     ]
 
 
@@ -87,6 +88,7 @@ PI32, PI64, PF32, PF64 = C.POINTER(I32), C.POINTER(I64), C.POINTER(F32), C.POINT
 _SIGS = {
     "mt_gemm": (C.c_int, [C.POINTER(GemmArgs), P]),
     "mt_gemm_launches_per_call": (C.c_int, []),
+    "mt_gemm_allreduce_wait": (C.c_int, [P, U32, P]),
     "mt_last_error": (C.c_char_p, []),
     "mt_version": (C.c_char_p, []),
     "mt_map_topology": (C.c_int, [C.POINTER(ClusterTopology), C.POINTER(ParallelConfig), C.POINTER(RankPlacement),

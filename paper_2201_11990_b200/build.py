@@ -18,8 +18,25 @@ OBJ = ROOT / "build" / "obj"
 LIB = PKG / "libmtnlg.so"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_root() -> Path | None:
+    """NCCL >= 2.28 (device API: symmetric windows, multimem pointers) — the copy shipped with torch."""
+    try:
+        import nvidia.nccl  # namespace package of the nvidia-nccl wheel
+        for p in nvidia.nccl.__path__:
+            if (Path(p) / "include" / "nccl_device.h").exists():
+                return Path(p)
+    except ImportError:
+        pass
+    return None
+
+
+NCCL = _nccl_root()
+if NCCL is None:
+    raise RuntimeError("NCCL >= 2.28 headers (nccl_device.h) not found: the fused TP all-reduce needs the NCCL device API")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-INCLUDES = [f"-I{ROOT / 'include'}", f"-I{CSRC}", "-I/usr/local/cuda/include"]
+INCLUDES = [f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{NCCL / 'include'}", "-I/usr/local/cuda/include"]
 NVCC_FLAGS = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fopenmp", "--expt-relaxed-constexpr"]
 CXX_FLAGS = ["-O3", "-std=c++20", "-fPIC", "-fopenmp", "-Wall", "-Wextra", "-Wno-unused-parameter"]
 
@@ -67,7 +84,8 @@ def build(verbose: bool = False, jobs: int = 8) -> Path:
     newest = max(o.stat().st_mtime for o in objs)
     if not LIB.exists() or LIB.stat().st_mtime < newest:
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs),
-              "-L/usr/lib/x86_64-linux-gnu", "-lnccl", "-Xcompiler", "-fopenmp", "-lgomp"])
+              f"-L{NCCL / 'lib'}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={NCCL / 'lib'}",
+              "-Xcompiler", "-fopenmp", "-lgomp"])
     return LIB
 
 

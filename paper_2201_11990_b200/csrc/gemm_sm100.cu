@@ -47,6 +47,13 @@ struct GemmParams {
   int full_tiles, splits, work_items;
   float* split_ws;  // fp32 partial tiles [tail][split][rank][128 x BN]
   int* split_cnt;   // arrival counters [tail][rank], self-resetting
+  // fused TP all-reduce of D (mt_gemm_allreduce); ar_ranks == 0 disables
+  __nv_bfloat16* ar_mc;
+  uint32_t* ar_flags;
+  const uint32_t* ar_peer[8];
+  uint32_t* ar_counter_mc;
+  uint32_t ar_epoch;
+  int ar_rank, ar_ranks;
 };
 
 // kPair: 2-CTA (cta_group::2) tiles of 256 x BN — each CTA of the pair holds 128 rows of A and
@@ -173,6 +180,77 @@ __device__ __forceinline__ void flush_piece(const CUtensorMap* map, uint32_t buf
 __device__ __forceinline__ void reuse_wait(uint32_t lane) {
   if (lane == 0) bulk_wait_read<1>();
   __syncwarp();
+}
+
+// Fused TP all-reduce of one output unit (this CTA's 128 rows x BN of tile w), run by the 128
+// epilogue threads after the unit's TMA stores were issued and its TMEM buffer released (the MMA of
+// the next tile proceeds meanwhile):
+//   1. wait until the unit's stores are complete, publish flag[unit] = epoch (system-scope release);
+//   2. on the owner rank only (round-robin over tiles): wait for every peer's flag, then sum the
+//      ranks' copies with multimem.ld_reduce (fp32 accumulate) and write the sum to all ranks with
+//      multimem.st; count the unit on every rank's completion counter (multimem.red.release).
+// Every rank runs the same persistent schedule and publishes a unit before it waits for any, so the
+// owner's wait is on work its peers complete unconditionally (no cyclic dependency).
+template <int BN, int BMT, bool kPair>
+__device__ __forceinline__ void allreduce_unit(const GemmParams& p, int w, int mb, int nb, uint32_t cta_rank,
+                                               uint32_t lane) {
+  const int unit = kPair ? 2 * w + (int)cta_rank : w;
+  if (lane == 0) bulk_wait<0>();
+  __syncwarp();
+  epi_bar();
+  const bool leader_thread = threadIdx.x == 128;
+  if (leader_thread) {
+    fence_proxy_async_global();
+    fence_acq_rel_sys();
+    st_release_sys_u32(p.ar_flags + unit, p.ar_epoch);
+  }
+  if ((w + (int)cta_rank) % p.ar_ranks != p.ar_rank) return;
+  if (leader_thread) {
+    for (int r = 0; r < p.ar_ranks; ++r) {
+      if (r == p.ar_rank) continue;
+      while ((int)(ld_acquire_sys_u32(p.ar_peer[r] + unit) - p.ar_epoch) < 0) {
+      }
+    }
+    fence_acq_rel_sys();
+  }
+  epi_bar();
+  const int row0 = mb * BMT + (int)cta_rank * kBM;
+  const int rows = min(kBM, p.m - row0);
+  const int col0 = nb * BN;
+  const int cpr = min(BN, p.n - col0) / 8;  // 16-byte chunks per row
+  const int total = rows > 0 ? rows * cpr : 0;
+  const int tid = (int)threadIdx.x - 128;
+  constexpr int U = 8;
+#pragma unroll 1
+  for (int base = tid; base < total; base += 128 * U) {
+    uint32_t v[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * 128;
+      if (i < total) {
+        const int r = i / cpr, c = i - r * cpr;
+        multimem_ld_reduce_bf16x8(p.ar_mc + (long long)(row0 + r) * p.ldd + col0 + c * 8, v[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * 128;
+      if (i < total) {
+        const int r = i / cpr, c = i - r * cpr;
+        multimem_st_bf16x8(p.ar_mc + (long long)(row0 + r) * p.ldd + col0 + c * 8, v[u]);
+      }
+    }
+  }
+  epi_bar();
+  if (leader_thread) {
+    fence_acq_rel_sys();
+    multimem_red_release_add_u32(p.ar_counter_mc, 1u);
+  }
+}
+
+__global__ void allreduce_wait_kernel(const uint32_t* counter, uint32_t target) {
+  while ((int)(ld_acquire_sys_u32(counter) - target) < 0) {
+  }
 }
 
 template <int BN, bool kAMN, bool kBMN, bool kPair>
@@ -471,6 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
       }
       ++it;
+      if (p.ar_ranks > 0) allreduce_unit<BN, BMT, kPair>(p, w, mb, nb, rank, lane);
     }
     if (lane == 0) bulk_wait<0>();
   }
@@ -593,7 +672,7 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   p.full_tiles = p.total_tiles;
   p.splits = 1;
   p.work_items = p.total_tiles;
-  if (a.causal == MT_CAUSAL_NONE && a.workspace != nullptr && split_enabled()) {
+  if (a.causal == MT_CAUSAL_NONE && a.workspace != nullptr && a.allreduce == nullptr && split_enabled()) {
     const int units = std::max(1, cap_units);
     const int full = (p.total_tiles / units) * units, tail = p.total_tiles - full;
     if (full > 0 && tail > 0 && tail * 2 <= units) {
@@ -629,6 +708,24 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   p.bias = static_cast<const __nv_bfloat16*>(a.bias);
   p.aux = static_cast<__nv_bfloat16*>(a.aux);
   p.ld_aux = a.ld_aux;
+  if (a.allreduce != nullptr) {
+    mt_gemm_allreduce& ar = *a.allreduce;
+    const long long units = (long long)p.total_tiles * (kPair ? 2 : 1);
+    if (ar.ranks < 2 || ar.ranks > 8 || ar.rank < 0 || ar.rank >= ar.ranks || units > ar.flag_capacity ||
+        !ar.d_multicast || !ar.flags_local || !ar.counter_multicast)
+      return 1;
+    p.ar_mc = static_cast<__nv_bfloat16*>(ar.d_multicast);
+    p.ar_flags = ar.flags_local;
+    for (int r = 0; r < ar.ranks; ++r) {
+      if (!ar.flags_peer[r]) return 1;
+      p.ar_peer[r] = ar.flags_peer[r];
+    }
+    p.ar_counter_mc = ar.counter_multicast;
+    p.ar_epoch = ar.epoch;
+    p.ar_rank = ar.rank;
+    p.ar_ranks = ar.ranks;
+    ar.units = units;
+  }
   auto kern = gemm_sm100_kernel<BN, kAMN, kBMN, kPair>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -715,6 +812,12 @@ bool pair_enabled() {
 
 extern "C" int mt_gemm_launches_per_call(void) { return 1; }
 
+extern "C" int mt_gemm_allreduce_wait(const uint32_t* counter_local, uint32_t target, void* stream) {
+  if (counter_local == nullptr) return 1;
+  mt::allreduce_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(counter_local, target);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
 extern "C" int mt_gemm(const mt_gemm_args* args, void* stream) {
   if (args == nullptr) return 1;
   const mt_gemm_args& a = *args;
@@ -728,6 +831,8 @@ extern "C" int mt_gemm(const mt_gemm_args* args, void* stream) {
     return 1;
   if (a.epilogue == MT_EPI_BIAS_GELU && a.bias == nullptr) return 1;
   if ((a.epilogue == MT_EPI_BIAS_GELU || a.epilogue == MT_EPI_GELU_BWD) && a.batch != 1) return 1;
+  if (a.allreduce != nullptr && (a.epilogue != MT_EPI_STORE_BF16 || a.batch != 1 || a.causal != MT_CAUSAL_NONE))
+    return 1;
   if (a.epilogue < 0 || a.epilogue > MT_EPI_ACCUM_F32 || a.causal < 0 || a.causal > MT_CAUSAL_K_GE_M) return 1;
   int bn = a.block_n;
   if (bn == 0) bn = mt::choose_block_n(a);

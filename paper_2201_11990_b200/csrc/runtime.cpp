@@ -124,6 +124,10 @@ struct Gemm {
     a.max_ctas = n;
     return *this;
   }
+  Gemm& allreduce(mt_gemm_allreduce* ar) {
+    a.allreduce = ar;
+    return *this;
+  }
   // Algorithmic FLOPs of this call (causal contractions count the lower triangle only).
   double flops() const {
     double f = 2.0 * double(a.m) * double(a.n) * double(a.k) * double(a.batch);
@@ -208,6 +212,30 @@ void validate_desc(const mt_layer_desc& d) {
   if ((int64_t{d.hidden} / d.tp_size) % 8 != 0) throw std::invalid_argument("h / TP must be a multiple of 8");
 }
 
+// Collective over the TP group (every rank reaches the same ensure calls in the same order).
+void release_symmetric(mt_ctx* c, mt_ctx::SymBuffer& sb) {
+  if (!sb.ptr) return;
+  if (sb.win_side) ncclCommWindowDeregister(c->tp_side, sb.win_side);
+  if (sb.win_tp) ncclCommWindowDeregister(c->tp, sb.win_tp);
+  ncclMemFree(sb.ptr);
+  sb = mt_ctx::SymBuffer{};
+}
+void ensure_symmetric(mt_ctx* c, mt_ctx::SymBuffer& sb, size_t bytes) {
+  bytes = (bytes + 4095) / 4096 * 4096;
+  if (bytes <= sb.bytes) return;
+  check_cuda(cudaDeviceSynchronize(), "sync");
+  release_symmetric(c, sb);
+  check_nccl(ncclMemAlloc(&sb.ptr, bytes), "ncclMemAlloc");
+  sb.bytes = bytes;
+  check_nccl(ncclCommWindowRegister(c->tp, sb.ptr, bytes, &sb.win_tp, NCCL_WIN_COLL_SYMMETRIC),
+             "ncclCommWindowRegister(tp)");
+  check_nccl(ncclCommWindowRegister(c->tp_side, sb.ptr, bytes, &sb.win_side, NCCL_WIN_COLL_SYMMETRIC),
+             "ncclCommWindowRegister(tp_side)");
+}
+// The [M, h] buffer i (0: row-parallel output / its gradient, 1: LN-input gradient) that the layers
+// all-reduce over TP: symmetric memory when enabled and allocated, else the plain scratch.
+void* tp_buffer(mt_ctx* c, int i) { return c->sym_h[i].ptr ? c->sym_h[i].ptr : c->scratch_h[i].ptr; }
+
 }  // namespace
 }  // namespace mt
 
@@ -240,6 +268,9 @@ extern "C" int mt_ctx_create(int32_t device, mt_ctx** out) {
 extern "C" int mt_ctx_destroy(mt_ctx* c) {
   return guarded([&] {
     if (!c) return;
+    if (c->fused_ar) fused_ar_destroy(c, c->fused_ar);
+    c->fused_ar = nullptr;
+    for (auto& sb : c->sym_h) release_symmetric(c, sb);
     for (ncclComm_t* cm : {&c->emb, &c->tp_side, &c->tp, &c->pp, &c->dp, &c->world})
       if (*cm) ncclCommDestroy(*cm);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -320,6 +351,9 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
         check_cuda(cudaEventCreateWithFlags(&c->ev_chunk_done[i], cudaEventDisableTiming), "event");
       }
       if (const char* e = getenv("MT_TP_CHUNKS")) c->tp_chunks = std::max(1, std::min(4, atoi(e)));
+      if (const char* e = getenv("MT_TP_SYMMETRIC")) c->tp_symmetric = e[0] == '1';
+      if (const char* e = getenv("MT_TP_FUSED")) c->tp_fused = e[0] == '1';
+      if (c->tp_fused) c->tp_symmetric = true;
     }
   });
 }
@@ -492,6 +526,10 @@ extern "C" int mt_layer_create(mt_ctx* c, const mt_layer_desc* d, mt_layer** out
     // shared scratch
     const int64_t M = l->M;
     for (auto& b : c->scratch_h) b.ensure(M * l->h * 2);
+    if (c->tp_symmetric && d->tp_size > 1 && c->tp && !c->shard_only) {
+      for (auto& sb : c->sym_h) ensure_symmetric(c, sb, static_cast<size_t>(M * l->h * 2));
+      if (c->tp_fused && !c->fused_ar) c->fused_ar = fused_ar_create(c);
+    }
     c->scratch_ffn.ensure(M * l->ffl * 2);
     c->scratch_ctx.ensure(M * l->hl * 2);
     c->scratch_qkv.ensure(M * l->qkvl * 2);
@@ -660,14 +698,24 @@ void row_parallel_block(mt_ctx* c, bool tpc, int64_t M, int64_t h, GemmFor gemm_
     }
   };
   if (!tpc) {
-    gemm_rows(0, M, 0);
+    gemm_rows(0, M, 0, nullptr);
+    mark(c, st, gemm_label);
+    epilogue(0, M);
+    mark(c, st, "fwd.bias_dropout_residual_ln");
+    return;
+  }
+  if (c->fused_ar && z == c->sym_h[0].ptr) {
+    // one kernel: GEMM tiles + their all-reduce over NVLink SHARP from the epilogue warps
+    gemm_rows(0, M, 0, fused_ar_begin(c));
+    fused_ar_end(c, st);
+    ++n;
     mark(c, st, gemm_label);
     epilogue(0, M);
     mark(c, st, "fwd.bias_dropout_residual_ln");
     return;
   }
   if (chunks == 1) {
-    gemm_rows(0, M, 0);
+    gemm_rows(0, M, 0, nullptr);
     mark(c, st, gemm_label);
     check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(row-parallel out)");
     ++n;
@@ -680,7 +728,7 @@ void row_parallel_block(mt_ctx* c, bool tpc, int64_t M, int64_t h, GemmFor gemm_
   check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device), "attr");
   const int cap = std::max(2, sms - c->comm_sms);
   for (int k = 0; k < chunks; ++k) {
-    gemm_rows(k * rows, rows, k == 0 ? 0 : cap);  // later chunks share the SMs with the chunk all-reduces
+    gemm_rows(k * rows, rows, k == 0 ? 0 : cap, nullptr);  // later chunks share SMs with the chunk all-reduces
     check_cuda(cudaEventRecord(c->ev_chunk_ready[k], st), "cudaEventRecord");
     check_cuda(cudaStreamWaitEvent(c->comm, c->ev_chunk_ready[k], 0), "cudaStreamWaitEvent");
     ncclComm_t comm = (k + 1 < chunks) ? c->tp_side : c->tp;  // the last chunk overlaps only small kernels
@@ -766,7 +814,7 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
   const uint64_t site_attn = key_of(d.seed, "attn.probs", d.layer_index, mb);
   const uint64_t site_out1 = key_of(d.seed, "attn.out", d.layer_index, mb);
   const uint64_t site_out2 = key_of(d.seed, "mlp.out", d.layer_index, mb);
-  void* z = c->scratch_h[0].ptr;
+  void* z = tp_buffer(c, 0);
   mark(c, st, "begin");
 
   ln_fwd(x, l->param_ptr(MT_P_LN1_GAMMA), l->param_ptr(MT_P_LN1_BETA), sv.ln1.ptr, mean1, rstd1, (int)M, (int)h,
@@ -811,10 +859,11 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
     const LnOut ln2{l->param_ptr(MT_P_LN2_GAMMA), l->param_ptr(MT_P_LN2_BETA), sv.ln2.ptr, mean2, rstd2, d.ln_eps};
     row_parallel_block(
         c, tpc, M, h,
-        [&](int64_t r0, int64_t nr, int cap) {
+        [&](int64_t r0, int64_t nr, int cap, mt_gemm_allreduce* ar) {
           Gemm(sv.ctx.as<uint16_t>() + r0 * hl, hl, false, l->param_ptr(MT_P_PROJ_W), hl, false,
                static_cast<uint16_t*>(z) + r0 * h, h, nr, h, hl)
               .max_ctas(cap)
+              .allreduce(ar)
               .run(st, n);
         },
         z, l->param_ptr(MT_P_PROJ_B), x, sv.x1.ptr, site_out1, th_h, scale_h, &ln2, st, n, "fwd.proj_gemm");
@@ -827,10 +876,11 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
   mark(c, st, "fwd.fc1_gemm");
   row_parallel_block(
       c, tpc, M, h,
-      [&](int64_t r0, int64_t nr, int cap) {
+      [&](int64_t r0, int64_t nr, int cap, mt_gemm_allreduce* ar) {
         Gemm(sv.act.as<uint16_t>() + r0 * ffl, ffl, false, l->param_ptr(MT_P_FC2_W), ffl, false,
              static_cast<uint16_t*>(z) + r0 * h, h, nr, h, ffl)
             .max_ctas(cap)
+            .allreduce(ar)
             .run(st, n);
       },
       z, l->param_ptr(MT_P_FC2_B), sv.x1.ptr, y, site_out2, th_h, scale_h, nullptr, st, n, "fwd.fc2_gemm");
@@ -877,8 +927,8 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStrea
   const uint64_t site_attn = key_of(d.seed, "attn.probs", d.layer_index, mb);
   const uint64_t site_out1 = key_of(d.seed, "attn.out", d.layer_index, mb);
   const uint64_t site_out2 = key_of(d.seed, "mlp.out", d.layer_index, mb);
-  void* dm = c->scratch_h[0].ptr;   // mlp-out grad, later attn-out grad (dz)
-  void* dln = c->scratch_h[1].ptr;  // grad wrt LN2 / LN1 output
+  void* dm = tp_buffer(c, 0);   // mlp-out grad, later attn-out grad (dz)
+  void* dln = tp_buffer(c, 1);  // grad wrt LN2 / LN1 output
   void* dx1 = c->scratch_h[2].ptr;  // grad wrt residual stream x1
   void* dpre = c->scratch_ffn.ptr;
   void* dctx = c->scratch_ctx.ptr;

@@ -14,10 +14,17 @@
 #include "curator/planner.hpp"
 #include "curator/schedule.hpp"
 #include "mtnlg.h"
+#include "mtnlg_gemm.h"
 
 struct mt_layer;
+struct mt_ctx;
 
 namespace mt {
+struct FusedAllReduce;  // tp_fused.cu
+FusedAllReduce* fused_ar_create(mt_ctx* c);
+void fused_ar_destroy(mt_ctx* c, FusedAllReduce* f);
+mt_gemm_allreduce* fused_ar_begin(mt_ctx* c);
+void fused_ar_end(mt_ctx* c, cudaStream_t st);
 
 // Failed CUDA / NCCL call -> DataError-class status 2.
 struct RuntimeFailure : std::runtime_error {
@@ -75,7 +82,21 @@ struct mt_ctx {
   curator::RankPlacement place;
   ncclComm_t world = nullptr, tp = nullptr, pp = nullptr, dp = nullptr;
   ncclComm_t tp_side = nullptr;  // same TP group, CTA-capped: collectives overlapped with GEMMs
-  ncclComm_t emb = nullptr;  // PP > 1: first + last stage of the same (dp, tp): tied word-embedding grads
+  ncclComm_t emb = nullptr;
+  // TP > 1: the two [M, h] buffers the layers all-reduce over TP (row-parallel outputs in the forward,
+  // LN-input gradients in the backward) can live in NCCL symmetric memory (ncclMemAlloc + window
+  // registered on tp and tp_side), so NCCL runs its symmetric (NVLS / load-store) all-reduce kernels
+  // on them (MT_TP_SYMMETRIC=1). Allocation and registration are collective over the TP group.
+  struct SymBuffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    ncclWindow_t win_tp = nullptr, win_side = nullptr;
+  } sym_h[2];
+  bool tp_symmetric = false;
+  // forward row-parallel GEMM + TP all-reduce fused in one kernel over NVLink SHARP (MT_TP_FUSED=1;
+  // implies symmetric buffers); state in tp_fused.cu
+  bool tp_fused = false;
+  mt::FusedAllReduce* fused_ar = nullptr;  // PP > 1: first + last stage of the same (dp, tp): tied word-embedding grads
   // compute-only measurement of one TP shard on a single GPU: the layer skips its TP collectives
   // (mt_ctx_shard_only); never set in a real multi-GPU run
   bool shard_only = false;
