@@ -182,30 +182,41 @@ __device__ __forceinline__ void reuse_wait(uint32_t lane) {
   __syncwarp();
 }
 
-// Fused TP all-reduce of one output unit (this CTA's 128 rows x BN of tile w), run by the 128
-// epilogue threads after the unit's TMA stores were issued and its TMEM buffer released (the MMA of
-// the next tile proceeds meanwhile):
-//   1. wait until the unit's stores are complete, publish flag[unit] = epoch (system-scope release);
-//   2. on the owner rank only (round-robin over tiles): wait for every peer's flag, then sum the
-//      ranks' copies with multimem.ld_reduce (fp32 accumulate) and write the sum to all ranks with
-//      multimem.st; count the unit on every rank's completion counter (multimem.red.release).
-// Every rank runs the same persistent schedule and publishes a unit before it waits for any, so the
-// owner's wait is on work its peers complete unconditionally (no cyclic dependency).
-template <int BN, int BMT, bool kPair>
-__device__ __forceinline__ void allreduce_unit(const GemmParams& p, int w, int mb, int nb, uint32_t cta_rank,
-                                               uint32_t lane) {
-  const int unit = kPair ? 2 * w + (int)cta_rank : w;
+// Fused TP all-reduce of the output, run by the 128 epilogue threads after a unit's (this CTA's
+// 128 rows x BN of tile w) TMA stores were issued and its TMEM buffer released, so the MMA of the
+// next tile proceeds meanwhile:
+//   publish: wait until the unit's stores are complete, flag[unit] = epoch (system-scope release);
+//   reduce (owner rank only, round-robin over tiles, deferred by one tile so the peers' flags are
+//   normally already set): wait for every peer's flag, sum the ranks' copies with
+//   multimem.ld_reduce (fp32 accumulate) and write the sum to all ranks with multimem.st, then count
+//   the unit on every rank's completion counter (multimem.red.release).
+// Every rank runs the same persistent schedule and publishes a unit before it waits for any, so an
+// owner only ever waits for units its peers publish unconditionally (no cyclic dependency).
+struct ArUnit {
+  int w = -1, mb = 0, nb = 0;
+};
+
+template <bool kPair>
+__device__ __forceinline__ int ar_unit_id(int w, uint32_t cta_rank) {
+  return kPair ? 2 * w + (int)cta_rank : w;
+}
+
+template <bool kPair>
+__device__ __forceinline__ void ar_publish(const GemmParams& p, int w, uint32_t cta_rank, uint32_t lane) {
   if (lane == 0) bulk_wait<0>();
   __syncwarp();
   epi_bar();
-  const bool leader_thread = threadIdx.x == 128;
-  if (leader_thread) {
+  if (threadIdx.x == 128) {
     fence_proxy_async_global();
     fence_acq_rel_sys();
-    st_release_sys_u32(p.ar_flags + unit, p.ar_epoch);
+    st_release_sys_u32(p.ar_flags + ar_unit_id<kPair>(w, cta_rank), p.ar_epoch);
   }
-  if ((w + (int)cta_rank) % p.ar_ranks != p.ar_rank) return;
-  if (leader_thread) {
+}
+
+template <int BN, int BMT, bool kPair>
+__device__ __forceinline__ void ar_reduce(const GemmParams& p, const ArUnit& u, uint32_t cta_rank) {
+  const int unit = ar_unit_id<kPair>(u.w, cta_rank);
+  if (threadIdx.x == 128) {
     for (int r = 0; r < p.ar_ranks; ++r) {
       if (r == p.ar_rank) continue;
       while ((int)(ld_acquire_sys_u32(p.ar_peer[r] + unit) - p.ar_epoch) < 0) {
@@ -214,9 +225,9 @@ __device__ __forceinline__ void allreduce_unit(const GemmParams& p, int w, int m
     fence_acq_rel_sys();
   }
   epi_bar();
-  const int row0 = mb * BMT + (int)cta_rank * kBM;
+  const int row0 = u.mb * BMT + (int)cta_rank * kBM;
   const int rows = min(kBM, p.m - row0);
-  const int col0 = nb * BN;
+  const int col0 = u.nb * BN;
   const int cpr = min(BN, p.n - col0) / 8;  // 16-byte chunks per row
   const int total = rows > 0 ? rows * cpr : 0;
   const int tid = (int)threadIdx.x - 128;
@@ -225,24 +236,24 @@ __device__ __forceinline__ void allreduce_unit(const GemmParams& p, int w, int m
   for (int base = tid; base < total; base += 128 * U) {
     uint32_t v[U][4];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + u * 128;
+    for (int k = 0; k < U; ++k) {
+      const int i = base + k * 128;
       if (i < total) {
         const int r = i / cpr, c = i - r * cpr;
-        multimem_ld_reduce_bf16x8(p.ar_mc + (long long)(row0 + r) * p.ldd + col0 + c * 8, v[u]);
+        multimem_ld_reduce_bf16x8(p.ar_mc + (long long)(row0 + r) * p.ldd + col0 + c * 8, v[k]);
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + u * 128;
+    for (int k = 0; k < U; ++k) {
+      const int i = base + k * 128;
       if (i < total) {
         const int r = i / cpr, c = i - r * cpr;
-        multimem_st_bf16x8(p.ar_mc + (long long)(row0 + r) * p.ldd + col0 + c * 8, v[u]);
+        multimem_st_bf16x8(p.ar_mc + (long long)(row0 + r) * p.ldd + col0 + c * 8, v[k]);
       }
     }
   }
   epi_bar();
-  if (leader_thread) {
+  if (threadIdx.x == 128) {
     fence_acq_rel_sys();
     multimem_red_release_add_u32(p.ar_counter_mc, 1u);
   }
@@ -404,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool f32 = ep == MT_EPI_STORE_F32 || ep == MT_EPI_ACCUM_F32;
     const float alpha = p.alpha;
     uint32_t it = 0;
+    ArUnit pending;  // fused all-reduce: owned unit whose reduction is deferred by one tile
     for (int w = t_first; w < p.work_items; w += t_stride) {
       Work wk;
       if (!get_work<BN, BMT>(p, w, wk)) continue;
@@ -549,8 +561,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
       }
       ++it;
-      if (p.ar_ranks > 0) allreduce_unit<BN, BMT, kPair>(p, w, mb, nb, rank, lane);
+      if (p.ar_ranks > 0) {
+        ar_publish<kPair>(p, w, rank, lane);
+        if (pending.w >= 0) ar_reduce<BN, BMT, kPair>(p, pending, rank);
+        pending.w = -1;
+        if ((w + (int)rank) % p.ar_ranks == p.ar_rank) pending = ArUnit{w, mb, nb};
+      }
     }
+    if (p.ar_ranks > 0 && pending.w >= 0) ar_reduce<BN, BMT, kPair>(p, pending, rank);
     if (lane == 0) bulk_wait<0>();
   }
 

@@ -3,7 +3,7 @@
 N=${N:-4}; CFG=${CFG:-gpt3}; port=29600
 for cfg in "$@"; do
   port=$((port + 3))
-  env $cfg timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+  env $cfg timeout -k 10 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
       --master-port $port bench.py --gpus $N --steps 5 --warmup 3 --no-cpu --config $CFG --op-timing > gpurun_out/ab.json 2>gpurun_out/ab.err
   grep "^{" gpurun_out/ab.json | tail -1 | python -c "
 import json,sys
