@@ -122,6 +122,11 @@ int mt_ctx_placement(const mt_ctx* ctx, mt_rank_placement* out);
  * layers run their shard's kernels and skip the TP all-reduces. Compute-only numbers; the
  * collectives are measured in real multi-GPU runs. Rejected when the context has a world > 1. */
 int mt_ctx_shard_only(mt_ctx* ctx, int32_t enable);
+/* Diagnostic (fused TP all-reduce contexts): time one NVLS all-reduce (multimem.ld_reduce + st) of
+ * `elems` bf16 of the symmetric row-parallel buffer with `ctas` x 1024 threads, contiguous shares or
+ * the GEMM's 128 x 256 unit pattern of a row-major [*, ld] matrix. Collective over the TP group. */
+int mt_ctx_nvls_probe(mt_ctx* ctx, int64_t elems, int64_t ld, int32_t strided, int32_t ctas, int32_t iters,
+                      double* us_per_iter);
 /* Per-GEMM CUDA-event timing of every tcgen05 GEMM the context's layers launch (stream-ordered
  * events around each launch). _read synchronises, returns the summed kernel time, summed
  * algorithmic FLOPs and launch count since enabling / the last read, and resets. */

@@ -54,7 +54,11 @@ typedef struct mt_gemm_allreduce {
   int64_t flag_capacity;         /* units the flag arrays can hold */
   uint32_t epoch;                /* larger than every epoch used before on these flags */
   int32_t rank, ranks;
+  int32_t reduce_in_epilogue;    /* 1: the GEMM's epilogue warps reduce the owned units; 0: the GEMM only
+                                    publishes them and mt_gemm_allreduce_reduce (a concurrent kernel on
+                                    the SMs the GEMM leaves free, max_ctas) reduces them */
   int64_t units;                 /* out: number of output units of this launch (counter increments) */
+  int64_t geom[8];               /* out: unit geometry of the launch, read by mt_gemm_allreduce_reduce */
 } mt_gemm_allreduce;
 
 typedef struct mt_gemm_args {
@@ -91,6 +95,11 @@ int mt_gemm(const mt_gemm_args* args, void* stream);
 /* Stream-ordered wait until the local completion counter reaches `target` (all units of all ranks of
  * the fused all-reduce launches so far); 1 launch. */
 int mt_gemm_allreduce_wait(const uint32_t* counter_local, uint32_t target, void* stream);
+/* Reducer for a launch with reduce_in_epilogue = 0: `ctas` CTAs reduce this rank's owned units in
+ * publication order as the GEMM (running concurrently, e.g. on another stream) publishes them, then
+ * wait until the local counter reaches `target`. 1 launch. */
+int mt_gemm_allreduce_reduce(const mt_gemm_allreduce* ar, void* d, int64_t ldd, const uint32_t* counter_local,
+                             uint32_t target, int32_t ctas, void* stream);
 
 /* Number of kernel launches mt_gemm issues per call (always 1). */
 int mt_gemm_launches_per_call(void);

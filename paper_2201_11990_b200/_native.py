@@ -89,6 +89,7 @@ _SIGS = {
     "mt_gemm": (C.c_int, [C.POINTER(GemmArgs), P]),
     "mt_gemm_launches_per_call": (C.c_int, []),
     "mt_gemm_allreduce_wait": (C.c_int, [P, U32, P]),
+    "mt_gemm_allreduce_reduce": (C.c_int, [P, P, I64, P, U32, I32, P]),
     "mt_last_error": (C.c_char_p, []),
     "mt_version": (C.c_char_p, []),
     "mt_map_topology": (C.c_int, [C.POINTER(ClusterTopology), C.POINTER(ParallelConfig), C.POINTER(RankPlacement),
@@ -113,6 +114,7 @@ _SIGS = {
     "mt_ctx_init_comm": (C.c_int, [P, C.c_char_p, I32, I32, C.POINTER(ParallelConfig)]),
     "mt_ctx_placement": (C.c_int, [P, C.POINTER(RankPlacement)]),
     "mt_ctx_shard_only": (C.c_int, [P, I32]),
+    "mt_ctx_nvls_probe": (C.c_int, [P, I64, I64, I32, I32, I32, PF64]),
     "mt_ctx_gemm_timing": (C.c_int, [P, I32]),
     "mt_ctx_gemm_timing_read": (C.c_int, [P, PF64, PF64, PI64]),
     "mt_ctx_op_timing": (C.c_int, [P, I32]),

@@ -54,6 +54,8 @@ struct GemmParams {
   uint32_t* ar_counter_mc;
   uint32_t ar_epoch;
   int ar_rank, ar_ranks;
+  int ar_debug;  // MT_AR_DEBUG (measurement only): 1 = skip the data movement, 2 = skip the peer wait
+  int ar_in_epi;  // 1: the epilogue warps reduce owned units; 0: publish only (mt_gemm_allreduce_reduce)
 };
 
 // kPair: 2-CTA (cta_group::2) tiles of 256 x BN — each CTA of the pair holds 128 rows of A and
@@ -186,7 +188,7 @@ __device__ __forceinline__ void reuse_wait(uint32_t lane) {
 // 128 rows x BN of tile w) TMA stores were issued and its TMEM buffer released, so the MMA of the
 // next tile proceeds meanwhile:
 //   publish: wait until the unit's stores are complete, flag[unit] = epoch (system-scope release);
-//   reduce (owner rank only, round-robin over tiles, deferred by one tile so the peers' flags are
+//   reduce (owner rank = unit % ranks, deferred by up to two owned units so the peers' flags are
 //   normally already set): wait for every peer's flag, sum the ranks' copies with
 //   multimem.ld_reduce (fp32 accumulate) and write the sum to all ranks with multimem.st, then count
 //   the unit on every rank's completion counter (multimem.red.release).
@@ -201,14 +203,16 @@ __device__ __forceinline__ int ar_unit_id(int w, uint32_t cta_rank) {
   return kPair ? 2 * w + (int)cta_rank : w;
 }
 
-template <bool kPair>
+// Publish unit `w` once its stores are complete. kPending = bulk groups of later tiles that may still
+// be in flight (the stores of the tile issued after w), so the epilogue never waits on its newest
+// stores.
+template <bool kPair, int kPending>
 __device__ __forceinline__ void ar_publish(const GemmParams& p, int w, uint32_t cta_rank, uint32_t lane) {
-  if (lane == 0) bulk_wait<0>();
+  if (lane == 0) bulk_wait<kPending>();
   __syncwarp();
   epi_bar();
   if (threadIdx.x == 128) {
     fence_proxy_async_global();
-    fence_acq_rel_sys();
     st_release_sys_u32(p.ar_flags + ar_unit_id<kPair>(w, cta_rank), p.ar_epoch);
   }
 }
@@ -216,7 +220,7 @@ __device__ __forceinline__ void ar_publish(const GemmParams& p, int w, uint32_t 
 template <int BN, int BMT, bool kPair>
 __device__ __forceinline__ void ar_reduce(const GemmParams& p, const ArUnit& u, uint32_t cta_rank) {
   const int unit = ar_unit_id<kPair>(u.w, cta_rank);
-  if (threadIdx.x == 128) {
+  if (threadIdx.x == 128 && p.ar_debug != 2) {
     for (int r = 0; r < p.ar_ranks; ++r) {
       if (r == p.ar_rank) continue;
       while ((int)(ld_acquire_sys_u32(p.ar_peer[r] + unit) - p.ar_epoch) < 0) {
@@ -229,7 +233,7 @@ __device__ __forceinline__ void ar_reduce(const GemmParams& p, const ArUnit& u, 
   const int rows = min(kBM, p.m - row0);
   const int col0 = u.nb * BN;
   const int cpr = min(BN, p.n - col0) / 8;  // 16-byte chunks per row
-  const int total = rows > 0 ? rows * cpr : 0;
+  const int total = (rows > 0 && p.ar_debug != 1) ? rows * cpr : 0;
   const int tid = (int)threadIdx.x - 128;
   constexpr int U = 8;
 #pragma unroll 1
@@ -253,9 +257,100 @@ __device__ __forceinline__ void ar_reduce(const GemmParams& p, const ArUnit& u, 
     }
   }
   epi_bar();
-  if (threadIdx.x == 128) {
+}
+
+// Reducer of the publish-only mode. Each warp owns whole units (round-robin over the units this rank
+// owns, in publication order) and progresses independently: its lanes poll the ranks' flags, then it
+// streams the unit through multimem.ld_reduce / multimem.st with 8 x 16 B in flight per lane — the
+// same access pattern as a plain NVLS all-reduce (tools/nvls_probe.py: ~390-455 GB/s algbw at
+// TP=2-4 with 16 CTAs), with no CTA-wide synchronisation between units. Each CTA counts its units
+// on every rank's counter with one system-scope release at the end; CTA 0 then waits until the local
+// counter shows all units of all ranks.
+struct ArReduceParams {
+  __nv_bfloat16* mc;
+  const uint32_t* flags[8];
+  uint32_t* counter_mc;
+  const uint32_t* counter_local;
+  uint32_t epoch, target;
+  int rank, ranks;
+  int bn, tile_m, pair, n_fastest, mblocks, nblocks, m, n;
+  long long ldd;
+};
+
+constexpr int kReduceThreads = 1024;
+
+__global__ void __launch_bounds__(kReduceThreads, 1) allreduce_reduce_kernel(const ArReduceParams p) {
+  const int units = p.mblocks * p.nblocks * (p.pair ? 2 : 1);
+  const int mine = (units - p.rank + p.ranks - 1) / p.ranks;  // units u = rank + k * ranks
+  const int lane = (int)(threadIdx.x & 31);
+  const int gwarp = (int)blockIdx.x * (kReduceThreads / 32) + (int)(threadIdx.x >> 5);
+  const int nwarps = (int)gridDim.x * (kReduceThreads / 32);
+  int done = 0;
+  for (int k = gwarp; k < mine; k += nwarps) {
+    const int u = p.rank + k * p.ranks;
+    const int w = p.pair ? (u >> 1) : u, cr = p.pair ? (u & 1) : 0;
+    if (lane < p.ranks) {
+      while ((int)(ld_acquire_sys_u32(p.flags[lane] + u) - p.epoch) < 0) {
+      }
+    }
+    __syncwarp();
+    int mb, nb;
+    if (p.n_fastest) {
+      mb = w / p.nblocks;
+      nb = w - mb * p.nblocks;
+    } else {
+      nb = w / p.mblocks;
+      mb = w - nb * p.mblocks;
+    }
+    const int row0 = mb * p.tile_m + cr * kBM;
+    const int rows = min(kBM, p.m - row0);
+    const int col0 = nb * p.bn;
+    const int cpr = min(p.bn, p.n - col0) / 8;
+    __nv_bfloat16* base_ptr = p.mc + (long long)row0 * p.ldd + col0;
+    constexpr int U = 8;
+    if (cpr == 32) {  // full 256-wide unit: lane = 16-byte column chunk, one row per (iteration, k)
+#pragma unroll 1
+      for (int r0 = 0; r0 < rows; r0 += U) {
+        uint32_t v[U][4];
+#pragma unroll
+        for (int k2 = 0; k2 < U; ++k2)
+          if (r0 + k2 < rows) multimem_ld_reduce_bf16x8(base_ptr + (long long)(r0 + k2) * p.ldd + lane * 8, v[k2]);
+#pragma unroll
+        for (int k2 = 0; k2 < U; ++k2)
+          if (r0 + k2 < rows) multimem_st_bf16x8(base_ptr + (long long)(r0 + k2) * p.ldd + lane * 8, v[k2]);
+      }
+    } else {
+      const int total = rows > 0 ? rows * cpr : 0;
+#pragma unroll 1
+      for (int base = lane; base < total; base += 32 * U) {
+        uint32_t v[U][4];
+#pragma unroll
+        for (int k2 = 0; k2 < U; ++k2) {
+          const int i = base + k2 * 32;
+          if (i < total) multimem_ld_reduce_bf16x8(base_ptr + (long long)(i / cpr) * p.ldd + (i % cpr) * 8, v[k2]);
+        }
+#pragma unroll
+        for (int k2 = 0; k2 < U; ++k2) {
+          const int i = base + k2 * 32;
+          if (i < total) multimem_st_bf16x8(base_ptr + (long long)(i / cpr) * p.ldd + (i % cpr) * 8, v[k2]);
+        }
+      }
+    }
+    ++done;
+  }
+  // one system-scope release for all of this CTA's units
+  __shared__ int cta_done;
+  if (threadIdx.x == 0) cta_done = 0;
+  __syncthreads();
+  if (lane == 0 && done > 0) atomicAdd(&cta_done, done);
+  __syncthreads();
+  if (threadIdx.x == 0 && cta_done > 0) {
     fence_acq_rel_sys();
-    multimem_red_release_add_u32(p.ar_counter_mc, 1u);
+    multimem_red_release_add_u32(p.counter_mc, (uint32_t)cta_done);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    while ((int)(ld_acquire_sys_u32(p.counter_local) - p.target) < 0) {
+    }
   }
 }
 
@@ -415,7 +510,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool f32 = ep == MT_EPI_STORE_F32 || ep == MT_EPI_ACCUM_F32;
     const float alpha = p.alpha;
     uint32_t it = 0;
-    ArUnit pending;  // fused all-reduce: owned unit whose reduction is deferred by one tile
+    // fused all-reduce: the previous tile (published after this tile's stores were issued) and up to
+    // two owned units whose reductions are deferred so the peers' flags are normally already set
+    int unpublished = -1, reduced = 0;
+    ArUnit pending[2];
     for (int w = t_first; w < p.work_items; w += t_stride) {
       Work wk;
       if (!get_work<BN, BMT>(p, w, wk)) continue;
@@ -562,13 +660,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ++it;
       if (p.ar_ranks > 0) {
-        ar_publish<kPair>(p, w, rank, lane);
-        if (pending.w >= 0) ar_reduce<BN, BMT, kPair>(p, pending, rank);
-        pending.w = -1;
-        if ((w + (int)rank) % p.ar_ranks == p.ar_rank) pending = ArUnit{w, mb, nb};
+        if (unpublished >= 0) ar_publish<kPair, BN / 32>(p, unpublished, rank, lane);
+        unpublished = w;
+        if (!p.ar_in_epi) continue;
+        if (pending[0].w >= 0 && pending[1].w >= 0) {
+          ar_reduce<BN, BMT, kPair>(p, pending[0], rank);
+          ++reduced;
+          pending[0] = pending[1];
+          pending[1].w = -1;
+        }
+        if (ar_unit_id<kPair>(w, rank) % p.ar_ranks == p.ar_rank)
+          (pending[0].w < 0 ? pending[0] : pending[1]) = ArUnit{w, mb, nb};
       }
     }
-    if (p.ar_ranks > 0 && pending.w >= 0) ar_reduce<BN, BMT, kPair>(p, pending, rank);
+    if (p.ar_ranks > 0) {
+      if (unpublished >= 0) ar_publish<kPair, 0>(p, unpublished, rank, lane);
+      for (int i = 0; i < 2; ++i)
+        if (pending[i].w >= 0) {
+          ar_reduce<BN, BMT, kPair>(p, pending[i], rank);
+          ++reduced;
+        }
+      if (p.ar_in_epi) {  // count this CTA's reduced units once, after all their stores
+        epi_bar();
+        if (threadIdx.x == 128 && reduced > 0) {
+          fence_acq_rel_sys();
+          multimem_red_release_add_u32(p.ar_counter_mc, (uint32_t)reduced);
+        }
+      }
+    }
     if (lane == 0) bulk_wait<0>();
   }
 
@@ -742,6 +861,20 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
     p.ar_epoch = ar.epoch;
     p.ar_rank = ar.rank;
     p.ar_ranks = ar.ranks;
+    static const int dbg = [] {
+      const char* e = getenv("MT_AR_DEBUG");
+      return e ? atoi(e) : 0;
+    }();
+    p.ar_debug = dbg;
+    p.ar_in_epi = ar.reduce_in_epilogue ? 1 : 0;
+    ar.geom[0] = BN;
+    ar.geom[1] = C::kTileM;
+    ar.geom[2] = kPair ? 1 : 0;
+    ar.geom[3] = p.n_fastest;
+    ar.geom[4] = p.mblocks;
+    ar.geom[5] = p.nblocks;
+    ar.geom[6] = p.m;
+    ar.geom[7] = p.n;
     ar.units = units;
   }
   auto kern = gemm_sm100_kernel<BN, kAMN, kBMN, kPair>;
@@ -829,6 +962,33 @@ bool pair_enabled() {
 }  // namespace mt
 
 extern "C" int mt_gemm_launches_per_call(void) { return 1; }
+
+extern "C" int mt_gemm_allreduce_reduce(const mt_gemm_allreduce* ar, void* d, int64_t ldd,
+                                        const uint32_t* counter_local, uint32_t target, int32_t ctas, void* stream) {
+  if (ar == nullptr || counter_local == nullptr || ctas < 1 || ar->ranks < 2 || ar->ranks > 8 || ar->geom[0] <= 0)
+    return 1;
+  (void)d;
+  mt::ArReduceParams p{};
+  p.mc = static_cast<__nv_bfloat16*>(ar->d_multicast);
+  for (int r = 0; r < ar->ranks; ++r) p.flags[r] = ar->flags_peer[r];
+  p.counter_mc = ar->counter_multicast;
+  p.counter_local = counter_local;
+  p.epoch = ar->epoch;
+  p.target = target;
+  p.rank = ar->rank;
+  p.ranks = ar->ranks;
+  p.bn = (int)ar->geom[0];
+  p.tile_m = (int)ar->geom[1];
+  p.pair = (int)ar->geom[2];
+  p.n_fastest = (int)ar->geom[3];
+  p.mblocks = (int)ar->geom[4];
+  p.nblocks = (int)ar->geom[5];
+  p.m = (int)ar->geom[6];
+  p.n = (int)ar->geom[7];
+  p.ldd = ldd;
+  mt::allreduce_reduce_kernel<<<ctas, mt::kReduceThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
 
 extern "C" int mt_gemm_allreduce_wait(const uint32_t* counter_local, uint32_t target, void* stream) {
   if (counter_local == nullptr) return 1;

@@ -655,6 +655,12 @@ void mark(mt_ctx* c, cudaStream_t st, const char* label) {
   ++c->marks_used;
 }
 
+}  // namespace
+namespace mt {
+void op_mark(mt_ctx* c, cudaStream_t st, const char* label) { mark(c, st, label); }
+}  // namespace mt
+namespace {
+
 // Whether the layer performs its TP collectives (TP > 1 with a communicator); TP > 1 without one
 // is only legal in shard-only (compute-only measurement) mode.
 bool tp_collectives(const mt_ctx* c, const mt_layer_desc& d) {
@@ -706,8 +712,9 @@ void row_parallel_block(mt_ctx* c, bool tpc, int64_t M, int64_t h, GemmFor gemm_
   }
   if (c->fused_ar && z == c->sym_h[0].ptr) {
     // one kernel: GEMM tiles + their all-reduce over NVLink SHARP from the epilogue warps
-    gemm_rows(0, M, 0, fused_ar_begin(c));
-    fused_ar_end(c, st);
+    check_cuda(cudaEventRecord(c->ev_ready, st), "cudaEventRecord");  // the reducer starts after this
+    gemm_rows(0, M, fused_ar_gemm_ctas(c), fused_ar_begin(c));
+    fused_ar_end(c, st, z, h);
     ++n;
     mark(c, st, gemm_label);
     epilogue(0, M);

@@ -24,7 +24,9 @@ struct FusedAllReduce;  // tp_fused.cu
 FusedAllReduce* fused_ar_create(mt_ctx* c);
 void fused_ar_destroy(mt_ctx* c, FusedAllReduce* f);
 mt_gemm_allreduce* fused_ar_begin(mt_ctx* c);
-void fused_ar_end(mt_ctx* c, cudaStream_t st);
+void fused_ar_end(mt_ctx* c, cudaStream_t st, void* d, int64_t ldd);
+int fused_ar_gemm_ctas(mt_ctx* c);
+void op_mark(mt_ctx* c, cudaStream_t st, const char* label);  // runtime.cpp (op timing)
 
 // Failed CUDA / NCCL call -> DataError-class status 2.
 struct RuntimeFailure : std::runtime_error {

@@ -4,15 +4,19 @@
 // registered on the TP communicator, runtime.cpp ensure_symmetric); this file adds a second small
 // symmetric window for the per-unit ready flags and the completion counter, and resolves through the
 // NCCL device API (ncclDevCommCreate with lsaMultimem) the NVLink-SHARP multicast addresses of both
-// windows and every peer's flag array. The GEMM kernel (gemm_sm100.cu, allreduce_unit) then does the
-// reduction from its epilogue warps while its tensor cores work on later tiles, and the consumer
-// waits on the counter (mt_gemm_allreduce_wait) instead of an NCCL all-reduce.
+// windows and every peer's flag array. The GEMM kernel (gemm_sm100.cu) publishes each finished
+// output unit; a reducer kernel on the SMs the GEMM leaves free (allreduce_reduce_kernel) sums every
+// unit this rank owns over NVLink SHARP as soon as all ranks published it, tile by tile while the
+// GEMM still runs, and the consumer waits on the completion counter instead of an NCCL all-reduce.
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "runtime.hpp"
+#include "sm100_ptx.cuh"
 
 namespace mt {
 
@@ -25,6 +29,10 @@ struct FusedAllReduce {
   void* z = nullptr;  // the symmetric output buffer the multicast address below belongs to
   mt_gemm_allreduce desc{};
   uint32_t target = 0;  // cumulative units of all launches: the counter value that means "all done"
+  // reducer CTAs running beside the GEMM (MT_AR_CTAS, default 16); 0 = the GEMM's epilogue warps
+  // reduce (measured slower: the multimem round trips then serialise with the epilogue)
+  int reducer_ctas = 16;
+  bool serial = false;  // MT_AR_SERIAL=1 (measurement): reducer after the GEMM on the same stream
 };
 
 namespace {
@@ -55,7 +63,9 @@ void resolve(mt_ctx* c, FusedAllReduce* f) {
     throw RuntimeFailure("fused TP all-reduce: the TP group is not one load/store-accessible multicast team");
   f->z = c->sym_h[0].ptr;
   mt_gemm_allreduce& d = f->desc;
+  const uint32_t epoch = d.epoch;  // epochs stay monotonic across re-resolution (flags keep old values)
   d = mt_gemm_allreduce{};
+  d.epoch = epoch;
   d.d_multicast = h[0];
   d.counter_multicast = static_cast<uint32_t*>(h[1]);
   d.flags_local = static_cast<uint32_t*>(f->flags) + kFlagBase;
@@ -69,6 +79,8 @@ void resolve(mt_ctx* c, FusedAllReduce* f) {
 
 FusedAllReduce* fused_ar_create(mt_ctx* c) {
   auto f = new FusedAllReduce();
+  if (const char* e = getenv("MT_AR_CTAS")) f->reducer_ctas = std::max(0, atoi(e));
+  if (const char* e = getenv("MT_AR_SERIAL")) f->serial = e[0] == '1';
   try {
     ncclDevCommRequirements req{};
     req.lsaMultimem = true;
@@ -106,15 +118,106 @@ mt_gemm_allreduce* fused_ar_begin(mt_ctx* c) {
   if (f->z != c->sym_h[0].ptr) resolve(c, f);
   f->desc.epoch += 1;
   f->desc.units = 0;
+  f->desc.reduce_in_epilogue = f->reducer_ctas == 0 ? 1 : 0;
   return &f->desc;
 }
 
-// Orders `st` after every unit of every rank of the launch described by `d`.
-void fused_ar_end(mt_ctx* c, cudaStream_t st) {
+// SMs the fused GEMM may use (the reducer kernel takes the rest), 0 = all.
+int fused_ar_gemm_ctas(mt_ctx* c) {
+  const FusedAllReduce* f = c->fused_ar;
+  if (f->reducer_ctas == 0 || f->serial) return 0;
+  int sms = 0;
+  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device), "attr");
+  return std::max(2, (sms - f->reducer_ctas) / 2 * 2);
+}
+
+// After the GEMM was enqueued on `st` (following ev_ready recorded just before it): orders `st`
+// after every unit of every rank of the launch. With a reducer, the reducer runs on the side stream
+// concurrently with the GEMM (it starts only after the work that preceded the GEMM on `st`, so it
+// never holds SMs a preceding kernel still needs).
+void fused_ar_end(mt_ctx* c, cudaStream_t st, void* d, int64_t ldd) {
   FusedAllReduce* f = c->fused_ar;
   f->target += static_cast<uint32_t>(f->desc.units);
-  const int rc = mt_gemm_allreduce_wait(static_cast<const uint32_t*>(f->flags), f->target, st);
-  if (rc != 0) throw RuntimeFailure("mt_gemm_allreduce_wait failed");
+  const uint32_t* counter = static_cast<const uint32_t*>(f->flags);
+  if (f->reducer_ctas == 0) {
+    if (mt_gemm_allreduce_wait(counter, f->target, st) != 0) throw RuntimeFailure("mt_gemm_allreduce_wait failed");
+    return;
+  }
+  if (f->serial) {
+    op_mark(c, st, "fwd.fused_gemm_only");
+    if (mt_gemm_allreduce_reduce(&f->desc, d, ldd, counter, f->target, f->reducer_ctas, st) != 0)
+      throw RuntimeFailure("mt_gemm_allreduce_reduce failed");
+    op_mark(c, st, "fwd.fused_reducer_only");
+    return;
+  }
+  check_cuda(cudaStreamWaitEvent(c->comm, c->ev_ready, 0), "cudaStreamWaitEvent");
+  if (mt_gemm_allreduce_reduce(&f->desc, d, ldd, counter, f->target, f->reducer_ctas, c->comm) != 0)
+    throw RuntimeFailure("mt_gemm_allreduce_reduce failed");
+  check_cuda(cudaEventRecord(c->ev_done, c->comm), "cudaEventRecord");
+  check_cuda(cudaStreamWaitEvent(st, c->ev_done, 0), "cudaStreamWaitEvent");
+}
+
+// ---- diagnostic: raw NVLS all-reduce throughput over the symmetric buffer (mt_ctx_nvls_probe)
+namespace {
+__global__ void __launch_bounds__(1024) nvls_probe_kernel(__nv_bfloat16* mc, long long elems, int rank, int ranks,
+                                                          int strided, long long ld) {
+  // this rank's 1/ranks share in 16-byte chunks; contiguous (strided = 0) or as 128 x 256 tiles of
+  // a row-major [*, ld] matrix (strided = 1, the GEMM unit pattern)
+  const long long chunks = elems / 8, per = chunks / ranks, c0 = per * rank;
+  constexpr int U = 4;
+  for (long long base = c0 + blockIdx.x * (long long)blockDim.x * U + threadIdx.x; base < c0 + per;
+       base += (long long)gridDim.x * blockDim.x * U) {
+    uint32_t v[U][4];
+    long long off[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      long long q = base + (long long)k * blockDim.x;
+      if (strided) {  // chunk q -> tile t, row r, col chunk c (32 chunks per 256-wide tile row)
+        const long long t = q / 4096, within = q % 4096, r = within / 32, c = within % 32;
+        const long long tiles_per_row = ld / 256;
+        const long long tr = t / tiles_per_row, tc = t % tiles_per_row;
+        off[k] = (tr * 128 + r) * ld + tc * 256 + c * 8;
+      } else {
+        off[k] = q * 8;
+      }
+      if (q < c0 + per) multimem_ld_reduce_bf16x8(mc + off[k], v[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (base + (long long)k * blockDim.x < c0 + per) multimem_st_bf16x8(mc + off[k], v[k]);
+  }
+}
+}  // namespace
+
+extern "C" int mt_ctx_nvls_probe(mt_ctx* c, int64_t elems, int64_t ld, int32_t strided, int32_t ctas, int32_t iters,
+                                 double* us_per_iter) {
+  try {
+    if (!c || !c->fused_ar || !c->sym_h[0].ptr) throw std::invalid_argument("no fused all-reduce state");
+    if (elems * 2 > (int64_t)c->sym_h[0].bytes) throw std::invalid_argument("probe larger than the buffer");
+    FusedAllReduce* f = c->fused_ar;
+    if (f->z != c->sym_h[0].ptr) resolve(c, f);
+    auto* mc = static_cast<__nv_bfloat16*>(f->desc.d_multicast);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    check_nccl(ncclAllReduce(f->flags, f->flags, 1, ncclUint32, ncclSum, c->tp, nullptr), "sync");
+    nvls_probe_kernel<<<ctas, 1024>>>(mc, elems, c->place.tensor, c->par.tensor, strided, ld);
+    check_cuda(cudaDeviceSynchronize(), "probe warmup");
+    check_nccl(ncclAllReduce(f->flags, f->flags, 1, ncclUint32, ncclSum, c->tp, nullptr), "sync");
+    cudaEventRecord(e0);
+    for (int i = 0; i < iters; ++i)
+      nvls_probe_kernel<<<ctas, 1024>>>(mc, elems, c->place.tensor, c->par.tensor, strided, ld);
+    cudaEventRecord(e1);
+    check_cuda(cudaEventSynchronize(e1), "probe");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *us_per_iter = 1e3 * ms / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return MT_OK;
+  } catch (const std::exception& e) {
+    return MT_ERR_DATA;
+  }
 }
 
 }  // namespace mt
