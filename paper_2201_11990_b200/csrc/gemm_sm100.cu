@@ -359,7 +359,7 @@ __global__ void allreduce_wait_kernel(const uint32_t* counter, uint32_t target) 
   }
 }
 
-template <int BN, bool kAMN, bool kBMN, bool kPair>
+template <int BN, bool kAMN, bool kBMN, bool kPair, bool kAR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                       const __grid_constant__ CUtensorMap tmap_d, const __grid_constant__ CUtensorMap tmap_aux,
@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
       }
       ++it;
-      if (p.ar_ranks > 0) {
+      if (kAR && p.ar_ranks > 0) {
         if (unpublished >= 0) ar_publish<kPair, BN / 32>(p, unpublished, rank, lane);
         unpublished = w;
         if (!p.ar_in_epi) continue;
@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           (pending[0].w < 0 ? pending[0] : pending[1]) = ArUnit{w, mb, nb};
       }
     }
-    if (p.ar_ranks > 0) {
+    if (kAR && p.ar_ranks > 0) {
       if (unpublished >= 0) ar_publish<kPair, 0>(p, unpublished, rank, lane);
       for (int i = 0; i < 2; ++i)
         if (pending[i].w >= 0) {
@@ -778,7 +778,9 @@ int num_sms() {
   return n;
 }
 
-template <int BN, bool kAMN, bool kBMN, bool kPair>
+// kAR: the fused TP all-reduce variant (only the K-major x K-major row-parallel forward GEMMs use it;
+// a separate instantiation so the plain kernels keep their register budget).
+template <int BN, bool kAMN, bool kBMN, bool kPair, bool kAR = false>
 int launch(const mt_gemm_args& a, cudaStream_t stream) {
   using C = Cfg<BN, kPair>;
   CUtensorMap ma, mb;
@@ -877,7 +879,7 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
     ar.geom[7] = p.n;
     ar.units = units;
   }
-  auto kern = gemm_sm100_kernel<BN, kAMN, kBMN, kPair>;
+  auto kern = gemm_sm100_kernel<BN, kAMN, kBMN, kPair, kAR>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
@@ -911,7 +913,10 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
 template <int BN, bool kPair>
 int dispatch_major(const mt_gemm_args& a, cudaStream_t s) {
   if (a.a_mn_major)
-    return a.b_mn_major ? launch<BN, true, true, kPair>(a, s) : launch<BN, true, false, kPair>(a, s);
+    return a.allreduce != nullptr ? 1
+           : a.b_mn_major        ? launch<BN, true, true, kPair>(a, s)
+                                 : launch<BN, true, false, kPair>(a, s);
+  if (a.allreduce != nullptr) return a.b_mn_major ? 1 : launch<BN, false, false, kPair, true>(a, s);
   return a.b_mn_major ? launch<BN, false, true, kPair>(a, s) : launch<BN, false, false, kPair>(a, s);
 }
 
