@@ -334,6 +334,8 @@ __device__ __forceinline__ float ex2_recompute(float x) {
   return y;
 }
 
+// Full 8-score vectors (v < nvalid / 8) take a branch-free path; only the row's last, partial
+// vector pays the per-element causal checks (the kernels were issue-bound on those checks).
 template <int VPL>
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(const uint4* __restrict__ S, uint4* __restrict__ P,
                                                           float* __restrict__ lse, int rows_total, int seq,
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const uint4* __restric
   const int nvec_row = seq >> 3;
   const uint4* srow = S + (size_t)warp * nvec_row;
   uint4* prow = P + (size_t)warp * nvec_row;
-  const int nvalid = i + 1, nvec = (nvalid + 7) >> 3;
+  const int nvalid = i + 1, nvec = (nvalid + 7) >> 3, nfull = nvalid >> 3, rem = nvalid & 7;
   uint4 raw[VPL];
   float mx = -INFINITY;
 #pragma unroll
@@ -360,9 +362,14 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const uint4* __restric
     if (v < nvec) {
       float x[8];
       unpack8_v(raw[t], x);
+      if (v < nfull) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (v * 8 + j < nvalid) mx = fmaxf(mx, x[j]);
+        for (int j = 0; j < 8; ++j) mx = fmaxf(mx, x[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < rem) mx = fmaxf(mx, x[j]);
+      }
     }
   }
   mx = warp_max(mx);
@@ -374,8 +381,14 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const uint4* __restric
     if (v < nvec) {
       float x[8];
       unpack8_v(raw[t], x);
+      if (v < nfull) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sum += (v * 8 + j < nvalid) ? ex2_recompute(fmaf(x[j], kLog2e, -mx2)) : 0.f;
+        for (int j = 0; j < 8; ++j) sum += ex2_recompute(fmaf(x[j], kLog2e, -mx2));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < rem) sum += ex2_recompute(fmaf(x[j], kLog2e, -mx2));
+      }
     }
   }
   sum = warp_sum(sum);
@@ -386,13 +399,14 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const uint4* __restric
   for (int t = 0; t < VPL; ++t) {
     const int v = lane + 32 * t;
     if (v < nvec) {
-      const uint32_t keep = keep_mask8(seed, base_idx + v * 8, thresh16);
+      uint32_t keep = keep_mask8(seed, base_idx + v * 8, thresh16);
+      if (v == nfull) keep &= (1u << rem) - 1u;  // causal tail of the row
       float x[8], o[8];
       unpack8_v(raw[t], x);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const bool ok = (v * 8 + j < nvalid) && ((keep >> j) & 1u);
-        o[j] = ok ? ex2_recompute(fmaf(x[j], kLog2e, -l2)) * scale : 0.f;
+        const float e = ex2_recompute(fmaf(x[j], kLog2e, -l2)) * scale;
+        o[j] = ((keep >> j) & 1u) ? e : 0.f;
       }
       prow[v] = pack8(o);
     }
@@ -414,7 +428,7 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const uint4* __restric
   const int nvec_row = seq >> 3;
   const uint4* srow = S + (size_t)warp * nvec_row;
   uint4* drow = dP + (size_t)warp * nvec_row;
-  const int nvalid = i + 1, nvec = (nvalid + 7) >> 3;
+  const int nvalid = i + 1, nvec = (nvalid + 7) >> 3, nfull = nvalid >> 3, rem = nvalid & 7;
   const float l2 = lse[warp] * kLog2e;
   const uint64_t base_idx = ((uint64_t)(head_base + bh) * seq + i) * (uint64_t)seq;
   uint4 rs[VPL], rg[VPL];
@@ -433,14 +447,16 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const uint4* __restric
     keep[t] = 0;
     if (v < nvec) {
       uint32_t k = keep_mask8(seed, base_idx + v * 8, thresh16);
-      if (v * 8 + 8 > nvalid) k &= (1u << (nvalid - v * 8)) - 1u;  // causal tail of the row
+      if (v == nfull) k &= (1u << rem) - 1u;  // causal tail of the row
       keep[t] = k;
       float sv[8], g[8];
       unpack8_v(rs[t], sv);
       unpack8_v(rg[t], g);
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if ((k >> j) & 1u) dot += ex2_recompute(fmaf(sv[j], kLog2e, -l2)) * g[j];
+      for (int j = 0; j < 8; ++j) {
+        const float pg = ex2_recompute(fmaf(sv[j], kLog2e, -l2)) * g[j];
+        dot += ((k >> j) & 1u) ? pg : 0.f;
+      }
     }
   }
   dot = warp_sum(dot) * scale;
@@ -451,12 +467,12 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const uint4* __restric
       float sv[8], g[8], o[8];
       unpack8_v(rs[t], sv);
       unpack8_v(rg[t], g);
+      const uint32_t valid = v < nfull ? 0xffu : (1u << rem) - 1u;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const bool valid = v * 8 + j < nvalid;
-        const float y = valid ? ex2_recompute(fmaf(sv[j], kLog2e, -l2)) : 0.f;
+        const float y = ex2_recompute(fmaf(sv[j], kLog2e, -l2));
         const float gj = ((keep[t] >> j) & 1u) ? g[j] * scale : 0.f;
-        o[j] = alpha * y * (gj - dot);
+        o[j] = ((valid >> j) & 1u) ? alpha * y * (gj - dot) : 0.f;
       }
       drow[v] = pack8(o);
     }
