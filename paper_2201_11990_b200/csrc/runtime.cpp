@@ -824,14 +824,24 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
   void* z = tp_buffer(c, 0);
   mark(c, st, "begin");
 
-  ln_fwd(x, l->param_ptr(MT_P_LN1_GAMMA), l->param_ptr(MT_P_LN1_BETA), sv.ln1.ptr, mean1, rstd1, (int)M, (int)h,
-         d.ln_eps, st);
-  ++n;
-  mark(c, st, "fwd.ln1");
-  Gemm(sv.ln1.ptr, h, false, l->param_ptr(MT_P_QKV_W), h, false, sv.qkv.ptr, ld3, M, ld3, h)
-      .bias(l->param_ptr(MT_P_QKV_B))
-      .run(st, n);
-  mark(c, st, "fwd.qkv_gemm");
+  // LN1 + QKV GEMM, by row chunks when the input arrives in chunks (input_gate)
+  const int in_chunks = (l->input_gate && l->input_chunks > 1 && M % (int64_t{l->input_chunks} * 128) == 0)
+                            ? l->input_chunks
+                            : 1;
+  const int64_t in_rows = M / in_chunks;
+  for (int k = 0; k < in_chunks; ++k) {
+    const int64_t r0 = k * in_rows;
+    if (l->input_gate) l->input_gate(k, st);
+    ln_fwd(static_cast<const uint16_t*>(x) + r0 * h, l->param_ptr(MT_P_LN1_GAMMA), l->param_ptr(MT_P_LN1_BETA),
+           sv.ln1.as<uint16_t>() + r0 * h, mean1 + r0, rstd1 + r0, (int)in_rows, (int)h, d.ln_eps, st);
+    ++n;
+    mark(c, st, "fwd.ln1");
+    Gemm(sv.ln1.as<uint16_t>() + r0 * h, h, false, l->param_ptr(MT_P_QKV_W), h, false,
+         sv.qkv.as<uint16_t>() + r0 * ld3, ld3, in_rows, ld3, h)
+        .bias(l->param_ptr(MT_P_QKV_B))
+        .run(st, n);
+    mark(c, st, "fwd.qkv_gemm");
+  }
   const float alpha = 1.f / std::sqrt((float)hd);
   for (int64_t bb = 0; bb < d.micro_batch; ++bb) {
     const uint16_t* q = sv.qkv.as<uint16_t>() + bb * s * ld3;

@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -156,6 +157,11 @@ struct mt_layer {
   // Logically zero gradients: the next backward writes (=) instead of accumulating (+=), which
   // saves both the memset and the read half of the fp32 read-modify-write in the wgrad epilogues.
   bool grads_fresh = false;
+  // Optional row-chunk gate on the layer input (set by the stage for the first layer when its input
+  // streams in from the host): forward runs LN1 + the QKV GEMM chunk by chunk, calling
+  // input_gate(k, stream) before chunk k so the copy of chunk k+1 overlaps the compute of chunk k.
+  int input_chunks = 1;
+  std::function<void(int, cudaStream_t)> input_gate;
   // optimizer state (created on the first optimizer step): fp32 master weights, Adam moments
   mt::DeviceBuffer opt_master, opt_m, opt_v;
   void* param_ptr(int p) const { return static_cast<uint16_t*>(params.ptr) + param_off[p]; }

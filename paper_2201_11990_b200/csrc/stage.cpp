@@ -6,6 +6,8 @@
 // NCCL group, and "send gradient backward + receive next activation" as another. After the last
 // backward the fp32 parameter gradients are all-reduced (mean) over the data-parallel group
 // (PAPER.md:103-131). TP all-reduces happen inside the layers.
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -41,6 +43,9 @@ struct mt_stage {
   mt_vocab* vocab = nullptr;
   std::vector<mt::DeviceBuffer> tokens;            // [MB][M] int32 (host-input path, first stage)
   int64_t h2d_bytes = 0, d2h_bytes = 0;            // host traffic of the last mt_stage_train_step
+  // host inputs arrive in row chunks (one event each) that layer 0 consumes as they land
+  static constexpr int kMaxInChunks = 4;
+  int in_chunks = kMaxInChunks;                    // MT_INPUT_CHUNKS (1 disables)
 };
 
 namespace {
@@ -95,6 +100,16 @@ struct Step {
                    "ncclAllGather(input slices)");
     ++launches;
   }
+  // Host input of the first stage split into row chunks: the copy of chunk k+1 overlaps LN1 + QKV
+  // GEMM of chunk k inside layer 0 (mt_layer::input_gate).
+  int in_chunks() const {
+    const int k = st->in_chunks, t = split_h2d() ? st->ctx->par.tensor : 1;
+    if (!in_host || !first() || lm() || st->layers.empty() || k <= 1) return 1;
+    return (st->M % (int64_t{k} * 128) == 0 && (st->M / k) % t == 0) ? k : 1;
+  }
+  size_t chunk_bytes() const { return bytes() / in_chunks(); }
+  size_t chunk_slice_bytes() const { return split_h2d() ? chunk_bytes() / st->ctx->par.tensor : chunk_bytes(); }
+  size_t chunk_slice_off() const { return split_h2d() ? chunk_slice_bytes() * st->ctx->place.tensor : 0; }
   ncclComm_t pp() const { return st->ctx->pp; }
   // Global microbatch id (data-parallel replicas see different samples): keys the synthetic
   // inputs/targets and the dropout masks of the microbatch.
@@ -112,13 +127,22 @@ struct Step {
     mt::check_cuda(cudaEventRecord(st->iter_start, s), "cudaEventRecord");
     mt::check_cuda(cudaStreamWaitEvent(st->copy, st->iter_start, 0), "cudaStreamWaitEvent");
     for (int mb = 0; mb < st->d.micro_batches; ++mb) {
-      if (in_host && first()) {
+      if (in_host && first() && in_chunks() > 1) {
+        for (int k = 0; k < in_chunks(); ++k) {
+          const size_t off = k * chunk_bytes() + chunk_slice_off();
+          mt::check_cuda(cudaMemcpyAsync(static_cast<char*>(st->act[mb][0].ptr) + off, in_host + mb * io_bytes() + off,
+                                         chunk_slice_bytes(), cudaMemcpyHostToDevice, st->copy),
+                         "H2D input chunk");
+          st->h2d_bytes += static_cast<int64_t>(chunk_slice_bytes());
+          mt::check_cuda(cudaEventRecord(st->in_ev[mb * mt_stage::kMaxInChunks + k], st->copy), "cudaEventRecord");
+        }
+      } else if (in_host && first()) {
         char* dst = static_cast<char*>(lm() ? st->tokens[mb].ptr : st->act[mb][0].ptr) + slice_off();
         mt::check_cuda(cudaMemcpyAsync(dst, in_host + mb * io_bytes() + slice_off(), slice_bytes(),
                                        cudaMemcpyHostToDevice, st->copy),
                        "H2D input");
         st->h2d_bytes += static_cast<int64_t>(slice_bytes());
-        mt::check_cuda(cudaEventRecord(st->in_ev[mb], st->copy), "cudaEventRecord");
+        mt::check_cuda(cudaEventRecord(st->in_ev[mb * mt_stage::kMaxInChunks], st->copy), "cudaEventRecord");
       }
       if (tgt_host && last()) {
         mt::check_cuda(cudaMemcpyAsync(static_cast<char*>(st->targets[mb].ptr) + slice_off(),
@@ -136,14 +160,16 @@ struct Step {
   void load_input(int mb) {
     void* dst = st->act[mb][0].ptr;
     if (lm()) {  // token ids -> embeddings (+ position, dropout; TP all-reduce of the vocab-parallel gather)
-      if (in_host) mt::check_cuda(cudaStreamWaitEvent(s, st->in_ev[mb], 0), "cudaStreamWaitEvent");
+      if (in_host)
+        mt::check_cuda(cudaStreamWaitEvent(s, st->in_ev[mb * mt_stage::kMaxInChunks], 0), "cudaStreamWaitEvent");
       ok(mt_vocab_embed_forward(st->vocab, tokens(mb), dst, gid(mb), s));
       launches += 2 + (st->ctx->par.tensor > 1 ? 1 : 0);
       return;
     }
     if (in_dev) return;  // read in place by layer 0
     if (in_host) {
-      mt::check_cuda(cudaStreamWaitEvent(s, st->in_ev[mb], 0), "cudaStreamWaitEvent");
+      if (in_chunks() > 1) return;  // layer 0 waits chunk by chunk (forward)
+      mt::check_cuda(cudaStreamWaitEvent(s, st->in_ev[mb * mt_stage::kMaxInChunks], 0), "cudaStreamWaitEvent");
       gather_slices(dst);
     } else {
       const uint64_t key = mt_stream_key(st->d.layer.seed, "input", 0, gid(mb));
@@ -152,9 +178,30 @@ struct Step {
     }
   }
   void forward(int mb) {
+    const int K = in_chunks();
+    if (K > 1) {
+      mt_layer* l0 = st->layers[0];
+      l0->input_chunks = K;
+      l0->input_gate = [this, mb, K](int k, cudaStream_t stream) {
+        mt::check_cuda(cudaStreamWaitEvent(stream, st->in_ev[mb * mt_stage::kMaxInChunks + k], 0),
+                       "cudaStreamWaitEvent");
+        if (split_h2d()) {
+          char* base = static_cast<char*>(st->act[mb][0].ptr) + k * chunk_bytes();
+          const size_t n = elems() / K / st->ctx->par.tensor;
+          mt::check_nccl(ncclAllGather(base + chunk_slice_off(), base, n, ncclBfloat16, st->ctx->tp, stream),
+                         "ncclAllGather(input chunk slices)");
+          ++launches;
+        }
+      };
+    }
     for (size_t i = 0; i < st->layers.size(); ++i) {
       const void* x = i == 0 ? input(mb) : st->act[mb][i].ptr;
-      ok(mt_layer_forward(st->layers[i], x, st->act[mb][i + 1].ptr, gid(mb), s));
+      const int rc = mt_layer_forward(st->layers[i], x, st->act[mb][i + 1].ptr, gid(mb), s);
+      if (i == 0 && K > 1) {
+        st->layers[0]->input_gate = nullptr;
+        st->layers[0]->input_chunks = 1;
+      }
+      ok(rc);
       int32_t f, b;
       mt_layer_launch_counts(st->layers[i], &f, &b);
       launches += f;
@@ -256,7 +303,8 @@ extern "C" int mt_stage_create(mt_ctx* c, const mt_stage_desc* d, mt_stage** out
     st->loss.ensure(4);
     mt::check_cuda(cudaStreamCreateWithFlags(&st->copy, cudaStreamNonBlocking), "copy stream");
     mt::check_cuda(cudaEventCreateWithFlags(&st->iter_start, cudaEventDisableTiming), "event");
-    st->in_ev.resize(d->micro_batches);
+    st->in_ev.resize(size_t(d->micro_batches) * mt_stage::kMaxInChunks);
+    if (const char* e = getenv("MT_INPUT_CHUNKS")) st->in_chunks = std::max(1, std::min(mt_stage::kMaxInChunks, atoi(e)));
     st->tgt_ev.resize(d->micro_batches);
     for (auto& e : st->in_ev) mt::check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : st->tgt_ev) mt::check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
