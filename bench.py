@@ -42,6 +42,9 @@ def layout_for(config: str, n: int) -> dict:
     if config == "mtnlg":
         return dict(hidden=20480, heads=128, seq=2048, b=1, layers=1, mb=1, tp=n, pp=1, dp=1,
                     model="MT-NLG-530B-shape layer", note=f"TP={n}")
+    if config == "dp":  # h=8192 2-layer slice replicated over DP = n, 4 microbatches per replica
+        return dict(hidden=8192, heads=64, seq=2048, b=1, layers=2, mb=4, tp=1, pp=1, dp=n,
+                    model="h=8192 2-layer slice, data parallel", note=f"DP={n} (MB=4)")
     if config == "tiny":
         return dict(hidden=256, heads=4, seq=128, b=4, layers=2, mb=1, tp=n, pp=1, dp=1,
                     model="tiny GPT (2 layers, h=256)", note=f"TP={n}")
@@ -375,7 +378,7 @@ def main() -> None:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="gpt3", choices=["gpt3", "mtnlg", "pp", "3d", "tiny"])
+    ap.add_argument("--config", default="gpt3", choices=["gpt3", "mtnlg", "pp", "3d", "dp", "tiny"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
     ap.add_argument("--shard-of", type=int, default=0,

@@ -145,6 +145,7 @@ struct Gemm {
       }
       check_cuda(cudaEventRecord(c->ev_pool[c->ev_used], s), "cudaEventRecord");
     }
+    if (c && c->gemm_cap > 0) a.max_ctas = a.max_ctas > 0 ? std::min(a.max_ctas, c->gemm_cap) : c->gemm_cap;
     if (c && c->gemm_ws.ptr) {
       a.workspace = c->gemm_ws.ptr;
       a.workspace_bytes = static_cast<int64_t>(c->gemm_ws.bytes);
@@ -271,7 +272,10 @@ extern "C" int mt_ctx_destroy(mt_ctx* c) {
     if (c->fused_ar) fused_ar_destroy(c, c->fused_ar);
     c->fused_ar = nullptr;
     for (auto& sb : c->sym_h) release_symmetric(c, sb);
-    for (ncclComm_t* cm : {&c->emb, &c->tp_side, &c->tp, &c->pp, &c->dp, &c->world})
+    if (c->dp_stream) cudaStreamDestroy(c->dp_stream);
+    if (c->ev_dp_ready) cudaEventDestroy(c->ev_dp_ready);
+    if (c->ev_dp_done) cudaEventDestroy(c->ev_dp_done);
+    for (ncclComm_t* cm : {&c->dp_side, &c->emb, &c->tp_side, &c->tp, &c->pp, &c->dp, &c->world})
       if (*cm) ncclCommDestroy(*cm);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (auto& m : c->marks) cudaEventDestroy(m.second);
@@ -335,6 +339,18 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
     check_nccl(ncclCommSplit(c->world, tp_color, me.tensor, &c->tp_side, &side_cfg), "ncclCommSplit(tp_side)");
     check_nccl(ncclCommSplit(c->world, pp_color, me.pipeline, &c->pp, nullptr), "ncclCommSplit(pp)");
     check_nccl(ncclCommSplit(c->world, dp_color, me.data, &c->dp, nullptr), "ncclCommSplit(dp)");
+    if (p.data > 1) {
+      if (const char* e = getenv("MT_DP_OVERLAP")) c->dp_overlap = e[0] != '0';
+      ncclConfig_t dcfg = NCCL_CONFIG_INITIALIZER;
+      dcfg.maxCTAs = std::max(1, c->comm_sms);
+      dcfg.minCTAs = std::min(dcfg.maxCTAs, 4);
+      check_nccl(ncclCommSplit(c->world, dp_color, me.data, &c->dp_side, &dcfg), "ncclCommSplit(dp_side)");
+      int lo = 0, hi = 0;
+      check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+      check_cuda(cudaStreamCreateWithPriority(&c->dp_stream, cudaStreamNonBlocking, hi), "dp stream");
+      check_cuda(cudaEventCreateWithFlags(&c->ev_dp_ready, cudaEventDisableTiming), "event");
+      check_cuda(cudaEventCreateWithFlags(&c->ev_dp_done, cudaEventDisableTiming), "event");
+    }
     if (p.pipeline > 1) {  // tied word embeddings live on the first and the last stage
       const bool ends = me.pipeline == 0 || me.pipeline == p.pipeline - 1;
       check_nccl(ncclCommSplit(c->world, ends ? pp_color : NCCL_SPLIT_NOCOLOR, me.pipeline, &c->emb, nullptr),

@@ -95,6 +95,14 @@ struct mt_ctx {
     size_t bytes = 0;
     ncclWindow_t win_tp = nullptr, win_side = nullptr;
   } sym_h[2];
+  // DP > 1: the gradient all-reduce of each layer is issued on dp_stream over a CTA-capped DP
+  // communicator (dp_side) as soon as the layer's last backward finished, overlapping the backward of
+  // the layers below it (MT_DP_OVERLAP=0 disables); GEMMs issued meanwhile are capped at gemm_cap CTAs
+  ncclComm_t dp_side = nullptr;
+  cudaStream_t dp_stream = nullptr;
+  cudaEvent_t ev_dp_ready = nullptr, ev_dp_done = nullptr;
+  bool dp_overlap = true;
+  int gemm_cap = 0;
   bool tp_symmetric = false;
   // forward row-parallel GEMM + TP all-reduce fused in one kernel over NVLink SHARP (MT_TP_FUSED=1;
   // implies symmetric buffers); state in tp_fused.cu

@@ -232,8 +232,14 @@ struct Step {
       ++launches;
     }
   }
+  bool dp_overlapped = false;  // this iteration's layer gradients were all-reduced during the backward
   // Backward of microbatch mb; gradient arrives in g (last stage: in act[mb][L]). Returns dx buffer.
+  // During the backward of the last microbatch each layer's gradients are final as soon as its
+  // backward is done: their DP all-reduce is issued right away on the DP side stream and overlaps
+  // the backward of the layers below (the GEMMs issued meanwhile leave the collective its SMs).
   void* backward(int mb, void* g) {
+    mt_ctx* c = st->ctx;
+    const bool overlap = c->dp_side && c->dp_overlap && mb == st->d.micro_batches - 1;
     void* cur = g;
     for (size_t i = st->layers.size(); i-- > 0;) {
       void* out = (cur == st->grad[0].ptr) ? st->grad[1].ptr : st->grad[0].ptr;
@@ -242,7 +248,21 @@ struct Step {
       mt_layer_launch_counts(st->layers[i], &f, &b);
       launches += b;
       cur = out;
+      if (overlap && i > 0) {  // layers below remain to overlap with (the bottom layer uses the full comm)
+        mt_layer* l = st->layers[i];
+        mt::check_cuda(cudaEventRecord(c->ev_dp_ready, s), "cudaEventRecord");
+        mt::check_cuda(cudaStreamWaitEvent(c->dp_stream, c->ev_dp_ready, 0), "cudaStreamWaitEvent");
+        mt::check_nccl(ncclAllReduce(l->grads.ptr, l->grads.ptr, l->param_total, ncclFloat32, ncclAvg, c->dp_side,
+                                     c->dp_stream),
+                       "ncclAllReduce(dp, overlapped)");
+        ++launches;
+        int sms = 0;
+        mt::check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device), "attr");
+        c->gemm_cap = std::max(2, (sms - c->comm_sms) / 2 * 2);
+        dp_overlapped = true;
+      }
     }
+    if (overlap) c->gemm_cap = 0;
     if (lm() && first()) {
       ok(mt_vocab_embed_backward(st->vocab, tokens(mb), cur, gid(mb), s));
       ++launches;
@@ -410,9 +430,16 @@ void run_iteration(Step& k, mt_stage* st, void* stream) {
       mt::vocab_allreduce_grads(st->vocab, st->ctx->dp, false, true, k.s);
       k.launches += 4;
     }
-    for (auto* l : st->layers) {
-      ok(mt_dp_allreduce_f32(st->ctx, l->grads.as<float>(), l->param_total, 1, stream));
+    if (k.dp_overlapped) {  // layers 1.. were all-reduced during the last backward; layer 0 here
+      ok(mt_dp_allreduce_f32(st->ctx, st->layers[0]->grads.as<float>(), st->layers[0]->param_total, 1, stream));
       ++k.launches;
+      mt::check_cuda(cudaEventRecord(st->ctx->ev_dp_done, st->ctx->dp_stream), "cudaEventRecord");
+      mt::check_cuda(cudaStreamWaitEvent(k.s, st->ctx->ev_dp_done, 0), "cudaStreamWaitEvent");
+    } else {
+      for (auto* l : st->layers) {
+        ok(mt_dp_allreduce_f32(st->ctx, l->grads.as<float>(), l->param_total, 1, stream));
+        ++k.launches;
+      }
     }
     if (k.last()) {
       ok(mt_dp_allreduce_f32(st->ctx, st->loss.as<float>(), 1, 1, stream));
