@@ -275,6 +275,7 @@ struct ArReduceParams {
   int rank, ranks;
   int bn, tile_m, pair, n_fastest, mblocks, nblocks, m, n;
   long long ldd;
+  int debug;  // MT_AR_DEBUG=2: skip the flag waits (measurement only)
 };
 
 constexpr int kReduceThreads = 1024;
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(kReduceThreads, 1) allreduce_reduce_kernel(con
   for (int k = gwarp; k < mine; k += nwarps) {
     const int u = p.rank + k * p.ranks;
     const int w = p.pair ? (u >> 1) : u, cr = p.pair ? (u & 1) : 0;
-    if (lane < p.ranks) {
+    if (lane < p.ranks && p.debug != 2) {
       while ((int)(ld_acquire_sys_u32(p.flags[lane] + u) - p.epoch) < 0) {
       }
     }
@@ -991,6 +992,11 @@ extern "C" int mt_gemm_allreduce_reduce(const mt_gemm_allreduce* ar, void* d, in
   p.m = (int)ar->geom[6];
   p.n = (int)ar->geom[7];
   p.ldd = ldd;
+  static const int dbg = [] {
+    const char* e = getenv("MT_AR_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  p.debug = dbg;
   mt::allreduce_reduce_kernel<<<ctas, mt::kReduceThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }

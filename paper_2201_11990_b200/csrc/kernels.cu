@@ -11,7 +11,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 
 #include "curator/dropout.hpp"
@@ -554,8 +556,19 @@ static void row_launch_shape(int h, int& threads, int& vpt) {
   vpt = (nvec + threads - 1) / threads;
 }
 
+// TMA-fed persistent row kernels (rows_sm100.cu); MT_ROW_KERNELS=0 selects the per-row kernels.
+static bool row_kernels_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MT_ROW_KERNELS");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 void ln_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int rows, int h,
             float eps, cudaStream_t s) {
+  if (row_kernels_enabled() && ln_fwd_rows(x, gamma, beta, y, mean, rstd, rows, h, eps, s)) return;
   int threads, vpt;
   row_launch_shape(h, threads, vpt);
 #define L(V)                                                                                                   \
@@ -576,7 +589,35 @@ void ln_bwd_dx(const void* dy, const void* x, const void* gamma, const float* me
 #undef L
 }
 
-size_t colsum_workspace_floats(int rows, int n) { return (size_t)2 * col_splits(rows) * n; }
+size_t colsum_workspace_floats(int rows, int n) {
+  return std::max((size_t)2 * col_splits(rows) * n, (size_t)2 * row_kernel_ctas(rows) * n);
+}
+
+void colsum_partials(const float* ws, float* out0, float* out1, int n, int splits, bool accumulate, cudaStream_t s) {
+  colsum_stage2<<<(n + 255) / 256, 256, 0, s>>>(ws, out0, out1, n, splits, accumulate);
+}
+
+int ln_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd, const void* resid,
+            void* dx, float* dgamma, float* dbeta, int rows, int h, float* ws, bool accumulate, cudaStream_t s) {
+  if (row_kernels_enabled() &&
+      ln_bwd_rows(dy, x, gamma, mean, rstd, resid, dx, dgamma, dbeta, rows, h, ws, accumulate, s))
+    return 2;
+  // parameter grads first: dx may overwrite x in place (the vocab head does that)
+  ln_bwd_params(dy, x, mean, rstd, dgamma, dbeta, rows, h, ws, accumulate, s);
+  ln_bwd_dx(dy, x, gamma, mean, rstd, resid, dx, rows, h, s);
+  return 3;
+}
+
+int bias_dropout_residual_ln(const void* z, const void* bias, const void* resid, void* out, const void* gamma,
+                              const void* beta, void* y, float* mean, float* rstd, int rows, int h, float eps,
+                              uint64_t seed, uint32_t thresh16, float scale, uint64_t elem_offset, cudaStream_t s) {
+  if (row_kernels_enabled() && bdr_ln_rows(z, bias, resid, out, gamma, beta, y, mean, rstd, rows, h, eps, seed,
+                                           thresh16, scale, elem_offset, s))
+    return 1;
+  bias_dropout_residual(z, bias, resid, out, rows, h, seed, thresh16, scale, s, elem_offset);
+  if (gamma != nullptr) ln_fwd(out, gamma, beta, y, mean, rstd, rows, h, eps, s);
+  return gamma != nullptr ? 2 : 1;
+}
 
 void ln_bwd_params(const void* dy, const void* x, const float* mean, const float* rstd, float* dgamma, float* dbeta,
                    int rows, int h, float* ws, bool accumulate, cudaStream_t s) {

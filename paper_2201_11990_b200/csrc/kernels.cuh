@@ -33,6 +33,27 @@ void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, floa
                cudaStream_t s);
 size_t colsum_workspace_floats(int rows, int n);
 
+// Fused LayerNorm backward: dx (= ln_bwd_dx) and dgamma/dbeta (= ln_bwd_params) in one pass over dy
+// and x (TMA-fed persistent row kernel, rows_sm100.cu; falls back to the two kernels above).
+int ln_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd, const void* resid,
+            void* dx, float* dgamma, float* dbeta, int rows, int h, float* workspace, bool accumulate, cudaStream_t s);
+// out = resid + dropout(z + bias) and, if gamma != nullptr, y = LN(out) (one pass).
+int bias_dropout_residual_ln(const void* z, const void* bias, const void* resid, void* out, const void* gamma,
+                              const void* beta, void* y, float* mean, float* rstd, int rows, int h, float eps,
+                              uint64_t site_seed, uint32_t thresh16, float scale, uint64_t elem_offset, cudaStream_t s);
+// dgamma/dbeta (+)= sum over `splits` fp32 partials ws[2][splits][h]
+void colsum_partials(const float* ws, float* out0, float* out1, int n, int splits, bool accumulate, cudaStream_t s);
+// rows_sm100.cu (return false when the shape does not fit; callers then use the per-row kernels)
+int row_kernel_ctas(int rows);
+bool ln_fwd_rows(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int rows, int h,
+                 float eps, cudaStream_t s);
+bool bdr_ln_rows(const void* z, const void* bias, const void* resid, void* out, const void* gamma, const void* beta,
+                 void* y, float* mean, float* rstd, int rows, int h, float eps, uint64_t seed, uint32_t thresh16,
+                 float scale, uint64_t elem_offset, cudaStream_t s);
+bool ln_bwd_rows(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
+                 const void* resid, void* dx, float* dgamma, float* dbeta, int rows, int h, float* ws, bool accumulate,
+                 cudaStream_t s);
+
 // Causal softmax over S (already scaled by 1/sqrt(hd)), rows of `batch_heads` independent
 // [seq x seq] blocks. P = dropout(softmax(S)); zeros above the diagonal up to the next
 // multiple of 256 columns (what the causal GEMMs read); lse saved per row.

@@ -710,14 +710,10 @@ void row_parallel_block(mt_ctx* c, bool tpc, int64_t M, int64_t h, GemmFor gemm_
     return static_cast<void*>(const_cast<uint16_t*>(static_cast<const uint16_t*>(p)) + r * h);
   };
   auto epilogue = [&](int64_t r0, int64_t nr) {
-    bias_dropout_residual(row_ptr(z, r0), bias, row_ptr(resid, r0), row_ptr(out, r0), (int)nr, (int)h, site, th, scale,
-                          st, static_cast<uint64_t>(r0 * h));
-    ++n;
-    if (ln) {
-      ln_fwd(row_ptr(out, r0), ln->gamma, ln->beta, row_ptr(ln->y, r0), ln->mean + r0, ln->rstd + r0, (int)nr, (int)h,
-             ln->eps, st);
-      ++n;
-    }
+    n += bias_dropout_residual_ln(row_ptr(z, r0), bias, row_ptr(resid, r0), row_ptr(out, r0), ln ? ln->gamma : nullptr,
+                             ln ? ln->beta : nullptr, ln ? row_ptr(ln->y, r0) : nullptr, ln ? ln->mean + r0 : nullptr,
+                             ln ? ln->rstd + r0 : nullptr, (int)nr, (int)h, ln ? ln->eps : 0.f, site, th, scale,
+                             static_cast<uint64_t>(r0 * h), st);
   };
   if (!tpc) {
     gemm_rows(0, M, 0, nullptr);
@@ -998,10 +994,8 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStrea
   mark(c, st, "bwd.fc1_wgrad");
   if (tpc) tp_allreduce_join(c, st);
   mark(c, st, "bwd.tp_allreduce_wait");
-  ln_bwd_dx(dln, sv.x1.ptr, l->param_ptr(MT_P_LN2_GAMMA), mean2, rstd2, dy, dx1, (int)M, (int)h, st);
-  ln_bwd_params(dln, sv.x1.ptr, mean2, rstd2, l->grad_ptr(MT_P_LN2_GAMMA), l->grad_ptr(MT_P_LN2_BETA), (int)M, (int)h,
-                ws, acc, st);
-  n += 3;
+  n += ln_bwd(dln, sv.x1.ptr, l->param_ptr(MT_P_LN2_GAMMA), mean2, rstd2, dy, dx1, l->grad_ptr(MT_P_LN2_GAMMA),
+              l->grad_ptr(MT_P_LN2_BETA), (int)M, (int)h, ws, acc, st);
   mark(c, st, "bwd.ln_bwd");
   // ---- attention block
   void* dz = dm;
@@ -1071,10 +1065,8 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStrea
   mark(c, st, "bwd.qkv_wgrad");
   if (tpc) tp_allreduce_join(c, st);
   mark(c, st, "bwd.tp_allreduce_wait");
-  ln_bwd_dx(dln, sv.x, l->param_ptr(MT_P_LN1_GAMMA), mean1, rstd1, dx1, dx, (int)M, (int)h, st);
-  ln_bwd_params(dln, sv.x, mean1, rstd1, l->grad_ptr(MT_P_LN1_GAMMA), l->grad_ptr(MT_P_LN1_BETA), (int)M, (int)h, ws,
-                acc, st);
-  n += 3;
+  n += ln_bwd(dln, sv.x, l->param_ptr(MT_P_LN1_GAMMA), mean1, rstd1, dx1, dx, l->grad_ptr(MT_P_LN1_GAMMA),
+              l->grad_ptr(MT_P_LN1_BETA), (int)M, (int)h, ws, acc, st);
   mark(c, st, "bwd.ln_bwd");
   check_cuda(cudaGetLastError(), "layer backward launch");
   l->bwd_launches = n;

@@ -399,10 +399,9 @@ extern "C" int mt_vocab_head_loss(mt_vocab* v, const void* y, const int32_t* tar
       check_nccl(ncclAllReduce(v->dyn.ptr, v->dyn.ptr, M * h, ncclBfloat16, ncclSum, v->ctx->tp, s), "AR dLNf");
     // tied-embedding gradient: dE_slice += dlogits^T LN_f(y)
     gemm(gemm_args(v->dlogits.ptr, vp, true, v->yn.ptr, h, true, v->g_word.ptr, h, vp, h, M, MT_EPI_ACCUM_F32), s);
-    // parameter grads first: dy may overwrite y in place (the stage driver does that)
-    mt::ln_bwd_params(v->dyn.ptr, y, mean, rstd, v->g_lnf_g.as<float>(), v->g_lnf_b.as<float>(), (int)M, (int)h,
-                      v->ws.as<float>(), true, s);
-    mt::ln_bwd_dx(v->dyn.ptr, y, v->lnf_g.ptr, mean, rstd, nullptr, dy, (int)M, (int)h, s);
+    // one pass over dLN_f and y (dy may overwrite y in place: the stage driver does that)
+    mt::ln_bwd(v->dyn.ptr, y, v->lnf_g.ptr, mean, rstd, nullptr, dy, v->g_lnf_g.as<float>(), v->g_lnf_b.as<float>(),
+               (int)M, (int)h, v->ws.as<float>(), true, s);
     check_cuda(cudaGetLastError(), "head loss");
   });
 }
