@@ -311,28 +311,43 @@ bool set_smem(K kern, size_t bytes) {
 
 int row_kernel_ctas(int rows) { return std::max(1, std::min(rows, sm_count())); }
 
+// Element-wise row kernels (no per-thread column state): 256-thread CTAs, as many per SM as the
+// shared-memory ring allows (2-deep rings; more resident warps hide the per-row dependency chains).
+struct RowLaunch {
+  int ctas, threads, stages;
+  size_t smem;
+};
+RowLaunch small_cta_launch(int rows, int nin, size_t row_bytes) {
+  RowLaunch l{};
+  l.threads = 256;
+  l.stages = 2;
+  l.smem = (size_t)l.stages * nin * row_bytes + 64;
+  const int per_sm = std::max(1, std::min(4, (int)((227 * 1024) / (l.smem + 1024))));
+  l.ctas = std::max(1, std::min(rows, per_sm * sm_count()));
+  return l;
+}
+
 bool ln_fwd_rows(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int rows, int h,
                  float eps, cudaStream_t s) {
-  const int nvec = h / 8, stages = ring_stages(1, (size_t)nvec * 16);
-  if (h % 8 || stages == 0) return false;
-  const size_t smem = (size_t)stages * nvec * 16 + 64;
-  if (!set_smem(ln_fwd_rows_kernel, smem)) return false;
-  ln_fwd_rows_kernel<<<row_kernel_ctas(rows), kRowThreads, smem, s>>>(
-      (const uint4*)x, (const uint4*)gamma, (const uint4*)beta, (uint4*)y, mean, rstd, rows, nvec, 1.f / h, eps,
-      stages);
+  const int nvec = h / 8;
+  if (h % 8 || ring_stages(1, (size_t)nvec * 16) == 0) return false;
+  const RowLaunch L = small_cta_launch(rows, 1, (size_t)nvec * 16);
+  if (!set_smem(ln_fwd_rows_kernel, L.smem)) return false;
+  ln_fwd_rows_kernel<<<L.ctas, L.threads, L.smem, s>>>((const uint4*)x, (const uint4*)gamma, (const uint4*)beta,
+                                                      (uint4*)y, mean, rstd, rows, nvec, 1.f / h, eps, L.stages);
   return cudaGetLastError() == cudaSuccess;
 }
 
 bool bdr_ln_rows(const void* z, const void* bias, const void* resid, void* out, const void* gamma, const void* beta,
                  void* y, float* mean, float* rstd, int rows, int h, float eps, uint64_t seed, uint32_t thresh16,
                  float scale, uint64_t elem_offset, cudaStream_t s) {
-  const int nvec = h / 8, stages = ring_stages(2, (size_t)nvec * 16);
-  if (h % 8 || stages == 0) return false;
-  const size_t smem = (size_t)stages * 2 * nvec * 16 + 64;
-  if (!set_smem(bdr_ln_rows_kernel, smem)) return false;
-  bdr_ln_rows_kernel<<<row_kernel_ctas(rows), kRowThreads, smem, s>>>(
+  const int nvec = h / 8;
+  if (h % 8 || ring_stages(2, (size_t)nvec * 16) == 0) return false;
+  const RowLaunch L = small_cta_launch(rows, 2, (size_t)nvec * 16);
+  if (!set_smem(bdr_ln_rows_kernel, L.smem)) return false;
+  bdr_ln_rows_kernel<<<L.ctas, L.threads, L.smem, s>>>(
       (const uint4*)z, (const uint4*)bias, (const uint4*)resid, (uint4*)out, (const uint4*)gamma, (const uint4*)beta,
-      (uint4*)y, mean, rstd, rows, nvec, 1.f / h, eps, seed, thresh16, scale, elem_offset, stages);
+      (uint4*)y, mean, rstd, rows, nvec, 1.f / h, eps, seed, thresh16, scale, elem_offset, L.stages);
   return cudaGetLastError() == cudaSuccess;
 }
 
