@@ -122,6 +122,12 @@ int mt_ctx_placement(const mt_ctx* ctx, mt_rank_placement* out);
  * layers run their shard's kernels and skip the TP all-reduces. Compute-only numbers; the
  * collectives are measured in real multi-GPU runs. Rejected when the context has a world > 1. */
 int mt_ctx_shard_only(mt_ctx* ctx, int32_t enable);
+/* Megatron sequence parallelism for TP > 1 (also MT_SEQ_PARALLEL=1 at mt_ctx_init_comm): layer
+ * inputs / outputs (and stage inputs, targets, PP transfers) are this TP rank's token rows
+ * [r * b*s/TP, (r+1) * b*s/TP); LayerNorm / bias-dropout-residual run on those rows only; the TP
+ * all-reduces become reduce-scatter + all-gather. The TP-replicated parameters' gradients are partial
+ * until mt_layer_finish_grads (the stage driver calls it). Set before creating layers. */
+int mt_ctx_set_sequence_parallel(mt_ctx* ctx, int32_t enable);
 /* Diagnostic (fused TP all-reduce contexts): time one NVLS all-reduce (multimem.ld_reduce + st) of
  * `elems` bf16 of the symmetric row-parallel buffer with `ctas` x 1024 threads, contiguous shares or
  * the GEMM's 128 x 256 unit pattern of a row-major [*, ld] matrix. Collective over the TP group. */
@@ -161,6 +167,9 @@ int mt_layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t micro_batc
  * executed FLOPs follow the reference cost model's recompute-inclusive 96 coefficient
  * (proj/src/planner.cpp:52-54). Only while no microbatch is in flight. */
 int mt_layer_set_recompute(mt_layer* l, int32_t enable);
+/* Sequence parallel: TP all-reduce of the replicated parameters' gradient partials (collective over
+ * the TP group; call once after the last backward of an iteration; no-op otherwise). */
+int mt_layer_finish_grads(mt_layer* l, void* stream);
 /* Kernel launches one forward / backward issues (for the bench's gpu_launches claim). */
 int mt_layer_launch_counts(const mt_layer* l, int32_t* fwd, int32_t* bwd);
 /* Device pointer to the flat fp32 gradient buffer of the layer and its element count. */

@@ -114,6 +114,8 @@ _SIGS = {
     "mt_ctx_init_comm": (C.c_int, [P, C.c_char_p, I32, I32, C.POINTER(ParallelConfig)]),
     "mt_ctx_placement": (C.c_int, [P, C.POINTER(RankPlacement)]),
     "mt_ctx_shard_only": (C.c_int, [P, I32]),
+    "mt_ctx_set_sequence_parallel": (C.c_int, [P, I32]),
+    "mt_layer_finish_grads": (C.c_int, [P, P]),
     "mt_ctx_nvls_probe": (C.c_int, [P, I64, I64, I32, I32, I32, PF64]),
     "mt_ctx_gemm_timing": (C.c_int, [P, I32]),
     "mt_ctx_gemm_timing_read": (C.c_int, [P, PF64, PF64, PI64]),

@@ -220,7 +220,8 @@ __global__ void __launch_bounds__(256) colsum_stage1(const uint4* __restrict__ a
                                                      const uint4* __restrict__ xin, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, uint4* __restrict__ out_dz,
                                                      float* __restrict__ ws, int rows, int nvec, int rows_per,
-                                                     uint64_t seed, uint32_t thresh16, float scale) {
+                                                     uint64_t seed, uint32_t thresh16, float scale,
+                                                     uint64_t elem_offset = 0) {
   constexpr int NO = OP == kColLnParams ? 2 : 1;
   __shared__ float part[NO][kColTY][32][9];
   const int cv = blockIdx.x * 32 + threadIdx.x;
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(256) colsum_stage1(const uint4* __restrict__ a
           acc[1][j] += v[j];
         }
       } else {
-        const uint64_t idx = ((uint64_t)r * nvec + cv) * 8;
+        const uint64_t idx = elem_offset + ((uint64_t)r * nvec + cv) * 8;
         const uint32_t keep = keep_mask8(seed, idx, thresh16);
         float o[8];
 #pragma unroll
@@ -638,11 +639,12 @@ void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, floa
 }
 
 void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int h, uint64_t seed, uint32_t thresh16,
-                           float scale, float* ws, bool accumulate, cudaStream_t s) {
+                           float scale, float* ws, bool accumulate, cudaStream_t s, uint64_t elem_offset) {
   const int nvec = h / 8, splits = col_splits(rows);
   dim3 grid((nvec + 31) / 32, splits), block(32, kColTY);
   colsum_stage1<kColDropout><<<grid, block, 0, s>>>((const uint4*)dy, nvec, nullptr, nullptr, nullptr, (uint4*)dz, ws,
-                                                    rows, nvec, (rows + splits - 1) / splits, seed, thresh16, scale);
+                                                    rows, nvec, (rows + splits - 1) / splits, seed, thresh16, scale,
+                                                    elem_offset);
   colsum_stage2<<<(h + 255) / 256, 256, 0, s>>>(ws, dbias, nullptr, h, splits, accumulate);
 }
 
@@ -686,10 +688,10 @@ void softmax_bwd(const void* S, const float* lse, void* dP, int batch_heads, int
 #undef L
 }
 
-void mse_loss(const void* y, const void* t, void* dy, float* loss, long long n, cudaStream_t s) {
+void mse_loss(const void* y, const void* t, void* dy, float* loss, long long n, cudaStream_t s, long long n_total) {
   const long long nvec = n / 8;
   mse_loss_kernel<<<grid_for(nvec, 256), 256, 0, s>>>((const uint4*)y, (const uint4*)t, (uint4*)dy, loss, nvec,
-                                                      1.f / (float)n);
+                                                      1.f / (float)(n_total > 0 ? n_total : n));
 }
 
 void fill_normal(void* out, long long rows, long long cols, long long global_cols, long long row0, long long col0,

@@ -27,7 +27,8 @@ void bias_dropout_residual(const void* z, const void* bias, const void* resid, v
                            uint64_t elem_offset = 0);
 // dz = dropout'(dy) ; dbias (+)= sum_rows dz
 void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int h, uint64_t site_seed,
-                           uint32_t thresh16, float scale, float* workspace, bool accumulate, cudaStream_t s);
+                           uint32_t thresh16, float scale, float* workspace, bool accumulate, cudaStream_t s,
+                           uint64_t elem_offset = 0);
 // dbias (+)= sum_rows x   (x bf16 [rows, n])
 void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, float* workspace, bool accumulate,
                cudaStream_t s);
@@ -75,7 +76,8 @@ int attention_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void
                   float drop_scale, const float* lse, float* D, void* dqkv, cudaStream_t s);
 
 // loss += sum 0.5 (y - t)^2 / n ; dy = (y - t) / n     (n = rows * h)
-void mse_loss(const void* y, const void* t, void* dy, float* loss, long long n, cudaStream_t s);
+// n_total: the element count the mean is over when y/t are one rank's rows of a larger tensor (0 = n)
+void mse_loss(const void* y, const void* t, void* dy, float* loss, long long n, cudaStream_t s, long long n_total = 0);
 
 // Seeded normal init of a TP shard of a row-major [global_rows x global_cols] tensor:
 // out[r][c] = bf16(mean + std * normal_at(key, (row0 + r) * global_cols + col0 + c)).

@@ -368,6 +368,7 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
       }
       if (const char* e = getenv("MT_TP_CHUNKS")) c->tp_chunks = std::max(1, std::min(4, atoi(e)));
       if (const char* e = getenv("MT_TP_SYMMETRIC")) c->tp_symmetric = e[0] == '1';
+      if (const char* e = getenv("MT_SEQ_PARALLEL")) c->seq_parallel = e[0] == '1';
       if (const char* e = getenv("MT_TP_FUSED")) c->tp_fused = e[0] == '1';
       if (c->tp_fused) c->tp_symmetric = true;
     }
@@ -657,6 +658,32 @@ void tp_allreduce_join(mt_ctx* c, cudaStream_t st) {
   check_cuda(cudaStreamWaitEvent(st, c->ev_done, 0), "cudaStreamWaitEvent");
 }
 
+// Sequence parallelism: rows [rank * ms, (rank + 1) * ms) of a [M, h] buffer are this rank's.
+template <class T>
+T* rows_of(T* p, int64_t r0, int64_t h) {
+  return reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(p) + static_cast<uintptr_t>(r0 * h * 2));
+}
+void sp_allgather(mt_ctx* c, void* buf, int64_t slice_elems, cudaStream_t st) {
+  check_nccl(ncclAllGather(static_cast<uint16_t*>(buf) + c->place.tensor * slice_elems, buf, slice_elems, ncclBfloat16,
+                           c->tp, st),
+             "ncclAllGather(sequence-parallel rows)");
+}
+void sp_reduce_scatter(mt_ctx* c, ncclComm_t comm, void* buf, int64_t slice_elems, cudaStream_t st) {
+  check_nccl(ncclReduceScatter(buf, static_cast<uint16_t*>(buf) + c->place.tensor * slice_elems, slice_elems,
+                               ncclBfloat16, ncclSum, comm, st),
+             "ncclReduceScatter(sequence-parallel rows)");
+}
+// reduce-scatter on the side stream (overlapping an independent GEMM); returns that GEMM's CTA cap
+int sp_reduce_scatter_async(mt_ctx* c, void* buf, int64_t slice_elems, cudaStream_t st) {
+  check_cuda(cudaEventRecord(c->ev_ready, st), "cudaEventRecord");
+  check_cuda(cudaStreamWaitEvent(c->comm, c->ev_ready, 0), "cudaStreamWaitEvent");
+  sp_reduce_scatter(c, c->tp_side, buf, slice_elems, c->comm);
+  check_cuda(cudaEventRecord(c->ev_done, c->comm), "cudaEventRecord");
+  int sms = 0;
+  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device), "attr");
+  return std::max(2, sms - c->comm_sms);
+}
+
 // Stream-ordered mark for per-op timing; the time between consecutive marks is attributed to the
 // op named by the later mark. No-op unless the context has op timing enabled.
 void mark(mt_ctx* c, cudaStream_t st, const char* label) {
@@ -700,10 +727,35 @@ struct LnOut {
   float eps;
 };
 
+struct SeqPar {
+  bool on = false;
+  int64_t ms = 0, r0 = 0;  // this rank's token rows [r0, r0 + ms)
+};
+
 template <class GemmFor>
-void row_parallel_block(mt_ctx* c, bool tpc, int64_t M, int64_t h, GemmFor gemm_rows, void* z, const void* bias,
-                        const void* resid, void* out, uint64_t site, uint32_t th, float scale, const LnOut* ln,
-                        cudaStream_t st, int& n, const char* gemm_label) {
+void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_t h, GemmFor gemm_rows, void* z,
+                        const void* bias, const void* resid, void* out, uint64_t site, uint32_t th, float scale,
+                        const LnOut* ln, cudaStream_t st, int& n, const char* gemm_label) {
+  if (sp.on) {
+    // sequence parallel: reduce-scatter the partial sums to this rank's rows, then the element-wise
+    // epilogue on those rows only, and all-gather the LayerNorm output the next GEMM needs in full
+    gemm_rows(0, M, 0, nullptr);
+    mark(c, st, gemm_label);
+    sp_reduce_scatter(c, c->tp, z, sp.ms * h, st);
+    ++n;
+    mark(c, st, "fwd.tp_reduce_scatter");
+    n += bias_dropout_residual_ln(rows_of(z, sp.r0, h), bias, resid, out, ln ? ln->gamma : nullptr,
+                                  ln ? ln->beta : nullptr, ln ? rows_of(ln->y, sp.r0, h) : nullptr,
+                                  ln ? ln->mean : nullptr, ln ? ln->rstd : nullptr, (int)sp.ms, (int)h,
+                                  ln ? ln->eps : 0.f, site, th, scale, static_cast<uint64_t>(sp.r0 * h), st);
+    mark(c, st, "fwd.bias_dropout_residual_ln");
+    if (ln) {
+      sp_allgather(c, ln->y, sp.ms * h, st);
+      ++n;
+      mark(c, st, "fwd.tp_allgather");
+    }
+    return;
+  }
   const int chunks = (tpc && M % (c->tp_chunks * 128) == 0) ? c->tp_chunks : 1;
   const int64_t rows = M / chunks;
   auto row_ptr = [&](const void* p, int64_t r) {
@@ -821,6 +873,10 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
   const int64_t M = l->M, h = l->h, hl = l->hl, ffl = l->ffl, ld3 = l->qkvl, s = d.seq, Hl = l->heads_local,
                 hd = l->head_dim;
   const bool tpc = tp_collectives(c, d);
+  SeqPar sp;
+  sp.on = tpc && c->seq_parallel;
+  sp.ms = sp.on ? M / d.tp_size : M;
+  sp.r0 = sp.on ? int64_t{d.tp_rank} * sp.ms : 0;
   sv.x = x;
   float* mean1 = sv.stats.as<float>();
   float* rstd1 = mean1 + M;
@@ -836,18 +892,28 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
   void* z = tp_buffer(c, 0);
   mark(c, st, "begin");
 
+  if (sp.on) {  // x holds this rank's rows: LN1 on them, then all-gather the LN1 output
+    ln_fwd(x, l->param_ptr(MT_P_LN1_GAMMA), l->param_ptr(MT_P_LN1_BETA), rows_of(sv.ln1.ptr, sp.r0, h), mean1, rstd1,
+           (int)sp.ms, (int)h, d.ln_eps, st);
+    ++n;
+    sp_allgather(c, sv.ln1.ptr, sp.ms * h, st);
+    ++n;
+    mark(c, st, "fwd.ln1");
+  }
   // LN1 + QKV GEMM, by row chunks when the input arrives in chunks (input_gate)
-  const int in_chunks = (l->input_gate && l->input_chunks > 1 && M % (int64_t{l->input_chunks} * 128) == 0)
+  const int in_chunks = (!sp.on && l->input_gate && l->input_chunks > 1 && M % (int64_t{l->input_chunks} * 128) == 0)
                             ? l->input_chunks
                             : 1;
   const int64_t in_rows = M / in_chunks;
   for (int k = 0; k < in_chunks; ++k) {
     const int64_t r0 = k * in_rows;
-    if (l->input_gate) l->input_gate(k, st);
-    ln_fwd(static_cast<const uint16_t*>(x) + r0 * h, l->param_ptr(MT_P_LN1_GAMMA), l->param_ptr(MT_P_LN1_BETA),
-           sv.ln1.as<uint16_t>() + r0 * h, mean1 + r0, rstd1 + r0, (int)in_rows, (int)h, d.ln_eps, st);
-    ++n;
-    mark(c, st, "fwd.ln1");
+    if (l->input_gate && !sp.on) l->input_gate(k, st);
+    if (!sp.on) {
+      ln_fwd(static_cast<const uint16_t*>(x) + r0 * h, l->param_ptr(MT_P_LN1_GAMMA), l->param_ptr(MT_P_LN1_BETA),
+             sv.ln1.as<uint16_t>() + r0 * h, mean1 + r0, rstd1 + r0, (int)in_rows, (int)h, d.ln_eps, st);
+      ++n;
+      mark(c, st, "fwd.ln1");
+    }
     Gemm(sv.ln1.as<uint16_t>() + r0 * h, h, false, l->param_ptr(MT_P_QKV_W), h, false,
          sv.qkv.as<uint16_t>() + r0 * ld3, ld3, in_rows, ld3, h)
         .bias(l->param_ptr(MT_P_QKV_B))
@@ -887,7 +953,7 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
   {
     const LnOut ln2{l->param_ptr(MT_P_LN2_GAMMA), l->param_ptr(MT_P_LN2_BETA), sv.ln2.ptr, mean2, rstd2, d.ln_eps};
     row_parallel_block(
-        c, tpc, M, h,
+        c, tpc, sp, M, h,
         [&](int64_t r0, int64_t nr, int cap, mt_gemm_allreduce* ar) {
           Gemm(sv.ctx.as<uint16_t>() + r0 * hl, hl, false, l->param_ptr(MT_P_PROJ_W), hl, false,
                static_cast<uint16_t*>(z) + r0 * h, h, nr, h, hl)
@@ -904,7 +970,7 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
       .run(st, n);
   mark(c, st, "fwd.fc1_gemm");
   row_parallel_block(
-      c, tpc, M, h,
+      c, tpc, sp, M, h,
       [&](int64_t r0, int64_t nr, int cap, mt_gemm_allreduce* ar) {
         Gemm(sv.act.as<uint16_t>() + r0 * ffl, ffl, false, l->param_ptr(MT_P_FC2_W), ffl, false,
              static_cast<uint16_t*>(z) + r0 * h, h, nr, h, ffl)
@@ -966,11 +1032,24 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStrea
   const bool acc = !l->grads_fresh;  // accumulate into the fp32 grads, or overwrite them
   l->grads_fresh = false;
   const int wg_epi = acc ? MT_EPI_ACCUM_F32 : MT_EPI_STORE_F32;
+  // sequence parallel: dy / dx / x / x1 hold this rank's token rows; the replicated parameters'
+  // gradients are partial sums over those rows until mt_layer_finish_grads
+  SeqPar sp;
+  sp.on = tpc && c->seq_parallel;
+  sp.ms = sp.on ? M / d.tp_size : M;
+  sp.r0 = sp.on ? int64_t{d.tp_rank} * sp.ms : 0;
+  const uint64_t eoff = static_cast<uint64_t>(sp.r0 * h);
+  if (sp.on) l->sp_partial = true;
 
   mark(c, st, "begin");
   // ---- MLP block
-  dropout_bwd_bias_grad(dy, dm, l->grad_ptr(MT_P_FC2_B), (int)M, (int)h, site_out2, th_h, scale_h, ws, acc, st);
+  dropout_bwd_bias_grad(dy, rows_of(dm, sp.r0, h), l->grad_ptr(MT_P_FC2_B), (int)sp.ms, (int)h, site_out2, th_h,
+                        scale_h, ws, acc, st, eoff);
   n += 2;
+  if (sp.on) {
+    sp_allgather(c, dm, sp.ms * h, st);
+    ++n;
+  }
   mark(c, st, "bwd.dropout_bias_grad");
   Gemm(dm, h, false, l->param_ptr(MT_P_FC2_W), ffl, true, dpre, ffl, M, ffl, h)
       .epi(MT_EPI_GELU_BWD)
@@ -984,7 +1063,8 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStrea
   mark(c, st, "bwd.fc1_dgrad");
   int cap = 0;
   if (tpc) {
-    cap = tp_allreduce_async(c, dln, M * h, st, "ncclAllReduce(ln2.grad)");
+    cap = sp.on ? sp_reduce_scatter_async(c, dln, sp.ms * h, st)
+                : tp_allreduce_async(c, dln, M * h, st, "ncclAllReduce(ln2.grad)");
     ++n;
   }
   bias_grad(dpre, l->grad_ptr(MT_P_FC1_B), (int)M, (int)ffl, ffl, ws, acc, st);
@@ -994,13 +1074,18 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStrea
   mark(c, st, "bwd.fc1_wgrad");
   if (tpc) tp_allreduce_join(c, st);
   mark(c, st, "bwd.tp_allreduce_wait");
-  n += ln_bwd(dln, sv.x1.ptr, l->param_ptr(MT_P_LN2_GAMMA), mean2, rstd2, dy, dx1, l->grad_ptr(MT_P_LN2_GAMMA),
-              l->grad_ptr(MT_P_LN2_BETA), (int)M, (int)h, ws, acc, st);
+  n += ln_bwd(rows_of(dln, sp.r0, h), sv.x1.ptr, l->param_ptr(MT_P_LN2_GAMMA), mean2, rstd2, dy, dx1,
+              l->grad_ptr(MT_P_LN2_GAMMA), l->grad_ptr(MT_P_LN2_BETA), (int)sp.ms, (int)h, ws, acc, st);
   mark(c, st, "bwd.ln_bwd");
   // ---- attention block
   void* dz = dm;
-  dropout_bwd_bias_grad(dx1, dz, l->grad_ptr(MT_P_PROJ_B), (int)M, (int)h, site_out1, th_h, scale_h, ws, acc, st);
+  dropout_bwd_bias_grad(dx1, rows_of(dz, sp.r0, h), l->grad_ptr(MT_P_PROJ_B), (int)sp.ms, (int)h, site_out1, th_h,
+                        scale_h, ws, acc, st, eoff);
   n += 2;
+  if (sp.on) {
+    sp_allgather(c, dz, sp.ms * h, st);
+    ++n;
+  }
   mark(c, st, "bwd.dropout_bias_grad");
   Gemm(dz, h, false, l->param_ptr(MT_P_PROJ_W), hl, true, dctx, hl, M, hl, h).run(st, n);
   mark(c, st, "bwd.proj_dgrad");
@@ -1055,7 +1140,8 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStrea
   mark(c, st, "bwd.qkv_dgrad");
   cap = 0;
   if (tpc) {
-    cap = tp_allreduce_async(c, dln, M * h, st, "ncclAllReduce(ln1.grad)");
+    cap = sp.on ? sp_reduce_scatter_async(c, dln, sp.ms * h, st)
+                : tp_allreduce_async(c, dln, M * h, st, "ncclAllReduce(ln1.grad)");
     ++n;
   }
   bias_grad(dqkv, l->grad_ptr(MT_P_QKV_B), (int)M, (int)ld3, ld3, ws, acc, st);
@@ -1065,14 +1151,43 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStrea
   mark(c, st, "bwd.qkv_wgrad");
   if (tpc) tp_allreduce_join(c, st);
   mark(c, st, "bwd.tp_allreduce_wait");
-  n += ln_bwd(dln, sv.x, l->param_ptr(MT_P_LN1_GAMMA), mean1, rstd1, dx1, dx, l->grad_ptr(MT_P_LN1_GAMMA),
-              l->grad_ptr(MT_P_LN1_BETA), (int)M, (int)h, ws, acc, st);
+  n += ln_bwd(rows_of(dln, sp.r0, h), sv.x, l->param_ptr(MT_P_LN1_GAMMA), mean1, rstd1, dx1, dx,
+              l->grad_ptr(MT_P_LN1_GAMMA), l->grad_ptr(MT_P_LN1_BETA), (int)sp.ms, (int)h, ws, acc, st);
   mark(c, st, "bwd.ln_bwd");
   check_cuda(cudaGetLastError(), "layer backward launch");
   l->bwd_launches = n;
 }
 
+// Sequence parallelism leaves the TP-replicated parameters' gradients (LayerNorms, row-parallel
+// biases) as per-rank partial sums over token rows; one grouped TP all-reduce completes them.
+void finish_layer_grads(mt_layer* l, cudaStream_t st) {
+  if (!l->sp_partial) return;
+  l->sp_partial = false;
+  if (l->grads_fresh) return;  // logically zero on every rank
+  mt_ctx* c = l->ctx;
+  check_nccl(ncclGroupStart(), "group");
+  for (int p : {MT_P_LN1_GAMMA, MT_P_LN1_BETA, MT_P_PROJ_B, MT_P_LN2_GAMMA, MT_P_LN2_BETA, MT_P_FC2_B})
+    check_nccl(ncclAllReduce(l->grad_ptr(p), l->grad_ptr(p), l->param_rows[p] * l->param_cols[p], ncclFloat32, ncclSum,
+                             c->tp, st),
+               "ncclAllReduce(replicated grads)");
+  check_nccl(ncclGroupEnd(), "group");
+}
+
 }  // namespace
+
+extern "C" int mt_layer_finish_grads(mt_layer* l, void* stream) {
+  return guarded([&] {
+    if (!l) throw std::invalid_argument("null layer");
+    finish_layer_grads(l, (cudaStream_t)stream);
+  });
+}
+
+extern "C" int mt_ctx_set_sequence_parallel(mt_ctx* c, int32_t enable) {
+  return guarded([&] {
+    if (!c) throw std::invalid_argument("null context");
+    c->seq_parallel = enable != 0;
+  });
+}
 
 extern "C" int mt_layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, void* stream) {
   return guarded([&] {

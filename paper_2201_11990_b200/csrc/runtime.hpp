@@ -103,6 +103,11 @@ struct mt_ctx {
   cudaEvent_t ev_dp_ready = nullptr, ev_dp_done = nullptr;
   bool dp_overlap = true;
   int gemm_cap = 0;
+  // Megatron sequence parallelism (MT_SEQ_PARALLEL=1 / mt_ctx_set_sequence_parallel): with TP > 1 the
+  // layer input/output and the LayerNorm / bias-dropout-residual work are split over the TP ranks by
+  // token rows (rank r owns rows [r M/t, (r+1) M/t)); the all-reduces become reduce-scatter +
+  // all-gather of the same volume, and the replicated [M, h] element-wise work shrinks by t.
+  bool seq_parallel = false;
   bool tp_symmetric = false;
   // forward row-parallel GEMM + TP all-reduce fused in one kernel over NVLink SHARP (MT_TP_FUSED=1;
   // implies symmetric buffers); state in tp_fused.cu
@@ -165,6 +170,7 @@ struct mt_layer {
   // Logically zero gradients: the next backward writes (=) instead of accumulating (+=), which
   // saves both the memset and the read half of the fp32 read-modify-write in the wgrad epilogues.
   bool grads_fresh = false;
+  bool sp_partial = false;  // sequence parallel: replicated-param grads await mt_layer_finish_grads
   // Optional row-chunk gate on the layer input (set by the stage for the first layer when its input
   // streams in from the host): forward runs LN1 + the QKV GEMM chunk by chunk, calling
   // input_gate(k, stream) before chunk k so the copy of chunk k+1 overlaps the compute of chunk k.

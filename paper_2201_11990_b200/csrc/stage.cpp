@@ -79,20 +79,31 @@ struct Step {
   int64_t launches = 0;
   bool first() const { return st->stage == 0; }
   bool last() const { return st->stage == st->stages - 1; }
-  size_t bytes() const { return static_cast<size_t>(st->M * st->h * 2); }
-  int64_t elems() const { return st->M * st->h; }
-  // bytes of one microbatch's input / target: bf16 activations, or int32 token ids with a vocab
-  size_t io_bytes() const { return st->vocab ? static_cast<size_t>(st->M * 4) : bytes(); }
   bool lm() const { return st->vocab != nullptr; }
+  // Sequence parallelism (mt_ctx_set_sequence_parallel): activations between layers, stage inputs /
+  // targets and PP transfers are this TP rank's token rows only.
+  bool sp() const {
+    const mt_ctx* c = st->ctx;
+    return !lm() && c->seq_parallel && c->par.tensor > 1 && c->tp && !c->shard_only;
+  }
+  int64_t full_elems() const { return st->M * st->h; }
+  int64_t elems() const { return sp() ? full_elems() / st->ctx->par.tensor : full_elems(); }
+  size_t bytes() const { return static_cast<size_t>(elems() * 2); }
+  // bytes of one microbatch's input / target in the caller's buffers (full rows; int32 ids with a vocab)
+  size_t io_bytes() const { return st->vocab ? static_cast<size_t>(st->M * 4) : static_cast<size_t>(full_elems() * 2); }
+  size_t sp_off() const { return sp() ? bytes() * st->ctx->place.tensor : 0; }  // this rank's rows in io buffers
   // TP > 1, host inputs: the t ranks of a TP group need the same activations / targets, so each
   // copies only its 1/t row slice over PCIe and the slices are all-gathered over NVLink (in place),
   // instead of t full host->device copies competing for host bandwidth.
   bool split_h2d() const {
     const mt_ctx* c = st->ctx;
-    return !lm() && c->par.tensor > 1 && c->tp && !c->shard_only && (elems() % c->par.tensor) == 0;
+    return !sp() && !lm() && c->par.tensor > 1 && c->tp && !c->shard_only && (elems() % c->par.tensor) == 0;
   }
-  size_t slice_bytes() const { return split_h2d() ? io_bytes() / st->ctx->par.tensor : io_bytes(); }
-  size_t slice_off() const { return split_h2d() ? slice_bytes() * st->ctx->place.tensor : 0; }
+  size_t slice_bytes() const {
+    return sp() ? bytes() : split_h2d() ? io_bytes() / st->ctx->par.tensor : io_bytes();
+  }
+  size_t slice_off() const { return sp() ? sp_off() : split_h2d() ? slice_bytes() * st->ctx->place.tensor : 0; }
+  size_t dst_off() const { return sp() ? 0 : slice_off(); }  // where the copied rows land on the device
   void gather_slices(void* buf) {
     if (!split_h2d()) return;
     const size_t n = elems() / st->ctx->par.tensor;
@@ -104,7 +115,7 @@ struct Step {
   // GEMM of chunk k inside layer 0 (mt_layer::input_gate).
   int in_chunks() const {
     const int k = st->in_chunks, t = split_h2d() ? st->ctx->par.tensor : 1;
-    if (!in_host || !first() || lm() || st->layers.empty() || k <= 1) return 1;
+    if (!in_host || !first() || lm() || sp() || st->layers.empty() || k <= 1) return 1;
     return (st->M % (int64_t{k} * 128) == 0 && (st->M / k) % t == 0) ? k : 1;
   }
   size_t chunk_bytes() const { return bytes() / in_chunks(); }
@@ -118,7 +129,8 @@ struct Step {
   }
 
   const void* input(int mb) const {
-    return (in_dev && first() && !lm()) ? static_cast<const void*>(in_dev + mb * io_bytes()) : st->act[mb][0].ptr;
+    return (in_dev && first() && !lm()) ? static_cast<const void*>(in_dev + mb * io_bytes() + sp_off())
+                                        : st->act[mb][0].ptr;
   }
   // Queue every microbatch's host->device copies on the copy stream (after the previous
   // iteration's compute released the buffers).
@@ -137,7 +149,7 @@ struct Step {
           mt::check_cuda(cudaEventRecord(st->in_ev[mb * mt_stage::kMaxInChunks + k], st->copy), "cudaEventRecord");
         }
       } else if (in_host && first()) {
-        char* dst = static_cast<char*>(lm() ? st->tokens[mb].ptr : st->act[mb][0].ptr) + slice_off();
+        char* dst = static_cast<char*>(lm() ? st->tokens[mb].ptr : st->act[mb][0].ptr) + dst_off();
         mt::check_cuda(cudaMemcpyAsync(dst, in_host + mb * io_bytes() + slice_off(), slice_bytes(),
                                        cudaMemcpyHostToDevice, st->copy),
                        "H2D input");
@@ -145,7 +157,7 @@ struct Step {
         mt::check_cuda(cudaEventRecord(st->in_ev[mb * mt_stage::kMaxInChunks], st->copy), "cudaEventRecord");
       }
       if (tgt_host && last()) {
-        mt::check_cuda(cudaMemcpyAsync(static_cast<char*>(st->targets[mb].ptr) + slice_off(),
+        mt::check_cuda(cudaMemcpyAsync(static_cast<char*>(st->targets[mb].ptr) + dst_off(),
                                        tgt_host + mb * io_bytes() + slice_off(), slice_bytes(),
                                        cudaMemcpyHostToDevice, st->copy),
                        "H2D target");
@@ -173,7 +185,7 @@ struct Step {
       gather_slices(dst);
     } else {
       const uint64_t key = mt_stream_key(st->d.layer.seed, "input", 0, gid(mb));
-      mt::fill_normal(dst, 1, elems(), elems(), 0, 0, key, 0.f, 1.f, s);
+      mt::fill_normal(dst, 1, elems(), full_elems(), 0, static_cast<long long>(sp_off() / 2), key, 0.f, 1.f, s);
       ++launches;
     }
   }
@@ -218,17 +230,18 @@ struct Step {
       }
       const void* tgt = st->target.ptr;
       if (tgt_dev) {
-        tgt = tgt_dev + mb * io_bytes();
+        tgt = tgt_dev + mb * io_bytes() + sp_off();
       } else if (tgt_host) {
         mt::check_cuda(cudaStreamWaitEvent(s, st->tgt_ev[mb], 0), "cudaStreamWaitEvent");
         gather_slices(st->targets[mb].ptr);
         tgt = st->targets[mb].ptr;
       } else {
         const uint64_t key = mt_stream_key(st->d.layer.seed, "target", 0, gid(mb));
-        mt::fill_normal(st->target.ptr, 1, elems(), elems(), 0, 0, key, 0.f, 1.f, s);
+        mt::fill_normal(st->target.ptr, 1, elems(), full_elems(), 0, static_cast<long long>(sp_off() / 2), key, 0.f, 1.f,
+                        s);
         ++launches;
       }
-      mt::mse_loss(y, tgt, y, st->loss.as<float>(), elems(), s);  // dy overwrites y in place
+      mt::mse_loss(y, tgt, y, st->loss.as<float>(), elems(), s, full_elems());  // dy overwrites y in place
       ++launches;
     }
   }
@@ -250,6 +263,7 @@ struct Step {
       cur = out;
       if (overlap && i > 0) {  // layers below remain to overlap with (the bottom layer uses the full comm)
         mt_layer* l = st->layers[i];
+        ok(mt_layer_finish_grads(l, s));  // sequence parallel: complete the replicated grads first
         mt::check_cuda(cudaEventRecord(c->ev_dp_ready, s), "cudaEventRecord");
         mt::check_cuda(cudaStreamWaitEvent(c->dp_stream, c->ev_dp_ready, 0), "cudaStreamWaitEvent");
         mt::check_nccl(ncclAllReduce(l->grads.ptr, l->grads.ptr, l->param_total, ncclFloat32, ncclAvg, c->dp_side,
@@ -419,6 +433,17 @@ void run_iteration(Step& k, mt_stage* st, void* stream) {
       ++k.launches;
     }
   }
+  // sequence parallel: complete the TP-replicated parameters' gradients (partial over token rows) and
+  // the loss (each TP rank summed its rows)
+  if (k.sp()) {
+    for (auto* l : st->layers) ok(mt_layer_finish_grads(l, k.s));
+    k.launches += static_cast<int64_t>(st->layers.size());
+    if (k.last()) {
+      mt::check_nccl(ncclAllReduce(st->loss.ptr, st->loss.ptr, 1, ncclFloat32, ncclSum, st->ctx->tp, k.s),
+                     "ncclAllReduce(loss, tp)");
+      ++k.launches;
+    }
+  }
   // tied word embedding: the first and the last stage both hold E and sum their gradients
   if (vocab_here && st->stages > 1) {
     mt::vocab_allreduce_grads(st->vocab, st->ctx->emb, true, false, k.s);
@@ -537,6 +562,8 @@ extern "C" int mt_stage_attach_vocab(mt_stage* st, mt_vocab* v) {
     if (!st || !v) throw std::invalid_argument("null argument");
     if (mt::vocab_tokens(v) != st->M || mt::vocab_hidden(v) != st->h)
       throw std::invalid_argument("vocab shape (micro_batch * seq, hidden) does not match the stage");
+    if (st->ctx->seq_parallel && st->ctx->par.tensor > 1)
+      throw std::invalid_argument("the vocab module does not support sequence parallelism yet");
     if (mt::vocab_tp(v) != st->ctx->par.tensor && !st->ctx->shard_only)
       throw std::invalid_argument("vocab tp_size does not match the tensor-parallel degree");
     if (st->stages > 1 && !st->ctx->emb && (st->stage == 0 || st->stage == st->stages - 1))

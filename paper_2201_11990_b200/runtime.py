@@ -46,6 +46,10 @@ class Context:
         par = ParallelConfig(tensor, pipeline, data, batch, micro_batches)
         check(lib().mt_ctx_init_comm(self._h, nccl_id, world_size, rank, C.byref(par)))
 
+    def set_sequence_parallel(self, enable: bool = True) -> None:
+        """Megatron sequence parallelism for TP > 1 (layer inputs/outputs become this rank's token rows)."""
+        check(lib().mt_ctx_set_sequence_parallel(self._h, int(enable)))
+
     def placement(self) -> RankPlacement:
         p = RankPlacement()
         check(lib().mt_ctx_placement(self._h, C.byref(p)))
@@ -96,6 +100,10 @@ class Layer:
 
     def set_recompute(self, enable: bool = True) -> None:
         check(lib().mt_layer_set_recompute(self._h, int(enable)))
+
+    def finish_grads(self, stream=None) -> None:
+        """Sequence parallel: complete the TP-replicated parameters' gradients (collective over TP)."""
+        check(lib().mt_layer_finish_grads(self._h, _stream(stream)))
 
     def launch_counts(self) -> tuple[int, int]:
         f, b = C.c_int32(), C.c_int32()

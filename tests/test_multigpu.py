@@ -143,8 +143,11 @@ def _worker(rank, world, port, mode, q):
                 lay.close()
                 c2.close()
             os.environ.pop("MT_TP_FUSED", None)
-        elif mode == "tp":
+        elif mode in ("tp", "tp_sp"):
             ctx.init_comm(obj[0], world, rank, tensor=world)
+            sp = mode == "tp_sp"
+            if sp:
+                ctx.set_sequence_parallel(True)
             d = PL.layer_desc(H, HEADS, S, B, tp_size=world, tp_rank=rank, seed=SEED, layer_index=0)
             lay = Layer(ctx, d)
             params = O.init_params(H, SEED, 0)
@@ -154,10 +157,13 @@ def _worker(rank, world, port, mode, q):
             x = O.normal(O.site_seed(SEED, "input", 0, 0), B * S, H)
             g = O.normal(O.site_seed(SEED, "grad", 0, 0), B * S, H, std=1e-2)
             dev = lambda a: torch.from_numpy(O.to_bf16_bits(a).view(np.int16)).view(torch.bfloat16).cuda()  # noqa
-            xd, gd = dev(x), dev(g)
+            rows = slice(rank * (B * S // world), (rank + 1) * (B * S // world)) if sp else slice(None)
+            xd, gd = dev(np.ascontiguousarray(x[rows])), dev(np.ascontiguousarray(g[rows]))
             yd, dxd = torch.empty_like(xd), torch.empty_like(xd)
             lay.forward(xd.data_ptr(), yd.data_ptr(), 0, s)
             lay.backward(gd.data_ptr(), dxd.data_ptr(), 0, s)
+            if sp:
+                lay.finish_grads(s)
             torch.cuda.synchronize()
             out["y"], out["dx"] = yd.float().cpu().numpy(), dxd.float().cpu().numpy()
             grads = []
@@ -169,10 +175,13 @@ def _worker(rank, world, port, mode, q):
             out["grads"] = grads
             lay.close()
         else:
-            tp, pp, dp = {"pp": (1, world, 1), "dp": (1, 1, world), "tp_stage": (world, 1, 1)}[mode]
+            tp, pp, dp = {"pp": (1, world, 1), "dp": (1, 1, world), "tp_stage": (world, 1, 1),
+                          "tp_stage_sp": (world, 1, 1)}[mode]
             layers, MB = (2 * pp, 4) if mode == "pp" else (1, 2)
             ctx.init_comm(obj[0], world, rank, tensor=tp, pipeline=pp, data=dp, batch=B * MB * dp, micro_batches=MB)
             place = ctx.placement()
+            if mode == "tp_stage_sp":
+                ctx.set_sequence_parallel(True)
             d = PL.layer_desc(H, HEADS, S, B, seed=SEED)
             st = Stage(ctx, d, layers, MB)
             per = layers // pp
@@ -190,7 +199,7 @@ def _worker(rank, world, port, mode, q):
                 loss = st.train_step(xh.data_ptr(), th.data_ptr(), s)
             out["loss"], out["place"] = loss, (place.data, place.pipeline, place.tensor)
             out["h2d"] = st.host_traffic()[0]
-            if mode == "tp_stage":  # TP shards: loss + host traffic only (layer grads: test_tensor_parallel_*)
+            if mode in ("tp_stage", "tp_stage_sp"):  # TP shards: loss + host traffic (grads: test_tensor_parallel_*)
                 st.close()
                 ctx.close()
                 q.put((rank, out))
@@ -237,10 +246,17 @@ def _run(mode, world=2):
 
 
 @pytest.mark.timeout(900)
-def test_tensor_parallel_layer_two_gpus():
+@pytest.mark.parametrize("mode", ["tp", "tp_sp"])
+def test_tensor_parallel_layer_two_gpus(mode):
+    """TP=2 layer vs the oracle; with sequence parallelism ("tp_sp") each rank holds half of the token
+    rows of x / y / dy / dx, and the replicated gradients are completed by finish_grads."""
     _need(2)
     from oracle import oracle as O
-    res = _run("tp")
+    res = _run(mode)
+    if mode == "tp_sp":
+        for k in ("y", "dx"):
+            full = np.concatenate([res[0][k], res[1][k]])
+            res[0][k] = res[1][k] = full
     ol = O.OracleLayer(H, HEADS, S, B, 2, dropout_hidden=0.1, dropout_attn=0.1, seed=SEED, layer_index=0,
                        bf16_emulate=True)
     x = O.normal(O.site_seed(SEED, "input", 0, 0), B * S, H)
@@ -347,11 +363,13 @@ def test_language_model_pipeline_two_gpus():
 
 
 @pytest.mark.timeout(900)
-def test_tensor_parallel_stage_host_inputs_two_gpus():
+@pytest.mark.parametrize("mode", ["tp_stage", "tp_stage_sp"])
+def test_tensor_parallel_stage_host_inputs_two_gpus(mode):
     """Stage at TP=2 fed from host buffers: each TP rank copies half of every input / target over
-    PCIe and the halves are all-gathered over NVLink; the loss equals the oracle's."""
+    PCIe (all-gathered over NVLink, or kept as the rank's rows under sequence parallelism); the loss
+    equals the oracle's."""
     _need(2)
-    res = _run("tp_stage")
+    res = _run(mode)
     loss, _ = _oracle_step([0], range(2))
     full = 2 * 2 * (B * S * H * 2)  # MB=2 inputs + targets, bf16
     for r in (0, 1):
