@@ -209,7 +209,8 @@ def run_ours(args, L: dict) -> None:
         lib().mt_ctx_shard_only(ctx._h, 1)
     place = ctx.placement()
     first, last = place.pipeline == 0, place.pipeline == L["pp"] - 1
-    desc = PL.layer_desc(L["hidden"], L["heads"], L["seq"], L["b"], dropout_hidden=0.1, dropout_attn=0.1,
+    desc = PL.layer_desc(L["hidden"], L["heads"], L["seq"], L["b"], dropout_hidden=args.dropout,
+                         dropout_attn=args.dropout,
                          seed=SEED, tp_size=L["tp"] if shard_only else 1)
     stage = Stage(ctx, desc, L["layers"], L["mb"])
     if args.recompute:
@@ -341,7 +342,7 @@ def run_ours(args, L: dict) -> None:
             "config": {"workload": f"{L['model']} fwd+bwd, {L['note']}", "hidden": L["hidden"], "heads": L["heads"],
                        "seq_len": L["seq"], "micro_batch": L["b"], "micro_batches": MB, "layers": L["layers"],
                        "global_batch": L["b"] * MB * L["dp"], "parallelism": f"tp{L['tp']}pp{L['pp']}dp{L['dp']}",
-                       "dropout": 0.1, "l2": "working set > L2 (weights alone exceed 126 MB); no flush"},
+                       "dropout": args.dropout, "l2": "working set > L2 (weights alone exceed 126 MB); no flush"},
             "tflops_per_gpu": tflops_gpu,
             **({"recompute": True, "hardware_tflops_per_gpu": tflops_gpu * 96.0 / 72.0} if args.recompute else {}),
             "peak_fraction": tflops_gpu / pk["bf16"],
@@ -381,6 +382,7 @@ def main() -> None:
     ap.add_argument("--config", default="gpt3", choices=["gpt3", "mtnlg", "pp", "3d", "dp", "tiny"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
+    ap.add_argument("--dropout", type=float, default=0.1, help="hidden and attention dropout (Megatron default 0.1)")
     ap.add_argument("--shard-of", type=int, default=0,
                     help="single GPU: run ONE rank's tensor-parallel shard of the config at TP=SHARD_OF with the "
                          "TP all-reduces skipped (compute-only per-GPU measurement, flagged in the JSON)")
