@@ -28,7 +28,11 @@ enum mt_epilogue {
   MT_EPI_BIAS_GELU = 1,    /* aux = bf16(acc + bias[n]) (pre-activation), D = bf16(gelu(aux))   */
   MT_EPI_GELU_BWD = 2,     /* D = bf16(acc * gelu'(aux[m][n]))   (aux = saved pre-activation)    */
   MT_EPI_STORE_F32 = 3,    /* D(f32) = alpha*acc                                                */
-  MT_EPI_ACCUM_F32 = 4     /* D(f32) += alpha*acc   (fp32 gradient accumulation across microbatches) */
+  MT_EPI_ACCUM_F32 = 4,    /* D(f32) += alpha*acc   (fp32 gradient accumulation across microbatches) */
+  MT_EPI_STORE_BF16_ROWSTATS = 5 /* D = bf16(alpha*acc), plus per (row, BN-column block) softmax statistics
+                                    of the stored values: aux = float2 [batch][m][ld_aux] {max, sum exp(x - max)}
+                                    over the block's columns (causal modes: columns <= row only); requires
+                                    block_n = 128 or 256 and ld_aux >= ceil(n / block_n) */
 };
 
 enum mt_causal {

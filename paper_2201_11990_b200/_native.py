@@ -26,7 +26,7 @@ class GemmArgs(C.Structure):
     ]
 
 
-EPI_STORE_BF16, EPI_BIAS_GELU, EPI_GELU_BWD, EPI_STORE_F32, EPI_ACCUM_F32 = range(5)
+EPI_STORE_BF16, EPI_BIAS_GELU, EPI_GELU_BWD, EPI_STORE_F32, EPI_ACCUM_F32, EPI_STORE_BF16_ROWSTATS = range(6)
 CAUSAL_NONE, CAUSAL_SKIP_UPPER_TILES, CAUSAL_K_LE_M, CAUSAL_K_GE_M = range(4)
 
 

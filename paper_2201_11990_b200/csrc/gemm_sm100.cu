@@ -42,6 +42,7 @@ struct GemmParams {
   const __nv_bfloat16* bias;
   __nv_bfloat16* aux;
   long long ld_aux;
+  float2* row_stats;  // MT_EPI_STORE_BF16_ROWSTATS: [batch][m][ld_aux]
   // split-K tail: work items [0, full_tiles) are whole tiles; the remaining total_tiles - full_tiles
   // tiles (fewer than one wave) are each split over `splits` k-ranges run by otherwise idle CTAs.
   int full_tiles, splits, work_items;
@@ -526,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = row0 + lane;
       const uint32_t tmem_row = tmem_base + ((quad * 32) << 16) + acc * C::kAccStride;
       const float* parts = nullptr;  // split-K: this CTA's partial tiles of the tail tile
+      float st_m = -INFINITY, st_l = 0.f;  // ROWSTATS: running max / sum of exp over this tile's columns
       if (wk.split >= 0) {
         // Publish this split's raw partial (rows of this thread), then count arrivals; the last
         // arriving split reduces the others' partials into its accumulator and runs the epilogue.
@@ -599,7 +601,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           bi ^= 1;
           continue;
         }
-        if (ep == MT_EPI_STORE_BF16 || ep == MT_EPI_BIAS_GELU) {
+        if (ep == MT_EPI_STORE_BF16_ROWSTATS) {
+          // statistics of the values as stored (bf16-rounded), causal columns <= row only
+          constexpr float kL2e = 1.4426950408889634f;
+          float pm = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float2 pr = unpack_bf16x2(pack_bf16x2(x[j], x[j + 1]));
+            x[j] = pr.x;
+            x[j + 1] = pr.y;
+          }
+          const int lim = (p.causal != MT_CAUSAL_NONE) ? min(p.n, row + 1) : p.n;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < lim) pm = fmaxf(pm, x[j]);
+          if (pm > -INFINITY) {
+            const float mn = fmaxf(st_m, pm);
+            float sum = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < lim) sum += exp2f((x[j] - mn) * kL2e);
+            st_l = st_l * exp2f((st_m - mn) * kL2e) + sum;
+            st_m = mn;
+          }
+        } else if (ep == MT_EPI_STORE_BF16 || ep == MT_EPI_BIAS_GELU) {
           if (p.bias != nullptr) {
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
@@ -651,6 +676,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         flush_piece(&tmap_d, stg + bi * 4096, lane, col0, row0, b, false);
         bi ^= 1;
       }
+      if (ep == MT_EPI_STORE_BF16_ROWSTATS && row < p.m)
+        p.row_stats[((long long)b * p.m + row) * p.ld_aux + nb] = make_float2(st_m, st_l);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -848,6 +875,7 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   p.bias = static_cast<const __nv_bfloat16*>(a.bias);
   p.aux = static_cast<__nv_bfloat16*>(a.aux);
   p.ld_aux = a.ld_aux;
+  p.row_stats = static_cast<float2*>(a.aux);
   if (a.allreduce != nullptr) {
     mt_gemm_allreduce& ar = *a.allreduce;
     const long long units = (long long)p.total_tiles * (kPair ? 2 : 1);
@@ -1022,7 +1050,12 @@ extern "C" int mt_gemm(const mt_gemm_args* args, void* stream) {
   if ((a.epilogue == MT_EPI_BIAS_GELU || a.epilogue == MT_EPI_GELU_BWD) && a.batch != 1) return 1;
   if (a.allreduce != nullptr && (a.epilogue != MT_EPI_STORE_BF16 || a.batch != 1 || a.causal != MT_CAUSAL_NONE))
     return 1;
-  if (a.epilogue < 0 || a.epilogue > MT_EPI_ACCUM_F32 || a.causal < 0 || a.causal > MT_CAUSAL_K_GE_M) return 1;
+  if (a.epilogue < 0 || a.epilogue > MT_EPI_STORE_BF16_ROWSTATS || a.causal < 0 || a.causal > MT_CAUSAL_K_GE_M)
+    return 1;
+  if (a.epilogue == MT_EPI_STORE_BF16_ROWSTATS &&
+      (a.aux == nullptr || (a.block_n != 128 && a.block_n != 256) || a.ld_aux < (a.n + a.block_n - 1) / a.block_n ||
+       a.bias != nullptr))
+    return 1;
   int bn = a.block_n;
   if (bn == 0) bn = mt::choose_block_n(a);
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -552,6 +552,7 @@ extern "C" int mt_layer_create(mt_ctx* c, const mt_layer_desc* d, mt_layer** out
     c->scratch_qkv.ensure(M * l->qkvl * 2);
     c->scratch_attn.ensure(l->fused_attn ? l->heads_local * int64_t{d->seq} * 4
                                          : l->heads_local * int64_t{d->seq} * d->seq * 2);
+    c->scratch_stats.ensure(l->heads_local * int64_t{d->seq} * ((d->seq + 127) / 128) * 8);
     size_t ws = 0;
     for (int64_t n : {l->h, l->ffl, l->qkvl}) ws = std::max(ws, mt::colsum_workspace_floats((int)M, (int)n));
     c->scratch_ws.ensure(ws * 4);
@@ -935,13 +936,27 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
     }
     uint16_t* S = sv.S.as<uint16_t>() + bb * Hl * s * s;
     uint16_t* P = sv.P.as<uint16_t>() + bb * Hl * s * s;
-    Gemm(q, ld3, false, q + hd, ld3, false, S, s, s, s, hd)
-        .batched(Hl, 3 * hd, 3 * hd, s * s)
-        .alpha(alpha)
-        .causal(MT_CAUSAL_SKIP_UPPER_TILES)
-        .run(st, n);
+    // the score GEMM also emits per-(row, column block) softmax statistics, so the softmax is one
+    // streaming pass (MT_SOFTMAX_STATS=0 selects the three-pass kernel)
+    static const bool stats_on = [] {
+      const char* e = getenv("MT_SOFTMAX_STATS");
+      return !(e && e[0] == '0');
+    }();
+    const int sbn = (s % 256 == 0) ? 256 : 128;
+    const bool use_stats = stats_on && s % 128 == 0;
+    Gemm sg(q, ld3, false, q + hd, ld3, false, S, s, s, s, hd);
+    sg.batched(Hl, 3 * hd, 3 * hd, s * s).alpha(alpha).causal(MT_CAUSAL_SKIP_UPPER_TILES);
+    if (use_stats) {
+      sg.epi(MT_EPI_STORE_BF16_ROWSTATS).aux(c->scratch_stats.ptr, s / sbn);
+      sg.a.block_n = sbn;
+    }
+    sg.run(st, n);
     mark(c, st, "fwd.attn_s_gemm");
-    softmax_fwd(S, P, lse, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, st);
+    if (use_stats)
+      softmax_fwd_stats(S, P, c->scratch_stats.ptr, (int)(s / sbn), sbn, lse, (int)Hl, (int)s, head_base, site_attn,
+                        th_a, scale_a, st);
+    else
+      softmax_fwd(S, P, lse, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, st);
     ++n;
     mark(c, st, "fwd.softmax");
     Gemm(P, s, false, q + 2 * hd, ld3, true, sv.ctx.as<uint16_t>() + bb * s * hl, hl, s, hd, s)
