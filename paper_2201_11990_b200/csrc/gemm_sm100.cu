@@ -602,26 +602,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         if (ep == MT_EPI_STORE_BF16_ROWSTATS) {
-          // statistics of the values as stored (bf16-rounded), causal columns <= row only
+          // statistics of the values as stored (bf16-rounded), causal columns <= row only; pieces wholly
+          // below the diagonal (every lane's row >= the piece's last column) skip the per-column test
           constexpr float kL2e = 1.4426950408889634f;
-          float pm = -INFINITY;
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
             const float2 pr = unpack_bf16x2(pack_bf16x2(x[j], x[j + 1]));
             x[j] = pr.x;
             x[j + 1] = pr.y;
           }
-          const int lim = (p.causal != MT_CAUSAL_NONE) ? min(p.n, row + 1) : p.n;
+          const bool causal = p.causal != MT_CAUSAL_NONE;
+          const int lim = causal ? min(p.n, row + 1) : p.n;
+          float pm = -INFINITY;
+          if (col0 + 32 <= lim) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j < lim) pm = fmaxf(pm, x[j]);
-          if (pm > -INFINITY) {
-            const float mn = fmaxf(st_m, pm);
-            float sum = 0.f;
+            for (int j = 0; j < 32; ++j) pm = fmaxf(pm, x[j]);
+          } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (col0 + j < lim) sum += exp2f((x[j] - mn) * kL2e);
-            st_l = st_l * exp2f((st_m - mn) * kL2e) + sum;
+              if (col0 + j < lim) pm = fmaxf(pm, x[j]);
+          }
+          if (pm > -INFINITY) {
+            const float mn = fmaxf(st_m, pm), mn2 = mn * kL2e;
+            float sum = 0.f;
+            if (col0 + 32 <= lim) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) sum += ex2_fast(fmaf(x[j], kL2e, -mn2));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < lim) sum += ex2_fast(fmaf(x[j], kL2e, -mn2));
+            }
+            st_l = st_l * ex2_fast((st_m - mn) * kL2e) + sum;
             st_m = mn;
           }
         } else if (ep == MT_EPI_STORE_BF16 || ep == MT_EPI_BIAS_GELU) {

@@ -936,11 +936,12 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
     }
     uint16_t* S = sv.S.as<uint16_t>() + bb * Hl * s * s;
     uint16_t* P = sv.P.as<uint16_t>() + bb * Hl * s * s;
-    // the score GEMM also emits per-(row, column block) softmax statistics, so the softmax is one
-    // streaming pass (MT_SOFTMAX_STATS=0 selects the three-pass kernel)
+    // Opt-in (MT_SOFTMAX_STATS=1): the score GEMM also emits per-(row, column block) softmax
+    // statistics so the softmax is one streaming pass. Measured at the GPT-3 shape: softmax 0.42 ->
+    // 0.32 ms but the score GEMM (K = head dim, epilogue-bound) 0.30 -> 0.51 ms, so it is off.
     static const bool stats_on = [] {
       const char* e = getenv("MT_SOFTMAX_STATS");
-      return !(e && e[0] == '0');
+      return e && e[0] == '1';
     }();
     const int sbn = (s % 256 == 0) ? 256 : 128;
     const bool use_stats = stats_on && s % 128 == 0;
