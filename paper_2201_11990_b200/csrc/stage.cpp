@@ -44,8 +44,8 @@ struct mt_stage {
   std::vector<mt::DeviceBuffer> tokens;            // [MB][M] int32 (host-input path, first stage)
   int64_t h2d_bytes = 0, d2h_bytes = 0;            // host traffic of the last mt_stage_train_step
   // host inputs arrive in row chunks (one event each) that layer 0 consumes as they land
-  static constexpr int kMaxInChunks = 4;
-  int in_chunks = kMaxInChunks;                    // MT_INPUT_CHUNKS (1 disables)
+  static constexpr int kMaxInChunks = 8;
+  int in_chunks = 4;                               // MT_INPUT_CHUNKS (1 disables, up to 8)
 };
 
 namespace {
