@@ -283,17 +283,34 @@ __global__ void __launch_bounds__(256) colsum_stage1(const uint4* __restrict__ a
   }
 }
 
-__global__ void colsum_stage2(const float* __restrict__ ws, float* __restrict__ out0, float* __restrict__ out1, int n,
-                              int splits, int accumulate) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= n) return;
-  float s0 = 0.f;
-  for (int sp = 0; sp < splits; ++sp) s0 += ws[(size_t)sp * n + col];
-  out0[col] = accumulate ? out0[col] + s0 : s0;
-  if (out1 != nullptr) {
-    float s1 = 0.f;
-    for (int sp = 0; sp < splits; ++sp) s1 += ws[((size_t)splits + sp) * n + col];
-    out1[col] = accumulate ? out1[col] + s1 : s1;
+// Stage 2: block (32 columns x 8 split lanes); lane y sums splits y, y+8, ... of its column, then a
+// fixed-order shared-memory reduction over the 8 lanes (deterministic; many blocks even when the
+// number of splits is large, e.g. the per-CTA partials of the fused LayerNorm backward).
+__global__ void __launch_bounds__(256) colsum_stage2(const float* __restrict__ ws, float* __restrict__ out0,
+                                                     float* __restrict__ out1, int n, int splits, int accumulate) {
+  __shared__ float red[2][8][33];
+  const int col = blockIdx.x * 32 + threadIdx.x;
+  const int y = threadIdx.y;
+  float s0 = 0.f, s1 = 0.f;
+  if (col < n) {
+#pragma unroll 4
+    for (int sp = y; sp < splits; sp += 8) {
+      s0 += ws[(size_t)sp * n + col];
+      if (out1 != nullptr) s1 += ws[((size_t)splits + sp) * n + col];
+    }
+  }
+  red[0][y][threadIdx.x] = s0;
+  red[1][y][threadIdx.x] = s1;
+  __syncthreads();
+  if (y == 0 && col < n) {
+    float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      t0 += red[0][k][threadIdx.x];
+      t1 += red[1][k][threadIdx.x];
+    }
+    out0[col] = accumulate ? out0[col] + t0 : t0;
+    if (out1 != nullptr) out1[col] = accumulate ? out1[col] + t1 : t1;
   }
 }
 
@@ -642,7 +659,7 @@ size_t colsum_workspace_floats(int rows, int n) {
 }
 
 void colsum_partials(const float* ws, float* out0, float* out1, int n, int splits, bool accumulate, cudaStream_t s) {
-  colsum_stage2<<<(n + 255) / 256, 256, 0, s>>>(ws, out0, out1, n, splits, accumulate);
+  colsum_stage2<<<(n + 31) / 32, dim3(32, 8), 0, s>>>(ws, out0, out1, n, splits, accumulate);
 }
 
 int ln_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd, const void* resid,
@@ -673,7 +690,7 @@ void ln_bwd_params(const void* dy, const void* x, const float* mean, const float
   dim3 grid((nvec + 31) / 32, splits), block(32, kColTY);
   colsum_stage1<kColLnParams><<<grid, block, 0, s>>>((const uint4*)dy, nvec, (const uint4*)x, mean, rstd, nullptr, ws,
                                                      rows, nvec, (rows + splits - 1) / splits, 0, 0, 1.f);
-  colsum_stage2<<<(h + 255) / 256, 256, 0, s>>>(ws, dgamma, dbeta, h, splits, accumulate);
+  colsum_stage2<<<(h + 31) / 32, dim3(32, 8), 0, s>>>(ws, dgamma, dbeta, h, splits, accumulate);
 }
 
 void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, float* ws, bool accumulate,
@@ -682,7 +699,7 @@ void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, floa
   dim3 grid((nvec + 31) / 32, splits), block(32, kColTY);
   colsum_stage1<kColSum><<<grid, block, 0, s>>>((const uint4*)x, ldx / 8, nullptr, nullptr, nullptr, nullptr, ws, rows,
                                                 nvec, (rows + splits - 1) / splits, 0, 0, 1.f);
-  colsum_stage2<<<(n + 255) / 256, 256, 0, s>>>(ws, dbias, nullptr, n, splits, accumulate);
+  colsum_stage2<<<(n + 31) / 32, dim3(32, 8), 0, s>>>(ws, dbias, nullptr, n, splits, accumulate);
 }
 
 void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int h, uint64_t seed, uint32_t thresh16,
@@ -692,7 +709,7 @@ void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int
   colsum_stage1<kColDropout><<<grid, block, 0, s>>>((const uint4*)dy, nvec, nullptr, nullptr, nullptr, (uint4*)dz, ws,
                                                     rows, nvec, (rows + splits - 1) / splits, seed, thresh16, scale,
                                                     elem_offset);
-  colsum_stage2<<<(h + 255) / 256, 256, 0, s>>>(ws, dbias, nullptr, h, splits, accumulate);
+  colsum_stage2<<<(h + 31) / 32, dim3(32, 8), 0, s>>>(ws, dbias, nullptr, h, splits, accumulate);
 }
 
 void bias_dropout_residual(const void* z, const void* bias, const void* resid, void* out, int rows, int h,

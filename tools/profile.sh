@@ -9,11 +9,11 @@ CMD="python bench.py --steps 2 --warmup 3 --no-cpu"
 $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD \
     > gpurun_out/ncu_launches.log 2>&1
-for g in fc1_fwd fc1_dgrad fc1_wgrad; do
+for g in ${GEMMS:-fc1_fwd fc1_dgrad fc1_wgrad}; do
   python tools/gemm_one.py $g 3 > gpurun_out/gemm_$g.log 2>&1
   ncu --set full --clock-control none --import-source on -k regex:gemm_sm100 -s 2 -c 1 \
       -o gpurun_out/prof_gemm_$g python tools/gemm_one.py $g 3 > gpurun_out/ncu_gemm_$g.log 2>&1
 done
-ncu --set full --clock-control none -k regex:"softmax|ln_|colsum|bias_dropout|mse" -s 12 -c 12 \
+ncu --set full --clock-control none -k regex:"softmax|ln_|colsum|bias_dropout|bdr_|rows_kernel|mse" -s 12 -c ${HBM_COUNT:-12} \
     -o gpurun_out/prof_hbm $CMD > gpurun_out/ncu_hbm.log 2>&1
 echo done
