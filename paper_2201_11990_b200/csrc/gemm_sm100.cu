@@ -156,6 +156,15 @@ __device__ __forceinline__ void stage_bf16(uint32_t buf, uint32_t lane, const fl
                  pack_bf16x2(x[8 * j + 4], x[8 * j + 5]), pack_bf16x2(x[8 * j + 6], x[8 * j + 7]));
   }
 }
+// wide bf16 piece: 32 rows x 64 columns = 128 B per row, SWIZZLE_128B (like the fp32 piece).
+__device__ __forceinline__ void stage_bf16_wide(uint32_t buf, uint32_t lane, const float (&x)[64]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t pos = j ^ (lane & 7);
+    st_shared_v4(buf + lane * 128 + pos * 16, pack_bf16x2(x[8 * j], x[8 * j + 1]), pack_bf16x2(x[8 * j + 2], x[8 * j + 3]),
+                 pack_bf16x2(x[8 * j + 4], x[8 * j + 5]), pack_bf16x2(x[8 * j + 6], x[8 * j + 7]));
+  }
+}
 // fp32 piece: 32 rows x 128 B, SWIZZLE_128B (chunk j of row t lands at chunk j ^ (t & 7)).
 __device__ __forceinline__ void stage_f32(uint32_t buf, uint32_t lane, const float (&x)[32]) {
 #pragma unroll
@@ -568,8 +577,119 @@ __global__ void __launch_bounds__(kThreads, 1)
         __threadfence();
         parts = base + (size_t)rank * (128 * BN) + (size_t)(quad * 32 + lane) * BN;
       }
+      // bf16 outputs with BN % 64 == 0: 64-column pieces (32 rows x 128 B, half the TMA stores,
+      // fences and warp syncs of 32-column pieces); fp32 outputs and BN = 160 use 32-column pieces
+      constexpr bool kWide = (BN % 64) == 0;
+      const int c_begin = (kWide && !f32) ? BN / 32 : 0;
+      if (kWide && !f32) {
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+        for (int c2 = 0; c2 < BN / 64; ++c2) {
+          const int col0 = nb * BN + c2 * 64;
+          if (col0 >= p.n) break;
+          float x[64];
+          {
+            uint32_t ra[32], rb[32];
+            tmem_ld_32x32b_x32(tmem_row + c2 * 64, ra);
+            tmem_ld_32x32b_x32(tmem_row + c2 * 64 + 32, rb);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              x[j] = __uint_as_float(ra[j]);
+              x[32 + j] = __uint_as_float(rb[j]);
+            }
+          }
+          if (parts != nullptr) {
+            for (int sp = 0; sp < p.splits; ++sp) {
+              if (sp == wk.split) continue;
+              const float* q = parts + (size_t)sp * 2 * (128 * BN) + c2 * 64;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float4 v = __ldcg(reinterpret_cast<const float4*>(q + 4 * j));
+                x[4 * j] += v.x;
+                x[4 * j + 1] += v.y;
+                x[4 * j + 2] += v.z;
+                x[4 * j + 3] += v.w;
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 64; ++j) x[j] *= alpha;
+          if (ep == MT_EPI_STORE_BF16_ROWSTATS) {
+            constexpr float kL2e = 1.4426950408889634f;
+#pragma unroll
+            for (int j = 0; j < 64; j += 2) {
+              const float2 pr = unpack_bf16x2(pack_bf16x2(x[j], x[j + 1]));
+              x[j] = pr.x;
+              x[j + 1] = pr.y;
+            }
+            const int lim = (p.causal != MT_CAUSAL_NONE) ? min(p.n, row + 1) : p.n;
+            float pm = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (col0 + j < lim) pm = fmaxf(pm, x[j]);
+            if (pm > -INFINITY) {
+              const float mn = fmaxf(st_m, pm), mn2 = mn * kL2e;
+              float sum = 0.f;
+#pragma unroll
+              for (int j = 0; j < 64; ++j)
+                if (col0 + j < lim) sum += ex2_fast(fmaf(x[j], kL2e, -mn2));
+              st_l = st_l * ex2_fast((st_m - mn) * kL2e) + sum;
+              st_m = mn;
+            }
+          } else if (ep == MT_EPI_STORE_BF16 || ep == MT_EPI_BIAS_GELU) {
+            if (p.bias != nullptr) {
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                if (col0 + 8 * v < p.n) {
+                  const uint4 bv = __ldg(reinterpret_cast<const uint4*>(p.bias + col0 + 8 * v));
+                  const uint32_t bw[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    const float2 f = unpack_bf16x2(bw[q]);
+                    x[8 * v + 2 * q] += f.x;
+                    x[8 * v + 2 * q + 1] += f.y;
+                  }
+                }
+              }
+            }
+            if (ep == MT_EPI_BIAS_GELU) {
+              reuse_wait(lane);
+              stage_bf16_wide(stg + bi * 4096, lane, x);
+              flush_piece(&tmap_aux, stg + bi * 4096, lane, col0, row0, 0, false);
+              bi ^= 1;
+#pragma unroll
+              for (int j = 0; j < 64; j += 2) {
+                const float2 pr = unpack_bf16x2(pack_bf16x2(x[j], x[j + 1]));
+                x[j] = gelu_tanh(pr.x);
+                x[j + 1] = gelu_tanh(pr.y);
+              }
+            }
+          } else {  // MT_EPI_GELU_BWD
+            if (row < p.m) {
+              const __nv_bfloat16* ap = p.aux + (long long)row * p.ld_aux + col0;
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                if (col0 + 8 * v < p.n) {
+                  const uint4 av = *reinterpret_cast<const uint4*>(ap + 8 * v);
+                  const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    const float2 f = unpack_bf16x2(aw[q]);
+                    x[8 * v + 2 * q] *= gelu_tanh_grad(f.x);
+                    x[8 * v + 2 * q + 1] *= gelu_tanh_grad(f.y);
+                  }
+                }
+              }
+            }
+          }
+          reuse_wait(lane);
+          stage_bf16_wide(stg + bi * 4096, lane, x);
+          flush_piece(&tmap_d, stg + bi * 4096, lane, col0, row0, b, false);
+          bi ^= 1;
+        }
+      }
+#pragma unroll 1
+      for (int c = c_begin; c < BN / 32; ++c) {
         const int col0 = nb * BN + c * 32;
         if (col0 >= p.n) break;
         uint32_t r[32];
@@ -791,7 +911,9 @@ bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
 
 // Epilogue store map: 32 x 32 pieces; bf16 rows are 64 B (64B swizzle), fp32 rows 128 B (128B swizzle).
 bool make_store_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t m, uint64_t batch, uint64_t ld,
-                    uint64_t batch_stride, bool f32) {
+                    uint64_t batch_stride, bool f32, bool wide = false) {
+  if (wide && !f32)  // 64 x 32 bf16 pieces (128 B rows)
+    return make_map_ex(map, base, n, m, batch, ld, batch_stride, 64, 32, false, CU_TENSOR_MAP_SWIZZLE_128B);
   return make_map_ex(map, base, n, m, batch, ld, batch_stride, 32, 32, f32,
                      f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
 }
@@ -831,9 +953,9 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
                    : make_map(&mb, a.b, k, n, batch, a.ldb, a.b_batch_stride, C::kBRows));
   const bool f32 = a.epilogue == MT_EPI_STORE_F32 || a.epilogue == MT_EPI_ACCUM_F32;
   CUtensorMap md, maux;
-  ok = ok && make_store_map(&md, a.d, n, m, batch, a.ldd, a.d_batch_stride, f32);
+  ok = ok && make_store_map(&md, a.d, n, m, batch, a.ldd, a.d_batch_stride, f32, BN % 64 == 0);
   if (a.epilogue == MT_EPI_BIAS_GELU)
-    ok = ok && make_store_map(&maux, a.aux, n, m, 1, a.ld_aux, 0, false);
+    ok = ok && make_store_map(&maux, a.aux, n, m, 1, a.ld_aux, 0, false, BN % 64 == 0);
   else
     maux = md;
   if (!ok) return 1;
