@@ -24,6 +24,9 @@
 namespace mt {
 namespace {
 
+#ifndef MT_GEMM_EPI_BUFS
+#define MT_GEMM_EPI_BUFS 2
+#endif
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kThreads = 256;
@@ -69,7 +72,8 @@ struct Cfg {
   static constexpr int kABytes = 128 * kBK * 2;  // one CTA always holds 128 rows of A
   static constexpr int kBBytes = kBNAlloc * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiBytes = 4 * 2 * 4096;  // 4 epilogue warps x 2 staging buffers x (32 rows x 128 B)
+  static constexpr int kEpiBufs = MT_GEMM_EPI_BUFS;  // staging buffers per epilogue warp (TMA stores in flight)
+  static constexpr int kEpiBytes = 4 * kEpiBufs * 4096;  // 4 epilogue warps x buffers x (32 rows x 128 B)
   static constexpr int kStagesRaw = (kSmemBudget - 2048 - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kEpiBytes + 256;
@@ -189,8 +193,9 @@ __device__ __forceinline__ void flush_piece(const CUtensorMap* map, uint32_t buf
   }
 }
 // Before overwriting a staging buffer: at most one older bulk group may still be reading smem.
+template <int NB>
 __device__ __forceinline__ void reuse_wait(uint32_t lane) {
-  if (lane == 0) bulk_wait_read<1>();
+  if (lane == 0) bulk_wait_read<NB - 1>();
   __syncwarp();
 }
 
@@ -515,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
     const uint32_t quad = warp - 4;
-    const uint32_t stg = smem_u32(epi_base) + quad * 8192;  // two 4 KB staging buffers
+    const uint32_t stg = smem_u32(epi_base) + quad * (C::kEpiBufs * 4096);  // kEpiBufs 4 KB staging buffers
     uint32_t bi = 0;
     const int ep = p.epilogue;
     const bool f32 = ep == MT_EPI_STORE_F32 || ep == MT_EPI_ACCUM_F32;
@@ -653,10 +658,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             if (ep == MT_EPI_BIAS_GELU) {
-              reuse_wait(lane);
+              reuse_wait<C::kEpiBufs>(lane);
               stage_bf16_wide(stg + bi * 4096, lane, x);
               flush_piece(&tmap_aux, stg + bi * 4096, lane, col0, row0, 0, false);
-              bi ^= 1;
+              bi = (bi + 1) % C::kEpiBufs;
 #pragma unroll
               for (int j = 0; j < 64; j += 2) {
                 const float2 pr = unpack_bf16x2(pack_bf16x2(x[j], x[j + 1]));
@@ -682,10 +687,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
-          reuse_wait(lane);
+          reuse_wait<C::kEpiBufs>(lane);
           stage_bf16_wide(stg + bi * 4096, lane, x);
           flush_piece(&tmap_d, stg + bi * 4096, lane, col0, row0, b, false);
-          bi ^= 1;
+          bi = (bi + 1) % C::kEpiBufs;
         }
       }
 #pragma unroll 1
@@ -715,10 +720,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) x[j] *= alpha;
         if (f32) {
-          reuse_wait(lane);
+          reuse_wait<C::kEpiBufs>(lane);
           stage_f32(stg + bi * 4096, lane, x);
           flush_piece(&tmap_d, stg + bi * 4096, lane, col0, row0, b, ep == MT_EPI_ACCUM_F32);
-          bi ^= 1;
+          bi = (bi + 1) % C::kEpiBufs;
           continue;
         }
         if (ep == MT_EPI_STORE_BF16_ROWSTATS) {
@@ -774,10 +779,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (ep == MT_EPI_BIAS_GELU) {
             // pre-activation (bf16) goes to aux; GeLU is applied to the rounded value the backward sees
-            reuse_wait(lane);
+            reuse_wait<C::kEpiBufs>(lane);
             stage_bf16(stg + bi * 4096, lane, x);
             flush_piece(&tmap_aux, stg + bi * 4096, lane, col0, row0, 0, false);
-            bi ^= 1;
+            bi = (bi + 1) % C::kEpiBufs;
 #pragma unroll
             for (int j = 0; j < 32; j += 2) {
               const float2 pr = unpack_bf16x2(pack_bf16x2(x[j], x[j + 1]));
@@ -803,10 +808,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        reuse_wait(lane);
+        reuse_wait<C::kEpiBufs>(lane);
         stage_bf16(stg + bi * 4096, lane, x);
         flush_piece(&tmap_d, stg + bi * 4096, lane, col0, row0, b, false);
-        bi ^= 1;
+        bi = (bi + 1) % C::kEpiBufs;
       }
       if (ep == MT_EPI_STORE_BF16_ROWSTATS && row < p.m)
         p.row_stats[((long long)b * p.m + row) * p.ld_aux + nb] = make_float2(st_m, st_l);
@@ -820,7 +825,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ++it;
       if (kAR && p.ar_ranks > 0) {
-        if (unpublished >= 0) ar_publish<kPair, BN / 32>(p, unpublished, rank, lane);
+        // bulk groups of the tile issued after `unpublished` (64-column bf16 pieces when BN % 64 == 0)
+        if (unpublished >= 0) ar_publish<kPair, (BN % 64 == 0) ? BN / 64 : BN / 32>(p, unpublished, rank, lane);
         unpublished = w;
         if (!p.ar_in_epi) continue;
         if (pending[0].w >= 0 && pending[1].w >= 0) {
