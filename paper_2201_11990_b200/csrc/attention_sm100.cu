@@ -871,4 +871,11 @@ int attention_fwd(const void* qkv, long long ld_qkv, int heads, int seq, int hd,
   }
 }
 
+// D[h][i] = dout_i . out_i per head (the softmax-backward row term; attention_sm100.cu's rowdot kernel)
+void attn_rowdot(const void* dout, const void* out, long long ld, int hd, int heads, int seq, float* D, cudaStream_t s) {
+  const int rows = heads * seq;
+  attn_bwd_rowdot_kernel<<<(rows + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dout),
+                                                         static_cast<const __nv_bfloat16*>(out), ld, hd, heads, seq, D);
+}
+
 }  // namespace mt

@@ -548,6 +548,41 @@ __global__ void __launch_bounds__(256) softmax_fwd_stats_kernel(const uint4* __r
   if (lane == 0) lse[warp] = lrow;
 }
 
+__global__ void __launch_bounds__(256) softmax_bwd_rowdot_kernel(const uint4* __restrict__ S,
+                                                                  const float* __restrict__ lse,
+                                                                  const float* __restrict__ D, uint4* __restrict__ dP,
+                                                                  int rows_total, int seq, long long head_base,
+                                                                  uint64_t seed, uint32_t thresh16, float scale,
+                                                                  float alpha) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows_total) return;
+  const int bh = warp / seq, i = warp - bh * seq;
+  const int nvec_row = seq >> 3;
+  const uint4* srow = S + (size_t)warp * nvec_row;
+  uint4* drow = dP + (size_t)warp * nvec_row;
+  const int nvalid = i + 1, nvec = (nvalid + 7) >> 3, nfull = nvalid >> 3, rem = nvalid & 7;
+  const float l2 = lse[warp] * kLog2e;
+  const float dot = D[warp];
+  const uint64_t base_idx = ((uint64_t)(head_base + bh) * seq + i) * (uint64_t)seq;
+  for (int v = lane; v < nvec; v += 32) {
+    const uint32_t keep = keep_mask8(seed, base_idx + v * 8, thresh16);
+    const uint32_t valid = v < nfull ? 0xffu : (1u << rem) - 1u;
+    float sv[8], g[8], o[8];
+    unpack8(srow[v], sv);
+    unpack8(drow[v], g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float y = ex2_recompute(fmaf(sv[j], kLog2e, -l2));
+      const float gj = ((keep >> j) & 1u) ? g[j] * scale : 0.f;
+      o[j] = ((valid >> j) & 1u) ? alpha * y * (gj - dot) : 0.f;
+    }
+    drow[v] = pack8(o);
+  }
+  const int zend = min(seq, (i / 256 + 1) * 256) >> 3;
+  for (int v = nvec + lane; v < zend; v += 32) drow[v] = make_uint4(0, 0, 0, 0);
+}
+
 // ------------------------------------------------------------------ loss, init
 __global__ void mse_loss_kernel(const uint4* __restrict__ y, const uint4* __restrict__ t, uint4* __restrict__ dy,
                                 float* __restrict__ loss, long long nvec, float inv_n) {
@@ -746,6 +781,14 @@ void softmax_fwd_stats(const void* S, void* P, const void* stats, int ld_stats, 
   const int rows = batch_heads * seq;
   softmax_fwd_stats_kernel<<<(rows + 7) / 8, 256, 0, s>>>((const uint4*)S, (uint4*)P, (const float2*)stats, ld_stats,
                                                           bn, lse, rows, seq, head_base, seed, thresh16, scale);
+}
+
+void softmax_bwd_rowdot(const void* S, const float* lse, const float* D, void* dP, int batch_heads, int seq,
+                        long long head_base, uint64_t seed, uint32_t thresh16, float scale, float alpha,
+                        cudaStream_t s) {
+  const int rows = batch_heads * seq;
+  softmax_bwd_rowdot_kernel<<<(rows + 7) / 8, 256, 0, s>>>((const uint4*)S, lse, D, (uint4*)dP, rows, seq, head_base,
+                                                           seed, thresh16, scale, alpha);
 }
 
 void softmax_bwd(const void* S, const float* lse, void* dP, int batch_heads, int seq, long long head_base,

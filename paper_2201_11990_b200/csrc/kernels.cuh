@@ -70,6 +70,13 @@ void softmax_fwd_stats(const void* S, void* P, const void* stats, int ld_stats, 
 void softmax_bwd(const void* S, const float* lse, void* dP, int batch_heads, int seq, long long head_base,
                  uint64_t site_seed, uint32_t thresh16, float scale, float alpha, cudaStream_t s);
 
+// One-pass softmax backward with the row term precomputed: D[bh * seq + i] = dctx_i . ctx_i of the
+// head (= sum_j P_ij dP_ij), so dS = alpha * p * (dP' - D) needs no in-kernel row reduction.
+void softmax_bwd_rowdot(const void* S, const float* lse, const float* D, void* dP, int batch_heads, int seq,
+                        long long head_base, uint64_t site_seed, uint32_t thresh16, float scale, float alpha,
+                        cudaStream_t s);
+void attn_rowdot(const void* dout, const void* out, long long ld, int hd, int heads, int seq, float* D, cudaStream_t s);
+
 // Fused causal flash attention on tcgen05 (attention_sm100.cu). Return 0 ok, 1 unsupported shape
 // (seq % 128 or head dim not in {64, 128, 160}), 2 CUDA error.
 int attention_fwd(const void* qkv, long long ld_qkv, int heads, int seq, int hd, long long head_base, float alpha,

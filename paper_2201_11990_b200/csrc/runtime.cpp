@@ -1138,8 +1138,21 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStrea
         .run(st, n);
     mark(c, st, "bwd.attn_dv_gemm");
     const long long head_base = bb * d.heads + int64_t{d.tp_rank} * Hl;
-    softmax_bwd(S, lse, dP, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, alpha, st);
-    ++n;
+    // row term D_i = dctx_i . ctx_i per head (= sum_j P_ij dP_ij) from a tiny kernel, so the softmax
+    // backward is one pass (MT_SOFTMAX_ROWDOT=0 selects the two-pass kernel)
+    static const bool rowdot_on = [] {
+      const char* e = getenv("MT_SOFTMAX_ROWDOT");
+      return !(e && e[0] == '0');
+    }();
+    if (rowdot_on) {
+      float* Dbuf = c->scratch_stats.as<float>();
+      attn_rowdot(dc, sv.ctx.as<uint16_t>() + bb * s * hl, hl, (int)hd, (int)Hl, (int)s, Dbuf, st);
+      softmax_bwd_rowdot(S, lse, Dbuf, dP, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, alpha, st);
+      n += 2;
+    } else {
+      softmax_bwd(S, lse, dP, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, alpha, st);
+      ++n;
+    }
     mark(c, st, "bwd.softmax");
     // dQ_h = dS_h K_h ; dK_h = dS_h^T Q_h   (dS already carries the 1/sqrt(d) factor)
     Gemm(dP, s, false, q + hd, ld3, true, dq, ld3, s, hd, s)
