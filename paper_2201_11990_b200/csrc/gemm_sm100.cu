@@ -59,7 +59,8 @@ struct GemmParams {
   uint32_t ar_epoch;
   int ar_rank, ar_ranks;
   int ar_debug;  // MT_AR_DEBUG (measurement only): 1 = skip the data movement, 2 = skip the peer wait
-  int ar_in_epi;  // 1: the epilogue warps reduce owned units; 0: publish only (mt_gemm_allreduce_reduce)
+  int ar_in_epi;
+  uint64_t store_policy;  // L2 hint on fp32 output stores (0 = none)  // 1: the epilogue warps reduce owned units; 0: publish only (mt_gemm_allreduce_reduce)
 };
 
 // kPair: 2-CTA (cta_group::2) tiles of 256 x BN — each CTA of the pair holds 128 rows of A and
@@ -180,15 +181,22 @@ __device__ __forceinline__ void stage_f32(uint32_t buf, uint32_t lane, const flo
 }
 
 // Issue the TMA op for the staged piece from lane 0 once all lanes' smem writes are visible.
+// policy != 0: L2 eviction hint for the store (MT_GEMM_STORE_HINT: fp32 outputs evict_first).
 __device__ __forceinline__ void flush_piece(const CUtensorMap* map, uint32_t buf, uint32_t lane, int col, int row, int b,
-                                            bool reduce) {
+                                            bool reduce, uint64_t policy = 0) {
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
-    if (reduce)
+    if (policy != 0) {
+      if (reduce)
+        tma_reduce_add_3d_hint(map, buf, col, row, b, policy);
+      else
+        tma_store_3d_hint(map, buf, col, row, b, policy);
+    } else if (reduce) {
       tma_reduce_add_3d(map, buf, col, row, b);
-    else
+    } else {
       tma_store_3d(map, buf, col, row, b);
+    }
     bulk_commit();
   }
 }
@@ -722,7 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (f32) {
           reuse_wait<C::kEpiBufs>(lane);
           stage_f32(stg + bi * 4096, lane, x);
-          flush_piece(&tmap_d, stg + bi * 4096, lane, col0, row0, b, ep == MT_EPI_ACCUM_F32);
+          flush_piece(&tmap_d, stg + bi * 4096, lane, col0, row0, b, ep == MT_EPI_ACCUM_F32, p.store_policy);
           bi = (bi + 1) % C::kEpiBufs;
           continue;
         }
@@ -1016,6 +1024,11 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   p.aux = static_cast<__nv_bfloat16*>(a.aux);
   p.ld_aux = a.ld_aux;
   p.row_stats = static_cast<float2*>(a.aux);
+  static const int store_hint = [] {
+    const char* e = getenv("MT_GEMM_STORE_HINT");
+    return e ? atoi(e) : 0;
+  }();
+  p.store_policy = (store_hint == 1) ? kEvictFirst : (store_hint == 2 ? kEvictLast : 0);
   if (a.allreduce != nullptr) {
     mt_gemm_allreduce& ar = *a.allreduce;
     const long long units = (long long)p.total_tiles * (kPair ? 2 : 1);
