@@ -38,6 +38,7 @@ struct mt_stage {
   cudaStream_t copy = nullptr;
   cudaEvent_t iter_start = nullptr;
   std::vector<cudaEvent_t> in_ev, tgt_ev;
+  std::vector<cudaEvent_t> tgt_gathered;            // TP-split targets all-gathered off the compute stream
   std::vector<mt::DeviceBuffer> targets;           // [MB][M, h] (host-target path)
   // language-model mode (mt_stage_attach_vocab): inputs/targets are int32 token ids [MB][M]
   mt_vocab* vocab = nullptr;
@@ -232,8 +233,12 @@ struct Step {
       if (tgt_dev) {
         tgt = tgt_dev + mb * io_bytes() + sp_off();
       } else if (tgt_host) {
-        mt::check_cuda(cudaStreamWaitEvent(s, st->tgt_ev[mb], 0), "cudaStreamWaitEvent");
-        gather_slices(st->targets[mb].ptr);
+        if (split_h2d() && st->ctx->comm) {  // gathered on the side stream at the start of the iteration
+          mt::check_cuda(cudaStreamWaitEvent(s, st->tgt_gathered[mb], 0), "cudaStreamWaitEvent");
+        } else {
+          mt::check_cuda(cudaStreamWaitEvent(s, st->tgt_ev[mb], 0), "cudaStreamWaitEvent");
+          gather_slices(st->targets[mb].ptr);
+        }
         tgt = st->targets[mb].ptr;
       } else {
         const uint64_t key = mt_stream_key(st->d.layer.seed, "target", 0, gid(mb));
@@ -342,6 +347,8 @@ extern "C" int mt_stage_create(mt_ctx* c, const mt_stage_desc* d, mt_stage** out
     st->tgt_ev.resize(d->micro_batches);
     for (auto& e : st->in_ev) mt::check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : st->tgt_ev) mt::check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    st->tgt_gathered.resize(d->micro_batches);
+    for (auto& e : st->tgt_gathered) mt::check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     if (st->stage == st->stages - 1) {
       st->targets.resize(d->micro_batches);
       for (auto& b : st->targets) b.ensure(bytes);
@@ -356,6 +363,7 @@ extern "C" int mt_stage_destroy(mt_stage* st) {
     for (auto* l : st->layers) mt_layer_destroy(l);
     for (auto e : st->in_ev) cudaEventDestroy(e);
     for (auto e : st->tgt_ev) cudaEventDestroy(e);
+    for (auto e : st->tgt_gathered) cudaEventDestroy(e);
     if (st->iter_start) cudaEventDestroy(st->iter_start);
     if (st->copy) cudaStreamDestroy(st->copy);
     delete st;
@@ -378,6 +386,20 @@ namespace {
 void run_iteration(Step& k, mt_stage* st, void* stream) {
   const int MB = st->d.micro_batches;
   k.prefetch_host();
+  // TP-split host targets (last stage): all-gather each microbatch's slices on the TP side stream /
+  // communicator as soon as its copy lands, so the gathers stay off the compute stream
+  if (k.tgt_host && k.last() && !k.lm() && k.split_h2d() && st->ctx->comm) {
+    mt_ctx* c = st->ctx;
+    const size_t n = static_cast<size_t>(k.elems() / c->par.tensor);
+    for (int mb = 0; mb < MB; ++mb) {
+      mt::check_cuda(cudaStreamWaitEvent(c->comm, st->tgt_ev[mb], 0), "cudaStreamWaitEvent");
+      char* buf = static_cast<char*>(st->targets[mb].ptr);
+      mt::check_nccl(ncclAllGather(buf + k.slice_off(), buf, n, ncclBfloat16, c->tp_side, c->comm),
+                     "ncclAllGather(target slices)");
+      mt::check_cuda(cudaEventRecord(st->tgt_gathered[mb], c->comm), "cudaEventRecord");
+      ++k.launches;
+    }
+  }
   for (auto* l : st->layers) ok(mt_layer_zero_grads(l, stream));
   const bool vocab_here = k.lm() && (k.first() || k.last());
   if (vocab_here) mt::vocab_zero_grads(st->vocab, k.s);
