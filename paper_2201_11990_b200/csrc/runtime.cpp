@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -370,7 +371,11 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
       if (const char* e = getenv("MT_TP_SYMMETRIC")) c->tp_symmetric = e[0] == '1';
       if (const char* e = getenv("MT_SEQ_PARALLEL")) c->seq_parallel = e[0] == '1';
       if (const char* e = getenv("MT_TP_FUSED")) c->tp_fused = e[0] == '1';
-      if (c->tp_fused) c->tp_symmetric = true;
+      // NVLink SHARP all-reduce kernel for the forward row-parallel outputs: on by default from TP = 4
+      // (GPT-3 layer at TP=4: 5.33 vs 5.38 ms/step; neutral at TP=2); MT_TP_NVLS=0/1 overrides
+      c->tp_nvls = p.tensor >= 4;
+      if (const char* e = getenv("MT_TP_NVLS")) c->tp_nvls = e[0] == '1';
+      if (c->tp_fused || c->tp_nvls) c->tp_symmetric = true;
     }
   });
 }
@@ -545,7 +550,26 @@ extern "C" int mt_layer_create(mt_ctx* c, const mt_layer_desc* d, mt_layer** out
     for (auto& b : c->scratch_h) b.ensure(M * l->h * 2);
     if (c->tp_symmetric && d->tp_size > 1 && c->tp && !c->shard_only) {
       for (auto& sb : c->sym_h) ensure_symmetric(c, sb, static_cast<size_t>(M * l->h * 2));
-      if (c->tp_fused && !c->fused_ar) c->fused_ar = fused_ar_create(c);
+      if ((c->tp_fused || c->tp_nvls) && !c->fused_ar) {
+        // all TP ranks must agree on the all-reduce path: fall back to NCCL everywhere if any rank
+        // cannot set up the multicast state
+        int ok = 1;
+        try {
+          c->fused_ar = fused_ar_create(c);
+        } catch (const std::exception& e) {
+          ok = 0;
+          fprintf(stderr, "[mtnlg] NVLS all-reduce unavailable (%s): using NCCL\n", e.what());
+        }
+        DeviceBuffer flag(sizeof(int));
+        check_cuda(cudaMemcpy(flag.ptr, &ok, sizeof(int), cudaMemcpyHostToDevice), "H2D");
+        check_nccl(ncclAllReduce(flag.ptr, flag.ptr, 1, ncclInt32, ncclMin, c->tp, nullptr), "ncclAllReduce(nvls ok)");
+        check_cuda(cudaMemcpy(&ok, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+        if (!ok) {
+          if (c->fused_ar) fused_ar_destroy(c, c->fused_ar);
+          c->fused_ar = nullptr;
+          c->tp_fused = c->tp_nvls = false;
+        }
+      }
     }
     c->scratch_ffn.ensure(M * l->ffl * 2);
     c->scratch_ctx.ensure(M * l->hl * 2);
@@ -775,7 +799,7 @@ void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_
     mark(c, st, "fwd.bias_dropout_residual_ln");
     return;
   }
-  if (c->fused_ar && z == c->sym_h[0].ptr) {
+  if (c->fused_ar && c->tp_fused && z == c->sym_h[0].ptr) {
     // one kernel: GEMM tiles + their all-reduce over NVLink SHARP from the epilogue warps
     check_cuda(cudaEventRecord(c->ev_ready, st), "cudaEventRecord");  // the reducer starts after this
     gemm_rows(0, M, fused_ar_gemm_ctas(c), fused_ar_begin(c));
@@ -789,8 +813,13 @@ void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_
   if (chunks == 1) {
     gemm_rows(0, M, 0, nullptr);
     mark(c, st, gemm_label);
-    check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(row-parallel out)");
-    ++n;
+    if (c->fused_ar && c->tp_nvls && z == c->sym_h[0].ptr) {
+      nvls_allreduce(c, M * h, st);  // NVLink SHARP all-reduce kernel + counter wait
+      n += 2;
+    } else {
+      check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(row-parallel out)");
+      ++n;
+    }
     mark(c, st, "fwd.tp_allreduce");
     epilogue(0, M);
     mark(c, st, "fwd.bias_dropout_residual_ln");

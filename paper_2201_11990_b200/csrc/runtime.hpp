@@ -27,6 +27,7 @@ void fused_ar_destroy(mt_ctx* c, FusedAllReduce* f);
 mt_gemm_allreduce* fused_ar_begin(mt_ctx* c);
 void fused_ar_end(mt_ctx* c, cudaStream_t st, void* d, int64_t ldd);
 int fused_ar_gemm_ctas(mt_ctx* c);
+void nvls_allreduce(mt_ctx* c, int64_t elems, cudaStream_t st);
 void op_mark(mt_ctx* c, cudaStream_t st, const char* label);  // runtime.cpp (op timing)
 
 // Failed CUDA / NCCL call -> DataError-class status 2.
@@ -112,6 +113,7 @@ struct mt_ctx {
   // forward row-parallel GEMM + TP all-reduce fused in one kernel over NVLink SHARP (MT_TP_FUSED=1;
   // implies symmetric buffers); state in tp_fused.cu
   bool tp_fused = false;
+  bool tp_nvls = false;  // forward row-parallel all-reduce by nvls_allreduce instead of NCCL (MT_TP_NVLS=1)
   mt::FusedAllReduce* fused_ar = nullptr;  // PP > 1: first + last stage of the same (dp, tp): tied word-embedding grads
   // compute-only measurement of one TP shard on a single GPU: the layer skips its TP collectives
   // (mt_ctx_shard_only); never set in a real multi-GPU run

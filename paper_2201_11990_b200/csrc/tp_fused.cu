@@ -220,4 +220,61 @@ extern "C" int mt_ctx_nvls_probe(mt_ctx* c, int64_t elems, int64_t ld, int32_t s
   }
 }
 
+// ---- standalone NVLS all-reduce of the symmetric row-parallel buffer (MT_TP_NVLS=1): one kernel,
+// entry barrier (every rank's GEMM output complete) -> this rank's 1/R share summed with
+// multimem.ld_reduce and broadcast with multimem.st -> exit count on every rank's counter; the
+// consumer waits on the counter (mt_gemm_allreduce_wait). Same counter as the fused path.
+namespace {
+__global__ void __launch_bounds__(1024) nvls_allreduce_kernel(__nv_bfloat16* mc, uint32_t* counter_mc,
+                                                              const uint32_t* counter_local, uint32_t entry_target,
+                                                              long long elems, int rank, int ranks) {
+  if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) {
+      fence_acq_rel_sys();
+      multimem_red_release_add_u32(counter_mc, 1u);
+    }
+    while ((int)(ld_acquire_sys_u32(counter_local) - entry_target) < 0) {
+    }
+  }
+  __syncthreads();
+  const long long chunks = elems / 8, per = (chunks + ranks - 1) / ranks, c0 = per * rank;
+  const long long c1 = c0 + per < chunks ? c0 + per : chunks;
+  constexpr int U = 4;
+  for (long long base = c0 + (long long)blockIdx.x * blockDim.x * U + threadIdx.x; base < c1;
+       base += (long long)gridDim.x * blockDim.x * U) {
+    uint32_t v[U][4];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long q = base + (long long)k * blockDim.x;
+      if (q < c1) multimem_ld_reduce_bf16x8(mc + q * 8, v[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long q = base + (long long)k * blockDim.x;
+      if (q < c1) multimem_st_bf16x8(mc + q * 8, v[k]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_acq_rel_sys();
+    multimem_red_release_add_u32(counter_mc, 1u);
+  }
+}
+}  // namespace
+
+// All-reduce (sum) of `elems` bf16 at offset 0 of the symmetric buffer sym_h[0] over the TP group.
+void nvls_allreduce(mt_ctx* c, int64_t elems, cudaStream_t st) {
+  FusedAllReduce* f = c->fused_ar;
+  if (f->z != c->sym_h[0].ptr) resolve(c, f);
+  const int ctas = std::max(1, f->reducer_ctas > 0 ? f->reducer_ctas : 16);
+  const uint32_t entry = f->target + static_cast<uint32_t>(c->par.tensor);
+  f->target = entry + static_cast<uint32_t>(c->par.tensor * ctas);
+  nvls_allreduce_kernel<<<ctas, 1024, 0, st>>>(static_cast<__nv_bfloat16*>(f->desc.d_multicast),
+                                               f->desc.counter_multicast, static_cast<const uint32_t*>(f->flags),
+                                               entry, elems, c->place.tensor, c->par.tensor);
+  check_cuda(cudaGetLastError(), "nvls_allreduce");
+  if (mt_gemm_allreduce_wait(static_cast<const uint32_t*>(f->flags), f->target, st) != 0)
+    throw RuntimeFailure("mt_gemm_allreduce_wait failed");
+}
+
 }  // namespace mt

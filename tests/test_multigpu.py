@@ -116,18 +116,18 @@ def _worker(rank, world, port, mode, q):
         elif mode == "tp_fused":
             # the same TP=2 layer with the forward all-reduces done by NCCL and by the fused
             # GEMM + multimem kernel; with 2 ranks both sum two bf16 values once -> bit-identical
-            ids = [obj[0]] + [None]
-            extra = [Context.unique_id() if rank == 0 else None]
+            extra = [Context.unique_id() if rank == 0 else None, Context.unique_id() if rank == 0 else None]
             dist.broadcast_object_list(extra, src=0)
-            ids[1] = extra[0]
+            ids = [obj[0], extra[0], extra[1]]
             d = PL.layer_desc(H, HEADS, S, B, tp_size=world, tp_rank=rank, seed=SEED, layer_index=0)
             params = O.init_params(H, SEED, 0)
             bits = [np.ascontiguousarray(O.to_bf16_bits(p)) for p in params]
             x = O.normal(O.site_seed(SEED, "input", 0, 0), B * S, H)
             g = O.normal(O.site_seed(SEED, "grad", 0, 0), B * S, H, std=1e-2)
             dev = lambda a: torch.from_numpy(O.to_bf16_bits(a).view(np.int16)).view(torch.bfloat16).cuda()  # noqa
-            for fused in (0, 1):
-                os.environ["MT_TP_FUSED"] = str(fused)
+            for fused in (0, 1, 2):  # NCCL, fused GEMM + all-reduce, standalone NVLS all-reduce kernel
+                os.environ["MT_TP_FUSED"] = "1" if fused == 1 else "0"
+                os.environ["MT_TP_NVLS"] = "1" if fused == 2 else "0"
                 c2 = Context(rank)
                 c2.init_comm(ids[fused], world, rank, tensor=world)
                 lay = Layer(c2, d)
@@ -143,6 +143,7 @@ def _worker(rank, world, port, mode, q):
                 lay.close()
                 c2.close()
             os.environ.pop("MT_TP_FUSED", None)
+            os.environ.pop("MT_TP_NVLS", None)
         elif mode in ("tp", "tp_sp"):
             ctx.init_comm(obj[0], world, rank, tensor=world)
             sp = mode == "tp_sp"
@@ -394,8 +395,27 @@ def test_fused_gemm_allreduce_matches_nccl_two_gpus():
     g = O.normal(O.site_seed(SEED, "grad", 0, 0), B * S, H, std=1e-2)
     y, dx = ol.forward(x, 2), ol.backward(g, 2)  # the worker's last repetition is microbatch 2
     for r in (0, 1):
-        assert rel(res[r]["y1"], y) < 5e-3 and rel(res[r]["dx1"], dx) < 1e-2
         assert rel(res[r]["y0"], y) < 5e-3
-        assert rel(res[r]["y1"], res[r]["y0"]) < 5e-3 and rel(res[r]["dx1"], res[r]["dx0"]) < 5e-3
-    assert np.array_equal(res[0]["y1"], res[1]["y1"])
-    assert np.array_equal(res[0]["dx1"], res[1]["dx1"])
+        for v in ("1", "2"):  # fused GEMM + all-reduce; standalone NVLS all-reduce kernel
+            assert rel(res[r]["y" + v], y) < 5e-3 and rel(res[r]["dx" + v], dx) < 1e-2
+            assert rel(res[r]["y" + v], res[r]["y0"]) < 5e-3 and rel(res[r]["dx" + v], res[r]["dx0"]) < 5e-3
+    for v in ("1", "2"):
+        assert np.array_equal(res[0]["y" + v], res[1]["y" + v])
+        assert np.array_equal(res[0]["dx" + v], res[1]["dx" + v])
+
+
+@pytest.mark.timeout(900)
+def test_tensor_parallel_layer_four_gpus():
+    """TP=4 layer (the NVLink SHARP all-reduce kernel is the default forward all-reduce from TP=4)
+    against the oracle: every rank's replicated output and input gradient."""
+    _need(4)
+    from oracle import oracle as O
+    res = _run("tp", world=4)
+    ol = O.OracleLayer(H, HEADS, S, B, 4, dropout_hidden=0.1, dropout_attn=0.1, seed=SEED, layer_index=0,
+                       bf16_emulate=True)
+    x = O.normal(O.site_seed(SEED, "input", 0, 0), B * S, H)
+    g = O.normal(O.site_seed(SEED, "grad", 0, 0), B * S, H, std=1e-2)
+    y, dx = ol.forward(x), ol.backward(g)
+    for r in range(4):
+        assert rel(res[r]["y"], y) < 5e-3 and rel(res[r]["dx"], dx) < 1e-2, r
+    assert all(np.array_equal(res[0]["y"], res[r]["y"]) for r in range(1, 4))
