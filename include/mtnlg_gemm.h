@@ -61,8 +61,12 @@ typedef struct mt_gemm_allreduce {
   int32_t reduce_in_epilogue;    /* 1: the GEMM's epilogue warps reduce the owned units; 0: the GEMM only
                                     publishes them and mt_gemm_allreduce_reduce (a concurrent kernel on
                                     the SMs the GEMM leaves free, max_ctas) reduces them */
+  int32_t groups;                /* > 0: column-group mode — the GEMM counts finished units per group of
+                                    column blocks on flags_local[g] (zeroed by the caller before the
+                                    launch) and mt_gemm_allreduce_reduce_groups reduces group by group */
   int64_t units;                 /* out: number of output units of this launch (counter increments) */
   int64_t geom[8];               /* out: unit geometry of the launch, read by mt_gemm_allreduce_reduce */
+  int64_t group_cols;            /* out: column blocks per group (0: group mode not applicable) */
 } mt_gemm_allreduce;
 
 typedef struct mt_gemm_args {
@@ -96,6 +100,11 @@ typedef struct mt_gemm_args {
 /* Launches on `stream` (a cudaStream_t). Returns 0 on success, 1 on bad arguments, 2 on CUDA error. */
 int mt_gemm(const mt_gemm_args* args, void* stream);
 
+/* Reducer of the column-group mode: `ctas` CTAs; per group, waits for this rank's GEMM (group_counters),
+ * a cross-rank barrier on the counter, then reduces this rank's rows of the group's columns; counts
+ * one exit per CTA. Counter after the launch = base + ranks * groups + ranks * ctas. */
+int mt_gemm_allreduce_reduce_groups(const mt_gemm_allreduce* ar, int64_t ldd, uint32_t* group_counters,
+                                    const uint32_t* counter_local, uint32_t base, int32_t ctas, void* stream);
 /* Stream-ordered wait until the local completion counter reaches `target` (all units of all ranks of
  * the fused all-reduce launches so far); 1 launch. */
 int mt_gemm_allreduce_wait(const uint32_t* counter_local, uint32_t target, void* stream);

@@ -90,6 +90,7 @@ _SIGS = {
     "mt_gemm_launches_per_call": (C.c_int, []),
     "mt_gemm_allreduce_wait": (C.c_int, [P, U32, P]),
     "mt_gemm_allreduce_reduce": (C.c_int, [P, P, I64, P, U32, I32, P]),
+    "mt_gemm_allreduce_reduce_groups": (C.c_int, [P, I64, P, P, U32, I32, P]),
     "mt_last_error": (C.c_char_p, []),
     "mt_version": (C.c_char_p, []),
     "mt_map_topology": (C.c_int, [C.POINTER(ClusterTopology), C.POINTER(ParallelConfig), C.POINTER(RankPlacement),

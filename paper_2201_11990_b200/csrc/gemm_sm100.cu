@@ -59,8 +59,9 @@ struct GemmParams {
   uint32_t ar_epoch;
   int ar_rank, ar_ranks;
   int ar_debug;  // MT_AR_DEBUG (measurement only): 1 = skip the data movement, 2 = skip the peer wait
-  int ar_in_epi;
-  uint64_t store_policy;  // L2 hint on fp32 output stores (0 = none)  // 1: the epilogue warps reduce owned units; 0: publish only (mt_gemm_allreduce_reduce)
+  int ar_in_epi;    // 1: the epilogue warps reduce owned units; 0: publish only (mt_gemm_allreduce_reduce)
+  int ar_group_cols;  // > 0: publish per group of column blocks (local counters) instead of per-unit flags
+  uint64_t store_policy;  // L2 hint on fp32 output stores (0 = none)
 };
 
 // kPair: 2-CTA (cta_group::2) tiles of 256 x BN — each CTA of the pair holds 128 rows of A and
@@ -236,7 +237,13 @@ __device__ __forceinline__ void ar_publish(const GemmParams& p, int w, uint32_t 
   epi_bar();
   if (threadIdx.x == 128) {
     fence_proxy_async_global();
-    st_release_sys_u32(p.ar_flags + ar_unit_id<kPair>(w, cta_rank), p.ar_epoch);
+    if (p.ar_group_cols > 0) {  // count the unit on its column group's (local) counter
+      int b, mb, nb;
+      tile_coords(p, w, b, mb, nb);
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.ar_flags + nb / p.ar_group_cols) : "memory");
+    } else {
+      st_release_sys_u32(p.ar_flags + ar_unit_id<kPair>(w, cta_rank), p.ar_epoch);
+    }
   }
 }
 
@@ -375,6 +382,69 @@ __global__ void __launch_bounds__(kReduceThreads, 1) allreduce_reduce_kernel(con
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     while ((int)(ld_acquire_sys_u32(p.counter_local) - p.target) < 0) {
     }
+  }
+}
+
+// Reducer of the column-group mode: groups of column blocks complete in order in the GEMM; for each
+// group, wait until this rank's GEMM published all its units (local counter), then a cross-rank
+// barrier on the multicast counter (one arrival per rank and group), then this rank's rows share of
+// the group's columns is summed with multimem.ld_reduce and broadcast with multimem.st by all CTAs.
+struct ArGroupParams {
+  __nv_bfloat16* mc;
+  const uint32_t* group_cnt;  // local per-group unit counters (zeroed before the GEMM)
+  uint32_t* counter_mc;
+  const uint32_t* counter_local;
+  uint32_t base;              // counter value before this launch
+  int rank, ranks, groups, group_cols, bn, m, n, mblocks, units_per_block;
+  long long ldd;
+};
+
+__global__ void __launch_bounds__(kReduceThreads, 1) allreduce_group_kernel(const ArGroupParams p) {
+  const int rows = p.m / p.ranks, r0 = p.rank * rows;  // this rank's share of every group
+  for (int g = 0; g < p.groups; ++g) {
+    const int cb0 = g * p.group_cols, cb1 = min((g + 1) * p.group_cols, (p.n + p.bn - 1) / p.bn);
+    if (cb0 >= cb1) break;
+    if (threadIdx.x == 0) {
+      const uint32_t expect = (uint32_t)((cb1 - cb0) * p.mblocks * p.units_per_block);
+      while (ld_acquire_gpu_u32(p.group_cnt + g) < expect) {
+      }
+      if (blockIdx.x == 0) {
+        fence_acq_rel_sys();
+        multimem_red_release_add_u32(p.counter_mc, 1u);
+      }
+      while ((int)(ld_acquire_sys_u32(p.counter_local) - (p.base + (uint32_t)(p.ranks * (g + 1)))) < 0) {
+      }
+    }
+    __syncthreads();
+    const int c0 = cb0 * p.bn, c1 = min(cb1 * p.bn, p.n);
+    const int cpr = (c1 - c0) / 8;
+    const long long total = (long long)rows * cpr;
+    constexpr int U = 4;
+    for (long long base = (long long)blockIdx.x * kReduceThreads * U + threadIdx.x; base < total;
+         base += (long long)gridDim.x * kReduceThreads * U) {
+      uint32_t v[U][4];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const long long i = base + (long long)k * kReduceThreads;
+        if (i < total) {
+          const long long r = i / cpr, c = i - r * cpr;
+          multimem_ld_reduce_bf16x8(p.mc + (r0 + r) * p.ldd + c0 + c * 8, v[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const long long i = base + (long long)k * kReduceThreads;
+        if (i < total) {
+          const long long r = i / cpr, c = i - r * cpr;
+          multimem_st_bf16x8(p.mc + (r0 + r) * p.ldd + c0 + c * 8, v[k]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_acq_rel_sys();
+    multimem_red_release_add_u32(p.counter_mc, 1u);
   }
 }
 
@@ -1053,6 +1123,11 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
     }();
     p.ar_debug = dbg;
     p.ar_in_epi = ar.reduce_in_epilogue ? 1 : 0;
+    p.ar_group_cols = 0;
+    if (ar.groups > 0 && !p.n_fastest) {  // column blocks complete in order: count them per group
+      p.ar_group_cols = (p.nblocks + ar.groups - 1) / ar.groups;
+      p.ar_in_epi = 0;
+    }
     ar.geom[0] = BN;
     ar.geom[1] = C::kTileM;
     ar.geom[2] = kPair ? 1 : 0;
@@ -1061,6 +1136,7 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
     ar.geom[5] = p.nblocks;
     ar.geom[6] = p.m;
     ar.geom[7] = p.n;
+    ar.group_cols = p.ar_group_cols;
     ar.units = units;
   }
   auto kern = gemm_sm100_kernel<BN, kAMN, kBMN, kPair, kAR>;
@@ -1181,6 +1257,32 @@ extern "C" int mt_gemm_allreduce_reduce(const mt_gemm_allreduce* ar, void* d, in
   }();
   p.debug = dbg;
   mt::allreduce_reduce_kernel<<<ctas, mt::kReduceThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+extern "C" int mt_gemm_allreduce_reduce_groups(const mt_gemm_allreduce* ar, int64_t ldd, uint32_t* group_counters,
+                                               const uint32_t* counter_local, uint32_t base, int32_t ctas,
+                                               void* stream) {
+  if (ar == nullptr || group_counters == nullptr || counter_local == nullptr || ctas < 1 || ar->group_cols <= 0 ||
+      ar->ranks < 2 || ar->geom[6] % ar->ranks != 0)
+    return 1;
+  mt::ArGroupParams p{};
+  p.mc = static_cast<__nv_bfloat16*>(ar->d_multicast);
+  p.group_cnt = group_counters;
+  p.counter_mc = ar->counter_multicast;
+  p.counter_local = counter_local;
+  p.base = base;
+  p.rank = ar->rank;
+  p.ranks = ar->ranks;
+  p.group_cols = (int)ar->group_cols;
+  p.bn = (int)ar->geom[0];
+  p.units_per_block = ar->geom[2] ? 2 : 1;
+  p.mblocks = (int)ar->geom[4];
+  p.m = (int)ar->geom[6];
+  p.n = (int)ar->geom[7];
+  p.groups = ((int)ar->geom[5] + p.group_cols - 1) / p.group_cols;
+  p.ldd = ldd;
+  mt::allreduce_group_kernel<<<ctas, mt::kReduceThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 

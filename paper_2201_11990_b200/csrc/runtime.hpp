@@ -26,6 +26,7 @@ FusedAllReduce* fused_ar_create(mt_ctx* c);
 void fused_ar_destroy(mt_ctx* c, FusedAllReduce* f);
 mt_gemm_allreduce* fused_ar_begin(mt_ctx* c);
 void fused_ar_end(mt_ctx* c, cudaStream_t st, void* d, int64_t ldd);
+void fused_ar_prepare(mt_ctx* c, cudaStream_t st);
 int fused_ar_gemm_ctas(mt_ctx* c);
 void nvls_allreduce(mt_ctx* c, int64_t elems, cudaStream_t st);
 void op_mark(mt_ctx* c, cudaStream_t st, const char* label);  // runtime.cpp (op timing)

@@ -33,6 +33,7 @@ struct FusedAllReduce {
   // reduce (measured slower: the multimem round trips then serialise with the epilogue)
   int reducer_ctas = 16;
   bool serial = false;  // MT_AR_SERIAL=1 (measurement): reducer after the GEMM on the same stream
+  int groups = 6;       // MT_AR_GROUPS: column-group granularity (0 = per-unit flags)
 };
 
 namespace {
@@ -81,6 +82,7 @@ FusedAllReduce* fused_ar_create(mt_ctx* c) {
   auto f = new FusedAllReduce();
   if (const char* e = getenv("MT_AR_CTAS")) f->reducer_ctas = std::max(0, atoi(e));
   if (const char* e = getenv("MT_AR_SERIAL")) f->serial = e[0] == '1';
+  if (const char* e = getenv("MT_AR_GROUPS")) f->groups = std::max(0, atoi(e));
   try {
     ncclDevCommRequirements req{};
     req.lsaMultimem = true;
@@ -119,7 +121,16 @@ mt_gemm_allreduce* fused_ar_begin(mt_ctx* c) {
   f->desc.epoch += 1;
   f->desc.units = 0;
   f->desc.reduce_in_epilogue = f->reducer_ctas == 0 ? 1 : 0;
+  f->desc.groups = f->reducer_ctas > 0 ? f->groups : 0;
+  f->desc.group_cols = 0;
   return &f->desc;
+}
+
+// Column-group mode: the group counters must read zero when the GEMM starts.
+void fused_ar_prepare(mt_ctx* c, cudaStream_t st) {
+  FusedAllReduce* f = c->fused_ar;
+  if (f->desc.groups > 0)
+    check_cuda(cudaMemsetAsync(f->desc.flags_local, 0, sizeof(uint32_t) * 64, st), "memset group counters");
 }
 
 // SMs the fused GEMM may use (the reducer kernel takes the rest), 0 = all.
@@ -137,8 +148,21 @@ int fused_ar_gemm_ctas(mt_ctx* c) {
 // never holds SMs a preceding kernel still needs).
 void fused_ar_end(mt_ctx* c, cudaStream_t st, void* d, int64_t ldd) {
   FusedAllReduce* f = c->fused_ar;
-  f->target += static_cast<uint32_t>(f->desc.units);
   const uint32_t* counter = static_cast<const uint32_t*>(f->flags);
+  if (f->desc.groups > 0 && f->desc.group_cols > 0) {
+    const int groups = static_cast<int>((f->desc.geom[5] + f->desc.group_cols - 1) / f->desc.group_cols);
+    const uint32_t base = f->target;
+    f->target = base + static_cast<uint32_t>(c->par.tensor * (groups + f->reducer_ctas));
+    check_cuda(cudaStreamWaitEvent(c->comm, c->ev_ready, 0), "cudaStreamWaitEvent");
+    if (mt_gemm_allreduce_reduce_groups(&f->desc, ldd, f->desc.flags_local, counter, base, f->reducer_ctas, c->comm) !=
+        0)
+      throw RuntimeFailure("mt_gemm_allreduce_reduce_groups failed");
+    check_cuda(cudaEventRecord(c->ev_done, c->comm), "cudaEventRecord");
+    check_cuda(cudaStreamWaitEvent(st, c->ev_done, 0), "cudaStreamWaitEvent");
+    if (mt_gemm_allreduce_wait(counter, f->target, st) != 0) throw RuntimeFailure("mt_gemm_allreduce_wait failed");
+    return;
+  }
+  f->target += static_cast<uint32_t>(f->desc.units);
   if (f->reducer_ctas == 0) {
     if (mt_gemm_allreduce_wait(counter, f->target, st) != 0) throw RuntimeFailure("mt_gemm_allreduce_wait failed");
     return;
