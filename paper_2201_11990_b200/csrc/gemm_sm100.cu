@@ -1079,12 +1079,14 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   // of the larger operand, and the smaller operand stays L2-resident across the sweep (e.g. the
   // wgrad of fc1, M = 4h/t >> N = h, would otherwise re-read its 200 MB A operand per n-block).
   p.n_fastest = (m > n) ? 1 : 0;
-  // Off by default: A/B on B200 (tools/gemm_ab.sh) measured evict_first/evict_last hints 0-7% slower.
+  // L2 eviction hints on the operand loads (streamed operand evict_first, re-read one evict_last):
+  // measured 5-10% slower for the m-fastest forward / dgrad GEMMs but ~2% faster for the n-fastest
+  // wgrad GEMMs (tools/gemm_one.py), so by default only the latter use them. MT_GEMM_HINTS=0/1 forces.
   static const int hints = [] {
     const char* e = getenv("MT_GEMM_HINTS");
-    return (e && e[0] == '1') ? 1 : 0;
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  p.hints = hints;
+  p.hints = hints >= 0 ? hints : (p.n_fastest ? 1 : 0);
   // (direct register->global fp32 stores were measured 8% slower than smem staging + TMA store)
   p.d_bf16 = static_cast<__nv_bfloat16*>(a.d);
   p.d_f32 = static_cast<float*>(a.d);
