@@ -205,11 +205,13 @@ template <int MAXV>
 __global__ void __launch_bounds__(kRowThreads, 1)
     ln_bwd_rows_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ x, const uint4* __restrict__ gamma,
                        const float* __restrict__ mean, const float* __restrict__ rstd, const uint4* __restrict__ resid,
-                       uint4* __restrict__ dx, float* __restrict__ ws, int rows, int nvec, float inv_h, int stages) {
+                       uint4* __restrict__ dx, float* __restrict__ ws, int rows, int nvec, float inv_h, int stages,
+                       int nin) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float red[32];
-  const Ring ring = make_ring(smem, stages, 2, (uint32_t)nvec * 16);
-  const void* src[2] = {dy, x};
+  // nin == 3: the residual-gradient rows are streamed through the ring too (when they fit in smem)
+  const Ring ring = make_ring(smem, stages, nin, (uint32_t)nvec * 16);
+  const void* src[3] = {dy, x, resid};
   float dg[MAXV][8], db[MAXV][8];
 #pragma unroll
   for (int i = 0; i < MAXV; ++i)
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(kRowThreads, 1)
         for (int j = 0; j < 8; ++j) o[j] = rs * (d[j] * g[j] - m1 - (xv[j] - mu) * rs * m2);
         if (resid != nullptr) {
           float r[8];
-          unpack8f(resid[row * nvec + v], r);
+          unpack8f(nin == 3 ? reinterpret_cast<const uint4*>(ring.slot(s, 2))[v] : resid[row * nvec + v], r);
 #pragma unroll
           for (int j = 0; j < 8; ++j) o[j] += r[j];
         }
@@ -356,10 +358,12 @@ bool bdr_ln_rows(const void* z, const void* bias, const void* resid, void* out, 
 bool ln_bwd_rows(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
                  const void* resid, void* dx, float* dgamma, float* dbeta, int rows, int h, float* ws, bool accumulate,
                  cudaStream_t s) {
-  const int nvec = h / 8, stages = ring_stages(2, (size_t)nvec * 16);
+  const int nvec = h / 8;
+  const int nin = (resid != nullptr && ring_stages(3, (size_t)nvec * 16) != 0) ? 3 : 2;
+  const int stages = ring_stages(nin, (size_t)nvec * 16);
   const int maxv = (nvec + kRowThreads - 1) / kRowThreads;
   if (h % 8 || stages == 0 || maxv > 6) return false;
-  const size_t smem = (size_t)stages * 2 * nvec * 16 + 64;
+  const size_t smem = (size_t)stages * nin * nvec * 16 + 64;
   const int ctas = row_kernel_ctas(rows);
   bool ok = true;
 #define L(V)                                                                                                       \
@@ -368,7 +372,7 @@ bool ln_bwd_rows(const void* dy, const void* x, const void* gamma, const float* 
     if (ok)                                                                                                        \
       ln_bwd_rows_kernel<V><<<ctas, kRowThreads, smem, s>>>((const uint4*)dy, (const uint4*)x, (const uint4*)gamma, \
                                                             mean, rstd, (const uint4*)resid, (uint4*)dx, ws, rows,  \
-                                                            nvec, 1.f / h, stages);                                 \
+                                                            nvec, 1.f / h, stages, nin);                            \
   } while (0)
   switch (maxv) {
     case 1: L(1); break;
