@@ -762,9 +762,9 @@ struct SeqPar {
 };
 
 template <class GemmFor>
-void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_t h, GemmFor gemm_rows, void* z,
-                        const void* bias, const void* resid, void* out, uint64_t site, uint32_t th, float scale,
-                        const LnOut* ln, cudaStream_t st, int& n, const char* gemm_label) {
+void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_t h, int64_t k_dim, GemmFor gemm_rows,
+                        void* z, const void* bias, const void* resid, void* out, uint64_t site, uint32_t th,
+                        float scale, const LnOut* ln, cudaStream_t st, int& n, const char* gemm_label) {
   if (sp.on) {
     // sequence parallel: reduce-scatter the partial sums to this rank's rows, then the element-wise
     // epilogue on those rows only, and all-gather the LayerNorm output the next GEMM needs in full
@@ -803,7 +803,10 @@ void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_
     mark(c, st, "fwd.bias_dropout_residual_ln");
     return;
   }
-  if (c->fused_ar && c->tp_fused && z == c->sym_h[0].ptr && M % c->par.tensor == 0) {
+  // fused GEMM + all-reduce when the GEMM is long enough to hide the reduction (K >= 4096); a short-K
+  // GEMM (e.g. the attention-out projection at TP >= 4) is followed by the standalone NVLS kernel
+  // instead (TP=4: proj 0.27 vs 0.32 ms fused)
+  if (c->fused_ar && c->tp_fused && z == c->sym_h[0].ptr && M % c->par.tensor == 0 && k_dim >= 4096) {
     // one kernel: GEMM tiles + their all-reduce over NVLink SHARP from the epilogue warps
     mt_gemm_allreduce* ar = fused_ar_begin(c);
     fused_ar_prepare(c, st);
@@ -819,7 +822,7 @@ void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_
   if (chunks == 1) {
     gemm_rows(0, M, 0, nullptr);
     mark(c, st, gemm_label);
-    if (c->fused_ar && c->tp_nvls && z == c->sym_h[0].ptr) {
+    if (c->fused_ar && (c->tp_nvls || c->tp_fused) && z == c->sym_h[0].ptr) {
       nvls_allreduce(c, M * h, st);  // NVLink SHARP all-reduce kernel + counter wait
       n += 2;
     } else {
@@ -1004,7 +1007,7 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
   {
     const LnOut ln2{l->param_ptr(MT_P_LN2_GAMMA), l->param_ptr(MT_P_LN2_BETA), sv.ln2.ptr, mean2, rstd2, d.ln_eps};
     row_parallel_block(
-        c, tpc, sp, M, h,
+        c, tpc, sp, M, h, hl,
         [&](int64_t r0, int64_t nr, int cap, mt_gemm_allreduce* ar) {
           Gemm(sv.ctx.as<uint16_t>() + r0 * hl, hl, false, l->param_ptr(MT_P_PROJ_W), hl, false,
                static_cast<uint16_t*>(z) + r0 * h, h, nr, h, hl)
@@ -1021,7 +1024,7 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
       .run(st, n);
   mark(c, st, "fwd.fc1_gemm");
   row_parallel_block(
-      c, tpc, sp, M, h,
+      c, tpc, sp, M, h, ffl,
       [&](int64_t r0, int64_t nr, int cap, mt_gemm_allreduce* ar) {
         Gemm(sv.act.as<uint16_t>() + r0 * ffl, ffl, false, l->param_ptr(MT_P_FC2_W), ffl, false,
              static_cast<uint16_t*>(z) + r0 * h, h, nr, h, ffl)
