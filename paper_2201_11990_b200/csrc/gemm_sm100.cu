@@ -512,8 +512,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t kTx = (C::kABytes + (kBMN ? C::kBBytes : C::kBRows * kBK * 2)) * (kPair ? 2 : 1);
       // The operand re-read across the raster sweep is kept in L2 (evict_last); the one whose tile is
       // shared by the concurrently resident CTAs streams through once (evict_first).
-      const uint64_t pol_a = !p.hints ? kEvictNormal : (p.n_fastest ? kEvictFirst : kEvictLast);
-      const uint64_t pol_b = !p.hints ? kEvictNormal : (p.n_fastest ? kEvictLast : kEvictFirst);
+      // hints == 2: only the re-read operand is marked evict_last (the streamed one stays normal, so
+      // concurrently resident CTAs sharing its tiles still hit L2)
+      const uint64_t pol_a = !p.hints ? kEvictNormal
+                                      : (p.n_fastest ? (p.hints == 2 ? kEvictNormal : kEvictFirst) : kEvictLast);
+      const uint64_t pol_b = !p.hints ? kEvictNormal
+                                      : (p.n_fastest ? kEvictLast : (p.hints == 2 ? kEvictNormal : kEvictFirst));
       uint32_t stage = 0, phase = 0;
       for (int w = t_first; w < p.work_items; w += t_stride) {
         Work wk;
@@ -1084,7 +1088,7 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   // wgrad GEMMs (tools/gemm_one.py), so by default only the latter use them. MT_GEMM_HINTS=0/1 forces.
   static const int hints = [] {
     const char* e = getenv("MT_GEMM_HINTS");
-    return e ? (e[0] == '1' ? 1 : 0) : -1;
+    return e ? atoi(e) : -1;
   }();
   p.hints = hints >= 0 ? hints : (p.n_fastest ? 1 : 0);
   // (direct register->global fp32 stores were measured 8% slower than smem staging + TMA store)
