@@ -32,3 +32,20 @@ def test_version_and_error_string():
     import ctypes as C
     rc = lib.mt_pipeline_efficiency(0, 4, C.byref(C.c_double()))
     assert rc == 1 and b"micro_batches" in lib.mt_last_error()
+
+
+def test_example_caller_compiles_against_the_header():
+    """examples/train_lm.cpp (the C++ binding INTEGRATION.md describes: planner types, stage, vocab,
+    blend feed, optimizer) must compile against include/mtnlg.h as documented."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    if shutil.which("g++") is None:
+        import pytest
+        pytest.skip("no g++")
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", f"-I{root / 'include'}",
+                        "-I/usr/local/cuda/include", str(root / "examples" / "train_lm.cpp")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
