@@ -176,9 +176,13 @@ def _worker(rank, world, port, mode, q):
             out["grads"] = grads
             lay.close()
         else:
-            tp, pp, dp = {"pp": (1, world, 1), "dp": (1, 1, world), "tp_stage": (world, 1, 1),
-                          "tp_stage_sp": (world, 1, 1)}[mode]
-            layers, MB = (2 * pp, 4) if mode == "pp" else (1, 2)
+            if mode.startswith("layout"):  # "layout-TP-PP-DP"
+                tp, pp, dp = (int(v) for v in mode.split("-")[1:])
+                layers, MB = 2 * pp, 4
+            else:
+                tp, pp, dp = {"pp": (1, world, 1), "dp": (1, 1, world), "tp_stage": (world, 1, 1),
+                              "tp_stage_sp": (world, 1, 1)}[mode]
+                layers, MB = (2 * pp, 4) if mode == "pp" else (1, 2)
             ctx.init_comm(obj[0], world, rank, tensor=tp, pipeline=pp, data=dp, batch=B * MB * dp, micro_batches=MB)
             place = ctx.placement()
             if mode == "tp_stage_sp":
@@ -208,9 +212,11 @@ def _worker(rank, world, port, mode, q):
             from paper_2201_11990_b200.runtime import adam_defaults
             out["grad_norm"] = None
             out["grads"] = []
+            dsh = PL.layer_desc(H, HEADS, S, B, tp_size=tp, tp_rank=place.tensor)
             for li in range(per):
                 gl = []
-                for i, p in enumerate(O.param_shapes(H)):
+                for i in range(len(O.param_shapes(H))):
+                    _, _, p = PL.param_shard(dsh, i)
                     a = np.empty(p[0] * p[1], np.float32)
                     st.layer(li).get_grad(i, a.ctypes.data)
                     gl.append(a.reshape(p))
@@ -419,3 +425,40 @@ def test_tensor_parallel_layer_four_gpus():
     for r in range(4):
         assert rel(res[r]["y"], y) < 5e-3 and rel(res[r]["dx"], dx) < 1e-2, r
     assert all(np.array_equal(res[0]["y"], res[r]["y"]) for r in range(1, 4))
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("layout", [(2, 2, 1), (2, 1, 2), (1, 2, 2)], ids=["tp2pp2", "tp2dp2", "pp2dp2"])
+def test_two_axis_layouts_four_gpus(layout):
+    """Every two-axis composition of the 3D layout on 4 GPUs (TPxPP, TPxDP, PPxDP; 2 layers per stage,
+    MB=4 per replica): the rank placement is curator::map_topology's (pp slowest, tp fastest), the loss
+    is the DP mean of the oracle's per-replica sums, every rank's gradient shard equals the matching
+    slice of the oracle's DP-mean gradients, and the clip norm is the global one."""
+    _need(4)
+    tp, pp, dp = layout
+    from paper_2201_11990_b200 import planner as PL
+    res = _run(f"layout-{tp}-{pp}-{dp}", world=4)
+    MB = 4
+    for r in range(4):  # rank = (pp * DP + dp) * TP + tp  (planner.cpp:110-126)
+        dpi, ppi, tpi = res[r]["place"]
+        assert r == (ppi * dp + dpi) * tp + tpi, (r, res[r]["place"])
+    loss, grads = _oracle_step(list(range(2 * pp)), range(dp * MB))
+    norm = np.sqrt(sum(float(((g / dp).astype(np.float64) ** 2).sum()) for lg in grads for g in lg))
+    for r in range(4):
+        dpi, ppi, tpi = res[r]["place"]
+        if ppi == pp - 1:
+            assert abs(res[r]["loss"] - loss / dp) / loss < 5e-3, (r, res[r]["loss"], loss / dp)
+        assert abs(res[r]["grad_norm"] - norm) / norm < 2e-2, (r, res[r]["grad_norm"], norm)
+        d = PL.layer_desc(H, HEADS, S, B, tp_size=tp, tp_rank=tpi)
+        for li in range(2):
+            for i in range(12):
+                _, (r0, c0), (nr, nc) = PL.param_shard(d, i)
+                ref = grads[2 * ppi + li][i][r0:r0 + nr, c0:c0 + nc] / dp
+                assert rel(res[r]["grads"][li][i], ref) < 2e-2, (r, li, i, rel(res[r]["grads"][li][i], ref))
+    # DP replicas hold bit-identical gradients after the all-reduce
+    for r in range(4):
+        for q in range(r + 1, 4):
+            if res[r]["place"][1:] == res[q]["place"][1:]:
+                for li in range(2):
+                    for i in range(12):
+                        assert np.array_equal(res[r]["grads"][li][i], res[q]["grads"][li][i]), (r, q, li, i)
