@@ -1017,6 +1017,19 @@ bool split_enabled() {
   return v == 1;
 }
 
+// Shortest K (in 64-wide k-blocks) the split-K tail is used for. Measured per shape on B200
+// (tools/gemm_split_ab.sh): +4-7% at K >= 20480 (320+ k-blocks), neutral at K = 12288 (192), and a
+// loss below — -5% at K = 9216, -11% at K = 6144, up to -40% at K = 1536 (the TP=8 projection) —
+// because the partial-tile round trip does not shrink with K while the tail work it spreads does.
+int split_min_kblocks() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MT_GEMM_SPLIT_MINK");
+    v = e ? std::max(1, atoi(e)) : 256;
+  }
+  return v;
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -1061,7 +1074,8 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   p.full_tiles = p.total_tiles;
   p.splits = 1;
   p.work_items = p.total_tiles;
-  if (a.causal == MT_CAUSAL_NONE && a.workspace != nullptr && a.allreduce == nullptr && split_enabled()) {
+  if (a.causal == MT_CAUSAL_NONE && a.workspace != nullptr && a.allreduce == nullptr && split_enabled() &&
+      p.kblocks >= split_min_kblocks()) {
     const int units = std::max(1, cap_units);
     const int full = (p.total_tiles / units) * units, tail = p.total_tiles - full;
     if (full > 0 && tail > 0 && tail * 2 <= units) {

@@ -127,8 +127,9 @@ def test_gemm_causal_modes(causal):
 @pytest.mark.parametrize("epi", [N.EPI_STORE_BF16, N.EPI_ACCUM_F32, N.EPI_BIAS_GELU])
 @pytest.mark.parametrize("max_ctas", [0, 132, 40])
 def test_gemm_split_k_tail(epi, max_ctas):
-    """Shapes whose last wave is partial take the split-K tail path (partials + last-arriver reduce)."""
-    m, n, k = 2048, 12288, 1024
+    """Shapes whose last wave is partial take the split-K tail path (partials + last-arriver reduce);
+    the tail is split only for K >= 256 k-blocks (16384)."""
+    m, n, k = 2048, 12288, 16384
     A = torch.randn(m, k, device="cuda").bfloat16()
     B = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
     bias = torch.randn(n, device="cuda").bfloat16()

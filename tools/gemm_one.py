@@ -25,6 +25,24 @@ SHAPES = {  # name: (m, n, k, a_mn, b_mn, epilogue)
     "wg_mm_f32": (4 * h, h, M, 1, 1, N.EPI_STORE_F32),
     "wg_mm_bf16": (4 * h, h, M, 1, 1, N.EPI_STORE_BF16),
     "wg_kk_bf16": (4 * h, h, M, 0, 0, N.EPI_STORE_BF16),
+    # GPT-3 h=12288 at TP=8 / TP=4 (per-GPU shard shapes)
+    "g8_proj_fwd": (M, h, h // 8, 0, 0, N.EPI_STORE_BF16),
+    "g4_proj_fwd": (M, h, h // 4, 0, 0, N.EPI_STORE_BF16),
+    "g8_proj_dgrad": (M, h // 8, h, 0, 1, N.EPI_STORE_BF16),
+    "g8_qkv_dgrad": (M, h, 3 * h // 8, 0, 1, N.EPI_STORE_BF16),
+    "g8_fc1_dgrad": (M, h, h // 2, 0, 1, N.EPI_STORE_BF16),
+    "g8_fc2_fwd": (M, h, h // 2, 0, 0, N.EPI_STORE_BF16),
+    "fc2_fwd_g2": (M, h, 2 * h, 0, 0, N.EPI_STORE_BF16),
+    "fc2_fwd_g4": (M, h, h, 0, 0, N.EPI_STORE_BF16),
+    "fc1_dgrad_g2": (M, h, 2 * h, 0, 1, N.EPI_STORE_BF16),
+    "qkv_dgrad_g4": (M, h, 3 * h // 4, 0, 1, N.EPI_STORE_BF16),
+    "qkv_dgrad_g1": (M, h, 3 * h, 0, 1, N.EPI_STORE_BF16),
+    "proj_fwd_g2": (M, h, h // 2, 0, 0, N.EPI_STORE_BF16),
+    "proj_dgrad_g4": (M, h // 4, h, 0, 1, N.EPI_STORE_BF16),
+    "qkv_wgrad_g8": (3 * h // 8, h, M, 1, 1, N.EPI_STORE_F32),
+    "fc1_wgrad_g8": (h // 2, h, M, 1, 1, N.EPI_STORE_F32),
+    "fc2_wgrad_g8": (h, h // 2, M, 1, 1, N.EPI_STORE_F32),
+    "proj_wgrad_g8": (h, h // 8, M, 1, 1, N.EPI_STORE_F32),
     # MT-NLG h=20480 at TP=8 (per-GPU shard shapes)
     "mt_qkv_fwd": (M, 7680, 20480, 0, 0, N.EPI_STORE_BF16),
     "mt_proj_fwd": (M, 20480, 2560, 0, 0, N.EPI_STORE_BF16),
