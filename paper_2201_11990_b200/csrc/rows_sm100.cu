@@ -57,6 +57,26 @@ __device__ __forceinline__ float row_sum(float v, float* red) {
   return t;
 }
 
+// Two row sums with one pair of barriers (same shuffle / slot order as row_sum, so bit-identical).
+__device__ __forceinline__ float2 row_sum2(float a, float b, float2* red2) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();  // red2 may still be read by the previous reduction
+  if (l == 0) red2[w] = make_float2(a, b);
+  __syncthreads();
+  float2 t = l < (int)(blockDim.x >> 5) ? red2[l] : make_float2(0.f, 0.f);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+    t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+  }
+  return t;
+}
+
 __device__ __forceinline__ uint32_t keep_mask8_rows(uint64_t seed, uint64_t idx, uint32_t thresh16) {
   if (thresh16 == 0) return 0xffu;
   uint32_t m = 0;
@@ -208,7 +228,7 @@ __global__ void __launch_bounds__(kRowThreads, 1)
                        uint4* __restrict__ dx, float* __restrict__ ws, int rows, int nvec, float inv_h, int stages,
                        int nin) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ float red[32];
+  __shared__ float2 red2[32];
   // nin == 3: the residual-gradient rows are streamed through the ring too (when they fit in smem)
   const Ring ring = make_ring(smem, stages, nin, (uint32_t)nvec * 16);
   const void* src[3] = {dy, x, resid};
@@ -247,8 +267,8 @@ __global__ void __launch_bounds__(kRowThreads, 1)
         }
       }
     }
-    const float m1 = row_sum(s1, red) * inv_h;
-    const float m2 = row_sum(s2, red) * inv_h;
+    const float2 sums = row_sum2(s1, s2, red2);
+    const float m1 = sums.x * inv_h, m2 = sums.y * inv_h;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
       const int v = threadIdx.x + i * kRowThreads;
