@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(1024) ln_bwd_dx_kernel(const uint4* __restrict
 // Stage 1: block (32 x 8): threadIdx.x -> 8-column vector, threadIdx.y -> row lane.
 // Each (blockIdx.y) split covers rows [split*rows_per, ...). Partials -> ws[out][split][col].
 constexpr int kColTY = 8;
+constexpr int kColU = 4;
 
 enum ColOp { kColSum = 0, kColLnParams = 1, kColDropout = 2 };
 
@@ -233,33 +234,48 @@ __global__ void __launch_bounds__(256) colsum_stage1(const uint4* __restrict__ a
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[o][j] = 0.f;
   if (cv < nvec) {
-    for (int r = r0 + threadIdx.y; r < r1; r += kColTY) {
-      float v[8];
-      unpack8(a[(long long)r * lda_vec + cv], v);
-      if (OP == kColSum) {
+    // kColU rows per thread in flight (loads first, then the same in-order accumulation)
+    for (int rb = r0 + threadIdx.y; rb < r1; rb += kColU * kColTY) {
+      uint4 va[kColU], vx[kColU];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[0][j] += v[j];
-      } else if (OP == kColLnParams) {
-        float xv[8];
-        unpack8(xin[(long long)r * nvec + cv], xv);
-        const float mu = mean[r], rs = rstd[r];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          acc[0][j] += v[j] * ((xv[j] - mu) * rs);
-          acc[1][j] += v[j];
+      for (int u = 0; u < kColU; ++u) {
+        const int r = rb + u * kColTY;
+        if (r < r1) {
+          va[u] = a[(long long)r * lda_vec + cv];
+          if (OP == kColLnParams) vx[u] = xin[(long long)r * nvec + cv];
         }
-      } else {
-        const uint64_t idx = elem_offset + ((uint64_t)r * nvec + cv) * 8;
-        const uint32_t keep = keep_mask8(seed, idx, thresh16);
-        float o[8];
+      }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = ((keep >> j) & 1u) ? v[j] * scale : 0.f;
-        const uint4 packed = pack8(o);
-        out_dz[(long long)r * nvec + cv] = packed;
-        float ob[8];
-        unpack8(packed, ob);  // bias grad of the stored (bf16) dz
+      for (int u = 0; u < kColU; ++u) {
+        const int r = rb + u * kColTY;
+        if (r >= r1) break;
+        float v[8];
+        unpack8(va[u], v);
+        if (OP == kColSum) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[0][j] += ob[j];
+          for (int j = 0; j < 8; ++j) acc[0][j] += v[j];
+        } else if (OP == kColLnParams) {
+          float xv[8];
+          unpack8(vx[u], xv);
+          const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            acc[0][j] += v[j] * ((xv[j] - mu) * rs);
+            acc[1][j] += v[j];
+          }
+        } else {
+          const uint64_t idx = elem_offset + ((uint64_t)r * nvec + cv) * 8;
+          const uint32_t keep = keep_mask8(seed, idx, thresh16);
+          float o[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] = ((keep >> j) & 1u) ? v[j] * scale : 0.f;
+          const uint4 packed = pack8(o);
+          out_dz[(long long)r * nvec + cv] = packed;
+          float ob[8];
+          unpack8(packed, ob);  // bias grad of the stored (bf16) dz
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[0][j] += ob[j];
+        }
       }
     }
   }
@@ -315,7 +331,12 @@ __global__ void __launch_bounds__(256) colsum_stage2(const float* __restrict__ w
 }
 
 int col_splits(int rows) {
-  int s = rows / 64;
+  static int per = 0;
+  if (per == 0) {
+    const char* e = getenv("MT_COL_ROWS_PER_SPLIT");
+    per = e ? std::max(8, atoi(e)) : 64;
+  }
+  int s = rows / per;
   return s < 1 ? 1 : (s > 64 ? 64 : s);
 }
 

@@ -32,6 +32,7 @@ struct FusedAllReduce {
   // reducer CTAs running beside the GEMM (MT_AR_CTAS, default 16); 0 = the GEMM's epilogue warps
   // reduce (measured slower: the multimem round trips then serialise with the epilogue)
   int reducer_ctas = 16;
+  int nvls_ctas = 0;  // CTAs of the standalone NVLS all-reduce kernel (0: reducer_ctas, or 16)
   bool serial = false;  // MT_AR_SERIAL=1 (measurement): reducer after the GEMM on the same stream
   int groups = 6;       // MT_AR_GROUPS: column-group granularity (0 = per-unit flags)
 };
@@ -81,6 +82,7 @@ void resolve(mt_ctx* c, FusedAllReduce* f) {
 FusedAllReduce* fused_ar_create(mt_ctx* c) {
   auto f = new FusedAllReduce();
   if (const char* e = getenv("MT_AR_CTAS")) f->reducer_ctas = std::max(0, atoi(e));
+  if (const char* e = getenv("MT_NVLS_CTAS")) f->nvls_ctas = std::max(0, atoi(e));
   if (const char* e = getenv("MT_AR_SERIAL")) f->serial = e[0] == '1';
   if (const char* e = getenv("MT_AR_GROUPS")) f->groups = std::max(0, atoi(e));
   try {
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(1024) nvls_allreduce_kernel(__nv_bfloat16* mc,
 void nvls_allreduce(mt_ctx* c, int64_t elems, cudaStream_t st) {
   FusedAllReduce* f = c->fused_ar;
   if (f->z != c->sym_h[0].ptr) resolve(c, f);
-  const int ctas = std::max(1, f->reducer_ctas > 0 ? f->reducer_ctas : 16);
+  const int ctas = f->nvls_ctas > 0 ? f->nvls_ctas : std::max(1, f->reducer_ctas > 0 ? f->reducer_ctas : 16);
   const uint32_t entry = f->target + static_cast<uint32_t>(c->par.tensor);
   f->target = entry + static_cast<uint32_t>(c->par.tensor * ctas);
   nvls_allreduce_kernel<<<ctas, 1024, 0, st>>>(static_cast<__nv_bfloat16*>(f->desc.d_multicast),
