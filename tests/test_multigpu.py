@@ -244,11 +244,27 @@ def _run(mode, world=2):
     procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=600) for _ in range(world))
-    for p in procs:
-        p.join(timeout=120)
-    for r, o in res.items():
-        assert "error" not in o, o.get("error")
+    import queue
+    import time
+    res, deadline = {}, time.monotonic() + 600
+    try:
+        # a rank that errors (or dies) leaves its peers blocked in NCCL: report it at once instead of
+        # waiting out the deadline, and name the ranks that never answered if the deadline passes
+        while len(res) < world:
+            try:
+                r, o = q.get(timeout=5)
+            except queue.Empty:
+                dead = [i for i, p in enumerate(procs) if p.exitcode not in (None, 0) and i not in res]
+                assert not dead, f"{mode}: rank(s) {dead} exited ({[procs[i].exitcode for i in dead]}) without a result"
+                assert time.monotonic() < deadline, f"{mode}: no result from rank(s) {sorted(set(range(world)) - set(res))}"
+                continue
+            res[r] = o
+            assert "error" not in o, f"rank {r}: {o['error']}"
+    finally:
+        for p in procs:
+            p.join(timeout=120 if len(res) == world else 1)
+            if p.is_alive():
+                p.terminate()
     return res
 
 
