@@ -39,6 +39,13 @@ CURATOR_HD inline constexpr bool dropout_keep(std::uint64_t site_seed, std::uint
   return u16 >= thresh16;
 }
 
+/// Dropout seed of training iteration `step`: iteration 0 keeps the base seed (so single-iteration
+/// parity fixtures do not depend on the step), later iterations mix the step in with the reference's
+/// mix64 so the masks of a microbatch differ from one training step to the next.
+CURATOR_HD inline constexpr std::uint64_t step_seed(std::uint64_t seed, std::uint64_t step) {
+  return step == 0 ? seed : mix64(seed, step);
+}
+
 /// Per-site seed: mix64(seed, fnv1a64(site) ^ (layer << 32 | microbatch)).
 inline std::uint64_t site_seed(std::uint64_t seed, std::string_view site, std::uint32_t layer, std::uint32_t microbatch) {
   return mix64(seed, fnv1a64(site) ^ ((static_cast<std::uint64_t>(layer) << 32) | microbatch));

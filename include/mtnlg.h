@@ -170,6 +170,10 @@ int mt_layer_set_recompute(mt_layer* l, int32_t enable);
 /* Sequence parallel: TP all-reduce of the replicated parameters' gradient partials (collective over
  * the TP group; call once after the last backward of an iteration; no-op otherwise). */
 int mt_layer_finish_grads(mt_layer* l, void* stream);
+/* Training step whose dropout masks the next forwards draw: every dropout site seeds from
+ * curator::step_seed(desc.seed, step) (= desc.seed at step 0), so masks differ across iterations; a
+ * backward replays the masks of its own forward. The stage driver sets it each iteration. */
+int mt_layer_set_step(mt_layer* l, uint64_t step);
 /* Kernel launches one forward / backward issues (for the bench's gpu_launches claim). */
 int mt_layer_launch_counts(const mt_layer* l, int32_t* fwd, int32_t* bwd);
 /* Device pointer to the flat fp32 gradient buffer of the layer and its element count. */
@@ -223,6 +227,8 @@ int mt_vocab_get_param(mt_vocab* v, int32_t param, void* host_bf16);
 int mt_vocab_zero_grads(mt_vocab* v, void* stream);
 /* x (device bf16 [b*s, h]) = dropout(E[tokens] + P[pos]); tokens device int32 [b*s]. */
 int mt_vocab_embed_forward(mt_vocab* v, const int32_t* tokens, void* x, uint32_t micro_batch, void* stream);
+/* Training step keying the embedding-dropout masks (as mt_layer_set_step). */
+int mt_vocab_set_step(mt_vocab* v, uint64_t step);
 /* scatter-add of the embedding gradient (dx = gradient w.r.t. the embedding output). */
 int mt_vocab_embed_backward(mt_vocab* v, const int32_t* tokens, const void* dx, uint32_t micro_batch, void* stream);
 /* loss_dev += mean cross-entropy of LN_f(y) E^T against targets; dy = d loss / d y (forward+backward). */
@@ -265,6 +271,11 @@ int mt_stage_optimizer_step(mt_stage* st, const mt_adam_desc* d, float* grad_nor
  * and the last stage (tied weights, Megatron); DP averages all vocab gradients; the optimizer step
  * covers the vocab parameters (word embedding counted once in the gradient norm). */
 int mt_stage_attach_vocab(mt_stage* st, mt_vocab* v);
+/* Training step of the next iteration (starts at 0, +1 per mt_stage_train_step[_dev]): the stage
+ * passes it to its layers and vocab (mt_layer_set_step) so dropout masks change every iteration;
+ * set it to resume a run or to replay an iteration bit-exactly. */
+int mt_stage_set_step(mt_stage* st, uint64_t step);
+int mt_stage_get_step(const mt_stage* st, uint64_t* step);
 /* Microbatches of the next iterations (1 .. the micro_batches the stage was created with): a batch
  * ramp (curator::batch_size_at) changes the global batch, hence the microbatch count, at fixed b. */
 int mt_stage_set_micro_batches(mt_stage* st, int32_t micro_batches);

@@ -170,6 +170,10 @@ typedef struct or_layer_desc {
   uint64_t seed;
   uint32_t layer_index;
   int32_t bf16_emulate;
+  // -1: the whole layer (all TP shards, the row-parallel partials summed = the TP all-reduce);
+  // r >= 0: only TP shard r with no all-reduce, which is what one GPU computes in the runtime's
+  // shard-only measurement mode (mt_ctx_shard_only; bench.py --shard-of t)
+  int32_t shard_rank;
 } or_layer_desc;
 
 // Parameter order and global shapes as in include/mtnlg.h (enum mt_param).
@@ -211,8 +215,11 @@ int or_num_threads(void) { return omp_get_max_threads(); }
 
 namespace {
 
+// s0 / ns: the TP shards computed ([s0, s0 + ns)); the column-parallel widths of that range are
+// Hc heads (global head index head0 + local head), cw = ns * h/t context columns, fw = ns * ff/t.
 struct Dims {
   int64_t b, s, h, H, hd, M, ff, t, Hl, hl, ffl;
+  int64_t s0, ns, Hc, head0, cw, fw;
 };
 Dims dims(const or_layer_desc& d) {
   Dims x;
@@ -227,6 +234,12 @@ Dims dims(const or_layer_desc& d) {
   x.Hl = x.H / x.t;
   x.hl = x.h / x.t;
   x.ffl = x.ff / x.t;
+  x.s0 = d.shard_rank >= 0 ? d.shard_rank : 0;
+  x.ns = d.shard_rank >= 0 ? 1 : x.t;
+  x.Hc = x.ns * x.Hl;
+  x.head0 = x.s0 * x.Hl;
+  x.cw = x.ns * x.hl;
+  x.fw = x.ns * x.ffl;
   return x;
 }
 
@@ -279,70 +292,70 @@ extern "C" void or_layer_forward(or_layer* l, const float* x_in, float* y_out, u
   const float scale_h = 1.f / (1.f - d.dropout_hidden), scale_a = 1.f / (1.f - d.dropout_attn);
   const uint32_t th_h = curator::dropout_threshold16(d.dropout_hidden), th_a = curator::dropout_threshold16(d.dropout_attn);
   const float alpha = 1.f / std::sqrt(static_cast<float>(D.hd));
+  const int64_t ld3 = 3 * D.cw;  // QKV columns of the computed shards, (local head, {q,k,v}, hd) order
 
   layer_norm(cx, sv.x, P[P_LN1G], P[P_LN1B], sv.ln1, sv.mean1, sv.rstd1, D.M, D.h, d.ln_eps);
-  // column-parallel QKV: the full output is the concatenation of the TP shards, so it is computed
-  // at once (rows of the global weight in (head, {q,k,v}, hd) order).
-  sv.qkv.assign(D.M * 3 * D.h, 0.f);
-  gemm_nt(sv.ln1.data(), D.h, P[P_QKVW], D.h, sv.qkv.data(), 3 * D.h, D.M, 3 * D.h, D.h);
+  // column-parallel QKV: the shards' outputs are contiguous row blocks of the global weight
+  // (rows in (head, {q,k,v}, hd) order), so the computed shards are one GEMM.
+  sv.qkv.assign(D.M * ld3, 0.f);
+  gemm_nt(sv.ln1.data(), D.h, P[P_QKVW] + D.s0 * 3 * D.hl * D.h, D.h, sv.qkv.data(), ld3, D.M, ld3, D.h);
+  const float* qkv_b = P[P_QKVB] + D.s0 * 3 * D.hl;
   for (int64_t r = 0; r < D.M; ++r)
-    for (int64_t c = 0; c < 3 * D.h; ++c) sv.qkv[r * 3 * D.h + c] += P[P_QKVB][c];
+    for (int64_t c = 0; c < ld3; ++c) sv.qkv[r * ld3 + c] += qkv_b[c];
   cx.round(sv.qkv);
 
-  // attention per (microbatch row bb, head)
+  // causal attention per (microbatch row bb, head): S = alpha Q K^T and ctx = P V as packed GEMMs
+  // (one head per thread), the softmax + dropout per row in between. Entries above the diagonal
+  // are never read (S) or zero (P).
   const int64_t s = D.s, hd = D.hd;
-  sv.S.assign(D.b * D.H * s * s, 0.f);
-  sv.P.assign(D.b * D.H * s * s, 0.f);
-  sv.lse.assign(D.b * D.H * s, 0.f);
-  sv.ctx.assign(D.M * D.h, 0.f);
+  sv.S.assign(D.b * D.Hc * s * s, 0.f);
+  sv.P.assign(D.b * D.Hc * s * s, 0.f);
+  sv.lse.assign(D.b * D.Hc * s, 0.f);
+  sv.ctx.assign(D.M * D.cw, 0.f);
   const uint64_t site_a = site(d, "attn.probs", mb);
 #pragma omp parallel for collapse(2) schedule(dynamic)
   for (int64_t bb = 0; bb < D.b; ++bb) {
-    for (int64_t hh = 0; hh < D.H; ++hh) {
-      const float* q = &sv.qkv[bb * s * 3 * D.h + hh * 3 * hd];
+    for (int64_t hh = 0; hh < D.Hc; ++hh) {
+      const float* q = &sv.qkv[bb * s * ld3 + hh * 3 * hd];
       const float* k = q + hd;
       const float* v = q + 2 * hd;
-      float* S = &sv.S[(bb * D.H + hh) * s * s];
-      float* Pm = &sv.P[(bb * D.H + hh) * s * s];
+      float* S = &sv.S[(bb * D.Hc + hh) * s * s];
+      float* Pm = &sv.P[(bb * D.Hc + hh) * s * s];
+      gemm(false, true, s, s, hd, q, ld3, k, ld3, S, s, false);  // nested: runs on this thread
+      const int64_t hg = D.head0 + hh;  // global head index (keys the attention-dropout stream)
       for (int64_t i = 0; i < s; ++i) {
         float mx = -INFINITY;
         for (int64_t j = 0; j <= i; ++j) {
-          float acc = 0.f;
-          for (int64_t e = 0; e < hd; ++e) acc += q[i * 3 * D.h + e] * k[j * 3 * D.h + e];
-          acc *= alpha;
+          float acc = S[i * s + j] * alpha;
           if (cx.emu) acc = bf16_round(acc);
           S[i * s + j] = acc;
           mx = std::max(mx, acc);
         }
+        for (int64_t j = i + 1; j < s; ++j) S[i * s + j] = 0.f;
         float sum = 0.f;
         for (int64_t j = 0; j <= i; ++j) sum += std::exp(S[i * s + j] - mx);
         const float lse = mx + std::log(sum);
-        sv.lse[(bb * D.H + hh) * s + i] = lse;
-        const uint64_t base = ((static_cast<uint64_t>(bb) * D.H + hh) * s + i) * static_cast<uint64_t>(s);
+        sv.lse[(bb * D.Hc + hh) * s + i] = lse;
+        const uint64_t base = ((static_cast<uint64_t>(bb) * D.H + hg) * s + i) * static_cast<uint64_t>(s);
         for (int64_t j = 0; j <= i; ++j) {
           float pv = std::exp(S[i * s + j] - mx) / sum;
           pv = curator::dropout_keep(site_a, base + j, th_a) ? pv * scale_a : 0.f;
           Pm[i * s + j] = cx.emu ? bf16_round(pv) : pv;
         }
       }
-      // ctx = P V
-      for (int64_t i = 0; i < s; ++i)
-        for (int64_t e = 0; e < hd; ++e) {
-          float acc = 0.f;
-          for (int64_t j = 0; j <= i; ++j) acc += Pm[i * s + j] * v[j * 3 * D.h + e];
-          sv.ctx[(bb * s + i) * D.h + hh * hd + e] = acc;
-        }
+      gemm(false, false, s, hd, s, Pm, s, v, ld3, &sv.ctx[bb * s * D.cw + hh * hd], D.cw, false);
     }
   }
   cx.round(sv.ctx);
 
-  // row-parallel attn-out: per TP shard partial (rounded like the GPU epilogue), summed (the all-reduce)
-  auto row_parallel = [&](const Vec& in, int64_t in_cols, const float* W, int64_t shard_cols, Vec& out) {
+  // row-parallel GEMM: per TP shard partial (rounded like the GPU epilogue), summed over the computed
+  // shards (the all-reduce; a single shard in shard mode) and rounded
+  auto row_parallel = [&](const Vec& in, int64_t in_cols, const float* W, int64_t w_cols, int64_t shard_cols, Vec& out) {
     out.assign(D.M * D.h, 0.f);
     Vec part(D.M * D.h);
-    for (int64_t r = 0; r < D.t; ++r) {
-      // shard r: input columns / weight columns [r*shard_cols, (r+1)*shard_cols)
-      gemm_nt(in.data() + r * shard_cols, in_cols, W + r * shard_cols, in_cols, part.data(), D.h, D.M, D.h,
+    for (int64_t r = 0; r < D.ns; ++r) {
+      // shard s0 + r: input columns [r*shard_cols, ...) of `in`, weight columns [(s0+r)*shard_cols, ...)
+      gemm_nt(in.data() + r * shard_cols, in_cols, W + (D.s0 + r) * shard_cols, w_cols, part.data(), D.h, D.M, D.h,
               shard_cols);
       cx.round(part);
       for (int64_t i = 0; i < D.M * D.h; ++i) out[i] += part[i];
@@ -350,38 +363,29 @@ extern "C" void or_layer_forward(or_layer* l, const float* x_in, float* y_out, u
     cx.round(out);
   };
   Vec z;
-  row_parallel(sv.ctx, D.h, P[P_PROJW], D.hl, z);
+  row_parallel(sv.ctx, D.cw, P[P_PROJW], D.h, D.hl, z);
   bias_dropout_residual(cx, z, P[P_PROJB], sv.x, sv.x1, D.M, D.h, site(d, "attn.out", mb), th_h, scale_h);
   layer_norm(cx, sv.x1, P[P_LN2G], P[P_LN2B], sv.ln2, sv.mean2, sv.rstd2, D.M, D.h, d.ln_eps);
-  sv.pre.assign(D.M * D.ff, 0.f);
-  gemm_nt(sv.ln2.data(), D.h, P[P_FC1W], D.h, sv.pre.data(), D.ff, D.M, D.ff, D.h);
-  sv.act.assign(D.M * D.ff, 0.f);
+  sv.pre.assign(D.M * D.fw, 0.f);
+  gemm_nt(sv.ln2.data(), D.h, P[P_FC1W] + D.s0 * D.ffl * D.h, D.h, sv.pre.data(), D.fw, D.M, D.fw, D.h);
+  sv.act.assign(D.M * D.fw, 0.f);
+  const float* fc1_b = P[P_FC1B] + D.s0 * D.ffl;
 #pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < D.M * D.ff; ++i) {
-    float pr = sv.pre[i] + P[P_FC1B][i % D.ff];
+  for (int64_t i = 0; i < D.M * D.fw; ++i) {
+    float pr = sv.pre[i] + fc1_b[i % D.fw];
     if (cx.emu) pr = bf16_round(pr);
     sv.pre[i] = pr;
     const float a = gelu(pr);
     sv.act[i] = cx.emu ? bf16_round(a) : a;
   }
   Vec m;
-  row_parallel(sv.act, D.ff, P[P_FC2W], D.ffl, m);
+  row_parallel(sv.act, D.fw, P[P_FC2W], D.ff, D.ffl, m);
   Vec y;
   bias_dropout_residual(cx, m, P[P_FC2B], sv.x1, y, D.M, D.h, site(d, "mlp.out", mb), th_h, scale_h);
   std::copy(y.begin(), y.end(), y_out);
 }
 
 namespace {
-
-// dX[M][k] = dY[M][n] * W[n][k]
-void dgrad(const float* dY, int64_t n, const float* W, int64_t k, float* dX, int64_t M) {
-  gemm(false, false, M, k, n, dY, n, W, k, dX, k, false);
-}
-
-// dW[n][k] += sum_tok dY[tok][n] * X[tok][k]
-void wgrad_acc(const float* dY, int64_t n, const float* X, int64_t k, float* dW, int64_t M) {
-  gemm(true, false, n, k, M, dY, n, X, k, dW, k, true);
-}
 
 void colsum_acc(const Vec& x, int64_t M, int64_t n, float* out) {
 #pragma omp parallel for schedule(static)
@@ -446,16 +450,17 @@ extern "C" void or_layer_backward(or_layer* l, const float* dy_in, float* dx_out
   const float scale_h = 1.f / (1.f - d.dropout_hidden), scale_a = 1.f / (1.f - d.dropout_attn);
   const uint32_t th_h = curator::dropout_threshold16(d.dropout_hidden), th_a = curator::dropout_threshold16(d.dropout_attn);
   const float alpha = 1.f / std::sqrt(static_cast<float>(D.hd));
-  const int64_t M = D.M, h = D.h, ff = D.ff, s = D.s, hd = D.hd;
+  const int64_t M = D.M, h = D.h, ff = D.ff, s = D.s, hd = D.hd, cw = D.cw, fw = D.fw, ld3 = 3 * cw;
   Vec dy(dy_in, dy_in + M * h);
 
-  // column-parallel "f" backward: per-shard dgrad partials rounded, summed, rounded (the TP all-reduce)
+  // column-parallel "f" backward: per-shard dgrad partials rounded, summed over the computed shards
+  // (the TP all-reduce), rounded. dout holds the computed shards' columns ([M, ns * shard_rows]);
+  // W is the global [.., h] weight, shard r owns its rows [(s0+r)*shard_rows, ...).
   auto col_parallel_dgrad = [&](const Vec& dout, int64_t out_cols, const float* W, int64_t shard_rows, Vec& din) {
     din.assign(M * h, 0.f);
     Vec part(M * h);
-    for (int64_t r = 0; r < D.t; ++r) {
-      // shard r: output columns of dout / rows of W [r*shard_rows, (r+1)*shard_rows)
-      gemm(false, false, M, h, shard_rows, dout.data() + r * shard_rows, out_cols, W + r * shard_rows * h, h,
+    for (int64_t r = 0; r < D.ns; ++r) {
+      gemm(false, false, M, h, shard_rows, dout.data() + r * shard_rows, out_cols, W + (D.s0 + r) * shard_rows * h, h,
            part.data(), h, false);
       cx.round(part);
       for (int64_t i = 0; i < M * h; ++i) din[i] += part[i];
@@ -467,16 +472,18 @@ extern "C" void or_layer_backward(or_layer* l, const float* dy_in, float* dx_out
   Vec dm;
   dropout_bwd(cx, dy, dm, M * h, site(d, "mlp.out", mb), th_h, scale_h);
   colsum_acc(dm, M, h, grads[P_FC2B]);
-  Vec dpre(M * ff);
-  dgrad(dm.data(), h, P[P_FC2W], ff, dpre.data(), M);
+  Vec dpre(M * fw);
+  // dpre = dm W2[:, shards] (W2 is [h, ff]), times GeLU'(pre)
+  gemm(false, false, M, fw, h, dm.data(), h, P[P_FC2W] + D.s0 * D.ffl, ff, dpre.data(), fw, false);
 #pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < M * ff; ++i) dpre[i] *= gelu_grad(sv.pre[i]);
+  for (int64_t i = 0; i < M * fw; ++i) dpre[i] *= gelu_grad(sv.pre[i]);
   cx.round(dpre);
-  wgrad_acc(dm.data(), h, sv.act.data(), ff, grads[P_FC2W], M);
-  colsum_acc(dpre, M, ff, grads[P_FC1B]);
-  wgrad_acc(dpre.data(), ff, sv.ln2.data(), h, grads[P_FC1W], M);
+  // dW2[:, shards] += dm^T act ; db1[shards] += colsum dpre ; dW1[shards, :] += dpre^T ln2
+  gemm(true, false, h, fw, M, dm.data(), h, sv.act.data(), fw, grads[P_FC2W] + D.s0 * D.ffl, ff, true);
+  colsum_acc(dpre, M, fw, grads[P_FC1B] + D.s0 * D.ffl);
+  gemm(true, false, fw, h, M, dpre.data(), fw, sv.ln2.data(), h, grads[P_FC1W] + D.s0 * D.ffl * h, h, true);
   Vec dln2;
-  col_parallel_dgrad(dpre, ff, P[P_FC1W], D.ffl, dln2);
+  col_parallel_dgrad(dpre, fw, P[P_FC1W], D.ffl, dln2);
   Vec dx1;
   ln_backward(cx, dln2, sv.x1, P[P_LN2G], sv.mean2, sv.rstd2, &dy, dx1, grads[P_LN2G], grads[P_LN2B], M, h);
 
@@ -484,35 +491,37 @@ extern "C" void or_layer_backward(or_layer* l, const float* dy_in, float* dx_out
   Vec dz;
   dropout_bwd(cx, dx1, dz, M * h, site(d, "attn.out", mb), th_h, scale_h);
   colsum_acc(dz, M, h, grads[P_PROJB]);
-  Vec dctx(M * h);
-  dgrad(dz.data(), h, P[P_PROJW], h, dctx.data(), M);
+  Vec dctx(M * cw);
+  gemm(false, false, M, cw, h, dz.data(), h, P[P_PROJW] + D.s0 * D.hl, h, dctx.data(), cw, false);
   cx.round(dctx);
-  wgrad_acc(dz.data(), h, sv.ctx.data(), h, grads[P_PROJW], M);
+  gemm(true, false, h, cw, M, dz.data(), h, sv.ctx.data(), cw, grads[P_PROJW] + D.s0 * D.hl, h, true);
 
-  Vec dqkv(M * 3 * h, 0.f);
+  // attention backward per (bb, head) as packed GEMMs, one head per thread:
+  //   dP = dctx V^T ; dS = alpha P~ (dP_kept - D_i) (softmax + dropout backward, row by row) ;
+  //   dV = P^T dctx ; dK = dS^T Q ; dQ = dS K
+  Vec dqkv(M * ld3, 0.f);
   const uint64_t site_a = site(d, "attn.probs", mb);
 #pragma omp parallel for collapse(2) schedule(dynamic)
   for (int64_t bb = 0; bb < D.b; ++bb) {
-    for (int64_t hh = 0; hh < D.H; ++hh) {
-      const int64_t ld3 = 3 * h;
+    for (int64_t hh = 0; hh < D.Hc; ++hh) {
       const float* q = &sv.qkv[bb * s * ld3 + hh * 3 * hd];
       const float* k = q + hd;
       const float* v = q + 2 * hd;
       float* dq = &dqkv[bb * s * ld3 + hh * 3 * hd];
       float* dk = dq + hd;
       float* dv = dq + 2 * hd;
-      const float* S = &sv.S[(bb * D.H + hh) * s * s];
-      const float* Pm = &sv.P[(bb * D.H + hh) * s * s];
-      const float* dc = &dctx[bb * s * h + hh * hd];
-      Vec dS(s * s, 0.f);
-      const uint64_t base0 = (static_cast<uint64_t>(bb) * D.H + hh) * s;
+      const float* S = &sv.S[(bb * D.Hc + hh) * s * s];
+      const float* Pm = &sv.P[(bb * D.Hc + hh) * s * s];
+      const float* dc = &dctx[bb * s * cw + hh * hd];
+      Vec dP(s * s), dS(s * s, 0.f);
+      gemm(false, true, s, s, hd, dc, cw, v, ld3, dP.data(), s, false);
+      const uint64_t base0 = (static_cast<uint64_t>(bb) * D.H + D.head0 + hh) * s;
+      Vec y(s), g(s);
       for (int64_t i = 0; i < s; ++i) {
-        const float lse = sv.lse[(bb * D.H + hh) * s + i];
-        Vec y(i + 1), g(i + 1);
+        const float lse = sv.lse[(bb * D.Hc + hh) * s + i];
         float dot = 0.f;
         for (int64_t j = 0; j <= i; ++j) {
-          float acc = 0.f;
-          for (int64_t e = 0; e < hd; ++e) acc += dc[i * h + e] * v[j * ld3 + e];
+          float acc = dP[i * s + j];
           if (cx.emu) acc = bf16_round(acc);
           const bool keep = curator::dropout_keep(site_a, (base0 + i) * static_cast<uint64_t>(s) + j, th_a);
           y[j] = std::exp(S[i * s + j] - lse);
@@ -524,29 +533,16 @@ extern "C" void or_layer_backward(or_layer* l, const float* dy_in, float* dx_out
           dS[i * s + j] = cx.emu ? bf16_round(ds) : ds;
         }
       }
-      for (int64_t j = 0; j < s; ++j)
-        for (int64_t e = 0; e < hd; ++e) {
-          float av = 0.f, ak = 0.f;
-          for (int64_t i = j; i < s; ++i) {
-            av += Pm[i * s + j] * dc[i * h + e];
-            ak += dS[i * s + j] * q[i * ld3 + e];
-          }
-          dv[j * ld3 + e] = av;
-          dk[j * ld3 + e] = ak;
-        }
-      for (int64_t i = 0; i < s; ++i)
-        for (int64_t e = 0; e < hd; ++e) {
-          float aq = 0.f;
-          for (int64_t j = 0; j <= i; ++j) aq += dS[i * s + j] * k[j * ld3 + e];
-          dq[i * ld3 + e] = aq;
-        }
+      gemm(true, false, s, hd, s, Pm, s, dc, cw, dv, ld3, false);
+      gemm(true, false, s, hd, s, dS.data(), s, q, ld3, dk, ld3, false);
+      gemm(false, false, s, hd, s, dS.data(), s, k, ld3, dq, ld3, false);
     }
   }
   cx.round(dqkv);
-  colsum_acc(dqkv, M, 3 * h, grads[P_QKVB]);
-  wgrad_acc(dqkv.data(), 3 * h, sv.ln1.data(), h, grads[P_QKVW], M);
+  colsum_acc(dqkv, M, ld3, grads[P_QKVB] + D.s0 * 3 * D.hl);
+  gemm(true, false, ld3, h, M, dqkv.data(), ld3, sv.ln1.data(), h, grads[P_QKVW] + D.s0 * 3 * D.hl * h, h, true);
   Vec dln1;
-  col_parallel_dgrad(dqkv, 3 * h, P[P_QKVW], 3 * D.hl, dln1);
+  col_parallel_dgrad(dqkv, ld3, P[P_QKVW], 3 * D.hl, dln1);
   Vec dx;
   ln_backward(cx, dln1, sv.x, P[P_LN1G], sv.mean1, sv.rstd1, &dx1, dx, grads[P_LN1G], grads[P_LN1B], M, h);
   std::copy(dx.begin(), dx.end(), dx_out);
@@ -568,6 +564,8 @@ extern "C" void or_fill_normal(float* out, int64_t rows, int64_t cols, int64_t g
 extern "C" uint64_t or_site_seed(uint64_t seed, const char* name, uint32_t layer, uint32_t mb) {
   return curator::site_seed(seed, name, layer, mb);
 }
+
+extern "C" uint64_t or_step_seed(uint64_t seed, uint64_t step) { return curator::step_seed(seed, step); }
 
 extern "C" int32_t or_dropout_keep(uint64_t site_seed, uint64_t idx, uint32_t th16) {
   return curator::dropout_keep(site_seed, idx, th16) ? 1 : 0;

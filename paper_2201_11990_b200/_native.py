@@ -133,6 +133,10 @@ _SIGS = {
     "mt_layer_backward": (C.c_int, [P, P, P, U32, P]),
     "mt_layer_launch_counts": (C.c_int, [P, PI32, PI32]),
     "mt_layer_set_recompute": (C.c_int, [P, I32]),
+    "mt_layer_set_step": (C.c_int, [P, U64]),
+    "mt_vocab_set_step": (C.c_int, [P, U64]),
+    "mt_stage_set_step": (C.c_int, [P, U64]),
+    "mt_stage_get_step": (C.c_int, [P, C.POINTER(U64)]),
     "mt_stage_set_recompute": (C.c_int, [P, I32]),
     "mt_vocab_create": (C.c_int, [P, C.POINTER(VocabDesc), C.POINTER(P)]),
     "mt_vocab_destroy": (C.c_int, [P]),

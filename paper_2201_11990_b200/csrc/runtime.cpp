@@ -662,6 +662,13 @@ extern "C" int mt_layer_set_recompute(mt_layer* l, int32_t enable) {
   });
 }
 
+extern "C" int mt_layer_set_step(mt_layer* l, uint64_t step) {
+  return guarded([&] {
+    if (!l) throw std::invalid_argument("null layer");
+    l->step = step;
+  });
+}
+
 extern "C" int mt_layer_launch_counts(const mt_layer* l, int32_t* f, int32_t* b) {
   return guarded([&] {
     *f = l->fwd_launches;
@@ -897,15 +904,19 @@ mt_layer::Saved& work_slot(mt_layer* l) {
   return *l->work;
 }
 
-void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t st, mt_layer::Saved& sv);
+// `mseed` = curator::step_seed(desc seed, training step): the seed the dropout sites derive from.
+void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, uint64_t mseed, cudaStream_t st,
+                  mt_layer::Saved& sv);
 
 void layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t st) {
   auto& slot = acquire_slot(l, mb);
   slot.x = x;
-  forward_into(l, x, y, mb, st, l->recompute ? work_slot(l) : slot);
+  slot.step = l->step;
+  forward_into(l, x, y, mb, curator::step_seed(l->d.seed, slot.step), st, l->recompute ? work_slot(l) : slot);
 }
 
-void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t st, mt_layer::Saved& sv) {
+void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, uint64_t mseed, cudaStream_t st,
+                  mt_layer::Saved& sv) {
   mt_ctx* c = l->ctx;
   tl_ctx = c;
   const mt_layer_desc& d = l->d;
@@ -925,9 +936,9 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
   const float scale_h = 1.f / (1.f - d.dropout_hidden), scale_a = 1.f / (1.f - d.dropout_attn);
   const uint32_t th_h = curator::dropout_threshold16(d.dropout_hidden);
   const uint32_t th_a = curator::dropout_threshold16(d.dropout_attn);
-  const uint64_t site_attn = key_of(d.seed, "attn.probs", d.layer_index, mb);
-  const uint64_t site_out1 = key_of(d.seed, "attn.out", d.layer_index, mb);
-  const uint64_t site_out2 = key_of(d.seed, "mlp.out", d.layer_index, mb);
+  const uint64_t site_attn = key_of(mseed, "attn.probs", d.layer_index, mb);
+  const uint64_t site_out1 = key_of(mseed, "attn.out", d.layer_index, mb);
+  const uint64_t site_out2 = key_of(mseed, "mlp.out", d.layer_index, mb);
   void* z = tp_buffer(c, 0);
   mark(c, st, "begin");
 
@@ -1037,27 +1048,30 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, cudaStream_t
   l->fwd_launches = n;
 }
 
-void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStream_t st, mt_layer::Saved& sv);
+void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, uint64_t mseed, cudaStream_t st,
+                   mt_layer::Saved& sv);
 
 void layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStream_t st) {
   auto it = l->saved.find(mb);
   if (it == l->saved.end()) throw std::invalid_argument("backward without a saved forward for this microbatch");
+  const uint64_t mseed = curator::step_seed(l->d.seed, it->second->step);  // the forward's masks
   if (l->recompute) {
     mt_layer::Saved& w = work_slot(l);
     const int fwd_n = l->fwd_launches;
-    forward_into(l, it->second->x, l->ctx->scratch_h[3].ptr, mb, st, w);  // regenerate the activations
+    forward_into(l, it->second->x, l->ctx->scratch_h[3].ptr, mb, mseed, st, w);  // regenerate the activations
     const int refwd = l->fwd_launches;
     l->fwd_launches = fwd_n;
-    backward_from(l, dy, dx, mb, st, w);
+    backward_from(l, dy, dx, mb, mseed, st, w);
     l->bwd_launches += refwd;
   } else {
-    backward_from(l, dy, dx, mb, st, *it->second);
+    backward_from(l, dy, dx, mb, mseed, st, *it->second);
   }
   l->free_slots.push_back(std::move(it->second));
   l->saved.erase(it);
 }
 
-void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStream_t st, mt_layer::Saved& sv) {
+void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, uint64_t mseed, cudaStream_t st,
+                   mt_layer::Saved& sv) {
   mt_ctx* c = l->ctx;
   tl_ctx = c;
   const mt_layer_desc& d = l->d;
@@ -1073,9 +1087,9 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, cudaStrea
   const float scale_h = 1.f / (1.f - d.dropout_hidden), scale_a = 1.f / (1.f - d.dropout_attn);
   const uint32_t th_h = curator::dropout_threshold16(d.dropout_hidden);
   const uint32_t th_a = curator::dropout_threshold16(d.dropout_attn);
-  const uint64_t site_attn = key_of(d.seed, "attn.probs", d.layer_index, mb);
-  const uint64_t site_out1 = key_of(d.seed, "attn.out", d.layer_index, mb);
-  const uint64_t site_out2 = key_of(d.seed, "mlp.out", d.layer_index, mb);
+  const uint64_t site_attn = key_of(mseed, "attn.probs", d.layer_index, mb);
+  const uint64_t site_out1 = key_of(mseed, "attn.out", d.layer_index, mb);
+  const uint64_t site_out2 = key_of(mseed, "mlp.out", d.layer_index, mb);
   void* dm = tp_buffer(c, 0);   // mlp-out grad, later attn-out grad (dz)
   void* dln = tp_buffer(c, 1);  // grad wrt LN2 / LN1 output
   void* dx1 = c->scratch_h[2].ptr;  // grad wrt residual stream x1

@@ -161,10 +161,14 @@ struct mt_layer {
   mt::DeviceBuffer grads;   // fp32
   struct Saved {
     const void* x = nullptr;
+    uint64_t step = 0;  // training step of the forward (keys the dropout masks the backward replays)
     mt::DeviceBuffer ln1, qkv, S, P, lse, ctx, x1, ln2, pre, act, stats;  // stats: mean1,rstd1,mean2,rstd2
   };
   std::map<uint32_t, std::unique_ptr<Saved>> saved;
   bool recompute = false;           // activation recompute (full-layer checkpointing)
+  // training step whose dropout masks the next forwards draw (curator::step_seed; set by the stage
+  // driver each iteration, mt_layer_set_step)
+  uint64_t step = 0;
   std::unique_ptr<Saved> work;      // recompute: the one set of intermediate buffers
   std::vector<std::unique_ptr<Saved>> free_slots;
   int fwd_launches = 0, bwd_launches = 0;

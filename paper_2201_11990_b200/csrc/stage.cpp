@@ -33,6 +33,9 @@ struct mt_stage {
   mt::DeviceBuffer target;                         // [M, h]
   mt::DeviceBuffer loss;                           // fp32 scalar
   int64_t launches = 0;
+  // training step of the next iteration: keys the dropout masks of every layer and of the embedding
+  // (curator::step_seed), so they change from one iteration to the next; incremented per iteration
+  uint64_t step = 0;
   // host-input path: all microbatches' H2D copies are queued up front on a copy stream and
   // overlap compute; each microbatch's first use waits on its own event
   cudaStream_t copy = nullptr;
@@ -400,8 +403,12 @@ void run_iteration(Step& k, mt_stage* st, void* stream) {
       ++k.launches;
     }
   }
-  for (auto* l : st->layers) ok(mt_layer_zero_grads(l, stream));
+  for (auto* l : st->layers) {
+    ok(mt_layer_zero_grads(l, stream));
+    ok(mt_layer_set_step(l, st->step));
+  }
   const bool vocab_here = k.lm() && (k.first() || k.last());
+  if (st->vocab) ok(mt_vocab_set_step(st->vocab, st->step));
   if (vocab_here) mt::vocab_zero_grads(st->vocab, k.s);
   mt::check_cuda(cudaMemsetAsync(st->loss.ptr, 0, 4, k.s), "memset loss");
   const int warmup = std::min(st->stages - st->stage - 1, MB);
@@ -492,7 +499,7 @@ void run_iteration(Step& k, mt_stage* st, void* stream) {
       ok(mt_dp_allreduce_f32(st->ctx, st->loss.as<float>(), 1, 1, stream));
       ++k.launches;
     }
-  }
+  }  ++st->step;
 }
 
 }  // namespace
@@ -597,6 +604,20 @@ extern "C" int mt_stage_attach_vocab(mt_stage* st, mt_vocab* v) {
       for (auto& b : st->tokens) b.ensure(tok_bytes);
     }
     // targets buffers (sized for bf16 activations) already hold M int32 ids
+  });
+}
+
+extern "C" int mt_stage_set_step(mt_stage* st, uint64_t step) {
+  return call([&] {
+    if (!st) throw std::invalid_argument("null stage");
+    st->step = step;
+  });
+}
+
+extern "C" int mt_stage_get_step(const mt_stage* st, uint64_t* step) {
+  return call([&] {
+    if (!st || !step) throw std::invalid_argument("null argument");
+    *step = st->step;
   });
 }
 

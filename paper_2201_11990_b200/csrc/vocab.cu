@@ -27,6 +27,7 @@ void set_error(const std::string& e);
 struct mt_vocab {
   mt_ctx* ctx = nullptr;
   mt_vocab_desc d{};
+  uint64_t step = 0;  // training step keying the embedding-dropout masks (curator::step_seed)
   int64_t vpad = 0, vp = 0, v0 = 0, M = 0, h = 0;
   mt::DeviceBuffer word, pos, lnf_g, lnf_b;        // bf16 params (word: [vp, h])
   mt::DeviceBuffer g_word, g_pos, g_lnf_g, g_lnf_b; // fp32 grads
@@ -338,6 +339,13 @@ void vocab_allreduce_grads(mt_vocab* v, ncclComm_t comm, bool word_only, bool av
 }
 }  // namespace mt
 
+extern "C" int mt_vocab_set_step(mt_vocab* v, uint64_t step) {
+  return call([&] {
+    if (!v) throw std::invalid_argument("null vocab");
+    v->step = step;
+  });
+}
+
 extern "C" int mt_vocab_zero_grads(mt_vocab* v, void* stream) {
   return call([&] { mt::vocab_zero_grads(v, (cudaStream_t)stream); });
 }
@@ -352,7 +360,7 @@ extern "C" int mt_vocab_embed_forward(mt_vocab* v, const int32_t* tokens, void* 
                                                                      v->v0, v->vp);
     if (tp_active(v))
       check_nccl(ncclAllReduce(x, x, int64_t{M} * h, ncclBfloat16, ncclSum, v->ctx->tp, s), "ncclAllReduce(embed)");
-    const uint64_t site = curator::site_seed(v->d.seed, "embed.dropout", 0, mb);
+    const uint64_t site = curator::site_seed(curator::step_seed(v->d.seed, v->step), "embed.dropout", 0, mb);
     embed_pos_dropout_kernel<<<dim3((h + 255) / 256, M), 256, 0, s>>>(
         (__nv_bfloat16*)x, (const __nv_bfloat16*)v->pos.ptr, h, v->d.seq, site,
         curator::dropout_threshold16(v->d.dropout), 1.f / (1.f - v->d.dropout));
@@ -365,7 +373,7 @@ extern "C" int mt_vocab_embed_backward(mt_vocab* v, const int32_t* tokens, const
   return call([&] {
     cudaStream_t s = (cudaStream_t)stream;
     const int h = (int)v->h, M = (int)v->M;
-    const uint64_t site = curator::site_seed(v->d.seed, "embed.dropout", 0, mb);
+    const uint64_t site = curator::site_seed(curator::step_seed(v->d.seed, v->step), "embed.dropout", 0, mb);
     embed_backward_kernel<<<dim3((h + 255) / 256, M), 256, 0, s>>>(
         tokens, (const __nv_bfloat16*)dx, v->g_word.as<float>(), v->g_pos.as<float>(), h, v->d.seq, v->v0, v->vp, site,
         curator::dropout_threshold16(v->d.dropout), 1.f / (1.f - v->d.dropout));

@@ -105,6 +105,10 @@ class Layer:
         """Sequence parallel: complete the TP-replicated parameters' gradients (collective over TP)."""
         check(lib().mt_layer_finish_grads(self._h, _stream(stream)))
 
+    def set_step(self, step: int) -> None:
+        """Training step keying the dropout masks of the next forwards (curator::step_seed)."""
+        check(lib().mt_layer_set_step(self._h, step))
+
     def launch_counts(self) -> tuple[int, int]:
         f, b = C.c_int32(), C.c_int32()
         check(lib().mt_layer_launch_counts(self._h, C.byref(f), C.byref(b)))
@@ -196,6 +200,15 @@ class Stage:
         a, b = C.c_int64(), C.c_int64()
         check(lib().mt_stage_host_traffic(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def set_step(self, step: int) -> None:
+        """Training step of the next iteration (dropout masks; +1 per train_step)."""
+        check(lib().mt_stage_set_step(self._h, step))
+
+    def step(self) -> int:
+        v = C.c_uint64()
+        check(lib().mt_stage_get_step(self._h, C.byref(v)))
+        return v.value
 
     def set_micro_batches(self, n: int) -> None:
         """Microbatches of the next iterations (<= the count the stage was created with)."""

@@ -161,3 +161,38 @@ def test_activation_recompute_is_bit_identical(fused, monkeypatch):
     assert (y0 == y1).all() and (dx0 == dx1).all()
     for a, b in zip(g0, g1):
         assert (a == b).all()
+
+
+def test_dropout_masks_follow_the_training_step():
+    """ADVICE r1: masks are keyed by curator::step_seed(seed, step) so they change every iteration; a
+    layer at step 3 matches the oracle run with that seed, and differs from step 0."""
+    hidden, heads, seq, mb = 256, 4, 128, 2
+    ctx = Context(0)
+    layer = Layer(ctx, PL.layer_desc(hidden, heads, seq, mb, dropout_hidden=0.1, dropout_attn=0.1, seed=SEED,
+                                     layer_index=2))
+    params = O.init_params(hidden, SEED, 2)
+    keep = [np.ascontiguousarray(O.to_bf16_bits(p)) for p in params]
+    for i, b in enumerate(keep):
+        layer.set_param(i, b.ctypes.data)
+    x = O.normal(O.site_seed(SEED, "input", 0, 0), mb * seq, hidden)
+    g = O.normal(O.site_seed(SEED, "grad", 0, 0), mb * seq, hidden, std=1e-2)
+    xd, gd = bf16_tensor(x), bf16_tensor(g)
+    s = torch.cuda.current_stream()
+    ys = {}
+    for step in (0, 3):
+        yd, dxd = torch.empty_like(xd), torch.empty_like(xd)
+        layer.set_step(step)
+        layer.zero_grads(s)
+        layer.forward(xd.data_ptr(), yd.data_ptr(), 0, s)
+        layer.set_step(99)  # the backward replays the forward's masks whatever the current step
+        layer.backward(gd.data_ptr(), dxd.data_ptr(), 0, s)
+        torch.cuda.synchronize()
+        ol = O.OracleLayer(hidden, heads, seq, mb, 1, dropout_hidden=0.1, dropout_attn=0.1,
+                           seed=O.step_seed(SEED, step), layer_index=2, bf16_emulate=True, params=params)
+        y_ref, dx_ref = ol.forward(x), ol.backward(g)
+        assert rel(to_np(yd), y_ref) < 5e-3 and rel(to_np(dxd), dx_ref) < 1e-2, step
+        ys[step] = to_np(yd)
+    assert rel(ys[3], ys[0]) > 1e-2
+    assert O.step_seed(SEED, 0) == SEED and O.step_seed(SEED, 3) != SEED
+    layer.close()
+    ctx.close()

@@ -127,6 +127,7 @@ def test_lm_stage_matches_manual_composition():
 
     # device-resident token path: same iteration, same loss
     loss_dev = torch.zeros(1, device="cuda")
+    st.set_step(0)  # replay the host-input iteration (same dropout masks)
     st.train_step_dev(tok_d.data_ptr(), tgt_d.data_ptr(), loss_dev.data_ptr(), s)
     torch.cuda.synchronize()
     assert abs(float(loss_dev.item()) - loss) <= 1e-6 * abs(loss)

@@ -200,7 +200,8 @@ def _worker(rank, world, port, mode, q):
             ts = np.stack([O.normal(O.site_seed(SEED, "target", 0, gi), B * S, H) for gi in gids])
             xh = torch.from_numpy(O.to_bf16_bits(xs).view(np.int16)).pin_memory()
             th = torch.from_numpy(O.to_bf16_bits(ts).view(np.int16)).pin_memory()
-            for _ in range(2):  # the second iteration must reproduce the first (grads re-zeroed)
+            for _ in range(2):  # replaying step 0, the second iteration must reproduce the first (grads re-zeroed)
+                st.set_step(0)
                 loss = st.train_step(xh.data_ptr(), th.data_ptr(), s)
             out["loss"], out["place"] = loss, (place.data, place.pipeline, place.tensor)
             out["h2d"] = st.host_traffic()[0]

@@ -120,3 +120,32 @@ def test_normal_stream_statistics_and_determinism():
     b = O.normal(12345, 512, 512, round_bf16=False)
     assert (a == b).all()
     assert abs(a.mean()) < 0.01 and abs(a.std() - 1) < 0.01
+
+
+def test_shard_init_matches_full_init_on_the_shard():
+    """init_params(shard=...) draws exactly the shard's region of the full init (the rest zero)."""
+    h, H, t = 256, 4, 2
+    full = O.init_params(h, 7, 1)
+    for r in range(t):
+        part = O.init_params(h, 7, 1, shard=(H, t, r))
+        for i in range(12):
+            r0, c0, nr, nc = O.shard_region(i, h, H, t, r)
+            assert np.array_equal(part[i][r0:r0 + nr, c0:c0 + nc], full[i][r0:r0 + nr, c0:c0 + nc])
+            mask = np.ones_like(full[i], bool)
+            mask[r0:r0 + nr, c0:c0 + nc] = False
+            assert not part[i][mask].any()
+
+
+def test_oracle_shard_mode_sums_to_the_full_layer_without_dropout():
+    """Shard mode at TP=1 (one shard = the whole layer, nothing to all-reduce) is the full layer bit for bit;
+    at TP>1 it is checked against the GPU's shard-only mode (tests/test_parity_bench.py)."""
+    h, H, s = 256, 4, 64
+    x = O.normal(O.site_seed(3, "input", 0, 0), s, h)
+    g = O.normal(O.site_seed(3, "grad", 0, 0), s, h, std=1e-2)
+    params = O.init_params(h, 3, 0)
+    a = O.OracleLayer(h, H, s, 1, 1, seed=3, params=params)
+    b = O.OracleLayer(h, H, s, 1, 1, seed=3, params=params, shard_rank=0)
+    assert np.array_equal(a.forward(x), b.forward(x))
+    assert np.array_equal(a.backward(g), b.backward(g))
+    for ga, gb in zip(a.grads, b.grads):
+        assert np.array_equal(ga, gb)

@@ -42,11 +42,13 @@ def test_host_input_iteration_equals_device_input_iteration(chunks, monkeypatch)
     x = torch.randn(MB, B * S, H, generator=g).to(torch.bfloat16)
     t = torch.randn(MB, B * S, H, generator=g).to(torch.bfloat16)
     xd, td, loss_d = x.cuda(), t.cuda(), torch.zeros(1, device="cuda")
+    st.set_step(0)
     st.train_step_dev(xd.data_ptr(), td.data_ptr(), loss_d.data_ptr(), s)
     torch.cuda.synchronize()
     want_loss, want = float(loss_d.item()), grads(st, L)
     xh, th = x.pin_memory(), t.pin_memory()
     for _ in range(2):
+        st.set_step(0)  # replay the device-input iteration's dropout masks
         loss = st.train_step(xh.data_ptr(), th.data_ptr(), s)
     assert abs(loss - want_loss) <= 1e-5 * abs(want_loss), (loss, want_loss)
     for a, b in zip(grads(st, L), want):
