@@ -117,6 +117,15 @@ int mt_ctx_destroy(mt_ctx* ctx);
 int mt_nccl_unique_id(unsigned char out[128]);
 int mt_ctx_init_comm(mt_ctx* ctx, const unsigned char id[128], int32_t world_size, int32_t rank,
                      const mt_parallel_config* par);
+/* Bounded wait for the work queued on `stream` (use it instead of a plain stream sync after the
+ * asynchronous mt_stage_train_step_dev when peers are involved). Every cross-rank wait of the runtime
+ * is bounded by MT_COMM_TIMEOUT_S (default 300 s): device-side spins of the fused / NVLS all-reduce
+ * kernels raise the context's error flag, and this wait (also used by mt_stage_train_step) aborts
+ * the NCCL communicators on the deadline, a device timeout or an NCCL async error and returns 2. */
+int mt_ctx_wait(mt_ctx* ctx, void* stream);
+/* 0 = healthy, 1 = a device-side peer wait timed out, 2 = the host aborted the iteration,
+ * 3 = communicators aborted (the context can no longer communicate: destroy it). */
+int mt_ctx_error(const mt_ctx* ctx, int32_t* state);
 int mt_ctx_placement(const mt_ctx* ctx, mt_rank_placement* out);
 /* Single-process measurement of ONE tensor-parallel shard (layers created with tp_size > 1): the
  * layers run their shard's kernels and skip the TP all-reduces. Compute-only numbers; the

@@ -28,11 +28,7 @@ enum mt_epilogue {
   MT_EPI_BIAS_GELU = 1,    /* aux = bf16(acc + bias[n]) (pre-activation), D = bf16(gelu(aux))   */
   MT_EPI_GELU_BWD = 2,     /* D = bf16(acc * gelu'(aux[m][n]))   (aux = saved pre-activation)    */
   MT_EPI_STORE_F32 = 3,    /* D(f32) = alpha*acc                                                */
-  MT_EPI_ACCUM_F32 = 4,    /* D(f32) += alpha*acc   (fp32 gradient accumulation across microbatches) */
-  MT_EPI_STORE_BF16_ROWSTATS = 5 /* D = bf16(alpha*acc), plus per (row, BN-column block) softmax statistics
-                                    of the stored values: aux = float2 [batch][m][ld_aux] {max, sum exp(x - max)}
-                                    over the block's columns (causal modes: columns <= row only); requires
-                                    block_n = 128 or 256 and ld_aux >= ceil(n / block_n) */
+  MT_EPI_ACCUM_F32 = 4     /* D(f32) += alpha*acc   (fp32 gradient accumulation across microbatches) */
 };
 
 enum mt_causal {
@@ -43,32 +39,30 @@ enum mt_causal {
 };
 
 /* Fused all-reduce of the output over a tensor-parallel group (NVLink SHARP / multimem): every rank
- * launches the same GEMM on its partial operands with d in symmetric memory; each 128-row x BN output
- * unit is published with a flag once stored, and its owner rank (round-robin over units) sums all
- * ranks' copies with multimem.ld_reduce (fp32 accumulation, one rounding) and writes the sum to every
- * rank with multimem.st from its epilogue warps while the tensor cores continue with later tiles.
- * mt_gemm_allreduce_wait(counter, target) then orders the consumers after all units of all ranks.
- * Requirements: STORE_BF16 epilogue, batch 1, no causal mode; d is the local address of offset 0 of
- * the symmetric buffer whose multicast address is d_multicast. */
+ * launches the same GEMM on its partial operands with d in symmetric memory. The GEMM counts each
+ * finished 128-row x BN output unit on its column group's local counter (column blocks complete in
+ * raster order); mt_gemm_allreduce_reduce_groups, running concurrently on the SMs the GEMM leaves free
+ * (max_ctas), waits per group for this rank's GEMM and a cross-rank barrier, then sums this rank's
+ * 1/ranks of the group's rows over all ranks with multimem.ld_reduce (fp32 accumulation, one rounding)
+ * and writes the sum to every rank with multimem.st — so all but the last group's reduction overlap
+ * the GEMM. mt_gemm_allreduce_wait(counter, target) then orders the consumers after every rank's
+ * reducer. Every cross-rank wait is bounded by timeout_ns: a peer that never arrives raises
+ * *error_flag and the kernels finish (with undefined data) instead of wedging the GPU.
+ * Requirements: STORE_BF16 epilogue, batch 1, no causal mode, M a multiple of ranks, m-fastest raster
+ * (M <= N); d is the local address of offset 0 of the symmetric buffer whose multicast address is
+ * d_multicast. */
 typedef struct mt_gemm_allreduce {
   void* d_multicast;             /* multicast address of d */
-  uint32_t* flags_local;         /* this rank's per-unit ready flags (symmetric memory) */
-  const uint32_t* flags_peer[8]; /* each rank's flag array, load/store accessible, by rank */
+  uint32_t* group_counters;      /* local per-group unit counters, zeroed before each launch (<= 64) */
   uint32_t* counter_multicast;   /* multicast address of the per-rank completion counter */
-  int64_t flag_capacity;         /* units the flag arrays can hold */
-  uint32_t epoch;                /* larger than every epoch used before on these flags */
   int32_t rank, ranks;
-  int32_t reduce_in_epilogue;    /* 1: the GEMM's epilogue warps reduce the owned units; 0: the GEMM only
-                                    publishes them and mt_gemm_allreduce_reduce (a concurrent kernel on
-                                    the SMs the GEMM leaves free, max_ctas) reduces them */
-  int32_t groups;                /* > 0: column-group mode — the GEMM counts finished units per group of
-                                    column blocks on flags_local[g] (zeroed by the caller before the
-                                    launch) and mt_gemm_allreduce_reduce_groups reduces group by group */
-  int64_t units;                 /* out: number of output units of this launch (counter increments) */
-  int64_t geom[8];               /* out: unit geometry of the launch, read by mt_gemm_allreduce_reduce */
-  int64_t group_cols;            /* out: column blocks per group (0: group mode not applicable) */
+  int32_t groups;                /* column groups (1..64) */
+  uint32_t* error_flag;          /* host-mapped word raised on a peer timeout (may be NULL) */
+  uint64_t timeout_ns;           /* bound of every cross-rank wait (> 0) */
+  int64_t units;                 /* out: number of output units of this launch */
+  int64_t geom[8];               /* out: unit geometry of the launch, read by the reducer */
+  int64_t group_cols;            /* out: column blocks per group */
 } mt_gemm_allreduce;
-
 typedef struct mt_gemm_args {
   const void* a;
   int64_t lda, a_batch_stride;
@@ -105,15 +99,9 @@ int mt_gemm(const mt_gemm_args* args, void* stream);
  * one exit per CTA. Counter after the launch = base + ranks * groups + ranks * ctas. */
 int mt_gemm_allreduce_reduce_groups(const mt_gemm_allreduce* ar, int64_t ldd, uint32_t* group_counters,
                                     const uint32_t* counter_local, uint32_t base, int32_t ctas, void* stream);
-/* Stream-ordered wait until the local completion counter reaches `target` (all units of all ranks of
- * the fused all-reduce launches so far); 1 launch. */
-int mt_gemm_allreduce_wait(const uint32_t* counter_local, uint32_t target, void* stream);
-/* Reducer for a launch with reduce_in_epilogue = 0: `ctas` CTAs reduce this rank's owned units in
- * publication order as the GEMM (running concurrently, e.g. on another stream) publishes them, then
- * wait until the local counter reaches `target`. 1 launch. */
-int mt_gemm_allreduce_reduce(const mt_gemm_allreduce* ar, void* d, int64_t ldd, const uint32_t* counter_local,
-                             uint32_t target, int32_t ctas, void* stream);
-
+/* Stream-ordered (bounded) wait until the local completion counter reaches `target`; 1 launch. */
+int mt_gemm_allreduce_wait(const mt_gemm_allreduce* ar, const uint32_t* counter_local, uint32_t target,
+                           void* stream);
 /* Number of kernel launches mt_gemm issues per call (always 1). */
 int mt_gemm_launches_per_call(void);
 

@@ -26,7 +26,7 @@ class GemmArgs(C.Structure):
     ]
 
 
-EPI_STORE_BF16, EPI_BIAS_GELU, EPI_GELU_BWD, EPI_STORE_F32, EPI_ACCUM_F32, EPI_STORE_BF16_ROWSTATS = range(6)
+EPI_STORE_BF16, EPI_BIAS_GELU, EPI_GELU_BWD, EPI_STORE_F32, EPI_ACCUM_F32 = range(5)
 CAUSAL_NONE, CAUSAL_SKIP_UPPER_TILES, CAUSAL_K_LE_M, CAUSAL_K_GE_M = range(4)
 
 
@@ -88,8 +88,7 @@ PI32, PI64, PF32, PF64 = C.POINTER(I32), C.POINTER(I64), C.POINTER(F32), C.POINT
 _SIGS = {
     "mt_gemm": (C.c_int, [C.POINTER(GemmArgs), P]),
     "mt_gemm_launches_per_call": (C.c_int, []),
-    "mt_gemm_allreduce_wait": (C.c_int, [P, U32, P]),
-    "mt_gemm_allreduce_reduce": (C.c_int, [P, P, I64, P, U32, I32, P]),
+    "mt_gemm_allreduce_wait": (C.c_int, [P, P, U32, P]),
     "mt_gemm_allreduce_reduce_groups": (C.c_int, [P, I64, P, P, U32, I32, P]),
     "mt_last_error": (C.c_char_p, []),
     "mt_version": (C.c_char_p, []),
@@ -115,6 +114,8 @@ _SIGS = {
     "mt_ctx_init_comm": (C.c_int, [P, C.c_char_p, I32, I32, C.POINTER(ParallelConfig)]),
     "mt_ctx_placement": (C.c_int, [P, C.POINTER(RankPlacement)]),
     "mt_ctx_shard_only": (C.c_int, [P, I32]),
+    "mt_ctx_wait": (C.c_int, [P, P]),
+    "mt_ctx_error": (C.c_int, [P, PI32]),
     "mt_ctx_set_sequence_parallel": (C.c_int, [P, I32]),
     "mt_layer_finish_grads": (C.c_int, [P, P]),
     "mt_ctx_nvls_probe": (C.c_int, [P, I64, I64, I32, I32, I32, PF64]),

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -45,22 +46,15 @@ struct GemmParams {
   const __nv_bfloat16* bias;
   __nv_bfloat16* aux;
   long long ld_aux;
-  float2* row_stats;  // MT_EPI_STORE_BF16_ROWSTATS: [batch][m][ld_aux]
   // split-K tail: work items [0, full_tiles) are whole tiles; the remaining total_tiles - full_tiles
   // tiles (fewer than one wave) are each split over `splits` k-ranges run by otherwise idle CTAs.
   int full_tiles, splits, work_items;
   float* split_ws;  // fp32 partial tiles [tail][split][rank][128 x BN]
   int* split_cnt;   // arrival counters [tail][rank], self-resetting
-  // fused TP all-reduce of D (mt_gemm_allreduce); ar_ranks == 0 disables
-  __nv_bfloat16* ar_mc;
-  uint32_t* ar_flags;
-  const uint32_t* ar_peer[8];
-  uint32_t* ar_counter_mc;
-  uint32_t ar_epoch;
-  int ar_rank, ar_ranks;
-  int ar_debug;  // MT_AR_DEBUG (measurement only): 1 = skip the data movement, 2 = skip the peer wait
-  int ar_in_epi;    // 1: the epilogue warps reduce owned units; 0: publish only (mt_gemm_allreduce_reduce)
-  int ar_group_cols;  // > 0: publish per group of column blocks (local counters) instead of per-unit flags
+  // fused TP all-reduce of D (mt_gemm_allreduce): every finished output unit is counted on its
+  // column group's local counter (ar_group_cols column blocks per group); 0 disables
+  uint32_t* ar_group_cnt;
+  int ar_group_cols;
   uint64_t store_policy;  // L2 hint on fp32 output stores (0 = none)
 };
 
@@ -208,182 +202,26 @@ __device__ __forceinline__ void reuse_wait(uint32_t lane) {
   __syncwarp();
 }
 
-// Fused TP all-reduce of the output, run by the 128 epilogue threads after a unit's (this CTA's
-// 128 rows x BN of tile w) TMA stores were issued and its TMEM buffer released, so the MMA of the
-// next tile proceeds meanwhile:
-//   publish: wait until the unit's stores are complete, flag[unit] = epoch (system-scope release);
-//   reduce (owner rank = unit % ranks, deferred by up to two owned units so the peers' flags are
-//   normally already set): wait for every peer's flag, sum the ranks' copies with
-//   multimem.ld_reduce (fp32 accumulate) and write the sum to all ranks with multimem.st, then count
-//   the unit on every rank's completion counter (multimem.red.release).
-// Every rank runs the same persistent schedule and publishes a unit before it waits for any, so an
-// owner only ever waits for units its peers publish unconditionally (no cyclic dependency).
-struct ArUnit {
-  int w = -1, mb = 0, nb = 0;
-};
-
-template <bool kPair>
-__device__ __forceinline__ int ar_unit_id(int w, uint32_t cta_rank) {
-  return kPair ? 2 * w + (int)cta_rank : w;
-}
-
-// Publish unit `w` once its stores are complete. kPending = bulk groups of later tiles that may still
-// be in flight (the stores of the tile issued after w), so the epilogue never waits on its newest
-// stores.
-template <bool kPair, int kPending>
-__device__ __forceinline__ void ar_publish(const GemmParams& p, int w, uint32_t cta_rank, uint32_t lane) {
+// Fused TP all-reduce of the output (column-group mode): once all TMA stores of output unit w (this
+// CTA's 128 rows x BN of a tile) are complete, the unit is counted on its column group's local
+// counter with a gpu-scope release. Column blocks finish in raster order (m-blocks fastest), so the
+// reducer kernel (allreduce_group_kernel, on the SMs the GEMM leaves free) can start the cross-rank
+// NVLink-SHARP reduction of group g while the tensor cores still work on later groups. kPending =
+// bulk groups of the tile issued after w that may still be in flight (never waited on here).
+template <int kPending>
+__device__ __forceinline__ void ar_publish(const GemmParams& p, int w, uint32_t lane) {
   if (lane == 0) bulk_wait<kPending>();
   __syncwarp();
   epi_bar();
   if (threadIdx.x == 128) {
     fence_proxy_async_global();
-    if (p.ar_group_cols > 0) {  // count the unit on its column group's (local) counter
-      int b, mb, nb;
-      tile_coords(p, w, b, mb, nb);
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.ar_flags + nb / p.ar_group_cols) : "memory");
-    } else {
-      st_release_sys_u32(p.ar_flags + ar_unit_id<kPair>(w, cta_rank), p.ar_epoch);
-    }
+    int b, mb, nb;
+    tile_coords(p, w, b, mb, nb);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.ar_group_cnt + nb / p.ar_group_cols) : "memory");
   }
 }
-
-template <int BN, int BMT, bool kPair>
-__device__ __forceinline__ void ar_reduce(const GemmParams& p, const ArUnit& u, uint32_t cta_rank) {
-  const int unit = ar_unit_id<kPair>(u.w, cta_rank);
-  if (threadIdx.x == 128 && p.ar_debug != 2) {
-    for (int r = 0; r < p.ar_ranks; ++r) {
-      if (r == p.ar_rank) continue;
-      while ((int)(ld_acquire_sys_u32(p.ar_peer[r] + unit) - p.ar_epoch) < 0) {
-      }
-    }
-    fence_acq_rel_sys();
-  }
-  epi_bar();
-  const int row0 = u.mb * BMT + (int)cta_rank * kBM;
-  const int rows = min(kBM, p.m - row0);
-  const int col0 = u.nb * BN;
-  const int cpr = min(BN, p.n - col0) / 8;  // 16-byte chunks per row
-  const int total = (rows > 0 && p.ar_debug != 1) ? rows * cpr : 0;
-  const int tid = (int)threadIdx.x - 128;
-  constexpr int U = 8;
-#pragma unroll 1
-  for (int base = tid; base < total; base += 128 * U) {
-    uint32_t v[U][4];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int i = base + k * 128;
-      if (i < total) {
-        const int r = i / cpr, c = i - r * cpr;
-        multimem_ld_reduce_bf16x8(p.ar_mc + (long long)(row0 + r) * p.ldd + col0 + c * 8, v[k]);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int i = base + k * 128;
-      if (i < total) {
-        const int r = i / cpr, c = i - r * cpr;
-        multimem_st_bf16x8(p.ar_mc + (long long)(row0 + r) * p.ldd + col0 + c * 8, v[k]);
-      }
-    }
-  }
-  epi_bar();
-}
-
-// Reducer of the publish-only mode. Each warp owns whole units (round-robin over the units this rank
-// owns, in publication order) and progresses independently: its lanes poll the ranks' flags, then it
-// streams the unit through multimem.ld_reduce / multimem.st with 8 x 16 B in flight per lane — the
-// same access pattern as a plain NVLS all-reduce (tools/nvls_probe.py: ~390-455 GB/s algbw at
-// TP=2-4 with 16 CTAs), with no CTA-wide synchronisation between units. Each CTA counts its units
-// on every rank's counter with one system-scope release at the end; CTA 0 then waits until the local
-// counter shows all units of all ranks.
-struct ArReduceParams {
-  __nv_bfloat16* mc;
-  const uint32_t* flags[8];
-  uint32_t* counter_mc;
-  const uint32_t* counter_local;
-  uint32_t epoch, target;
-  int rank, ranks;
-  int bn, tile_m, pair, n_fastest, mblocks, nblocks, m, n;
-  long long ldd;
-  int debug;  // MT_AR_DEBUG=2: skip the flag waits (measurement only)
-};
 
 constexpr int kReduceThreads = 1024;
-
-__global__ void __launch_bounds__(kReduceThreads, 1) allreduce_reduce_kernel(const ArReduceParams p) {
-  const int units = p.mblocks * p.nblocks * (p.pair ? 2 : 1);
-  const int mine = (units - p.rank + p.ranks - 1) / p.ranks;  // units u = rank + k * ranks
-  const int lane = (int)(threadIdx.x & 31);
-  const int gwarp = (int)blockIdx.x * (kReduceThreads / 32) + (int)(threadIdx.x >> 5);
-  const int nwarps = (int)gridDim.x * (kReduceThreads / 32);
-  int done = 0;
-  for (int k = gwarp; k < mine; k += nwarps) {
-    const int u = p.rank + k * p.ranks;
-    const int w = p.pair ? (u >> 1) : u, cr = p.pair ? (u & 1) : 0;
-    if (lane < p.ranks && p.debug != 2) {
-      while ((int)(ld_acquire_sys_u32(p.flags[lane] + u) - p.epoch) < 0) {
-      }
-    }
-    __syncwarp();
-    int mb, nb;
-    if (p.n_fastest) {
-      mb = w / p.nblocks;
-      nb = w - mb * p.nblocks;
-    } else {
-      nb = w / p.mblocks;
-      mb = w - nb * p.mblocks;
-    }
-    const int row0 = mb * p.tile_m + cr * kBM;
-    const int rows = min(kBM, p.m - row0);
-    const int col0 = nb * p.bn;
-    const int cpr = min(p.bn, p.n - col0) / 8;
-    __nv_bfloat16* base_ptr = p.mc + (long long)row0 * p.ldd + col0;
-    constexpr int U = 8;
-    if (cpr == 32) {  // full 256-wide unit: lane = 16-byte column chunk, one row per (iteration, k)
-#pragma unroll 1
-      for (int r0 = 0; r0 < rows; r0 += U) {
-        uint32_t v[U][4];
-#pragma unroll
-        for (int k2 = 0; k2 < U; ++k2)
-          if (r0 + k2 < rows) multimem_ld_reduce_bf16x8(base_ptr + (long long)(r0 + k2) * p.ldd + lane * 8, v[k2]);
-#pragma unroll
-        for (int k2 = 0; k2 < U; ++k2)
-          if (r0 + k2 < rows) multimem_st_bf16x8(base_ptr + (long long)(r0 + k2) * p.ldd + lane * 8, v[k2]);
-      }
-    } else {
-      const int total = rows > 0 ? rows * cpr : 0;
-#pragma unroll 1
-      for (int base = lane; base < total; base += 32 * U) {
-        uint32_t v[U][4];
-#pragma unroll
-        for (int k2 = 0; k2 < U; ++k2) {
-          const int i = base + k2 * 32;
-          if (i < total) multimem_ld_reduce_bf16x8(base_ptr + (long long)(i / cpr) * p.ldd + (i % cpr) * 8, v[k2]);
-        }
-#pragma unroll
-        for (int k2 = 0; k2 < U; ++k2) {
-          const int i = base + k2 * 32;
-          if (i < total) multimem_st_bf16x8(base_ptr + (long long)(i / cpr) * p.ldd + (i % cpr) * 8, v[k2]);
-        }
-      }
-    }
-    ++done;
-  }
-  // one system-scope release for all of this CTA's units
-  __shared__ int cta_done;
-  if (threadIdx.x == 0) cta_done = 0;
-  __syncthreads();
-  if (lane == 0 && done > 0) atomicAdd(&cta_done, done);
-  __syncthreads();
-  if (threadIdx.x == 0 && cta_done > 0) {
-    fence_acq_rel_sys();
-    multimem_red_release_add_u32(p.counter_mc, (uint32_t)cta_done);
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    while ((int)(ld_acquire_sys_u32(p.counter_local) - p.target) < 0) {
-    }
-  }
-}
 
 // Reducer of the column-group mode: groups of column blocks complete in order in the GEMM; for each
 // group, wait until this rank's GEMM published all its units (local counter), then a cross-rank
@@ -397,6 +235,8 @@ struct ArGroupParams {
   uint32_t base;              // counter value before this launch
   int rank, ranks, groups, group_cols, bn, m, n, mblocks, units_per_block;
   long long ldd;
+  uint32_t* err;              // peer-timeout flag (bounded_wait_geq)
+  unsigned long long timeout_ns;
 };
 
 __global__ void __launch_bounds__(kReduceThreads, 1) allreduce_group_kernel(const ArGroupParams p) {
@@ -406,14 +246,12 @@ __global__ void __launch_bounds__(kReduceThreads, 1) allreduce_group_kernel(cons
     if (cb0 >= cb1) break;
     if (threadIdx.x == 0) {
       const uint32_t expect = (uint32_t)((cb1 - cb0) * p.mblocks * p.units_per_block);
-      while (ld_acquire_gpu_u32(p.group_cnt + g) < expect) {
-      }
+      bounded_wait_geq<false>(p.group_cnt + g, expect, p.err, p.timeout_ns);  // this rank's GEMM (same GPU)
       if (blockIdx.x == 0) {
         fence_acq_rel_sys();
         multimem_red_release_add_u32(p.counter_mc, 1u);
       }
-      while ((int)(ld_acquire_sys_u32(p.counter_local) - (p.base + (uint32_t)(p.ranks * (g + 1)))) < 0) {
-      }
+      bounded_wait_geq<true>(p.counter_local, p.base + (uint32_t)(p.ranks * (g + 1)), p.err, p.timeout_ns);
     }
     __syncthreads();
     const int c0 = cb0 * p.bn, c1 = min(cb1 * p.bn, p.n);
@@ -448,9 +286,9 @@ __global__ void __launch_bounds__(kReduceThreads, 1) allreduce_group_kernel(cons
   }
 }
 
-__global__ void allreduce_wait_kernel(const uint32_t* counter, uint32_t target) {
-  while ((int)(ld_acquire_sys_u32(counter) - target) < 0) {
-  }
+__global__ void allreduce_wait_kernel(const uint32_t* counter, uint32_t target, uint32_t* err,
+                                      unsigned long long timeout_ns) {
+  bounded_wait_geq<true>(counter, target, err, timeout_ns);
 }
 
 template <int BN, bool kAMN, bool kBMN, bool kPair, bool kAR>
@@ -608,10 +446,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool f32 = ep == MT_EPI_STORE_F32 || ep == MT_EPI_ACCUM_F32;
     const float alpha = p.alpha;
     uint32_t it = 0;
-    // fused all-reduce: the previous tile (published after this tile's stores were issued) and up to
-    // two owned units whose reductions are deferred so the peers' flags are normally already set
-    int unpublished = -1, reduced = 0;
-    ArUnit pending[2];
+    // fused all-reduce: the previous tile, published once this tile's stores were issued
+    int unpublished = -1;
     for (int w = t_first; w < p.work_items; w += t_stride) {
       Work wk;
       if (!get_work<BN, BMT>(p, w, wk)) continue;
@@ -623,7 +459,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = row0 + lane;
       const uint32_t tmem_row = tmem_base + ((quad * 32) << 16) + acc * C::kAccStride;
       const float* parts = nullptr;  // split-K: this CTA's partial tiles of the tail tile
-      float st_m = -INFINITY, st_l = 0.f;  // ROWSTATS: running max / sum of exp over this tile's columns
       if (wk.split >= 0) {
         // Publish this split's raw partial (rows of this thread), then count arrivals; the last
         // arriving split reduces the others' partials into its accumulator and runs the epilogue.
@@ -674,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int col0 = nb * BN + c2 * 64;
           if (col0 >= p.n) break;
           float x[64];
-          {
+          if (parts == nullptr) {
             uint32_t ra[32], rb[32];
             tmem_ld_32x32b_x32(tmem_row + c2 * 64, ra);
             tmem_ld_32x32b_x32(tmem_row + c2 * 64 + 32, rb);
@@ -684,10 +519,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               x[j] = __uint_as_float(ra[j]);
               x[32 + j] = __uint_as_float(rb[j]);
             }
-          }
-          if (parts != nullptr) {
+          } else {
+            // split-K tail: the fixed-order sum of every split's published partial (this split's own
+            // included), so the result does not depend on which split arrived last
+#pragma unroll
+            for (int j = 0; j < 64; ++j) x[j] = 0.f;
             for (int sp = 0; sp < p.splits; ++sp) {
-              if (sp == wk.split) continue;
               const float* q = parts + (size_t)sp * 2 * (128 * BN) + c2 * 64;
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
@@ -701,29 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
 #pragma unroll
           for (int j = 0; j < 64; ++j) x[j] *= alpha;
-          if (ep == MT_EPI_STORE_BF16_ROWSTATS) {
-            constexpr float kL2e = 1.4426950408889634f;
-#pragma unroll
-            for (int j = 0; j < 64; j += 2) {
-              const float2 pr = unpack_bf16x2(pack_bf16x2(x[j], x[j + 1]));
-              x[j] = pr.x;
-              x[j + 1] = pr.y;
-            }
-            const int lim = (p.causal != MT_CAUSAL_NONE) ? min(p.n, row + 1) : p.n;
-            float pm = -INFINITY;
-#pragma unroll
-            for (int j = 0; j < 64; ++j)
-              if (col0 + j < lim) pm = fmaxf(pm, x[j]);
-            if (pm > -INFINITY) {
-              const float mn = fmaxf(st_m, pm), mn2 = mn * kL2e;
-              float sum = 0.f;
-#pragma unroll
-              for (int j = 0; j < 64; ++j)
-                if (col0 + j < lim) sum += ex2_fast(fmaf(x[j], kL2e, -mn2));
-              st_l = st_l * ex2_fast((st_m - mn) * kL2e) + sum;
-              st_m = mn;
-            }
-          } else if (ep == MT_EPI_STORE_BF16 || ep == MT_EPI_BIAS_GELU) {
+          if (ep == MT_EPI_STORE_BF16 || ep == MT_EPI_BIAS_GELU) {
             if (p.bias != nullptr) {
 #pragma unroll
               for (int v = 0; v < 8; ++v) {
@@ -779,15 +594,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = c_begin; c < BN / 32; ++c) {
         const int col0 = nb * BN + c * 32;
         if (col0 >= p.n) break;
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_row + c * 32, r);
-        tmem_ld_wait();
         float x[32];
+        if (parts == nullptr) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_row + c * 32, r);
+          tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
-        if (parts != nullptr) {
+          for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
+        } else {  // split-K tail: fixed-order sum of all splits' partials (see the 64-column path)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) x[j] = 0.f;
           for (int sp = 0; sp < p.splits; ++sp) {
-            if (sp == wk.split) continue;
             const float* q = parts + (size_t)sp * 2 * (128 * BN) + c * 32;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -808,42 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           bi = (bi + 1) % C::kEpiBufs;
           continue;
         }
-        if (ep == MT_EPI_STORE_BF16_ROWSTATS) {
-          // statistics of the values as stored (bf16-rounded), causal columns <= row only; pieces wholly
-          // below the diagonal (every lane's row >= the piece's last column) skip the per-column test
-          constexpr float kL2e = 1.4426950408889634f;
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const float2 pr = unpack_bf16x2(pack_bf16x2(x[j], x[j + 1]));
-            x[j] = pr.x;
-            x[j + 1] = pr.y;
-          }
-          const bool causal = p.causal != MT_CAUSAL_NONE;
-          const int lim = causal ? min(p.n, row + 1) : p.n;
-          float pm = -INFINITY;
-          if (col0 + 32 <= lim) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) pm = fmaxf(pm, x[j]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < lim) pm = fmaxf(pm, x[j]);
-          }
-          if (pm > -INFINITY) {
-            const float mn = fmaxf(st_m, pm), mn2 = mn * kL2e;
-            float sum = 0.f;
-            if (col0 + 32 <= lim) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) sum += ex2_fast(fmaf(x[j], kL2e, -mn2));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (col0 + j < lim) sum += ex2_fast(fmaf(x[j], kL2e, -mn2));
-            }
-            st_l = st_l * ex2_fast((st_m - mn) * kL2e) + sum;
-            st_m = mn;
-          }
-        } else if (ep == MT_EPI_STORE_BF16 || ep == MT_EPI_BIAS_GELU) {
+        if (ep == MT_EPI_STORE_BF16 || ep == MT_EPI_BIAS_GELU) {
           if (p.bias != nullptr) {
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
@@ -895,8 +677,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         flush_piece(&tmap_d, stg + bi * 4096, lane, col0, row0, b, false);
         bi = (bi + 1) % C::kEpiBufs;
       }
-      if (ep == MT_EPI_STORE_BF16_ROWSTATS && row < p.m)
-        p.row_stats[((long long)b * p.m + row) * p.ld_aux + nb] = make_float2(st_m, st_l);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -906,36 +686,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
       }
       ++it;
-      if (kAR && p.ar_ranks > 0) {
+      if (kAR && p.ar_group_cols > 0) {
         // bulk groups of the tile issued after `unpublished` (64-column bf16 pieces when BN % 64 == 0)
-        if (unpublished >= 0) ar_publish<kPair, (BN % 64 == 0) ? BN / 64 : BN / 32>(p, unpublished, rank, lane);
+        if (unpublished >= 0) ar_publish<(BN % 64 == 0) ? BN / 64 : BN / 32>(p, unpublished, lane);
         unpublished = w;
-        if (!p.ar_in_epi) continue;
-        if (pending[0].w >= 0 && pending[1].w >= 0) {
-          ar_reduce<BN, BMT, kPair>(p, pending[0], rank);
-          ++reduced;
-          pending[0] = pending[1];
-          pending[1].w = -1;
-        }
-        if (ar_unit_id<kPair>(w, rank) % p.ar_ranks == p.ar_rank)
-          (pending[0].w < 0 ? pending[0] : pending[1]) = ArUnit{w, mb, nb};
       }
     }
-    if (kAR && p.ar_ranks > 0) {
-      if (unpublished >= 0) ar_publish<kPair, 0>(p, unpublished, rank, lane);
-      for (int i = 0; i < 2; ++i)
-        if (pending[i].w >= 0) {
-          ar_reduce<BN, BMT, kPair>(p, pending[i], rank);
-          ++reduced;
-        }
-      if (p.ar_in_epi) {  // count this CTA's reduced units once, after all their stores
-        epi_bar();
-        if (threadIdx.x == 128 && reduced > 0) {
-          fence_acq_rel_sys();
-          multimem_red_release_add_u32(p.ar_counter_mc, (uint32_t)reduced);
-        }
-      }
-    }
+    if (kAR && p.ar_group_cols > 0 && unpublished >= 0) ar_publish<0>(p, unpublished, lane);
     if (lane == 0) bulk_wait<0>();
   }
 
@@ -1113,7 +870,6 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   p.bias = static_cast<const __nv_bfloat16*>(a.bias);
   p.aux = static_cast<__nv_bfloat16*>(a.aux);
   p.ld_aux = a.ld_aux;
-  p.row_stats = static_cast<float2*>(a.aux);
   // fp32 outputs (wgrad) are written once and never re-read by this GEMM: evict_first keeps the
   // re-read operand tiles in L2 (tools/gemm_one.py wg_mm_f32: 1864 -> 1832 us); MT_GEMM_STORE_HINT=0 disables
   static const int store_hint = [] {
@@ -1122,32 +878,13 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   }();
   p.store_policy = (store_hint == 1) ? kEvictFirst : (store_hint == 2 ? kEvictLast : 0);
   if (a.allreduce != nullptr) {
+    // column-group mode: column blocks complete in raster order only when m-blocks vary fastest
     mt_gemm_allreduce& ar = *a.allreduce;
-    const long long units = (long long)p.total_tiles * (kPair ? 2 : 1);
-    if (ar.ranks < 2 || ar.ranks > 8 || ar.rank < 0 || ar.rank >= ar.ranks || units > ar.flag_capacity ||
-        !ar.d_multicast || !ar.flags_local || !ar.counter_multicast)
+    if (ar.ranks < 2 || ar.ranks > 8 || ar.rank < 0 || ar.rank >= ar.ranks || ar.groups < 1 || ar.groups > 64 ||
+        !ar.d_multicast || !ar.group_counters || !ar.counter_multicast || p.n_fastest)
       return 1;
-    p.ar_mc = static_cast<__nv_bfloat16*>(ar.d_multicast);
-    p.ar_flags = ar.flags_local;
-    for (int r = 0; r < ar.ranks; ++r) {
-      if (!ar.flags_peer[r]) return 1;
-      p.ar_peer[r] = ar.flags_peer[r];
-    }
-    p.ar_counter_mc = ar.counter_multicast;
-    p.ar_epoch = ar.epoch;
-    p.ar_rank = ar.rank;
-    p.ar_ranks = ar.ranks;
-    static const int dbg = [] {
-      const char* e = getenv("MT_AR_DEBUG");
-      return e ? atoi(e) : 0;
-    }();
-    p.ar_debug = dbg;
-    p.ar_in_epi = ar.reduce_in_epilogue ? 1 : 0;
-    p.ar_group_cols = 0;
-    if (ar.groups > 0 && !p.n_fastest) {  // column blocks complete in order: count them per group
-      p.ar_group_cols = (p.nblocks + ar.groups - 1) / ar.groups;
-      p.ar_in_epi = 0;
-    }
+    p.ar_group_cnt = ar.group_counters;
+    p.ar_group_cols = (p.nblocks + ar.groups - 1) / ar.groups;
     ar.geom[0] = BN;
     ar.geom[1] = C::kTileM;
     ar.geom[2] = kPair ? 1 : 0;
@@ -1157,14 +894,19 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
     ar.geom[6] = p.m;
     ar.geom[7] = p.n;
     ar.group_cols = p.ar_group_cols;
-    ar.units = units;
+    ar.units = (long long)p.total_tiles * (kPair ? 2 : 1);
   }
   auto kern = gemm_sm100_kernel<BN, kAMN, kBMN, kPair, kAR>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  // the dynamic shared-memory opt-in is per device: one bit per device that has it, set by any thread
+  // (setting it twice is harmless), so one context per GPU per host thread works in one process
+  static std::atomic<uint64_t> attr_devices{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 2;
+  const uint64_t bit = uint64_t{1} << (dev & 63);
+  if (!(attr_devices.load(std::memory_order_acquire) & bit)) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
       return 2;
-    attr_set = true;
+    attr_devices.fetch_or(bit, std::memory_order_release);
   }
   if (!kPair) {
     const int cap = a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms();
@@ -1248,43 +990,11 @@ bool pair_enabled() {
 
 extern "C" int mt_gemm_launches_per_call(void) { return 1; }
 
-extern "C" int mt_gemm_allreduce_reduce(const mt_gemm_allreduce* ar, void* d, int64_t ldd,
-                                        const uint32_t* counter_local, uint32_t target, int32_t ctas, void* stream) {
-  if (ar == nullptr || counter_local == nullptr || ctas < 1 || ar->ranks < 2 || ar->ranks > 8 || ar->geom[0] <= 0)
-    return 1;
-  (void)d;
-  mt::ArReduceParams p{};
-  p.mc = static_cast<__nv_bfloat16*>(ar->d_multicast);
-  for (int r = 0; r < ar->ranks; ++r) p.flags[r] = ar->flags_peer[r];
-  p.counter_mc = ar->counter_multicast;
-  p.counter_local = counter_local;
-  p.epoch = ar->epoch;
-  p.target = target;
-  p.rank = ar->rank;
-  p.ranks = ar->ranks;
-  p.bn = (int)ar->geom[0];
-  p.tile_m = (int)ar->geom[1];
-  p.pair = (int)ar->geom[2];
-  p.n_fastest = (int)ar->geom[3];
-  p.mblocks = (int)ar->geom[4];
-  p.nblocks = (int)ar->geom[5];
-  p.m = (int)ar->geom[6];
-  p.n = (int)ar->geom[7];
-  p.ldd = ldd;
-  static const int dbg = [] {
-    const char* e = getenv("MT_AR_DEBUG");
-    return e ? atoi(e) : 0;
-  }();
-  p.debug = dbg;
-  mt::allreduce_reduce_kernel<<<ctas, mt::kReduceThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
-  return cudaGetLastError() == cudaSuccess ? 0 : 2;
-}
-
 extern "C" int mt_gemm_allreduce_reduce_groups(const mt_gemm_allreduce* ar, int64_t ldd, uint32_t* group_counters,
                                                const uint32_t* counter_local, uint32_t base, int32_t ctas,
                                                void* stream) {
   if (ar == nullptr || group_counters == nullptr || counter_local == nullptr || ctas < 1 || ar->group_cols <= 0 ||
-      ar->ranks < 2 || ar->geom[6] % ar->ranks != 0)
+      ar->ranks < 2 || ar->geom[6] % ar->ranks != 0 || ar->timeout_ns == 0)
     return 1;
   mt::ArGroupParams p{};
   p.mc = static_cast<__nv_bfloat16*>(ar->d_multicast);
@@ -1302,13 +1012,17 @@ extern "C" int mt_gemm_allreduce_reduce_groups(const mt_gemm_allreduce* ar, int6
   p.n = (int)ar->geom[7];
   p.groups = ((int)ar->geom[5] + p.group_cols - 1) / p.group_cols;
   p.ldd = ldd;
+  p.err = ar->error_flag;
+  p.timeout_ns = ar->timeout_ns;
   mt::allreduce_group_kernel<<<ctas, mt::kReduceThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
-extern "C" int mt_gemm_allreduce_wait(const uint32_t* counter_local, uint32_t target, void* stream) {
-  if (counter_local == nullptr) return 1;
-  mt::allreduce_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(counter_local, target);
+extern "C" int mt_gemm_allreduce_wait(const mt_gemm_allreduce* ar, const uint32_t* counter_local, uint32_t target,
+                                      void* stream) {
+  if (ar == nullptr || counter_local == nullptr || ar->timeout_ns == 0) return 1;
+  mt::allreduce_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(counter_local, target, ar->error_flag,
+                                                                            ar->timeout_ns);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -1327,12 +1041,7 @@ extern "C" int mt_gemm(const mt_gemm_args* args, void* stream) {
   if ((a.epilogue == MT_EPI_BIAS_GELU || a.epilogue == MT_EPI_GELU_BWD) && a.batch != 1) return 1;
   if (a.allreduce != nullptr && (a.epilogue != MT_EPI_STORE_BF16 || a.batch != 1 || a.causal != MT_CAUSAL_NONE))
     return 1;
-  if (a.epilogue < 0 || a.epilogue > MT_EPI_STORE_BF16_ROWSTATS || a.causal < 0 || a.causal > MT_CAUSAL_K_GE_M)
-    return 1;
-  if (a.epilogue == MT_EPI_STORE_BF16_ROWSTATS &&
-      (a.aux == nullptr || (a.block_n != 128 && a.block_n != 256) || a.ld_aux < (a.n + a.block_n - 1) / a.block_n ||
-       a.bias != nullptr))
-    return 1;
+  if (a.epilogue < 0 || a.epilogue > MT_EPI_ACCUM_F32 || a.causal < 0 || a.causal > MT_CAUSAL_K_GE_M) return 1;
   int bn = a.block_n;
   if (bn == 0) bn = mt::choose_block_n(a);
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -457,117 +457,6 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const uint4* __restric
   if (lane == 0) lse[warp] = l;
 }
 
-template <int VPL>
-__global__ void __launch_bounds__(256) softmax_bwd_kernel(const uint4* __restrict__ S, const float* __restrict__ lse,
-                                                          uint4* __restrict__ dP, int rows_total, int seq,
-                                                          long long head_base, uint64_t seed, uint32_t thresh16,
-                                                          float scale, float alpha) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= rows_total) return;
-  const int bh = warp / seq, i = warp - bh * seq;
-  const int nvec_row = seq >> 3;
-  const uint4* srow = S + (size_t)warp * nvec_row;
-  uint4* drow = dP + (size_t)warp * nvec_row;
-  const int nvalid = i + 1, nvec = (nvalid + 7) >> 3, nfull = nvalid >> 3, rem = nvalid & 7;
-  const float l2 = lse[warp] * kLog2e;
-  const uint64_t base_idx = ((uint64_t)(head_base + bh) * seq + i) * (uint64_t)seq;
-  uint4 rs[VPL], rg[VPL];
-  uint32_t keep[VPL];
-#pragma unroll
-  for (int t = 0; t < VPL; ++t) {
-    const int v = lane + 32 * t;
-    const bool in = v < nvec;
-    rs[t] = in ? srow[v] : make_uint4(0, 0, 0, 0);
-    rg[t] = in ? drow[v] : make_uint4(0, 0, 0, 0);
-  }
-  float dot = 0.f;
-#pragma unroll
-  for (int t = 0; t < VPL; ++t) {
-    const int v = lane + 32 * t;
-    keep[t] = 0;
-    if (v < nvec) {
-      uint32_t k = keep_mask8(seed, base_idx + v * 8, thresh16);
-      if (v == nfull) k &= (1u << rem) - 1u;  // causal tail of the row
-      keep[t] = k;
-      float sv[8], g[8];
-      unpack8_v(rs[t], sv);
-      unpack8_v(rg[t], g);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float pg = ex2_recompute(fmaf(sv[j], kLog2e, -l2)) * g[j];
-        dot += ((k >> j) & 1u) ? pg : 0.f;
-      }
-    }
-  }
-  dot = warp_sum(dot) * scale;
-#pragma unroll
-  for (int t = 0; t < VPL; ++t) {
-    const int v = lane + 32 * t;
-    if (v < nvec) {
-      float sv[8], g[8], o[8];
-      unpack8_v(rs[t], sv);
-      unpack8_v(rg[t], g);
-      const uint32_t valid = v < nfull ? 0xffu : (1u << rem) - 1u;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float y = ex2_recompute(fmaf(sv[j], kLog2e, -l2));
-        const float gj = ((keep[t] >> j) & 1u) ? g[j] * scale : 0.f;
-        o[j] = ((valid >> j) & 1u) ? alpha * y * (gj - dot) : 0.f;
-      }
-      drow[v] = pack8(o);
-    }
-  }
-  const int zend = min(seq, (i / 256 + 1) * 256) >> 3;
-  for (int v = nvec + lane; v < zend; v += 32) drow[v] = make_uint4(0, 0, 0, 0);
-}
-
-// Causal softmax forward in ONE pass over the scores: the score GEMM's epilogue
-// (MT_EPI_STORE_BF16_ROWSTATS) already produced, per row and 128/256-column block, the max and the
-// sum of exp of the stored values; the row's log-sum-exp combines those few partials, and each score
-// is read once, turned into its dropped probability and written (vs three register passes plus a
-// max and a sum reduction in softmax_fwd_kernel, which was issue-bound).
-__global__ void __launch_bounds__(256) softmax_fwd_stats_kernel(const uint4* __restrict__ S, uint4* __restrict__ P,
-                                                                const float2* __restrict__ stats, int ld_stats,
-                                                                int bn, float* __restrict__ lse, int rows_total,
-                                                                int seq, long long head_base, uint64_t seed,
-                                                                uint32_t thresh16, float scale) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= rows_total) return;
-  const int bh = warp / seq, i = warp - bh * seq;
-  const int nblk = i / bn + 1;  // column blocks holding causal entries of row i
-  float m = -INFINITY, l = 0.f;
-  if (lane < nblk) {
-    const float2 st = stats[(size_t)warp * ld_stats + lane];
-    m = st.x;
-    l = st.y;
-  }
-  const float mx = warp_max(m);
-  const float part = (lane < nblk && l > 0.f) ? l * exp2f((m - mx) * kLog2e) : 0.f;
-  const float lrow = mx + logf(warp_sum(part));
-  const float l2 = lrow * kLog2e;
-  const int nvec_row = seq >> 3;
-  const uint4* srow = S + (size_t)warp * nvec_row;
-  uint4* prow = P + (size_t)warp * nvec_row;
-  const int nvalid = i + 1, nvec = (nvalid + 7) >> 3, nfull = nvalid >> 3, rem = nvalid & 7;
-  const uint64_t base_idx = ((uint64_t)(head_base + bh) * seq + i) * (uint64_t)seq;
-  for (int v = lane; v < nvec; v += 32) {
-    uint32_t keep = keep_mask8(seed, base_idx + v * 8, thresh16);
-    if (v == nfull) keep &= (1u << rem) - 1u;
-    float x[8], o[8];
-    unpack8(srow[v], x);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float e = ex2_recompute(fmaf(x[j], kLog2e, -l2)) * scale;
-      o[j] = ((keep >> j) & 1u) ? e : 0.f;
-    }
-    prow[v] = pack8(o);
-  }
-  const int zend = min(seq, (i / 256 + 1) * 256) >> 3;
-  for (int v = nvec + lane; v < zend; v += 32) prow[v] = make_uint4(0, 0, 0, 0);
-  if (lane == 0) lse[warp] = lrow;
-}
 
 __global__ void __launch_bounds__(256) softmax_bwd_rowdot_kernel(const uint4* __restrict__ S,
                                                                   const float* __restrict__ lse,
@@ -797,13 +686,6 @@ void softmax_fwd(const void* S, void* P, float* lse, int batch_heads, int seq, l
 #undef L
 }
 
-void softmax_fwd_stats(const void* S, void* P, const void* stats, int ld_stats, int bn, float* lse, int batch_heads,
-                       int seq, long long head_base, uint64_t seed, uint32_t thresh16, float scale, cudaStream_t s) {
-  const int rows = batch_heads * seq;
-  softmax_fwd_stats_kernel<<<(rows + 7) / 8, 256, 0, s>>>((const uint4*)S, (uint4*)P, (const float2*)stats, ld_stats,
-                                                          bn, lse, rows, seq, head_base, seed, thresh16, scale);
-}
-
 void softmax_bwd_rowdot(const void* S, const float* lse, const float* D, void* dP, int batch_heads, int seq,
                         long long head_base, uint64_t seed, uint32_t thresh16, float scale, float alpha,
                         cudaStream_t s) {
@@ -812,16 +694,6 @@ void softmax_bwd_rowdot(const void* S, const float* lse, const float* D, void* d
                                                            seed, thresh16, scale, alpha);
 }
 
-void softmax_bwd(const void* S, const float* lse, void* dP, int batch_heads, int seq, long long head_base,
-                 uint64_t seed, uint32_t thresh16, float scale, float alpha, cudaStream_t s) {
-  const int rows = batch_heads * seq;
-  const int blocks = (rows + 7) / 8;
-#define L(V)                                                                                                      \
-  softmax_bwd_kernel<V><<<blocks, 256, 0, s>>>((const uint4*)S, lse, (uint4*)dP, rows, seq, head_base, seed, thresh16, \
-                                               scale, alpha)
-  MT_VPL_DISPATCH(seq, L);
-#undef L
-}
 
 void mse_loss(const void* y, const void* t, void* dy, float* loss, long long n, cudaStream_t s, long long n_total) {
   const long long nvec = n / 8;

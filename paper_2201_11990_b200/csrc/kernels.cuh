@@ -62,13 +62,6 @@ bool ln_bwd_rows(const void* dy, const void* x, const void* gamma, const float* 
 // block index and head_base maps local blocks to global (microbatch-row, head) ids.
 void softmax_fwd(const void* S, void* P, float* lse, int batch_heads, int seq, long long head_base,
                  uint64_t site_seed, uint32_t thresh16, float scale, cudaStream_t s);
-// One-pass variant: `stats` = float2 [batch_heads * seq][ld_stats] per-(row, bn-column block) {max,
-// sum exp} of S from the score GEMM's MT_EPI_STORE_BF16_ROWSTATS epilogue. Same outputs.
-void softmax_fwd_stats(const void* S, void* P, const void* stats, int ld_stats, int bn, float* lse, int batch_heads,
-                       int seq, long long head_base, uint64_t seed, uint32_t thresh16, float scale, cudaStream_t s);
-// In place: dP (dropped-prob grad) -> dS * alpha.
-void softmax_bwd(const void* S, const float* lse, void* dP, int batch_heads, int seq, long long head_base,
-                 uint64_t site_seed, uint32_t thresh16, float scale, float alpha, cudaStream_t s);
 
 // One-pass softmax backward with the row term precomputed: D[bh * seq + i] = dctx_i . ctx_i of the
 // head (= sum_j P_ij dP_ij), so dS = alpha * p * (dP' - D) needs no in-kernel row reduction.

@@ -12,11 +12,13 @@
 #include "runtime.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <thread>
 
 #include "curator/dropout.hpp"
 #include "curator/errors.hpp"
@@ -38,6 +40,101 @@ void check_cuda(cudaError_t e, const char* what) {
 }
 void check_nccl(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) throw RuntimeFailure(std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+void abort_comms(mt_ctx* c) {
+  std::lock_guard<std::mutex> lk(c->abort_mu);
+  if (c->aborted) return;
+  if (c->err_host) __atomic_store_n(c->err_host, 2u, __ATOMIC_SEQ_CST);  // 2 = host abort: device spins return
+  c->aborted = true;
+  for (ncclComm_t* cm : {&c->dp_side, &c->emb, &c->tp_side, &c->tp, &c->pp, &c->dp, &c->world})
+    if (*cm) {
+      ncclComm_t h = *cm;
+      *cm = nullptr;
+      ncclCommAbort(h);  // releases NCCL calls blocked on the host and NCCL kernels on the device
+    }
+}
+
+void watchdog_start(mt_ctx* c) {
+  if (c->watchdog) return;
+  c->watchdog = std::make_unique<Watchdog>();
+  Watchdog* w = c->watchdog.get();
+  w->thread = std::thread([c, w] {
+    std::unique_lock<std::mutex> lk(w->mu);
+    while (!w->stop) {
+      w->cv.wait_for(lk, std::chrono::milliseconds(50));
+      const int64_t d = w->deadline_ns.load();
+      if (d != 0 && std::chrono::steady_clock::now().time_since_epoch().count() > d) {
+        w->deadline_ns = 0;
+        lk.unlock();
+        fprintf(stderr, "[mtnlg] rank %d: an API call exceeded the %.0f s communication bound; aborting the "
+                        "context's NCCL communicators\n", c->rank, c->timeout_ns * 1e-9);
+        abort_comms(c);
+        lk.lock();
+      }
+    }
+  });
+}
+
+void watchdog_stop(mt_ctx* c) {
+  if (!c->watchdog) return;
+  {
+    std::lock_guard<std::mutex> lk(c->watchdog->mu);
+    c->watchdog->stop = true;
+  }
+  c->watchdog->cv.notify_all();
+  c->watchdog->thread.join();
+  c->watchdog.reset();
+}
+
+WatchdogArm::WatchdogArm(mt_ctx* ctx) : c(ctx) {
+  if (!c || !c->watchdog) return;
+  if (c->watchdog->depth++ == 0)
+    c->watchdog->deadline_ns = (std::chrono::steady_clock::now() + std::chrono::nanoseconds(c->timeout_ns) +
+                                std::chrono::seconds(5))
+                                   .time_since_epoch()
+                                   .count();
+}
+WatchdogArm::~WatchdogArm() {
+  if (!c || !c->watchdog) return;
+  if (--c->watchdog->depth == 0) c->watchdog->deadline_ns = 0;
+}
+
+void wait_stream(mt_ctx* c, cudaStream_t s, const char* what) {
+  using clock = std::chrono::steady_clock;
+  const auto t0 = clock::now();
+  const auto deadline = t0 + std::chrono::nanoseconds(c->timeout_ns) + std::chrono::seconds(5);
+  auto fail = [&](const std::string& why) {
+    abort_comms(c);
+    // the aborted NCCL kernels and the released device spins let the queued work drain
+    const auto drain = clock::now() + std::chrono::seconds(60);
+    while (cudaStreamQuery(s) == cudaErrorNotReady && clock::now() < drain)
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    throw RuntimeFailure(std::string(what) + ": " + why +
+                         " (a peer rank is dead or diverged; the context's communicators were aborted)");
+  };
+  for (int polls = 0;; ++polls) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) check_cuda(e, what);
+    if ((polls & 63) == 0) {
+      if (c->err_host && __atomic_load_n(c->err_host, __ATOMIC_SEQ_CST) != 0)
+        fail("device-side wait for a peer timed out");
+      for (ncclComm_t cm : {c->world, c->tp, c->tp_side, c->pp, c->dp, c->dp_side, c->emb}) {
+        ncclResult_t r = ncclSuccess;
+        if (cm && ncclCommGetAsyncError(cm, &r) == ncclSuccess && r != ncclSuccess && r != ncclInProgress)
+          fail(std::string("NCCL asynchronous error: ") + ncclGetErrorString(r));
+      }
+      if (clock::now() > deadline) fail("timed out waiting for the iteration");
+    }
+    // spin-yield for the first ~2 ms (keeps the e2e timing tight), then sleep between polls
+    if (clock::now() - t0 < std::chrono::milliseconds(2))
+      std::this_thread::yield();
+    else
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  if (c->err_host && __atomic_load_n(c->err_host, __ATOMIC_SEQ_CST) != 0)
+    fail("device-side wait for a peer timed out");
 }
 
 DeviceBuffer::DeviceBuffer(size_t n) { ensure(n); }
@@ -217,8 +314,8 @@ void validate_desc(const mt_layer_desc& d) {
 // Collective over the TP group (every rank reaches the same ensure calls in the same order).
 void release_symmetric(mt_ctx* c, mt_ctx::SymBuffer& sb) {
   if (!sb.ptr) return;
-  if (sb.win_side) ncclCommWindowDeregister(c->tp_side, sb.win_side);
-  if (sb.win_tp) ncclCommWindowDeregister(c->tp, sb.win_tp);
+  if (sb.win_side && c->tp_side) ncclCommWindowDeregister(c->tp_side, sb.win_side);
+  if (sb.win_tp && c->tp) ncclCommWindowDeregister(c->tp, sb.win_tp);
   ncclMemFree(sb.ptr);
   sb = mt_ctx::SymBuffer{};
 }
@@ -261,6 +358,15 @@ extern "C" int mt_ctx_create(int32_t device, mt_ctx** out) {
     check_cuda(cudaSetDevice(device), "cudaSetDevice");
     auto* c = new mt_ctx();
     c->device = device;
+    if (const char* e = getenv("MT_COMM_TIMEOUT_S")) {
+      const double sec = atof(e);
+      if (sec > 0) c->timeout_ns = static_cast<uint64_t>(sec * 1e9);
+    }
+    check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(uint32_t), cudaHostAllocMapped),
+               "cudaHostAlloc(error flag)");
+    *c->err_host = 0;
+    check_cuda(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0),
+               "cudaHostGetDevicePointer(error flag)");
     c->gemm_ws.ensure(MT_GEMM_WORKSPACE_BYTES);
     check_cuda(cudaMemset(c->gemm_ws.ptr, 0, MT_GEMM_WORKSPACE_BYTES), "cudaMemset(gemm workspace)");
     *out = c;
@@ -270,6 +376,7 @@ extern "C" int mt_ctx_create(int32_t device, mt_ctx** out) {
 extern "C" int mt_ctx_destroy(mt_ctx* c) {
   return guarded([&] {
     if (!c) return;
+    watchdog_stop(c);
     if (c->fused_ar) fused_ar_destroy(c, c->fused_ar);
     c->fused_ar = nullptr;
     for (auto& sb : c->sym_h) release_symmetric(c, sb);
@@ -277,16 +384,13 @@ extern "C" int mt_ctx_destroy(mt_ctx* c) {
     if (c->ev_dp_ready) cudaEventDestroy(c->ev_dp_ready);
     if (c->ev_dp_done) cudaEventDestroy(c->ev_dp_done);
     for (ncclComm_t* cm : {&c->dp_side, &c->emb, &c->tp_side, &c->tp, &c->pp, &c->dp, &c->world})
-      if (*cm) ncclCommDestroy(*cm);
+      if (*cm) ncclCommDestroy(*cm);  // aborted communicators were already released (nullptr)
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (auto& m : c->marks) cudaEventDestroy(m.second);
     if (c->comm) cudaStreamDestroy(c->comm);
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
     if (c->ev_done) cudaEventDestroy(c->ev_done);
-    for (int i = 0; i < 4; ++i) {
-      if (c->ev_chunk_ready[i]) cudaEventDestroy(c->ev_chunk_ready[i]);
-      if (c->ev_chunk_done[i]) cudaEventDestroy(c->ev_chunk_done[i]);
-    }
+    if (c->err_host) cudaFreeHost(c->err_host);
     delete c;
   });
 }
@@ -321,6 +425,8 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
     c->place = ranks[rank];
     check_cuda(cudaSetDevice(c->device), "cudaSetDevice");
     if (world_size == 1) return;
+    watchdog_start(c);
+    WatchdogArm arm(c);  // communicator creation also waits for every peer
     ncclUniqueId id;
     std::memcpy(&id, id_bytes, 128);
     check_nccl(ncclCommInitRank(&c->world, world_size, id, rank), "ncclCommInitRank");
@@ -363,11 +469,6 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
       check_cuda(cudaStreamCreateWithPriority(&c->comm, cudaStreamNonBlocking, hi), "comm stream");
       check_cuda(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming), "event");
       check_cuda(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming), "event");
-      for (int i = 0; i < 4; ++i) {
-        check_cuda(cudaEventCreateWithFlags(&c->ev_chunk_ready[i], cudaEventDisableTiming), "event");
-        check_cuda(cudaEventCreateWithFlags(&c->ev_chunk_done[i], cudaEventDisableTiming), "event");
-      }
-      if (const char* e = getenv("MT_TP_CHUNKS")) c->tp_chunks = std::max(1, std::min(4, atoi(e)));
       if (const char* e = getenv("MT_TP_SYMMETRIC")) c->tp_symmetric = e[0] == '1';
       if (const char* e = getenv("MT_SEQ_PARALLEL")) c->seq_parallel = e[0] == '1';
       // forward row-parallel GEMM + all-reduce fused (column-group NVLS reducer beside the GEMM): on by
@@ -381,6 +482,21 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
       if (const char* e = getenv("MT_TP_NVLS")) c->tp_nvls = e[0] == '1';
       if (c->tp_fused || c->tp_nvls) c->tp_symmetric = true;
     }
+  });
+}
+
+extern "C" int mt_ctx_wait(mt_ctx* c, void* stream) {
+  return guarded([&] {
+    if (!c) throw std::invalid_argument("null ctx");
+    WatchdogArm arm(c);
+    wait_stream(c, (cudaStream_t)stream, "mt_ctx_wait");
+  });
+}
+
+extern "C" int mt_ctx_error(const mt_ctx* c, int32_t* state) {
+  return guarded([&] {
+    if (!c || !state) throw std::invalid_argument("null argument");
+    *state = c->aborted ? 3 : static_cast<int32_t>(__atomic_load_n(c->err_host, __ATOMIC_SEQ_CST));
   });
 }
 
@@ -744,16 +860,16 @@ namespace {
 // is only legal in shard-only (compute-only measurement) mode.
 bool tp_collectives(const mt_ctx* c, const mt_layer_desc& d) {
   if (d.tp_size <= 1) return false;
+  if (c->aborted) throw RuntimeFailure("the context's communicators were aborted after a peer failure");
   if (c->tp) return true;
   if (c->shard_only) return false;
   throw std::invalid_argument("TP > 1 needs mt_ctx_init_comm (or mt_ctx_shard_only for a compute-only shard run)");
 }
 
 // Row-parallel output block of the forward: z = in W^T (partial sums), TP all-reduce ("g"), then
-// out = resid + dropout(z + bias) and optionally LayerNorm(out). With TP > 1 the rows are split into
-// c->tp_chunks chunks: the all-reduce of chunk k runs on the comm stream while the GEMM of chunk k+1
-// runs on the SMs left free for it, and the bias/dropout/LayerNorm of chunk k overlaps the
-// all-reduce of chunk k+1. Row chunks keep their global dropout element indices.
+// out = resid + dropout(z + bias) and optionally LayerNorm(out). With TP > 1 the all-reduce is fused
+// into the GEMM (NVLink SHARP reducer beside it) when K is long enough to hide it, else an NVLS or
+// NCCL all-reduce follows the GEMM.
 struct LnOut {
   const void* gamma;
   const void* beta;
@@ -792,8 +908,6 @@ void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_
     }
     return;
   }
-  const int chunks = (tpc && M % (c->tp_chunks * 128) == 0) ? c->tp_chunks : 1;
-  const int64_t rows = M / chunks;
   auto row_ptr = [&](const void* p, int64_t r) {
     return static_cast<void*>(const_cast<uint16_t*>(static_cast<const uint16_t*>(p)) + r * h);
   };
@@ -826,41 +940,18 @@ void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_
     mark(c, st, "fwd.bias_dropout_residual_ln");
     return;
   }
-  if (chunks == 1) {
-    gemm_rows(0, M, 0, nullptr);
-    mark(c, st, gemm_label);
-    if (c->fused_ar && (c->tp_nvls || c->tp_fused) && z == c->sym_h[0].ptr) {
-      nvls_allreduce(c, M * h, st);  // NVLink SHARP all-reduce kernel + counter wait
-      n += 2;
-    } else {
-      check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(row-parallel out)");
-      ++n;
-    }
-    mark(c, st, "fwd.tp_allreduce");
-    epilogue(0, M);
-    mark(c, st, "fwd.bias_dropout_residual_ln");
-    return;
-  }
-  int sms = 0;
-  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device), "attr");
-  const int cap = std::max(2, sms - c->comm_sms);
-  for (int k = 0; k < chunks; ++k) {
-    gemm_rows(k * rows, rows, k == 0 ? 0 : cap, nullptr);  // later chunks share SMs with the chunk all-reduces
-    check_cuda(cudaEventRecord(c->ev_chunk_ready[k], st), "cudaEventRecord");
-    check_cuda(cudaStreamWaitEvent(c->comm, c->ev_chunk_ready[k], 0), "cudaStreamWaitEvent");
-    ncclComm_t comm = (k + 1 < chunks) ? c->tp_side : c->tp;  // the last chunk overlaps only small kernels
-    check_nccl(ncclAllReduce(row_ptr(z, k * rows), row_ptr(z, k * rows), rows * h, ncclBfloat16, ncclSum, comm,
-                             c->comm),
-               "ncclAllReduce(row-parallel chunk)");
-    ++n;
-    check_cuda(cudaEventRecord(c->ev_chunk_done[k], c->comm), "cudaEventRecord");
-  }
+  gemm_rows(0, M, 0, nullptr);
   mark(c, st, gemm_label);
-  for (int k = 0; k < chunks; ++k) {
-    check_cuda(cudaStreamWaitEvent(st, c->ev_chunk_done[k], 0), "cudaStreamWaitEvent");
-    epilogue(k * rows, rows);
+  if (c->fused_ar && (c->tp_nvls || c->tp_fused) && z == c->sym_h[0].ptr) {
+    nvls_allreduce(c, M * h, st);  // NVLink SHARP all-reduce kernel + counter wait
+    n += 2;
+  } else {
+    check_nccl(ncclAllReduce(z, z, M * h, ncclBfloat16, ncclSum, c->tp, st), "ncclAllReduce(row-parallel out)");
+    ++n;
   }
-  mark(c, st, "fwd.tp_allreduce+bias_dropout_residual_ln");
+  mark(c, st, "fwd.tp_allreduce");
+  epilogue(0, M);
+  mark(c, st, "fwd.bias_dropout_residual_ln");
 }
 
 void ensure_slot_buffers(mt_layer* l, mt_layer::Saved& sv) {
@@ -985,28 +1076,13 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, uint64_t mse
     }
     uint16_t* S = sv.S.as<uint16_t>() + bb * Hl * s * s;
     uint16_t* P = sv.P.as<uint16_t>() + bb * Hl * s * s;
-    // Opt-in (MT_SOFTMAX_STATS=1): the score GEMM also emits per-(row, column block) softmax
-    // statistics so the softmax is one streaming pass. Measured at the GPT-3 shape: softmax 0.42 ->
-    // 0.32 ms but the score GEMM (K = head dim, epilogue-bound) 0.30 -> 0.51 ms, so it is off.
-    static const bool stats_on = [] {
-      const char* e = getenv("MT_SOFTMAX_STATS");
-      return e && e[0] == '1';
-    }();
-    const int sbn = (s % 256 == 0) ? 256 : 128;
-    const bool use_stats = stats_on && s % 128 == 0;
-    Gemm sg(q, ld3, false, q + hd, ld3, false, S, s, s, s, hd);
-    sg.batched(Hl, 3 * hd, 3 * hd, s * s).alpha(alpha).causal(MT_CAUSAL_SKIP_UPPER_TILES);
-    if (use_stats) {
-      sg.epi(MT_EPI_STORE_BF16_ROWSTATS).aux(c->scratch_stats.ptr, s / sbn);
-      sg.a.block_n = sbn;
-    }
-    sg.run(st, n);
+    Gemm(q, ld3, false, q + hd, ld3, false, S, s, s, s, hd)
+        .batched(Hl, 3 * hd, 3 * hd, s * s)
+        .alpha(alpha)
+        .causal(MT_CAUSAL_SKIP_UPPER_TILES)
+        .run(st, n);
     mark(c, st, "fwd.attn_s_gemm");
-    if (use_stats)
-      softmax_fwd_stats(S, P, c->scratch_stats.ptr, (int)(s / sbn), sbn, lse, (int)Hl, (int)s, head_base, site_attn,
-                        th_a, scale_a, st);
-    else
-      softmax_fwd(S, P, lse, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, st);
+    softmax_fwd(S, P, lse, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, st);
     ++n;
     mark(c, st, "fwd.softmax");
     Gemm(P, s, false, q + 2 * hd, ld3, true, sv.ctx.as<uint16_t>() + bb * s * hl, hl, s, hd, s)
@@ -1191,20 +1267,11 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, uint64_t 
     mark(c, st, "bwd.attn_dv_gemm");
     const long long head_base = bb * d.heads + int64_t{d.tp_rank} * Hl;
     // row term D_i = dctx_i . ctx_i per head (= sum_j P_ij dP_ij) from a tiny kernel, so the softmax
-    // backward is one pass (MT_SOFTMAX_ROWDOT=0 selects the two-pass kernel)
-    static const bool rowdot_on = [] {
-      const char* e = getenv("MT_SOFTMAX_ROWDOT");
-      return !(e && e[0] == '0');
-    }();
-    if (rowdot_on) {
-      float* Dbuf = c->scratch_stats.as<float>();
-      attn_rowdot(dc, sv.ctx.as<uint16_t>() + bb * s * hl, hl, (int)hd, (int)Hl, (int)s, Dbuf, st);
-      softmax_bwd_rowdot(S, lse, Dbuf, dP, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, alpha, st);
-      n += 2;
-    } else {
-      softmax_bwd(S, lse, dP, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, alpha, st);
-      ++n;
-    }
+    // backward is one pass over S and dP
+    float* Dbuf = c->scratch_stats.as<float>();
+    attn_rowdot(dc, sv.ctx.as<uint16_t>() + bb * s * hl, hl, (int)hd, (int)Hl, (int)s, Dbuf, st);
+    softmax_bwd_rowdot(S, lse, Dbuf, dP, (int)Hl, (int)s, head_base, site_attn, th_a, scale_a, alpha, st);
+    n += 2;
     mark(c, st, "bwd.softmax");
     // dQ_h = dS_h K_h ; dK_h = dS_h^T Q_h   (dS already carries the 1/sqrt(d) factor)
     Gemm(dP, s, false, q + hd, ld3, true, dq, ld3, s, hd, s)
@@ -1273,6 +1340,7 @@ extern "C" int mt_ctx_set_sequence_parallel(mt_ctx* c, int32_t enable) {
 extern "C" int mt_layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb, void* stream) {
   return guarded([&] {
     if (!l || !x || !y) throw std::invalid_argument("null argument");
+    WatchdogArm arm(l->ctx);
     layer_forward(l, x, y, mb, (cudaStream_t)stream);
   });
 }
@@ -1280,6 +1348,7 @@ extern "C" int mt_layer_forward(mt_layer* l, const void* x, void* y, uint32_t mb
 extern "C" int mt_layer_backward(mt_layer* l, const void* dy, void* dx, uint32_t mb, void* stream) {
   return guarded([&] {
     if (!l || !dy || !dx) throw std::invalid_argument("null argument");
+    WatchdogArm arm(l->ctx);
     layer_backward(l, dy, dx, mb, (cudaStream_t)stream);
   });
 }

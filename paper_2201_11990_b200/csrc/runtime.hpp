@@ -4,12 +4,15 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <atomic>
+#include <condition_variable>
 #include <cstdint>
 #include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "curator/planner.hpp"
@@ -38,6 +41,32 @@ struct RuntimeFailure : std::runtime_error {
 
 void check_cuda(cudaError_t e, const char* what);
 void check_nccl(ncclResult_t r, const char* what);
+// Bounded host wait for the work queued on `s` (the iteration's sync point): polls the stream, the
+// NCCL communicators' async errors and the device error flag; on a peer timeout / NCCL error / the
+// context's deadline it releases the device spins, aborts the communicators and throws
+// RuntimeFailure (status 2). Replaces cudaStreamSynchronize on paths that wait for peers.
+void wait_stream(mt_ctx* c, cudaStream_t s, const char* what);
+void abort_comms(mt_ctx* c);
+
+// Host watchdog of a multi-rank context: a thread that aborts the context's NCCL communicators when
+// an armed API call (one that may block in NCCL — e.g. a lazily connected collective waiting for a
+// peer that never calls it — or wait for peers' kernels) runs past the context's bound. The blocked
+// NCCL call then returns an error and the API call returns status 2. Arming nests (depth counter).
+struct Watchdog {
+  std::thread thread;
+  std::mutex mu;
+  std::condition_variable cv;
+  bool stop = false;
+  std::atomic<int64_t> deadline_ns{0};  // steady_clock time since epoch; 0 = disarmed
+  int depth = 0;                        // nesting of armed calls (the context's own thread only)
+};
+void watchdog_start(mt_ctx* c);
+void watchdog_stop(mt_ctx* c);
+struct WatchdogArm {  // RAII: arms the context's watchdog for the duration of an API call
+  mt_ctx* c;
+  explicit WatchdogArm(mt_ctx* ctx);
+  ~WatchdogArm();
+};
 
 // Device buffer owned by the runtime.
 struct DeviceBuffer {
@@ -134,9 +163,18 @@ struct mt_ctx {
   cudaStream_t comm = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
   int comm_sms = 16;  // SMs kept free for the collective during an overlapped GEMM
-  int tp_chunks = 1;  // >1: forward row-parallel GEMM + all-reduce pipelined over row chunks (MT_TP_CHUNKS;
-                      // measured slower at TP=4 so far, kept opt-in)
-  cudaEvent_t ev_chunk_ready[4] = {}, ev_chunk_done[4] = {};
+  // Hang safety. Every device-side cross-rank spin (fused / NVLS all-reduce kernels) is bounded by
+  // timeout_ns and raises *err_dev (a host-mapped word, also readable as *err_host) when a peer never
+  // arrives; the host-side waits of an iteration poll the stream with the same bound and, on expiry,
+  // raise the flag (which releases the device spins) and abort the NCCL communicators (which
+  // releases NCCL's kernels), so a dead or diverged rank surfaces as status 2 instead of a wedged GPU.
+  // MT_COMM_TIMEOUT_S (default 300) sets the bound.
+  uint32_t* err_host = nullptr;
+  uint32_t* err_dev = nullptr;
+  uint64_t timeout_ns = 300ull * 1000000000ull;
+  std::atomic<bool> aborted{false};  // NCCL communicators were aborted: the context can no longer communicate
+  std::mutex abort_mu;
+  std::unique_ptr<mt::Watchdog> watchdog;  // world > 1 only
   // optional per-op timing (MT_OP_TIMING=1): stream-ordered marks between consecutive layer ops
   bool op_timing = false;
   std::vector<std::pair<const char*, cudaEvent_t>> marks;

@@ -304,4 +304,32 @@ __device__ __forceinline__ void st_release_sys_u32(void* p, uint32_t v) {
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Bounded spin on a cross-rank (or cross-kernel) counter: returns true once (int)(load(p) - target) >= 0.
+// A peer that never arrives (dead or diverged rank) must not wedge the GPU: after timeout_ns, or as
+// soon as *err is non-zero (an earlier timeout, or the host watchdog aborting the iteration), the
+// wait gives up, raises *err (1 = device timeout) and returns false; the kernel then finishes with
+// undefined data and the host reports status 2. err is a host-mapped word (system scope).
+template <bool kSys>
+__device__ __forceinline__ bool bounded_wait_geq(const uint32_t* p, uint32_t target, uint32_t* err, uint64_t timeout_ns) {
+  auto ld = [&] { return kSys ? ld_acquire_sys_u32(p) : ld_acquire_gpu_u32(p); };
+  if ((int)(ld() - target) >= 0) return true;
+  const uint64_t t0 = global_ns();
+  for (uint32_t n = 1;; ++n) {
+    if ((int)(ld() - target) >= 0) return true;
+    if ((n & 255) == 0) {
+      if (err != nullptr && *reinterpret_cast<volatile uint32_t*>(err) != 0) return false;
+      if (global_ns() - t0 > timeout_ns) {
+        if (err != nullptr) atomicCAS_system(err, 0u, 1u);
+        return false;
+      }
+    }
+  }
+}
+
 }  // namespace mt

@@ -32,6 +32,7 @@ struct mt_stage {
   mt::DeviceBuffer grad[2];                        // ping-pong [M, h]
   mt::DeviceBuffer target;                         // [M, h]
   mt::DeviceBuffer loss;                           // fp32 scalar
+  float* loss_host = nullptr;                      // pinned: the loss D2H never blocks the host (bounded wait)
   int64_t launches = 0;
   // training step of the next iteration: keys the dropout masks of every layer and of the embedding
   // (curator::step_seed), so they change from one iteration to the next; incremented per iteration
@@ -343,6 +344,8 @@ extern "C" int mt_stage_create(mt_ctx* c, const mt_stage_desc* d, mt_stage** out
     for (auto& g : st->grad) g.ensure(bytes);
     st->target.ensure(bytes);
     st->loss.ensure(4);
+    mt::check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&st->loss_host), sizeof(float), cudaHostAllocDefault),
+                   "cudaHostAlloc(loss)");
     mt::check_cuda(cudaStreamCreateWithFlags(&st->copy, cudaStreamNonBlocking), "copy stream");
     mt::check_cuda(cudaEventCreateWithFlags(&st->iter_start, cudaEventDisableTiming), "event");
     st->in_ev.resize(size_t(d->micro_batches) * mt_stage::kMaxInChunks);
@@ -369,6 +372,7 @@ extern "C" int mt_stage_destroy(mt_stage* st) {
     for (auto e : st->tgt_gathered) cudaEventDestroy(e);
     if (st->iter_start) cudaEventDestroy(st->iter_start);
     if (st->copy) cudaStreamDestroy(st->copy);
+    if (st->loss_host) cudaFreeHost(st->loss_host);
     delete st;
   });
 }
@@ -508,19 +512,21 @@ extern "C" int mt_stage_train_step(mt_stage* st, const void* inputs_host, const 
                                    void* stream) {
   return call([&] {
     if (!st) throw std::invalid_argument("null stage");
+    if (st->ctx->aborted) throw mt::RuntimeFailure("the context's communicators were aborted after a peer failure");
+    mt::WatchdogArm arm(st->ctx);  // a call blocked on a dead peer is released after the context's bound
     Step k{st, (cudaStream_t)stream, static_cast<const char*>(inputs_host), static_cast<const char*>(targets_host)};
     st->h2d_bytes = st->d2h_bytes = 0;
     if (k.lm() && ((k.first() && !inputs_host) || (k.last() && !targets_host)))
       throw std::invalid_argument("a stage with a vocab needs token inputs (first stage) and targets (last stage)");
     run_iteration(k, st, stream);
     if (loss_out) {
-      float host = 0.f;
-      if (k.last()) {
-        mt::check_cuda(cudaMemcpyAsync(&host, st->loss.ptr, 4, cudaMemcpyDeviceToHost, k.s), "D2H loss");
+      *st->loss_host = 0.f;
+      if (k.last()) {  // pinned destination: an asynchronous copy, so the wait below stays bounded
+        mt::check_cuda(cudaMemcpyAsync(st->loss_host, st->loss.ptr, 4, cudaMemcpyDeviceToHost, k.s), "D2H loss");
         st->d2h_bytes += 4;
       }
-      mt::check_cuda(cudaStreamSynchronize(k.s), "sync");
-      *loss_out = host;
+      mt::wait_stream(st->ctx, k.s, "mt_stage_train_step");  // bounded: a dead peer -> status 2
+      *loss_out = *st->loss_host;
     }
     st->launches = k.launches;
   });
@@ -530,6 +536,8 @@ extern "C" int mt_stage_train_step_dev(mt_stage* st, const void* inputs_dev, con
                                        void* stream) {
   return call([&] {
     if (!st) throw std::invalid_argument("null stage");
+    if (st->ctx->aborted) throw mt::RuntimeFailure("the context's communicators were aborted after a peer failure");
+    mt::WatchdogArm arm(st->ctx);  // a call blocked on a dead peer is released after the context's bound
     Step k{st, (cudaStream_t)stream, nullptr, nullptr};
     k.in_dev = static_cast<const char*>(inputs_dev);
     k.tgt_dev = static_cast<const char*>(targets_dev);
@@ -550,6 +558,7 @@ extern "C" int mt_stage_optimizer_step(mt_stage* st, const mt_adam_desc* d, floa
     if (d->step < 1) throw std::invalid_argument("step must be >= 1");
     cudaStream_t s = (cudaStream_t)stream;
     mt_ctx* c = st->ctx;
+    mt::WatchdogArm arm(c);
     c->opt_scratch.ensure(4 * sizeof(float));
     float* sq = c->opt_scratch.as<float>();
     mt::check_cuda(cudaMemsetAsync(sq, 0, 2 * sizeof(float), s), "memset");

@@ -2,12 +2,13 @@
 //
 // The [M, h] row-parallel output buffer lives in NCCL symmetric memory (ncclMemAlloc + a window
 // registered on the TP communicator, runtime.cpp ensure_symmetric); this file adds a second small
-// symmetric window for the per-unit ready flags and the completion counter, and resolves through the
-// NCCL device API (ncclDevCommCreate with lsaMultimem) the NVLink-SHARP multicast addresses of both
-// windows and every peer's flag array. The GEMM kernel (gemm_sm100.cu) publishes each finished
-// output unit; a reducer kernel on the SMs the GEMM leaves free (allreduce_reduce_kernel) sums every
-// unit this rank owns over NVLink SHARP as soon as all ranks published it, tile by tile while the
-// GEMM still runs, and the consumer waits on the completion counter instead of an NCCL all-reduce.
+// symmetric window for the completion counter and the per-column-group unit counters, and resolves
+// through the NCCL device API (ncclDevCommCreate with lsaMultimem) the NVLink-SHARP multicast
+// addresses of both windows. The GEMM kernel (gemm_sm100.cu) counts each finished output unit on its
+// column group; a reducer kernel on the SMs the GEMM leaves free (allreduce_group_kernel) reduces
+// each group over NVLink SHARP as soon as every rank finished it, while the GEMM still runs later
+// groups, and the consumer waits on the completion counter instead of an NCCL all-reduce. Every
+// cross-rank wait is bounded (mt_ctx timeout): a dead peer raises the context's error flag.
 #include <nccl.h>
 #include <nccl_device.h>
 
@@ -23,80 +24,72 @@ namespace mt {
 struct FusedAllReduce {
   ncclDevComm dev{};
   bool dev_created = false;
-  void* flags = nullptr;  // [0]: completion counter; [kFlagBase..): per-unit flags
+  void* flags = nullptr;  // [0]: completion counter (own 256-byte line); [kGroupBase..+64): group counters
   size_t flags_bytes = 0;
   ncclWindow_t flags_win = nullptr;
   void* z = nullptr;  // the symmetric output buffer the multicast address below belongs to
   mt_gemm_allreduce desc{};
-  uint32_t target = 0;  // cumulative units of all launches: the counter value that means "all done"
-  // reducer CTAs running beside the GEMM (MT_AR_CTAS, default 16); 0 = the GEMM's epilogue warps
-  // reduce (measured slower: the multimem round trips then serialise with the epilogue)
-  int reducer_ctas = 16;
-  int nvls_ctas = 0;  // CTAs of the standalone NVLS all-reduce kernel (0: reducer_ctas, or 16)
-  bool serial = false;  // MT_AR_SERIAL=1 (measurement): reducer after the GEMM on the same stream
-  int groups = 6;       // MT_AR_GROUPS: column-group granularity (0 = per-unit flags)
+  uint32_t target = 0;  // cumulative arrivals of all launches: the counter value that means "all done"
+  int reducer_ctas = 16;  // reducer CTAs running beside the GEMM (MT_AR_CTAS)
+  int nvls_ctas = 0;      // CTAs of the standalone NVLS all-reduce kernel (MT_NVLS_CTAS; 0: reducer_ctas)
+  int groups = 6;         // column groups per fused launch (the reduction of group g overlaps groups > g)
 };
 
 namespace {
 
-constexpr int64_t kFlagBase = 64;  // counter on its own 256-byte line
-constexpr int64_t kCapacity = 1 << 16;
+constexpr int64_t kGroupBase = 64;
 
 __global__ void resolve_kernel(ncclWindow_t zwin, ncclWindow_t fwin, ncclDevComm dc, void** out) {
   out[0] = ncclGetLsaMultimemPointer(zwin, 0, dc);
   out[1] = ncclGetLsaMultimemPointer(fwin, 0, dc);
-  for (int r = 0; r < dc.lsaSize && r < 8; ++r) out[2 + r] = ncclGetLsaPointer(fwin, 0, r);
-  out[10] = reinterpret_cast<void*>(static_cast<uintptr_t>(dc.lsaSize));
-  out[11] = reinterpret_cast<void*>(static_cast<uintptr_t>(dc.lsaRank));
+  out[2] = reinterpret_cast<void*>(static_cast<uintptr_t>(dc.lsaSize));
+  out[3] = reinterpret_cast<void*>(static_cast<uintptr_t>(dc.lsaRank));
 }
 
-// Multicast / peer addresses of the current symmetric buffers (collective: every TP rank resolves
-// at the same point because buffer allocation is collective).
+// Multicast addresses of the current symmetric buffers (collective: every TP rank resolves at the
+// same point because buffer allocation is collective).
 void resolve(mt_ctx* c, FusedAllReduce* f) {
   void** d_out = nullptr;
-  check_cuda(cudaMalloc(&d_out, 12 * sizeof(void*)), "cudaMalloc");
+  check_cuda(cudaMalloc(&d_out, 4 * sizeof(void*)), "cudaMalloc");
   resolve_kernel<<<1, 1>>>(c->sym_h[0].win_tp, f->flags_win, f->dev, d_out);
-  void* h[12] = {};
+  void* h[4] = {};
   check_cuda(cudaMemcpy(h, d_out, sizeof h, cudaMemcpyDeviceToHost), "resolve multicast addresses");
   cudaFree(d_out);
-  const int lsa_size = static_cast<int>(reinterpret_cast<uintptr_t>(h[10]));
-  const int lsa_rank = static_cast<int>(reinterpret_cast<uintptr_t>(h[11]));
+  const int lsa_size = static_cast<int>(reinterpret_cast<uintptr_t>(h[2]));
+  const int lsa_rank = static_cast<int>(reinterpret_cast<uintptr_t>(h[3]));
   if (lsa_size != c->par.tensor || lsa_rank != c->place.tensor || !h[0] || !h[1])
     throw RuntimeFailure("fused TP all-reduce: the TP group is not one load/store-accessible multicast team");
   f->z = c->sym_h[0].ptr;
   mt_gemm_allreduce& d = f->desc;
-  const uint32_t epoch = d.epoch;  // epochs stay monotonic across re-resolution (flags keep old values)
   d = mt_gemm_allreduce{};
-  d.epoch = epoch;
   d.d_multicast = h[0];
   d.counter_multicast = static_cast<uint32_t*>(h[1]);
-  d.flags_local = static_cast<uint32_t*>(f->flags) + kFlagBase;
-  for (int r = 0; r < c->par.tensor; ++r) d.flags_peer[r] = static_cast<const uint32_t*>(h[2 + r]) + kFlagBase;
-  d.flag_capacity = kCapacity;
+  d.group_counters = static_cast<uint32_t*>(f->flags) + kGroupBase;
   d.rank = c->place.tensor;
   d.ranks = c->par.tensor;
+  d.groups = f->groups;
+  d.error_flag = c->err_dev;
+  d.timeout_ns = c->timeout_ns;
 }
 
 }  // namespace
 
 FusedAllReduce* fused_ar_create(mt_ctx* c) {
   auto f = new FusedAllReduce();
-  if (const char* e = getenv("MT_AR_CTAS")) f->reducer_ctas = std::max(0, atoi(e));
+  if (const char* e = getenv("MT_AR_CTAS")) f->reducer_ctas = std::max(1, atoi(e));
   if (const char* e = getenv("MT_NVLS_CTAS")) f->nvls_ctas = std::max(0, atoi(e));
-  if (const char* e = getenv("MT_AR_SERIAL")) f->serial = e[0] == '1';
-  if (const char* e = getenv("MT_AR_GROUPS")) f->groups = std::max(0, atoi(e));
   try {
     ncclDevCommRequirements req{};
     req.lsaMultimem = true;
     check_nccl(ncclDevCommCreate(c->tp, &req, &f->dev), "ncclDevCommCreate(tp, multimem)");
     f->dev_created = true;
-    f->flags_bytes = static_cast<size_t>((kFlagBase + kCapacity) * 4 + 4095) / 4096 * 4096;
+    f->flags_bytes = 4096;
     check_nccl(ncclMemAlloc(&f->flags, f->flags_bytes), "ncclMemAlloc(flags)");
     check_nccl(ncclCommWindowRegister(c->tp, f->flags, f->flags_bytes, &f->flags_win, NCCL_WIN_COLL_SYMMETRIC),
                "ncclCommWindowRegister(flags)");
     check_cuda(cudaMemset(f->flags, 0, f->flags_bytes), "cudaMemset(flags)");
     check_cuda(cudaDeviceSynchronize(), "sync");
-    // every rank's flags are zero before any rank can publish into them
+    // every rank's counter is zero before any rank can arrive on it
     check_nccl(ncclAllReduce(f->flags, f->flags, 1, ncclUint32, ncclSum, c->tp, nullptr), "ncclAllReduce(sync)");
     check_cuda(cudaDeviceSynchronize(), "sync");
     resolve(c, f);
@@ -110,9 +103,11 @@ FusedAllReduce* fused_ar_create(mt_ctx* c) {
 void fused_ar_destroy(mt_ctx* c, FusedAllReduce* f) {
   if (!f) return;
   cudaDeviceSynchronize();
-  if (f->flags_win) ncclCommWindowDeregister(c->tp, f->flags_win);
-  if (f->flags) ncclMemFree(f->flags);
-  if (f->dev_created) ncclDevCommDestroy(c->tp, &f->dev);
+  if (c->tp) {  // an aborted communicator (peer timeout) owns nothing we may deregister
+    if (f->flags_win) ncclCommWindowDeregister(c->tp, f->flags_win);
+    if (f->flags) ncclMemFree(f->flags);
+    if (f->dev_created) ncclDevCommDestroy(c->tp, &f->dev);
+  }
   delete f;
 }
 
@@ -120,67 +115,44 @@ void fused_ar_destroy(mt_ctx* c, FusedAllReduce* f) {
 mt_gemm_allreduce* fused_ar_begin(mt_ctx* c) {
   FusedAllReduce* f = c->fused_ar;
   if (f->z != c->sym_h[0].ptr) resolve(c, f);
-  f->desc.epoch += 1;
   f->desc.units = 0;
-  f->desc.reduce_in_epilogue = f->reducer_ctas == 0 ? 1 : 0;
-  f->desc.groups = f->reducer_ctas > 0 ? f->groups : 0;
   f->desc.group_cols = 0;
   return &f->desc;
 }
 
-// Column-group mode: the group counters must read zero when the GEMM starts.
+// The group counters must read zero when the GEMM starts.
 void fused_ar_prepare(mt_ctx* c, cudaStream_t st) {
   FusedAllReduce* f = c->fused_ar;
-  if (f->desc.groups > 0)
-    check_cuda(cudaMemsetAsync(f->desc.flags_local, 0, sizeof(uint32_t) * 64, st), "memset group counters");
+  check_cuda(cudaMemsetAsync(f->desc.group_counters, 0, sizeof(uint32_t) * 64, st), "memset group counters");
 }
 
-// SMs the fused GEMM may use (the reducer kernel takes the rest), 0 = all.
+// SMs the fused GEMM may use (the reducer kernel takes the rest).
 int fused_ar_gemm_ctas(mt_ctx* c) {
   const FusedAllReduce* f = c->fused_ar;
-  if (f->reducer_ctas == 0 || f->serial) return 0;
   int sms = 0;
   check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device), "attr");
   return std::max(2, (sms - f->reducer_ctas) / 2 * 2);
 }
 
-// After the GEMM was enqueued on `st` (following ev_ready recorded just before it): orders `st`
-// after every unit of every rank of the launch. With a reducer, the reducer runs on the side stream
-// concurrently with the GEMM (it starts only after the work that preceded the GEMM on `st`, so it
-// never holds SMs a preceding kernel still needs).
+// After the GEMM was enqueued on `st` (following ev_ready recorded just before it): the reducer runs
+// on the side stream concurrently with the GEMM (it starts only after the work that preceded the
+// GEMM on `st`, so it never holds SMs a preceding kernel still needs); `st` is then ordered after
+// every rank's reducer by the completion counter.
 void fused_ar_end(mt_ctx* c, cudaStream_t st, void* d, int64_t ldd) {
+  (void)d;
   FusedAllReduce* f = c->fused_ar;
   const uint32_t* counter = static_cast<const uint32_t*>(f->flags);
-  if (f->desc.groups > 0 && f->desc.group_cols > 0) {
-    const int groups = static_cast<int>((f->desc.geom[5] + f->desc.group_cols - 1) / f->desc.group_cols);
-    const uint32_t base = f->target;
-    f->target = base + static_cast<uint32_t>(c->par.tensor * (groups + f->reducer_ctas));
-    check_cuda(cudaStreamWaitEvent(c->comm, c->ev_ready, 0), "cudaStreamWaitEvent");
-    if (mt_gemm_allreduce_reduce_groups(&f->desc, ldd, f->desc.flags_local, counter, base, f->reducer_ctas, c->comm) !=
-        0)
-      throw RuntimeFailure("mt_gemm_allreduce_reduce_groups failed");
-    check_cuda(cudaEventRecord(c->ev_done, c->comm), "cudaEventRecord");
-    check_cuda(cudaStreamWaitEvent(st, c->ev_done, 0), "cudaStreamWaitEvent");
-    if (mt_gemm_allreduce_wait(counter, f->target, st) != 0) throw RuntimeFailure("mt_gemm_allreduce_wait failed");
-    return;
-  }
-  f->target += static_cast<uint32_t>(f->desc.units);
-  if (f->reducer_ctas == 0) {
-    if (mt_gemm_allreduce_wait(counter, f->target, st) != 0) throw RuntimeFailure("mt_gemm_allreduce_wait failed");
-    return;
-  }
-  if (f->serial) {
-    op_mark(c, st, "fwd.fused_gemm_only");
-    if (mt_gemm_allreduce_reduce(&f->desc, d, ldd, counter, f->target, f->reducer_ctas, st) != 0)
-      throw RuntimeFailure("mt_gemm_allreduce_reduce failed");
-    op_mark(c, st, "fwd.fused_reducer_only");
-    return;
-  }
+  if (f->desc.group_cols <= 0) throw RuntimeFailure("fused GEMM + all-reduce: column-group geometry missing");
+  const int groups = static_cast<int>((f->desc.geom[5] + f->desc.group_cols - 1) / f->desc.group_cols);
+  const uint32_t base = f->target;
+  f->target = base + static_cast<uint32_t>(c->par.tensor * (groups + f->reducer_ctas));
   check_cuda(cudaStreamWaitEvent(c->comm, c->ev_ready, 0), "cudaStreamWaitEvent");
-  if (mt_gemm_allreduce_reduce(&f->desc, d, ldd, counter, f->target, f->reducer_ctas, c->comm) != 0)
-    throw RuntimeFailure("mt_gemm_allreduce_reduce failed");
+  if (mt_gemm_allreduce_reduce_groups(&f->desc, ldd, f->desc.group_counters, counter, base, f->reducer_ctas, c->comm) !=
+      0)
+    throw RuntimeFailure("mt_gemm_allreduce_reduce_groups failed");
   check_cuda(cudaEventRecord(c->ev_done, c->comm), "cudaEventRecord");
   check_cuda(cudaStreamWaitEvent(st, c->ev_done, 0), "cudaStreamWaitEvent");
+  if (mt_gemm_allreduce_wait(&f->desc, counter, f->target, st) != 0) throw RuntimeFailure("mt_gemm_allreduce_wait failed");
 }
 
 // ---- diagnostic: raw NVLS all-reduce throughput over the symmetric buffer (mt_ctx_nvls_probe)
@@ -253,14 +225,14 @@ extern "C" int mt_ctx_nvls_probe(mt_ctx* c, int64_t elems, int64_t ld, int32_t s
 namespace {
 __global__ void __launch_bounds__(1024) nvls_allreduce_kernel(__nv_bfloat16* mc, uint32_t* counter_mc,
                                                               const uint32_t* counter_local, uint32_t entry_target,
-                                                              long long elems, int rank, int ranks) {
+                                                              long long elems, int rank, int ranks, uint32_t* err,
+                                                              unsigned long long timeout_ns) {
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) {
       fence_acq_rel_sys();
       multimem_red_release_add_u32(counter_mc, 1u);
     }
-    while ((int)(ld_acquire_sys_u32(counter_local) - entry_target) < 0) {
-    }
+    bounded_wait_geq<true>(counter_local, entry_target, err, timeout_ns);
   }
   __syncthreads();
   const long long chunks = elems / 8, per = (chunks + ranks - 1) / ranks, c0 = per * rank;
@@ -292,14 +264,15 @@ __global__ void __launch_bounds__(1024) nvls_allreduce_kernel(__nv_bfloat16* mc,
 void nvls_allreduce(mt_ctx* c, int64_t elems, cudaStream_t st) {
   FusedAllReduce* f = c->fused_ar;
   if (f->z != c->sym_h[0].ptr) resolve(c, f);
-  const int ctas = f->nvls_ctas > 0 ? f->nvls_ctas : std::max(1, f->reducer_ctas > 0 ? f->reducer_ctas : 16);
+  const int ctas = f->nvls_ctas > 0 ? f->nvls_ctas : f->reducer_ctas;
   const uint32_t entry = f->target + static_cast<uint32_t>(c->par.tensor);
   f->target = entry + static_cast<uint32_t>(c->par.tensor * ctas);
   nvls_allreduce_kernel<<<ctas, 1024, 0, st>>>(static_cast<__nv_bfloat16*>(f->desc.d_multicast),
                                                f->desc.counter_multicast, static_cast<const uint32_t*>(f->flags),
-                                               entry, elems, c->place.tensor, c->par.tensor);
+                                               entry, elems, c->place.tensor, c->par.tensor, c->err_dev,
+                                               c->timeout_ns);
   check_cuda(cudaGetLastError(), "nvls_allreduce");
-  if (mt_gemm_allreduce_wait(static_cast<const uint32_t*>(f->flags), f->target, st) != 0)
+  if (mt_gemm_allreduce_wait(&f->desc, static_cast<const uint32_t*>(f->flags), f->target, st) != 0)
     throw RuntimeFailure("mt_gemm_allreduce_wait failed");
 }
 

@@ -50,6 +50,15 @@ class Context:
         """Megatron sequence parallelism for TP > 1 (layer inputs/outputs become this rank's token rows)."""
         check(lib().mt_ctx_set_sequence_parallel(self._h, int(enable)))
 
+    def wait(self, stream=None) -> None:
+        """Bounded wait for `stream` (status 2 / DataError if a peer rank is dead or diverged)."""
+        check(lib().mt_ctx_wait(self._h, _stream(stream)))
+
+    def error_state(self) -> int:
+        v = C.c_int32()
+        check(lib().mt_ctx_error(self._h, C.byref(v)))
+        return v.value
+
     def placement(self) -> RankPlacement:
         p = RankPlacement()
         check(lib().mt_ctx_placement(self._h, C.byref(p)))

@@ -128,14 +128,16 @@ def test_gemm_causal_modes(causal):
 @pytest.mark.parametrize("max_ctas", [0, 132, 40])
 def test_gemm_split_k_tail(epi, max_ctas):
     """Shapes whose last wave is partial take the split-K tail path (partials + last-arriver reduce);
-    the tail is split only for K >= 256 k-blocks (16384)."""
+    the tail is split only for K >= 256 k-blocks (16384). The last arriver sums the splits' partials in
+    a fixed order, so repeated launches are bit-identical."""
     m, n, k = 2048, 12288, 16384
     A = torch.randn(m, k, device="cuda").bfloat16()
     B = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
     bias = torch.randn(n, device="cuda").bfloat16()
     ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
     ref = A.float() @ B.float().t()
-    for _ in range(2):  # second launch checks the counters were reset
+    outs = []
+    for _ in range(3):  # later launches check the counters were reset and the sum order is fixed
         if epi == N.EPI_ACCUM_F32:
             D = torch.ones(m, n, device="cuda")
             _gemm(A, B, D, m, n, k, epi=epi, ws=ws, max_ctas=max_ctas)
@@ -150,41 +152,10 @@ def test_gemm_split_k_tail(epi, max_ctas):
             D = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
             _gemm(A, B, D, m, n, k, ws=ws, max_ctas=max_ctas)
             _close(D, ref)
+        outs.append(D.clone())
     assert int(ws[: 64 * 1024].sum()) == 0  # counters left zeroed
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int16) if o.dtype == torch.bfloat16 else o.view(torch.int32),
+                           outs[0].view(torch.int16) if o.dtype == torch.bfloat16 else outs[0].view(torch.int32))
 
 
-@pytest.mark.parametrize("bn", [128, 256])
-@pytest.mark.parametrize("causal", [0, 1])
-def test_gemm_rowstats_epilogue(bn, causal):
-    """MT_EPI_STORE_BF16_ROWSTATS (the score GEMM of the one-pass softmax): D as STORE_BF16, plus per
-    (row, bn-column block) {max, sum exp(x - max)} of the stored bf16 values, causal columns <= row."""
-    heads, s, hd = 3, 512, 64
-    g = torch.Generator(device="cuda").manual_seed(7)
-    Q = torch.randn(heads, s, hd, device="cuda", generator=g).bfloat16()
-    K = torch.randn(heads, s, hd, device="cuda", generator=g).bfloat16()
-    D = torch.zeros(heads, s, s, device="cuda", dtype=torch.bfloat16)
-    nblk = s // bn
-    stats = torch.full((heads, s, nblk, 2), float("nan"), device="cuda")
-    alpha = 0.125
-    _gemm(Q, K, D, s, s, hd, batch=heads, abs_=s * hd, bbs=s * hd, dbs=s * s, alpha=alpha,
-          epi=N.EPI_STORE_BF16_ROWSTATS, causal=causal, aux=stats, ld_aux=nblk, bn=bn)
-    ref = alpha * Q.float() @ K.float().transpose(1, 2)
-    mask = torch.ones(s, s, device="cuda", dtype=torch.bool).tril() if causal else None
-    if causal:
-        _close(D.float() * mask, ref * mask)
-    else:
-        _close(D, ref)
-    Df = D.float()
-    for t in range(nblk):
-        blk = Df[:, :, t * bn:(t + 1) * bn]
-        valid = torch.ones_like(blk, dtype=torch.bool)
-        if causal:
-            cols = torch.arange(t * bn, (t + 1) * bn, device="cuda")
-            valid = (cols[None, :] <= torch.arange(s, device="cuda")[:, None]).expand_as(blk)
-        rows = valid.any(-1)  # rows with at least one causal entry in this block
-        m = torch.where(valid, blk, torch.tensor(float("-inf"), device="cuda")).amax(-1)
-        l = torch.where(valid, torch.exp(blk - m[..., None]), torch.zeros_like(blk)).sum(-1)
-        got = stats[:, :, t]
-        computed = rows if not causal else rows  # (blocks above the diagonal tile are skipped)
-        assert torch.allclose(got[..., 0][computed], m[computed], rtol=0, atol=1e-6)
-        assert torch.allclose(got[..., 1][computed], l[computed], rtol=1e-4, atol=1e-4)

@@ -124,12 +124,15 @@ def test_layer_rejects_bad_config():
     ctx.close()
 
 
+@pytest.mark.parametrize("shape", [(1024, 8, 256, 2), (4096, 32, 2048, 2)], ids=["h1024", "h4096_splitk"])
 @pytest.mark.parametrize("fused", [False, True], ids=["unfused_attn", "flash_attn"])
-def test_activation_recompute_is_bit_identical(fused, monkeypatch):
+def test_activation_recompute_is_bit_identical(fused, shape, monkeypatch):
     """with recompute the backward re-runs the forward (same dropout masks) — the
-    outputs, input gradients and parameter gradients must be bit-identical to the stored path."""
+    outputs, input gradients and parameter gradients must be bit-identical to the stored path. The
+    h=4096, M=4096 case runs fc2 forward / fc1 dgrad (K = 16384) through the split-K tail (256 pair
+    tiles = 3 waves + 34), whose fixed-order partial sum keeps the re-run bit-identical."""
     monkeypatch.setenv("MT_ATTN_FUSED", "1" if fused else "0")
-    hidden, heads, seq, mb = 1024, 8, 256, 2
+    hidden, heads, seq, mb = shape
     out = []
     for rc in (False, True):
         ctx = Context(0)

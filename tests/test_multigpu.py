@@ -144,6 +144,53 @@ def _worker(rank, world, port, mode, q):
                 c2.close()
             os.environ.pop("MT_TP_FUSED", None)
             os.environ.pop("MT_TP_NVLS", None)
+        elif mode == "peer_hangs":
+            # rank 1 builds the same TP=2 stage, then stops taking part (a hung / diverged peer); rank 0's
+            # iteration must come back with status 2 within the context's bound (MT_COMM_TIMEOUT_S) —
+            # its NCCL all-reduces are released by the host watchdog's ncclCommAbort, the fused
+            # GEMM + NVLS reducer (fc2, K = 4h/2 = 4096) by the device-side bounded waits
+            import time
+            from paper_2201_11990_b200._native import DataError
+            ctx.init_comm(obj[0], world, rank, tensor=world, batch=1, micro_batches=1)
+            hh = 2048
+            st = Stage(ctx, PL.layer_desc(hh, 16, S, B, seed=SEED), 1, 1)
+            st.init_params(1, s)
+            torch.cuda.synchronize()
+            dist.barrier()
+            if rank == 1:
+                time.sleep(float(os.environ["MT_COMM_TIMEOUT_S"]) * 4 + 20)
+                out["status"] = "idle peer"
+                q.put((rank, out))
+                q.close()
+                q.join_thread()  # flush the result before the hard exit
+                os._exit(0)  # never touch the communicators again
+            xh = torch.zeros(B * S, hh, dtype=torch.bfloat16).pin_memory()
+            print("[peer_hangs] rank 0 starts its step alone", flush=True)
+            import faulthandler
+            faulthandler.dump_traceback_later(90, exit=False)  # where the step blocks, if the bound fails
+            t0 = time.monotonic()
+            try:
+                st.train_step(xh.data_ptr(), xh.data_ptr(), s)
+                out["status"] = "completed"
+            except DataError as e:
+                out["status"], out["msg"] = 2, str(e)
+            out["secs"] = time.monotonic() - t0
+            print(f"[peer_hangs] rank 0 step returned after {out['secs']:.1f}s: {out['status']}", flush=True)
+            out["state"] = ctx.error_state()
+            faulthandler.dump_traceback_later(30, exit=False)
+            # the GPU must still make progress after the abort (nothing left spinning on it)
+            probe = torch.ones(1 << 20, device="cuda")
+            out["gpu_alive"] = float((probe * 2).sum().item()) == 2.0 * (1 << 20)
+            print("[peer_hangs] gpu alive", out["gpu_alive"], flush=True)
+            st.close()
+            print("[peer_hangs] stage closed", flush=True)
+            ctx.close()
+            print("[peer_hangs] context closed", flush=True)
+            faulthandler.cancel_dump_traceback_later()
+            q.put((rank, out))
+            q.close()
+            q.join_thread()
+            os._exit(0)
         elif mode in ("tp", "tp_sp"):
             ctx.init_comm(obj[0], world, rank, tensor=world)
             sp = mode == "tp_sp"
@@ -479,3 +526,18 @@ def test_two_axis_layouts_four_gpus(layout):
                 for li in range(2):
                     for i in range(12):
                         assert np.array_equal(res[r]["grads"][li][i], res[q]["grads"][li][i]), (r, q, li, i)
+
+
+@pytest.mark.timeout(240)
+def test_hung_peer_surfaces_as_status_2(monkeypatch):
+    """a peer that stops participating must not wedge the GPU. With a 10 s bound, rank
+    0's training step returns status 2 (DataError) within the bound (+ drain), and the context reports
+    its communicators aborted."""
+    _need(2)
+    monkeypatch.setenv("MT_COMM_TIMEOUT_S", "10")
+    res = _run("peer_hangs")
+    r0 = res[0]
+    assert r0["status"] == 2, r0
+    assert r0["secs"] < 10 + 5 + 60, r0
+    assert r0["state"] == 3 and r0["gpu_alive"], r0
+    assert "peer" in r0["msg"], r0
