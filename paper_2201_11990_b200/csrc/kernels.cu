@@ -77,6 +77,32 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return warp_sum(t);
 }
 
+// Dropout stream in Weyl form: curator::dropout_bits(site, g) = splitmix64(site + g * gamma) =
+// sm64_final(weyl(site, g)) with weyl = site + (g + 1) * gamma, so consecutive groups of 4 elements
+// are one 64-bit add apart (the softmax kernels walk their row's groups without a 64-bit multiply
+// per group).
+__device__ __forceinline__ uint64_t drop_weyl(uint64_t site, uint64_t group) {
+  return site + (group + 1) * curator::kSplitMixGamma;
+}
+__device__ __forceinline__ uint64_t sm64_final(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+// o[j] = keep_j ? x[j] * mul : 0 for the 8 elements of groups (z, z + gamma): keep_j is the 16-bit
+// field j & 3 of the group's 64 bits >= thresh16, compared and selected directly.
+__device__ __forceinline__ void drop_scale8(uint64_t z, uint32_t thresh16, const float (&x)[8], float mul,
+                                            float (&o)[8]) {
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const uint64_t b = sm64_final(z + (uint64_t)g * curator::kSplitMixGamma);
+    const uint32_t lo = (uint32_t)b, hi = (uint32_t)(b >> 32);
+    const uint32_t u[4] = {lo & 0xffffu, lo >> 16, hi & 0xffffu, hi >> 16};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[4 * g + q] = u[q] >= thresh16 ? x[4 * g + q] * mul : 0.f;
+  }
+}
+
 // Drop mask for 8 consecutive elements starting at idx (idx % 4 == 0): two SplitMix64 groups
 // (include/curator/dropout.hpp).
 __device__ __forceinline__ uint32_t keep_mask8(uint64_t seed, uint64_t idx, uint32_t thresh16) {
@@ -375,13 +401,20 @@ __device__ __forceinline__ float ex2_recompute(float x) {
   return y;
 }
 
-// Full 8-score vectors (v < nvalid / 8) take a branch-free path; only the row's last, partial
-// vector pays the per-element causal checks (the kernels were issue-bound on those checks).
+// One warp per score row (VPL 8-score vectors per lane). The row's causal tail (columns > i) and the
+// lanes past it are set to -inf, so the passes need no per-element causal checks:
+//   max   on packed bf16x2 (one HMNMX2 per two scores; exact, the scores are bf16),
+//   exp2  once per score in fp32 (kept in registers for rows up to 2048 columns), summed,
+//   P     = keep ? e * (scale / sum) : 0, packed to bf16.
+// ~13 instructions per score vs ~21 for three unpacking passes with a recomputed exp (the kernel was
+// issue-bound at 0.39 of HBM roofline, ncu profiles/r02_hbm_ncu.md).
 template <int VPL>
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(const uint4* __restrict__ S, uint4* __restrict__ P,
                                                           float* __restrict__ lse, int rows_total, int seq,
                                                           long long head_base, uint64_t seed, uint32_t thresh16,
                                                           float scale) {
+  constexpr bool kKeep = VPL <= 8;  // fp32 exps stay in registers (64 per lane at most)
+  constexpr uint32_t kNegInf2 = 0xff80ff80u;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows_total) return;
@@ -391,72 +424,76 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const uint4* __restric
   uint4* prow = P + (size_t)warp * nvec_row;
   const int nvalid = i + 1, nvec = (nvalid + 7) >> 3, nfull = nvalid >> 3, rem = nvalid & 7;
   uint4 raw[VPL];
-  float mx = -INFINITY;
 #pragma unroll
   for (int t = 0; t < VPL; ++t) {
     const int v = lane + 32 * t;
-    raw[t] = v < nvec ? srow[v] : make_uint4(0, 0, 0, 0);
-  }
+    raw[t] = v < nvec ? srow[v] : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
+    if (v == nfull && rem != 0) {  // causal tail: scores j >= rem of the row's last vector -> -inf
+      uint32_t w[4] = {raw[t].x, raw[t].y, raw[t].z, raw[t].w};
 #pragma unroll
-  for (int t = 0; t < VPL; ++t) {
-    const int v = lane + 32 * t;
-    if (v < nvec) {
-      float x[8];
-      unpack8_v(raw[t], x);
-      if (v < nfull) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) mx = fmaxf(mx, x[j]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < rem) mx = fmaxf(mx, x[j]);
+      for (int q = 0; q < 4; ++q) {
+        if (2 * q >= rem) w[q] = kNegInf2;
+        else if (2 * q + 1 >= rem) w[q] = (w[q] & 0xffffu) | 0xff800000u;
       }
+      raw[t] = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
-  mx = warp_max(mx);
+  __nv_bfloat162 m2v = __halves2bfloat162(__ushort_as_bfloat16(0xff80), __ushort_as_bfloat16(0xff80));
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    const uint32_t w[4] = {raw[t].x, raw[t].y, raw[t].z, raw[t].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) m2v = __hmax2(m2v, *reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+  }
+  const float mx = warp_max(fmaxf(__low2float(m2v), __high2float(m2v)));
   const float mx2 = mx * kLog2e;
+  float e[kKeep ? VPL : 1][8];
   float sum = 0.f;
 #pragma unroll
   for (int t = 0; t < VPL; ++t) {
-    const int v = lane + 32 * t;
-    if (v < nvec) {
+    if (lane + 32 * t < nvec) {
       float x[8];
       unpack8_v(raw[t], x);
-      if (v < nfull) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) sum += ex2_recompute(fmaf(x[j], kLog2e, -mx2));
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < rem) sum += ex2_recompute(fmaf(x[j], kLog2e, -mx2));
+      for (int j = 0; j < 8; ++j) {
+        const float ej = ex2_recompute(fmaf(x[j], kLog2e, -mx2));  // exp2(-inf) = 0 on the causal tail
+        sum += ej;
+        if constexpr (kKeep) e[t][j] = ej;
       }
     }
   }
   sum = warp_sum(sum);
-  const float l = mx + logf(sum);
-  const float l2 = l * kLog2e;
+  const float inv = scale / sum;
   const uint64_t base_idx = ((uint64_t)(head_base + bh) * seq + i) * (uint64_t)seq;
+  // this lane's first group; its later vectors are 32 * 2 groups further each
+  uint64_t z = drop_weyl(seed, (base_idx >> 2) + 2 * (uint64_t)lane);
+  const uint64_t z_step = 64 * curator::kSplitMixGamma;
 #pragma unroll
-  for (int t = 0; t < VPL; ++t) {
+  for (int t = 0; t < VPL; ++t, z += z_step) {
     const int v = lane + 32 * t;
     if (v < nvec) {
-      uint32_t keep = keep_mask8(seed, base_idx + v * 8, thresh16);
-      if (v == nfull) keep &= (1u << rem) - 1u;  // causal tail of the row
       float x[8], o[8];
-      unpack8_v(raw[t], x);
+      if constexpr (kKeep) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float e = ex2_recompute(fmaf(x[j], kLog2e, -l2)) * scale;
-        o[j] = ((keep >> j) & 1u) ? e : 0.f;
+        for (int j = 0; j < 8; ++j) x[j] = e[t][j];
+      } else {
+        unpack8_v(raw[t], x);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = ex2_recompute(fmaf(x[j], kLog2e, -mx2));
+      }
+      if (thresh16 != 0) {
+        drop_scale8(z, thresh16, x, inv, o);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = x[j] * inv;
       }
       prow[v] = pack8(o);
     }
   }
   const int zend = min(seq, (i / 256 + 1) * 256) >> 3;
   for (int v = nvec + lane; v < zend; v += 32) prow[v] = make_uint4(0, 0, 0, 0);
-  if (lane == 0) lse[warp] = l;
+  if (lane == 0) lse[warp] = mx + logf(sum);
 }
-
 
 __global__ void __launch_bounds__(256) softmax_bwd_rowdot_kernel(const uint4* __restrict__ S,
                                                                   const float* __restrict__ lse,
@@ -475,17 +512,22 @@ __global__ void __launch_bounds__(256) softmax_bwd_rowdot_kernel(const uint4* __
   const float l2 = lse[warp] * kLog2e;
   const float dot = D[warp];
   const uint64_t base_idx = ((uint64_t)(head_base + bh) * seq + i) * (uint64_t)seq;
-  for (int v = lane; v < nvec; v += 32) {
-    const uint32_t keep = keep_mask8(seed, base_idx + v * 8, thresh16);
+  uint64_t z = drop_weyl(seed, (base_idx >> 2) + 2 * (uint64_t)lane);  // Weyl state of this lane's groups
+  for (int v = lane; v < nvec; v += 32, z += 64 * curator::kSplitMixGamma) {
     const uint32_t valid = v < nfull ? 0xffu : (1u << rem) - 1u;
-    float sv[8], g[8], o[8];
+    float sv[8], g[8], gk[8], o[8];
     unpack8(srow[v], sv);
     unpack8(drow[v], g);
+    if (thresh16 != 0) {
+      drop_scale8(z, thresh16, g, scale, gk);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) gk[j] = g[j] * scale;
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float y = ex2_recompute(fmaf(sv[j], kLog2e, -l2));
-      const float gj = ((keep >> j) & 1u) ? g[j] * scale : 0.f;
-      o[j] = ((valid >> j) & 1u) ? alpha * y * (gj - dot) : 0.f;
+      o[j] = ((valid >> j) & 1u) ? alpha * y * (gk[j] - dot) : 0.f;
     }
     drow[v] = pack8(o);
   }

@@ -120,49 +120,35 @@ __device__ __forceinline__ Ring make_ring(uint8_t* smem, int stages, int nin, ui
   return r;
 }
 
-// LayerNorm of one row held in smem (bf16 [h]): y = (x - mean) * rstd * gamma + beta.
-__device__ __forceinline__ void ln_row(const uint4* xs, const uint4* __restrict__ gamma, const uint4* __restrict__ beta,
-                                       uint4* __restrict__ y, float* mean_out, float* rstd_out, int nvec, float inv_h,
-                                       float eps, float* red) {
-  float s = 0.f;
-  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-    float x[8];
-    unpack8f(xs[v], x);
+// Forward row kernels: every thread owns the fixed vectors v = tid + i*T (i < VPT) of every row, so the
+// per-column parameters (gamma, beta, bias) are loaded once per CTA into registers, each row is
+// unpacked from smem into fp32 registers once, and the LayerNorm needs a single block reduction per
+// row: shifted sums s1 = sum(x - c), s2 = sum((x - c)^2) around c = the row's first element
+// (mean = c + s1/h, var = s2/h - (s1/h)^2, robust to a large row mean). The ring slot is handed back
+// to the bulk-copy engine right after that reduction (all reads of the row happened before it).
+// 1 + ~9 instructions per element vs ~21 for the three-pass smem version (ncu: issue-bound at 0.5
+// of HBM roofline, profiles/r02_hbm_ncu.md).
+template <int VPT>
+__device__ __forceinline__ void load_params(const uint4* __restrict__ p, uint4 (&out)[VPT], int nvec, int T) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) s += x[j];
-  }
-  const float mu = row_sum(s, red) * inv_h;
-  float q = 0.f;
-  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-    float x[8];
-    unpack8f(xs[v], x);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) q += (x[j] - mu) * (x[j] - mu);
-  }
-  const float rs = rsqrtf(row_sum(q, red) * inv_h + eps);
-  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-    float x[8], g[8], b[8], o[8];
-    unpack8f(xs[v], x);
-    unpack8f(__ldg(gamma + v), g);
-    unpack8f(__ldg(beta + v), b);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = (x[j] - mu) * rs * g[j] + b[j];
-    y[v] = pack8f(o);
-  }
-  if (threadIdx.x == 0) {
-    *mean_out = mu;
-    *rstd_out = rs;
+  for (int i = 0; i < VPT; ++i) {
+    const int v = (int)threadIdx.x + i * T;
+    out[i] = v < nvec ? __ldg(p + v) : make_uint4(0, 0, 0, 0);
   }
 }
 
-__global__ void __launch_bounds__(kRowThreads, 1)
-    ln_fwd_rows_kernel(const uint4* __restrict__ x, const uint4* __restrict__ gamma, const uint4* __restrict__ beta,
-                       uint4* __restrict__ y, float* __restrict__ mean, float* __restrict__ rstd, int rows, int nvec,
-                       float inv_h, float eps, int stages) {
+template <int T, int VPT>
+__global__ void __launch_bounds__(T) ln_fwd_rows_kernel(const uint4* __restrict__ x, const uint4* __restrict__ gamma,
+                                                        const uint4* __restrict__ beta, uint4* __restrict__ y,
+                                                        float* __restrict__ mean, float* __restrict__ rstd, int rows,
+                                                        int nvec, float inv_h, float eps, int stages) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ float red[32];
+  __shared__ float2 red2[32];
   const Ring ring = make_ring(smem, stages, 1, (uint32_t)nvec * 16);
   const void* src[1] = {x};
+  uint4 gp[VPT], bp[VPT];
+  load_params<VPT>(gamma, gp, nvec, T);
+  load_params<VPT>(beta, bp, nvec, T);
   const int nk = rows > (int)blockIdx.x ? (rows - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   if (threadIdx.x == 0)
     for (int k = 0; k < min(stages, nk); ++k) ring.issue(k, src, blockIdx.x + (long long)k * gridDim.x);
@@ -170,24 +156,74 @@ __global__ void __launch_bounds__(kRowThreads, 1)
     const int s = k % stages;
     const long long row = blockIdx.x + (long long)k * gridDim.x;
     mbar_wait(smem_u32(&ring.bar[s]), (k / stages) & 1);
-    ln_row(reinterpret_cast<const uint4*>(ring.slot(s, 0)), gamma, beta, y + row * nvec, mean + row, rstd + row, nvec,
-           inv_h, eps, red);
-    __syncthreads();  // slot s fully consumed
+    const uint4* xs = reinterpret_cast<const uint4*>(ring.slot(s, 0));
+    uint4 xp[VPT];  // the row stays packed (bf16) in registers: 4 registers per 8 values
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int v = (int)threadIdx.x + i * T;
+      xp[i] = v < nvec ? xs[v] : make_uint4(0, 0, 0, 0);
+    }
+    const float c = __uint_as_float(reinterpret_cast<const uint32_t*>(xs)[0] << 16);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      if ((int)threadIdx.x + i * T < nvec) {
+        float o[8];
+        unpack8f(xp[i], o);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float d = o[j] - c;
+          s1 += d;
+          s2 = fmaf(d, d, s2);
+        }
+      }
+    }
+    // the reduction is also the barrier after which every thread has read slot s: refill it now
+    const float2 t = row_sum2(s1, s2, red2);
     if (threadIdx.x == 0 && k + stages < nk) ring.issue(s, src, blockIdx.x + (long long)(k + stages) * gridDim.x);
+    const float md = t.x * inv_h;
+    const float mu = c + md;
+    const float rs = rsqrtf(fmaxf(t.y * inv_h - md * md, 0.f) + eps);
+    const float nmr = -mu * rs;
+    uint4* yr = y + row * nvec;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int v = (int)threadIdx.x + i * T;
+      if (v < nvec) {
+        float o[8], g[8], b[8], r[8];
+        unpack8f(xp[i], o);
+        unpack8f(gp[i], g);
+        unpack8f(bp[i], b);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = fmaf(fmaf(o[j], rs, nmr), g[j], b[j]);
+        yr[v] = pack8f(r);
+      }
+    }
+    if (threadIdx.x == 0) {
+      mean[row] = mu;
+      rstd[row] = rs;
+    }
   }
 }
 
-// out = resid + dropout(z + bias) (written), then optionally y = LayerNorm(out).
-__global__ void __launch_bounds__(kRowThreads, 1)
+// out = resid + dropout(z + bias) (written), then optionally y = LayerNorm(out) from the same registers.
+template <int T, int VPT, bool kLN>
+__global__ void __launch_bounds__(T)
     bdr_ln_rows_kernel(const uint4* __restrict__ z, const uint4* __restrict__ bias, const uint4* __restrict__ resid,
                        uint4* __restrict__ out, const uint4* __restrict__ gamma, const uint4* __restrict__ beta,
                        uint4* __restrict__ y, float* __restrict__ mean, float* __restrict__ rstd, int rows, int nvec,
                        float inv_h, float eps, uint64_t seed, uint32_t thresh16, float scale, uint64_t elem_offset,
                        int stages) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ float red[32];
+  __shared__ float2 red2[32];
   const Ring ring = make_ring(smem, stages, 2, (uint32_t)nvec * 16);
   const void* src[2] = {z, resid};
+  uint4 bi[VPT], gp[kLN ? VPT : 1], bp[kLN ? VPT : 1];
+  load_params<VPT>(bias, bi, nvec, T);
+  if constexpr (kLN) {
+    load_params<VPT>(gamma, gp, nvec, T);
+    load_params<VPT>(beta, bp, nvec, T);
+  }
   const int nk = rows > (int)blockIdx.x ? (rows - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   if (threadIdx.x == 0)
     for (int k = 0; k < min(stages, nk); ++k) ring.issue(k, src, blockIdx.x + (long long)k * gridDim.x);
@@ -195,26 +231,75 @@ __global__ void __launch_bounds__(kRowThreads, 1)
     const int s = k % stages;
     const long long row = blockIdx.x + (long long)k * gridDim.x;
     mbar_wait(smem_u32(&ring.bar[s]), (k / stages) & 1);
-    uint4* zs = reinterpret_cast<uint4*>(ring.slot(s, 0));
+    const uint4* zs = reinterpret_cast<const uint4*>(ring.slot(s, 0));
     const uint4* rs_ = reinterpret_cast<const uint4*>(ring.slot(s, 1));
-    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-      float a[8], b[8], r[8], o[8];
-      unpack8f(zs[v], a);
-      unpack8f(__ldg(bias + v), b);
-      unpack8f(rs_[v], r);
-      const uint32_t keep = keep_mask8_rows(seed, elem_offset + ((uint64_t)row * nvec + v) * 8, thresh16);
+    uint4 ob[VPT];  // the stored (bf16) residual stream, which is what the LayerNorm sees
+    uint4* outr = out + row * nvec;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = r[j] + (((keep >> j) & 1u) ? (a[j] + b[j]) * scale : 0.f);
-      const uint4 packed = pack8f(o);
-      out[row * nvec + v] = packed;
-      zs[v] = packed;  // LN input (each thread rewrites only its own vectors)
+    for (int i = 0; i < VPT; ++i) {
+      const int v = (int)threadIdx.x + i * T;
+      ob[i] = make_uint4(0, 0, 0, 0);
+      if (v < nvec) {
+        float a[8], b[8], r[8], o[8];
+        unpack8f(zs[v], a);
+        unpack8f(bi[i], b);
+        unpack8f(rs_[v], r);
+        const uint32_t keep = keep_mask8_rows(seed, elem_offset + ((uint64_t)row * nvec + v) * 8, thresh16);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = r[j] + (((keep >> j) & 1u) ? (a[j] + b[j]) * scale : 0.f);
+        ob[i] = pack8f(o);
+        outr[v] = ob[i];
+      }
     }
-    if (gamma != nullptr) {
+    if constexpr (!kLN) {
+      __syncthreads();  // every thread read slot s
+      if (threadIdx.x == 0 && k + stages < nk) ring.issue(s, src, blockIdx.x + (long long)(k + stages) * gridDim.x);
+      continue;
+    } else {
+      // shift: the row's first output element (thread 0 owns vector 0); broadcast through smem
+      __shared__ float c_sh;
+      if (threadIdx.x == 0) c_sh = __uint_as_float(ob[0].x << 16);
+      float s1 = 0.f, s2 = 0.f;
       __syncthreads();
-      ln_row(zs, gamma, beta, y + row * nvec, mean + row, rstd + row, nvec, inv_h, eps, red);
+      const float c = c_sh;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        if ((int)threadIdx.x + i * T < nvec) {
+          float o[8];
+          unpack8f(ob[i], o);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float d = o[j] - c;
+            s1 += d;
+            s2 = fmaf(d, d, s2);
+          }
+        }
+      }
+      const float2 t = row_sum2(s1, s2, red2);  // also: every thread finished reading slot s
+      if (threadIdx.x == 0 && k + stages < nk) ring.issue(s, src, blockIdx.x + (long long)(k + stages) * gridDim.x);
+      const float md = t.x * inv_h;
+      const float mu = c + md;
+      const float rs = rsqrtf(fmaxf(t.y * inv_h - md * md, 0.f) + eps);
+      const float nmr = -mu * rs;
+      uint4* yr = y + row * nvec;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        const int v = (int)threadIdx.x + i * T;
+        if (v < nvec) {
+          float o[8], g[8], b[8], r[8];
+          unpack8f(ob[i], o);
+          unpack8f(gp[i], g);
+          unpack8f(bp[i], b);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) r[j] = fmaf(fmaf(o[j], rs, nmr), g[j], b[j]);
+          yr[v] = pack8f(r);
+        }
+      }
+      if (threadIdx.x == 0) {
+        mean[row] = mu;
+        rstd[row] = rs;
+      }
     }
-    __syncthreads();
-    if (threadIdx.x == 0 && k + stages < nk) ring.issue(s, src, blockIdx.x + (long long)(k + stages) * gridDim.x);
   }
 }
 
@@ -237,6 +322,8 @@ __global__ void __launch_bounds__(kRowThreads, 1)
   for (int i = 0; i < MAXV; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) dg[i][j] = db[i][j] = 0.f;
+  uint4 gp[MAXV];  // gamma of this thread's vectors, loaded once per CTA
+  load_params<MAXV>(gamma, gp, nvec, kRowThreads);
   const int nk = rows > (int)blockIdx.x ? (rows - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   if (threadIdx.x == 0)
     for (int k = 0; k < min(stages, nk); ++k) ring.issue(k, src, blockIdx.x + (long long)k * gridDim.x);
@@ -255,7 +342,7 @@ __global__ void __launch_bounds__(kRowThreads, 1)
         float d[8], xv[8], g[8];
         unpack8f(dys[v], d);
         unpack8f(xs[v], xv);
-        unpack8f(__ldg(gamma + v), g);
+        unpack8f(gp[i], g);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const float xh = (xv[j] - mu) * rs;
@@ -276,7 +363,7 @@ __global__ void __launch_bounds__(kRowThreads, 1)
         float d[8], xv[8], g[8], o[8];
         unpack8f(dys[v], d);
         unpack8f(xs[v], xv);
-        unpack8f(__ldg(gamma + v), g);
+        unpack8f(gp[i], g);
 #pragma unroll
         for (int j = 0; j < 8; ++j) o[j] = rs * (d[j] * g[j] - m1 - (xv[j] - mu) * rs * m2);
         if (resid != nullptr) {
@@ -333,16 +420,19 @@ bool set_smem(K kern, size_t bytes) {
 
 int row_kernel_ctas(int rows) { return std::max(1, std::min(rows, sm_count())); }
 
-// Element-wise row kernels (no per-thread column state): 256-thread CTAs, as many per SM as the
-// shared-memory ring allows (2-deep rings; more resident warps hide the per-row dependency chains).
+// Forward row kernels: T threads per CTA owning VPT <= 6 vectors (8 bf16) of every row each; as many
+// CTAs per SM as shared memory (3-deep ring) and registers allow.
 struct RowLaunch {
-  int ctas, threads, stages;
+  int ctas, threads, vpt, stages;
   size_t smem;
 };
-RowLaunch small_cta_launch(int rows, int nin, size_t row_bytes) {
+RowLaunch fwd_launch(int rows, int nvec, int nin) {
   RowLaunch l{};
-  l.threads = 256;
-  l.stages = 2;
+  l.threads = nvec <= 3 * 256 ? 256 : 512;  // 512 threads = 16 warps for the wide rows (one CTA per SM)
+  l.vpt = (nvec + l.threads - 1) / l.threads;
+  l.stages = 3;
+  const size_t row_bytes = (size_t)nvec * 16;
+  while (l.stages > 2 && (size_t)l.stages * nin * row_bytes + 64 > (size_t)kRowSmemBudget) --l.stages;
   l.smem = (size_t)l.stages * nin * row_bytes + 64;
   const int per_sm = std::max(1, std::min(4, (int)((227 * 1024) / (l.smem + 1024))));
   l.ctas = std::max(1, std::min(rows, per_sm * sm_count()));
@@ -352,25 +442,82 @@ RowLaunch small_cta_launch(int rows, int nin, size_t row_bytes) {
 bool ln_fwd_rows(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int rows, int h,
                  float eps, cudaStream_t s) {
   const int nvec = h / 8;
-  if (h % 8 || ring_stages(1, (size_t)nvec * 16) == 0) return false;
-  const RowLaunch L = small_cta_launch(rows, 1, (size_t)nvec * 16);
-  if (!set_smem(ln_fwd_rows_kernel, L.smem)) return false;
-  ln_fwd_rows_kernel<<<L.ctas, L.threads, L.smem, s>>>((const uint4*)x, (const uint4*)gamma, (const uint4*)beta,
-                                                      (uint4*)y, mean, rstd, rows, nvec, 1.f / h, eps, L.stages);
-  return cudaGetLastError() == cudaSuccess;
+  if (h % 8 || ring_stages(1, (size_t)nvec * 16) == 0 || nvec > 6 * 512) return false;
+  const RowLaunch L = fwd_launch(rows, nvec, 1);
+  bool ok = true;
+#define LN(T, V)                                                                                                \
+  do {                                                                                                          \
+    ok = set_smem(ln_fwd_rows_kernel<T, V>, L.smem);                                                            \
+    if (ok)                                                                                                     \
+      ln_fwd_rows_kernel<T, V><<<L.ctas, T, L.smem, s>>>((const uint4*)x, (const uint4*)gamma, (const uint4*)beta, \
+                                                          (uint4*)y, mean, rstd, rows, nvec, 1.f / h, eps, L.stages); \
+  } while (0)
+  if (L.threads == 256) {
+    switch (L.vpt) {
+      case 1: LN(256, 1); break;
+      case 2: LN(256, 2); break;
+      default: LN(256, 3); break;
+    }
+  } else {
+    switch (L.vpt) {
+      case 2: LN(512, 2); break;
+      case 3: LN(512, 3); break;
+      case 4: LN(512, 4); break;
+      case 5: LN(512, 5); break;
+      default: LN(512, 6); break;
+    }
+  }
+#undef LN
+  return ok && cudaGetLastError() == cudaSuccess;
 }
 
 bool bdr_ln_rows(const void* z, const void* bias, const void* resid, void* out, const void* gamma, const void* beta,
                  void* y, float* mean, float* rstd, int rows, int h, float eps, uint64_t seed, uint32_t thresh16,
                  float scale, uint64_t elem_offset, cudaStream_t s) {
   const int nvec = h / 8;
-  if (h % 8 || ring_stages(2, (size_t)nvec * 16) == 0) return false;
-  const RowLaunch L = small_cta_launch(rows, 2, (size_t)nvec * 16);
-  if (!set_smem(bdr_ln_rows_kernel, L.smem)) return false;
-  bdr_ln_rows_kernel<<<L.ctas, L.threads, L.smem, s>>>(
-      (const uint4*)z, (const uint4*)bias, (const uint4*)resid, (uint4*)out, (const uint4*)gamma, (const uint4*)beta,
-      (uint4*)y, mean, rstd, rows, nvec, 1.f / h, eps, seed, thresh16, scale, elem_offset, L.stages);
-  return cudaGetLastError() == cudaSuccess;
+  if (h % 8 || ring_stages(2, (size_t)nvec * 16) == 0 || nvec > 6 * 512) return false;
+  const RowLaunch L = fwd_launch(rows, nvec, 2);
+  bool ok = true;
+#define BDR(T, V, LNF)                                                                                                \
+  do {                                                                                                                \
+    ok = set_smem(bdr_ln_rows_kernel<T, V, LNF>, L.smem);                                                             \
+    if (ok)                                                                                                           \
+      bdr_ln_rows_kernel<T, V, LNF><<<L.ctas, T, L.smem, s>>>(                                                        \
+          (const uint4*)z, (const uint4*)bias, (const uint4*)resid, (uint4*)out, (const uint4*)gamma,                 \
+          (const uint4*)beta, (uint4*)y, mean, rstd, rows, nvec, 1.f / h, eps, seed, thresh16, scale, elem_offset,    \
+          L.stages);                                                                                                  \
+  } while (0)
+#define BDR_V256(LNF)                \
+  switch (L.vpt) {                   \
+    case 1: BDR(256, 1, LNF); break; \
+    case 2: BDR(256, 2, LNF); break; \
+    default: BDR(256, 3, LNF); break; \
+  }
+#define BDR_V512(LNF)                \
+  switch (L.vpt) {                   \
+    case 2: BDR(512, 2, LNF); break; \
+    case 3: BDR(512, 3, LNF); break; \
+    case 4: BDR(512, 4, LNF); break; \
+    case 5: BDR(512, 5, LNF); break; \
+    default: BDR(512, 6, LNF); break; \
+  }
+  if (L.threads == 256) {
+    if (gamma != nullptr) {
+      BDR_V256(true)
+    } else {
+      BDR_V256(false)
+    }
+  } else {
+    if (gamma != nullptr) {
+      BDR_V512(true)
+    } else {
+      BDR_V512(false)
+    }
+  }
+#undef BDR_V256
+#undef BDR_V512
+#undef BDR
+  return ok && cudaGetLastError() == cudaSuccess;
 }
 
 // Fused LayerNorm backward (dx and gamma/beta gradients in one pass). ws must hold
