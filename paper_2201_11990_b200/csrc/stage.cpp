@@ -506,6 +506,19 @@ void run_iteration(Step& k, mt_stage* st, void* stream) {
   }  ++st->step;
 }
 
+// A collective that fails because the watchdog aborted the communicators reports why.
+template <class F>
+void run_aborted_aware(mt_ctx* c, F&& f) {
+  try {
+    f();
+  } catch (const std::exception& e) {
+    if (c->aborted)
+      throw mt::RuntimeFailure(std::string("a peer did not respond within the communication bound; the context's "
+                                           "communicators were aborted (") + e.what() + ")");
+    throw;
+  }
+}
+
 }  // namespace
 
 extern "C" int mt_stage_train_step(mt_stage* st, const void* inputs_host, const void* targets_host, float* loss_out,
@@ -518,7 +531,7 @@ extern "C" int mt_stage_train_step(mt_stage* st, const void* inputs_host, const 
     st->h2d_bytes = st->d2h_bytes = 0;
     if (k.lm() && ((k.first() && !inputs_host) || (k.last() && !targets_host)))
       throw std::invalid_argument("a stage with a vocab needs token inputs (first stage) and targets (last stage)");
-    run_iteration(k, st, stream);
+    run_aborted_aware(st->ctx, [&] { run_iteration(k, st, stream); });
     if (loss_out) {
       *st->loss_host = 0.f;
       if (k.last()) {  // pinned destination: an asynchronous copy, so the wait below stays bounded
@@ -543,7 +556,7 @@ extern "C" int mt_stage_train_step_dev(mt_stage* st, const void* inputs_dev, con
     k.tgt_dev = static_cast<const char*>(targets_dev);
     if (k.first() && !k.in_dev) throw std::invalid_argument("first stage needs device inputs");
     if (k.last() && !k.tgt_dev) throw std::invalid_argument("last stage needs device targets");
-    run_iteration(k, st, stream);
+    run_aborted_aware(st->ctx, [&] { run_iteration(k, st, stream); });
     if (loss_dev && k.last())
       mt::check_cuda(cudaMemcpyAsync(loss_dev, st->loss.ptr, 4, cudaMemcpyDeviceToDevice, k.s), "D2D loss");
     st->launches = k.launches;

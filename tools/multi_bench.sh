@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 for cfg in $CFGS; do
   port=$((port + 7))
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
-      --master-port $port bench.py --gpus $N --steps ${STEPS:-5} --warmup 3 --config $cfg \
+      --master-port $port bench.py --gpus $N --steps ${STEPS:-5} --warmup 3 --config $cfg ${EXTRA:-} \
       > gpurun_out/mb_${cfg}_n$N.json 2> gpurun_out/mb_${cfg}_n$N.err
   echo "$cfg rc=$?"
   python - "$cfg" "$N" <<'PY'
