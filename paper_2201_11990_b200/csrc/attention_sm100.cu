@@ -17,8 +17,11 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <type_traits>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "curator/dropout.hpp"
@@ -53,6 +56,8 @@ struct AttnParams {
   __nv_bfloat16* out;     // ctx: row i, head h at out + i * ld_out + h * out_head_stride
   long long ld_out, out_head_stride;
   float* lse;             // [heads][seq]
+  uint32_t* mask;         // optional attention-dropout keep bits [heads][seq][seq / 32] (bit c % 32 of word
+                          // c / 32 = score (row, c) kept); written for the causal blocks only
 };
 
 __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -76,6 +81,33 @@ __device__ __forceinline__ float ex2(float x) {
 // Row r's 16-byte chunk j (of 8 bf16) inside a 128-row, 128 B-per-row SW128 tile.
 __device__ __forceinline__ uint32_t sw128_addr(uint32_t base, uint32_t r, uint32_t j) {
   return base + r * 128 + ((j ^ (r & 7)) << 4);
+}
+
+// Attention-dropout stream in Weyl form (curator::dropout_bits(site, g) = splitmix64(site + g*gamma)):
+// consecutive groups of 4 scores are one 64-bit add apart.
+__device__ __forceinline__ uint64_t drop_weyl_attn(uint64_t site, uint64_t group) {
+  return site + (group + 1) * curator::kSplitMixGamma;
+}
+// pv[t] = keep_t ? e[t] : 0 for the 8 scores of groups (z, z + gamma) (16-bit field t & 3 >= thresh16).
+// Returns the 8 keep bits (bit t = score t kept).
+__device__ __forceinline__ uint32_t drop_select8(uint64_t z, uint32_t thresh16, const float (&e)[8], float (&pv)[8]) {
+  uint32_t keep = 0;
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    uint64_t b = z + (uint64_t)g * curator::kSplitMixGamma;
+    b = (b ^ (b >> 30)) * 0xbf58476d1ce4e5b9ull;
+    b = (b ^ (b >> 27)) * 0x94d049bb133111ebull;
+    b ^= b >> 31;
+    const uint32_t lo = (uint32_t)b, hi = (uint32_t)(b >> 32);
+    const uint32_t u[4] = {lo & 0xffffu, lo >> 16, hi & 0xffffu, hi >> 16};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool k = u[q] >= thresh16;
+      pv[4 * g + q] = k ? e[4 * g + q] : 0.f;
+      keep |= (k ? 1u : 0u) << (4 * g + q);
+    }
+  }
+  return keep;
 }
 
 template <int HD>
@@ -318,6 +350,288 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   if (warp == 2) tmem_dealloc<C::kTmemCols>(tmem);
 }
 
+// ---------------------------------------------------------------- forward, two query tiles per CTA
+// attn_fwd2_kernel<HD> (HD <= 128): one CTA per (head, pair of consecutive 128-row query blocks
+// qa = 2p, qb = 2p + 1), 384 threads:
+//   warp 0        TMA producer: Q_a, Q_b once; then K_j, V_j through a 3-slot ring (K_j, V_j and
+//                 K_{j+1} resident together), shared by both query tiles
+//   warp 1        MMA issuer:  S_x = Q_x K_j^T into S_x's TMEM columns; O_x += P_x V_j
+//   warp 2        TMEM allocator (S_a [0,128), S_b [128,256), O_a [256,384), O_b [384,512))
+//   warps 4..7    softmax of tile a, warps 8..11 softmax of tile b (one row per thread)
+// The two softmax warpgroups alternate with the tensor core (while one computes exps and the
+// dropout mask of block j, the MMAs of the other tile run), which is what the single-tile kernel
+// lacked (it was latency-bound, 0.63 ms for the GPT-3 layer's forward attention). Each row's block
+// is read from TMEM in two 64-column halves (max, then exp / mask / pack) to stay within the 170
+// registers a 384-thread CTA allows. Semantics are attn_fwd_kernel's (online softmax with lazy
+// rescale, counter-based attention dropout, lse in natural log).
+template <int HD>
+struct Fwd2Cfg {
+  static constexpr int kChunks = (HD + 63) / 64;
+  static constexpr int kTileBytes = kChunks * 16384;
+  static constexpr int kPBytes = 2 * 16384;
+  static constexpr int kRing = 3;
+  static constexpr int kSmem = 1024 + kTileBytes * (2 + kRing) + 2 * kPBytes + 256;
+  static_assert(kSmem <= 232448, "fwd2 shared memory");
+  static_assert(HD <= 128, "fwd2 TMEM layout holds two 128-column accumulators");
+};
+constexpr int kFwd2Threads = 384;
+
+template <int HD>
+__global__ void __launch_bounds__(kFwd2Threads, 1)
+    attn_fwd2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                     const __grid_constant__ CUtensorMap tv, const AttnParams p) {
+  using C = Fwd2Cfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sQ = smem_u32(smem);                    // 2 tiles
+  const uint32_t sR = sQ + 2 * C::kTileBytes;            // ring of kRing tiles
+  const uint32_t sP = sR + C::kRing * C::kTileBytes;     // 2 P tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kTileBytes * (2 + C::kRing) + 2 * C::kPBytes);
+  uint64_t* q_full = bars + 0;
+  uint64_t* r_full = bars + 1;   // [3]
+  uint64_t* r_empty = bars + 4;  // [3]
+  uint64_t* s_full = bars + 7;   // [2] S_x of the current block in TMEM
+  uint64_t* p_full = bars + 9;   // [2] P_x in smem (S_x read, O_x rescaled)
+  uint64_t* o_done = bars + 11;  // [2] PV_x complete (P_x smem free, O_x stable)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int pair = p.nqb / 2 - 1 - (int)blockIdx.x;  // heaviest pair first
+  const int head = blockIdx.y;
+  const int q_lo = 2 * pair, q_hi = 2 * pair + 1;     // tile a, tile b
+  const int nkv = q_hi + 1;                           // kv blocks 0..q_hi (tile a uses 0..q_lo)
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tq);
+    tma_prefetch_desc(&tk);
+    tma_prefetch_desc(&tv);
+    mbar_init(smem_u32(q_full), 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(smem_u32(r_full + i), 1);
+      mbar_init(smem_u32(r_empty + i), 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(smem_u32(s_full + x), 1);
+      mbar_init(smem_u32(p_full + x), 4);
+      mbar_init(smem_u32(o_done + x), 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------------ TMA producer
+      mbar_arrive_expect_tx(smem_u32(q_full), 2 * C::kTileBytes);
+      for (int x = 0; x < 2; ++x)
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_3d(sQ + x * C::kTileBytes + c * 16384, &tq, smem_u32(q_full), c * 64, (q_lo + x) * 128, head);
+      for (int t = 0; t < 2 * nkv; ++t) {  // K_0, V_0, K_1, V_1, ...
+        const int slot = t % 3, ph = (t / 3) & 1;
+        mbar_wait(smem_u32(r_empty + slot), ph ^ 1);
+        mbar_arrive_expect_tx(smem_u32(r_full + slot), C::kTileBytes);
+        const CUtensorMap* m = (t & 1) ? &tv : &tk;
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_3d(sR + slot * C::kTileBytes + c * 16384, m, smem_u32(r_full + slot), c * 64, (t >> 1) * 128, head);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K_j (K-major)
+      constexpr uint32_t idesc_o = umma_idesc_bf16(128, HD, 0, 1);   // P (K-major) x V_j (MN-major)
+      auto slot_of = [](int t) { return t % 3; };
+      auto wait_item = [&](int t) { mbar_wait(smem_u32(r_full + t % 3), (t / 3) & 1); };
+      auto issue_s = [&](int x, int j) {
+        const uint32_t kbase = sR + slot_of(2 * j) * C::kTileBytes;
+        const uint32_t qbase = sQ + x * C::kTileBytes;
+        const uint32_t d = tmem + x * 128;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_bf16(d, umma_desc_sw128(qbase + off, 16, 1024), umma_desc_sw128(kbase + off, 16, 1024), idesc_s,
+                    kk > 0 ? 1u : 0u);
+        }
+        tc_commit(smem_u32(s_full + x));
+      };
+      auto issue_pv = [&](int x, int j) {
+        mbar_wait(smem_u32(p_full + x), j & 1);
+        tc_fence_after();
+        const uint32_t vbase = sR + slot_of(2 * j + 1) * C::kTileBytes;
+        const uint32_t pbase = sP + x * C::kPBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // K = 128 kv positions
+          umma_bf16(tmem + 256 + x * 128, umma_desc_sw128(pbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                    umma_desc_sw128(vbase + kk * 2048, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(smem_u32(o_done + x));
+      };
+      mbar_wait(smem_u32(q_full), 0);
+      wait_item(0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      tc_commit(smem_u32(r_empty + slot_of(0)));
+      for (int j = 0; j < nkv; ++j) {
+        const bool a_here = j <= q_lo, a_next = j + 1 <= q_lo, b_next = j + 1 < nkv;
+        wait_item(2 * j + 1);  // V_j
+        if (a_here) issue_pv(0, j);
+        if (b_next) {
+          wait_item(2 * j + 2);  // K_{j+1}
+          tc_fence_after();
+        }
+        // S_a(j+1): softmax a finished reading S_a(j) before it wrote P_a(j) (waited in issue_pv)
+        if (a_next) issue_s(0, j + 1);
+        issue_pv(1, j);
+        tc_commit(smem_u32(r_empty + slot_of(2 * j + 1)));  // V_j consumed by both tiles
+        if (b_next) {
+          issue_s(1, j + 1);
+          tc_commit(smem_u32(r_empty + slot_of(2 * j + 2)));  // K_{j+1} consumed
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ softmax (two warpgroups)
+    const int x = (int)(warp - 4) / 4;  // 0: tile a, 1: tile b
+    const uint32_t quad = (warp - 4) & 3;
+    const int r = quad * 32 + lane;
+    const int qblk = q_lo + x;
+    const int qrow = qblk * 128 + r;
+    const int nblk = qblk + 1;
+    const uint32_t lane_base = tmem + ((quad * 32) << 16);
+    const uint32_t s_col = x * 128, o_col = 256 + x * 128;
+    const uint32_t pbuf = sP + x * C::kPBytes;
+    float m2 = -INFINITY;  // running (lazily updated) max, log2 domain
+    float l = 0.f;         // running sum of exp2(s - m2) over valid scores (dropped ones included)
+    const uint64_t row_idx = ((uint64_t)(p.head_base + head) * p.seq + qrow) * (uint64_t)p.seq;
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(smem_u32(s_full + x), j & 1);
+      tc_fence_after();
+      const bool diag = (j == qblk);
+      // pass 1: block max over the two 64-column halves (the causal mask only on the diagonal block:
+      // the off-diagonal blocks take a branch-free path — the kernel is integer-ALU bound)
+      auto block_max = [&](auto diag_tag) {
+        constexpr bool kDiag = decltype(diag_tag)::value;
+        float bm = -INFINITY;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t u[64];
+          tmem_ld_32x32b_x32(lane_base + s_col + h * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
+          tmem_ld_32x32b_x32(lane_base + s_col + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+          tmem_ld_wait();
+          float pm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int t = 0; t < 64; ++t) {
+            const float v = (kDiag && h * 64 + t > r) ? -INFINITY : __uint_as_float(u[t]);
+            pm[t & 3] = fmaxf(pm[t & 3], v);
+          }
+          bm = fmaxf(bm, fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])));
+        }
+        return bm;
+      };
+      float bmax = diag ? block_max(std::true_type{}) : block_max(std::false_type{});
+      bmax *= p.alpha_log2;
+      float corr = 1.f;
+      bool rescale = false;
+      if (bmax > m2 + 8.f || m2 == -INFINITY) {  // lazy rescale (2^8 headroom), as attn_fwd_kernel
+        const float mnew = fmaxf(bmax, m2);
+        corr = (m2 == -INFINITY) ? 0.f : ex2(m2 - mnew);
+        rescale = (m2 != -INFINITY);
+        m2 = mnew;
+      }
+      // P_x smem and O_x: PV_x(j-1) must be done
+      if (j > 0) mbar_wait(smem_u32(o_done + x), (j - 1) & 1);
+      tc_fence_after();
+      if (__any_sync(0xffffffffu, rescale)) {
+        for (int c = 0; c * 32 < HD; ++c) {
+          uint32_t u[32];
+          tmem_ld_32x32b_x32(lane_base + o_col + c * 32, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < 32; ++t) u[t] = __float_as_uint(__uint_as_float(u[t]) * corr);
+          tmem_st_32x32b_x32(lane_base + o_col + c * 32, u);
+        }
+        tmem_st_wait();
+      }
+      // pass 2: exps, row sum, dropout, bf16 P_x straight into smem; the keep bits of the block go to
+      // the optional mask buffer (the backward then reads them instead of re-hashing)
+      float ps[4] = {0.f, 0.f, 0.f, 0.f};
+      uint64_t z = drop_weyl_attn(p.seed, (row_idx + (uint64_t)j * 128) >> 2);
+      uint32_t kw[4] = {0u, 0u, 0u, 0u};
+      auto block_exp = [&](auto diag_tag) {
+        constexpr bool kDiag = decltype(diag_tag)::value;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t u[64];
+          tmem_ld_32x32b_x32(lane_base + s_col + h * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
+          tmem_ld_32x32b_x32(lane_base + s_col + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+          tmem_ld_wait();
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {  // 8 chunks of 8 columns
+            float e[8], pv[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              const int col = h * 64 + g * 8 + t;
+              const float sv = (kDiag && col > r) ? -INFINITY : __uint_as_float(u[g * 8 + t]);
+              e[t] = ex2(fmaf(sv, p.alpha_log2, -m2));  // exp2(-inf) = 0 for masked columns
+              ps[t & 3] += e[t];
+            }
+            if (p.thresh16) {
+              const uint32_t keep = drop_select8(z, p.thresh16, e, pv);
+              kw[(h * 64 + g * 8) >> 5] |= keep << ((g * 8) & 31);
+            } else {
+#pragma unroll
+              for (int t = 0; t < 8; ++t) pv[t] = e[t];
+            }
+            z += 2 * curator::kSplitMixGamma;
+            st_shared_v4(sw128_addr(pbuf + h * 16384, r, g), pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]),
+                         pack_bf16x2(pv[4], pv[5]), pack_bf16x2(pv[6], pv[7]));
+          }
+        }
+      };
+      if (diag)
+        block_exp(std::true_type{});
+      else
+        block_exp(std::false_type{});
+      if (p.mask != nullptr && p.thresh16)
+        *reinterpret_cast<uint4*>(p.mask + ((size_t)head * p.seq + qrow) * (p.seq >> 5) + j * 4) =
+            make_uint4(kw[0], kw[1], kw[2], kw[3]);
+      l = l * corr + ((ps[0] + ps[1]) + (ps[2] + ps[3]));
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(p_full + x));  // also: S_x read (the next S_x may overwrite it)
+    }
+    // epilogue: O / l * dropout scale -> bf16 ctx ; lse
+    mbar_wait(smem_u32(o_done + x), (nblk - 1) & 1);
+    tc_fence_after();
+    const float inv = p.drop_scale / l;
+    __nv_bfloat16* orow = p.out + (long long)qrow * p.ld_out + (long long)head * p.out_head_stride;
+    for (int c = 0; c * 32 < HD; ++c) {
+      uint32_t u[32];
+      tmem_ld_32x32b_x32(lane_base + o_col + c * 32, u);
+      tmem_ld_wait();
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        *reinterpret_cast<uint4*>(orow + c * 32 + v * 8) =
+            make_uint4(pack_bf16x2(__uint_as_float(u[8 * v]) * inv, __uint_as_float(u[8 * v + 1]) * inv),
+                       pack_bf16x2(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv),
+                       pack_bf16x2(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv),
+                       pack_bf16x2(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv));
+      }
+    }
+    p.lse[(long long)head * p.seq + qrow] = (m2 + __log2f(l)) * 0.6931471805599453f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 // ---------------------------------------------------------------- backward
 // D[h][i] = sum_d dO[i][h][d] * O[i][h][d]   (= sum_j P_drop dP_drop, the softmax-backward row term)
 __global__ void attn_bwd_rowdot_kernel(const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
@@ -349,7 +663,9 @@ struct AttnBwdParams {
   const float* D;    // [heads][seq]
   __nv_bfloat16* dq; // dqkv: row i, head h: + i * ld_dq + h * 3hd (+0 Q, +hd K, +2hd V)
   long long ld_dq;
+  const uint32_t* mask;  // keep bits written by the forward ([heads][seq][seq/32]); nullptr: re-hash
 };
+
 
 template <int HD>
 struct BwdCfg {
@@ -371,6 +687,15 @@ __device__ __forceinline__ uint32_t keep8(uint64_t seed, uint64_t idx, uint32_t 
       if (((bits >> (16 * q)) & 0xffffu) >= thresh16) m |= 1u << (4 * h2 + q);
   }
   return m;
+}
+
+// Keep bits of the 8 scores (qrow, col .. col + 7) of `head` (col % 8 == 0): from the forward's mask
+// buffer when present (one load instead of two SplitMix64 evaluations), else the counter-based hash.
+__device__ __forceinline__ uint32_t keep8_bwd(const AttnBwdParams& p, int head, int qrow, int col, uint64_t idx) {
+  if (p.thresh16 == 0) return 0xffu;
+  if (p.mask != nullptr)
+    return (__ldg(p.mask + ((size_t)head * p.seq + qrow) * (p.seq >> 5) + (col >> 5)) >> (col & 31)) & 0xffu;
+  return keep8(p.seed, idx, p.thresh16);
 }
 
 // Issue a 128 x N x K (K = 16 * ksteps) MMA chain with both operands given as smem descriptor generators.
@@ -497,21 +822,28 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_wait(smem_u32(s_full), ph);
       tc_fence_after();
       float pr[128];
+      auto probs = [&](auto diag_tag) {  // the causal mask only on the diagonal block (branch-free elsewhere)
+        constexpr bool kDiag = decltype(diag_tag)::value;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t u[32];
-        tmem_ld_32x32b_x32(lane_base + kSC + c * 32, u);
-        tmem_ld_wait();
+        for (int c = 0; c < 4; ++c) {
+          uint32_t u[32];
+          tmem_ld_32x32b_x32(lane_base + kSC + c * 32, u);
+          tmem_ld_wait();
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int col = c * 32 + t;
-          pr[col] = (diag && col > r) ? 0.f : ex2(__uint_as_float(u[t]) * p.alpha_log2 - lse2);
+          for (int t = 0; t < 32; ++t) {
+            const int col = c * 32 + t;
+            pr[col] = (kDiag && col > r) ? 0.f : ex2(__uint_as_float(u[t]) * p.alpha_log2 - lse2);
+          }
         }
-      }
+      };
+      if (diag)
+        probs(std::true_type{});
+      else
+        probs(std::false_type{});
       if (b > 0) mbar_wait(smem_u32(blk_done), ph ^ 1);  // P / dS smem free
 #pragma unroll
       for (int g = 0; g < 16; ++g) {
-        const uint32_t keep = keep8(p.seed, row_idx + g * 8, p.thresh16);
+        const uint32_t keep = keep8_bwd(p, head, qrow, jb * 128 + g * 8, row_idx + g * 8);
         float v[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) v[t] = ((keep >> t) & 1u) ? pr[g * 8 + t] : 0.f;
@@ -532,7 +864,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tmem_ld_wait();
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          const uint32_t keep = keep8(p.seed, row_idx + c * 32 + g * 8, p.thresh16);
+          const uint32_t keep = keep8_bwd(p, head, qrow, jb * 128 + c * 32 + g * 8, row_idx + c * 32 + g * 8);
           float v[8];
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
@@ -666,28 +998,36 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_wait(smem_u32(sd_full), ph);
       tc_fence_after();
       if (j > 0) mbar_wait(smem_u32(blk_done), ph ^ 1);  // dS smem free (previous dQ MMA done)
+      auto dscores = [&](auto diag_tag) {  // the causal mask only on the diagonal block
+        constexpr bool kDiag = decltype(diag_tag)::value;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t us[32], ud[32];
-        tmem_ld_32x32b_x32(lane_base + kSC + c * 32, us);
-        tmem_ld_32x32b_x32(lane_base + kDP + c * 32, ud);
-        tmem_ld_wait();
+        for (int c = 0; c < 4; ++c) {
+          uint32_t us[32], ud[32];
+          tmem_ld_32x32b_x32(lane_base + kSC + c * 32, us);
+          tmem_ld_32x32b_x32(lane_base + kDP + c * 32, ud);
+          tmem_ld_wait();
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const uint32_t keep = keep8(p.seed, row_idx + c * 32 + g * 8, p.thresh16);
-          float v[8];
+          for (int g = 0; g < 4; ++g) {
+            const uint32_t keep = keep8_bwd(p, head, qrow, j * 128 + c * 32 + g * 8, row_idx + c * 32 + g * 8);
+            float v[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const int col = c * 32 + g * 8 + t;
-            const float pr = (diag && col > r) ? 0.f : ex2(__uint_as_float(us[g * 8 + t]) * p.alpha_log2 - lse2);
-            const float dp = ((keep >> t) & 1u) ? __uint_as_float(ud[g * 8 + t]) * p.drop_scale : 0.f;
-            v[t] = pr * (dp - Di);
+            for (int t = 0; t < 8; ++t) {
+              const int col = c * 32 + g * 8 + t;
+              const float pr =
+                  (kDiag && col > r) ? 0.f : ex2(__uint_as_float(us[g * 8 + t]) * p.alpha_log2 - lse2);
+              const float dp = ((keep >> t) & 1u) ? __uint_as_float(ud[g * 8 + t]) * p.drop_scale : 0.f;
+              v[t] = pr * (dp - Di);
+            }
+            const int gg = c * 4 + g;
+            st_shared_v4(sw128_addr(sS + (gg >> 3) * 16384, r, gg & 7), pack_bf16x2(v[0], v[1]),
+                         pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
           }
-          const int gg = c * 4 + g;
-          st_shared_v4(sw128_addr(sS + (gg >> 3) * 16384, r, gg & 7), pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
-                       pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
         }
-      }
+      };
+      if (diag)
+        dscores(std::true_type{});
+      else
+        dscores(std::false_type{});
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
@@ -734,6 +1074,20 @@ EncodeFn encode() {
   return fn;
 }
 
+// Dynamic shared-memory opt-in, once per (kernel, device) (one context per GPU per host thread).
+template <auto kKern>
+bool set_smem_once(int bytes) {
+  static std::atomic<uint64_t> done{0};  // one instance per kernel (template argument = the kernel)
+  auto kern = kKern;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  const uint64_t bit = uint64_t{1} << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return true;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  done.fetch_or(bit, std::memory_order_release);
+  return true;
+}
+
 // Per-head [seq x hd] bf16 operand: dims (hd, seq, heads), row stride ld, head stride hs; box (64, 128).
 bool head_map(CUtensorMap* m, const void* base, int hd, int seq, int heads, long long ld, long long hs) {
   EncodeFn enc = encode();
@@ -750,7 +1104,8 @@ bool head_map(CUtensorMap* m, const void* base, int hd, int seq, int heads, long
 template <int HD>
 int launch_fwd(const void* qkv, long long ld_qkv, int heads, int seq, long long head_base, float alpha,
                uint64_t seed, uint32_t thresh16, float drop_scale, void* out, long long ld_out, float* lse,
-               cudaStream_t s) {
+               uint32_t* mask, cudaStream_t s) {
+  (void)mask;  // the single-tile kernel re-hashes in the backward
   using C = AttnCfg<HD>;
   CUtensorMap mq, mk, mv;
   const auto* q = static_cast<const uint16_t*>(qkv);
@@ -770,21 +1125,44 @@ int launch_fwd(const void* qkv, long long ld_qkv, int heads, int seq, long long 
   p.ld_out = ld_out;
   p.out_head_stride = HD;
   p.lse = lse;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(attn_fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
-        cudaSuccess)
-      return 2;
-    attr = true;
-  }
+  if (!set_smem_once<attn_fwd_kernel<HD>>(C::kSmem)) return 2;
   attn_fwd_kernel<HD><<<dim3(p.nqb, heads), kAttnThreads, C::kSmem, s>>>(mq, mk, mv, p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+template <int HD>
+int launch_fwd2(const void* qkv, long long ld_qkv, int heads, int seq, long long head_base, float alpha,
+                uint64_t seed, uint32_t thresh16, float drop_scale, void* out, long long ld_out, float* lse,
+                uint32_t* mask, cudaStream_t s) {
+  using C = Fwd2Cfg<HD>;
+  CUtensorMap mq, mk, mv;
+  const auto* q = static_cast<const uint16_t*>(qkv);
+  if (!head_map(&mq, q, HD, seq, heads, ld_qkv, 3 * HD) || !head_map(&mk, q + HD, HD, seq, heads, ld_qkv, 3 * HD) ||
+      !head_map(&mv, q + 2 * HD, HD, seq, heads, ld_qkv, 3 * HD))
+    return 1;
+  AttnParams p{};
+  p.seq = seq;
+  p.nqb = seq / 128;
+  p.heads = heads;
+  p.head_base = head_base;
+  p.alpha_log2 = alpha * kLog2e;
+  p.seed = seed;
+  p.thresh16 = thresh16;
+  p.drop_scale = drop_scale;
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.ld_out = ld_out;
+  p.out_head_stride = HD;
+  p.lse = lse;
+  p.mask = mask;
+  if (!set_smem_once<attn_fwd2_kernel<HD>>(C::kSmem)) return 2;
+  attn_fwd2_kernel<HD><<<dim3(p.nqb / 2, heads), kFwd2Threads, C::kSmem, s>>>(mq, mk, mv, p);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
 template <int HD>
 int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* dctx, long long ld_ctx, int heads,
                int seq, long long head_base, float alpha, uint64_t seed, uint32_t thresh16, float drop_scale,
-               const float* lse, float* D, void* dqkv, cudaStream_t s) {
+               const float* lse, float* D, void* dqkv, const uint32_t* mask, cudaStream_t s) {
   using C = BwdCfg<HD>;
   const auto* q = static_cast<const uint16_t*>(qkv);
   CUtensorMap mq, mk, mv, mdo;
@@ -810,17 +1188,10 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
   p.D = D;
   p.dq = static_cast<__nv_bfloat16*>(dqkv);
   p.ld_dq = ld_qkv;
+  p.mask = mask;
   constexpr int kSmemKV = 1024 + 4 * C::kTileBytes + C::kMBytes + 256;
   constexpr int kSmemQ = 1024 + 4 * C::kTileBytes + C::kMBytes + 256;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(attn_bwd_dkdv_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemKV) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(attn_bwd_dq_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemQ) !=
-            cudaSuccess)
-      return 2;
-    attr = true;
-  }
+  if (!set_smem_once<attn_bwd_dkdv_kernel<HD>>(kSmemKV) || !set_smem_once<attn_bwd_dq_kernel<HD>>(kSmemQ)) return 2;
   attn_bwd_dkdv_kernel<HD><<<dim3(p.nqb, heads), kAttnThreads, kSmemKV, s>>>(mq, mk, mv, mdo, p);
   attn_bwd_dq_kernel<HD><<<dim3(p.nqb, heads), kAttnThreads, kSmemQ, s>>>(mq, mk, mv, mdo, p);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
@@ -830,21 +1201,22 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
 
 // Fused causal attention backward for `heads` heads of one microbatch row: from qkv, the forward's
 // ctx (O), its gradient dctx (dO) and the saved lse, writes dQ, dK, dV into dqkv (same layout as
-// qkv). D is a [heads][seq] fp32 scratch. Returns 0 ok, 1 unsupported shape, 2 CUDA error.
+// qkv). D is a [heads][seq] fp32 scratch. mask: the forward's dropout keep bits, or nullptr (the
+// kernels re-derive them from the counter-based stream). Returns 0 ok, 1 unsupported shape, 2 CUDA error.
 int attention_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* dctx, long long ld_ctx, int heads,
                   int seq, int hd, long long head_base, float alpha, uint64_t seed, uint32_t thresh16,
-                  float drop_scale, const float* lse, float* D, void* dqkv, cudaStream_t s) {
+                  float drop_scale, const float* lse, float* D, void* dqkv, const uint32_t* mask, cudaStream_t s) {
   if (seq % 128 != 0 || seq <= 0) return 1;
   switch (hd) {
     case 64:
       return launch_bwd<64>(qkv, ld_qkv, ctx, dctx, ld_ctx, heads, seq, head_base, alpha, seed, thresh16, drop_scale,
-                            lse, D, dqkv, s);
+                            lse, D, dqkv, mask, s);
     case 128:
       return launch_bwd<128>(qkv, ld_qkv, ctx, dctx, ld_ctx, heads, seq, head_base, alpha, seed, thresh16, drop_scale,
-                             lse, D, dqkv, s);
+                             lse, D, dqkv, mask, s);
     case 160:
       return launch_bwd<160>(qkv, ld_qkv, ctx, dctx, ld_ctx, heads, seq, head_base, alpha, seed, thresh16, drop_scale,
-                             lse, D, dqkv, s);
+                             lse, D, dqkv, mask, s);
     default:
       return 1;
   }
@@ -852,20 +1224,33 @@ int attention_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void
 
 // Fused causal attention forward for `heads` heads of one microbatch row:
 // qkv [seq][heads][3][hd] (row stride ld_qkv), out ctx [seq][heads][hd] (row stride ld_out),
-// lse [heads][seq]. Returns 0 ok, 1 unsupported shape, 2 CUDA error.
+// lse [heads][seq]. mask (optional, [heads][seq][seq/32] uint32): receives the dropout keep bits of
+// the causal blocks (two-tile kernel only; returns *mask_written = 1 then). Returns 0 ok, 1
+// unsupported shape, 2 CUDA error.
 int attention_fwd(const void* qkv, long long ld_qkv, int heads, int seq, int hd, long long head_base, float alpha,
                   uint64_t seed, uint32_t thresh16, float drop_scale, void* out, long long ld_out, float* lse,
-                  cudaStream_t s) {
+                  uint32_t* mask, int* mask_written, cudaStream_t s) {
   if (seq % 128 != 0 || seq <= 0) return 1;
+  static const bool two_tiles = [] {
+    const char* e = getenv("MT_ATTN_FWD2");
+    return !(e && e[0] == '0');
+  }();
+  const bool fwd2 = two_tiles && (seq / 128) % 2 == 0;
+  if (mask_written) *mask_written = (fwd2 && mask != nullptr && (hd == 64 || hd == 128)) ? 1 : 0;
   switch (hd) {
     case 64:
-      return launch_fwd<64>(qkv, ld_qkv, heads, seq, head_base, alpha, seed, thresh16, drop_scale, out, ld_out, lse, s);
+      return fwd2 ? launch_fwd2<64>(qkv, ld_qkv, heads, seq, head_base, alpha, seed, thresh16, drop_scale, out, ld_out,
+                                    lse, mask, s)
+                  : launch_fwd<64>(qkv, ld_qkv, heads, seq, head_base, alpha, seed, thresh16, drop_scale, out, ld_out,
+                                   lse, mask, s);
     case 128:
-      return launch_fwd<128>(qkv, ld_qkv, heads, seq, head_base, alpha, seed, thresh16, drop_scale, out, ld_out, lse,
-                             s);
+      return fwd2 ? launch_fwd2<128>(qkv, ld_qkv, heads, seq, head_base, alpha, seed, thresh16, drop_scale, out, ld_out,
+                                     lse, mask, s)
+                  : launch_fwd<128>(qkv, ld_qkv, heads, seq, head_base, alpha, seed, thresh16, drop_scale, out, ld_out,
+                                    lse, mask, s);
     case 160:
       return launch_fwd<160>(qkv, ld_qkv, heads, seq, head_base, alpha, seed, thresh16, drop_scale, out, ld_out, lse,
-                             s);
+                             mask, s);
     default:
       return 1;
   }

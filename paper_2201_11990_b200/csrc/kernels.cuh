@@ -74,10 +74,10 @@ void attn_rowdot(const void* dout, const void* out, long long ld, int hd, int he
 // (seq % 128 or head dim not in {64, 128, 160}), 2 CUDA error.
 int attention_fwd(const void* qkv, long long ld_qkv, int heads, int seq, int hd, long long head_base, float alpha,
                   uint64_t seed, uint32_t thresh16, float drop_scale, void* out, long long ld_out, float* lse,
-                  cudaStream_t s);
+                  uint32_t* mask, int* mask_written, cudaStream_t s);
 int attention_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* dctx, long long ld_ctx, int heads,
                   int seq, int hd, long long head_base, float alpha, uint64_t seed, uint32_t thresh16,
-                  float drop_scale, const float* lse, float* D, void* dqkv, cudaStream_t s);
+                  float drop_scale, const float* lse, float* D, void* dqkv, const uint32_t* mask, cudaStream_t s);
 
 // loss += sum 0.5 (y - t)^2 / n ; dy = (y - t) / n     (n = rows * h)
 // n_total: the element count the mean is over when y/t are one rank's rows of a larger tensor (0 = n)

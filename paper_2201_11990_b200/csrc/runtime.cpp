@@ -961,6 +961,8 @@ void ensure_slot_buffers(mt_layer* l, mt_layer::Saved& sv) {
   if (!l->fused_attn) {
     sv.S.ensure(b * Hl * s * s * 2);
     sv.P.ensure(b * Hl * s * s * 2);
+  } else if (l->d.dropout_attn > 0.f) {
+    sv.mask.ensure(b * Hl * s * (s / 32) * 4);
   }
   sv.lse.ensure(b * Hl * s * 4);
   sv.ctx.ensure(M * l->hl * 2);
@@ -1067,8 +1069,11 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, uint64_t mse
     float* lse = sv.lse.as<float>() + bb * Hl * s;
     const long long head_base = bb * d.heads + int64_t{d.tp_rank} * Hl;
     if (l->fused_attn) {
+      int written = 0;
+      uint32_t* mask = sv.mask.ptr ? sv.mask.as<uint32_t>() + bb * Hl * s * (s / 32) : nullptr;
       const int rc = attention_fwd(q, ld3, (int)Hl, (int)s, (int)hd, head_base, alpha, site_attn, th_a, scale_a,
-                                   sv.ctx.as<uint16_t>() + bb * s * hl, hl, lse, st);
+                                   sv.ctx.as<uint16_t>() + bb * s * hl, hl, lse, mask, &written, st);
+      sv.mask_valid = written != 0;
       if (rc != 0) throw RuntimeFailure("attention_fwd failed");
       ++n;
       mark(c, st, "fwd.flash_attention");
@@ -1244,7 +1249,8 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, uint64_t 
       const long long head_base = bb * d.heads + int64_t{d.tp_rank} * Hl;
       const int rc = attention_bwd(q, ld3, sv.ctx.as<uint16_t>() + bb * s * hl, dc, hl, (int)Hl, (int)s, (int)hd,
                                    head_base, alpha, site_attn, th_a, scale_a, sv.lse.as<float>() + bb * Hl * s,
-                                   c->scratch_attn.as<float>(), dq, st);
+                                   c->scratch_attn.as<float>(), dq,
+                                   sv.mask_valid ? sv.mask.as<uint32_t>() + bb * Hl * s * (s / 32) : nullptr, st);
       if (rc != 0) throw RuntimeFailure("attention_bwd failed");
       n += 3;
       mark(c, st, "bwd.flash_attention");

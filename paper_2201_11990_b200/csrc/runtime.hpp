@@ -201,6 +201,8 @@ struct mt_layer {
     const void* x = nullptr;
     uint64_t step = 0;  // training step of the forward (keys the dropout masks the backward replays)
     mt::DeviceBuffer ln1, qkv, S, P, lse, ctx, x1, ln2, pre, act, stats;  // stats: mean1,rstd1,mean2,rstd2
+    mt::DeviceBuffer mask;      // fused attention: the forward's dropout keep bits [b][heads/t][s][s/32]
+    bool mask_valid = false;    // the forward wrote `mask` (the backward reads it instead of re-hashing)
   };
   std::map<uint32_t, std::unique_ptr<Saved>> saved;
   bool recompute = false;           // activation recompute (full-layer checkpointing)
