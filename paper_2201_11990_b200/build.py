@@ -14,7 +14,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-OBJ = ROOT / "build" / "obj"
+# MT_NVCC_DEFINES (A/B builds of compile-time variants, e.g. "-DMT_GEMM_EPI_BUFS=4"): separate object dir
+_VARIANT = os.environ.get("MT_NVCC_DEFINES", "").split()
+OBJ = ROOT / "build" / ("obj" if not _VARIANT else "obj_" + "_".join(d.lstrip("-D").replace("=", "") for d in _VARIANT))
 LIB = PKG / "libmtnlg.so"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -37,7 +39,7 @@ if NCCL is None:
     raise RuntimeError("NCCL >= 2.28 headers (nccl_device.h) not found: the fused TP all-reduce needs the NCCL device API")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 INCLUDES = [f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{NCCL / 'include'}", "-I/usr/local/cuda/include"]
-NVCC_FLAGS = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fopenmp", "--expt-relaxed-constexpr"]
+NVCC_FLAGS = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fopenmp", "--expt-relaxed-constexpr"] + _VARIANT
 CXX_FLAGS = ["-O3", "-std=c++20", "-fPIC", "-fopenmp", "-Wall", "-Wextra", "-Wno-unused-parameter"]
 
 
@@ -82,7 +84,7 @@ def build(verbose: bool = False, jobs: int = 8) -> Path:
             _drain(procs)
     _drain(procs)
     newest = max(o.stat().st_mtime for o in objs)
-    if not LIB.exists() or LIB.stat().st_mtime < newest:
+    if _VARIANT or not LIB.exists() or LIB.stat().st_mtime < newest:
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs),
               f"-L{NCCL / 'lib'}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={NCCL / 'lib'}",
               "-Xcompiler", "-fopenmp", "-lgomp"])
