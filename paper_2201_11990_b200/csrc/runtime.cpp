@@ -127,11 +127,12 @@ void wait_stream(mt_ctx* c, cudaStream_t s, const char* what) {
       }
       if (clock::now() > deadline) fail("timed out waiting for the iteration");
     }
-    // spin-yield for the first ~2 ms (keeps the e2e timing tight), then sleep between polls
-    if (clock::now() - t0 < std::chrono::milliseconds(2))
+    // spin-yield for the first second (an iteration is 2-300 ms: a sleeping poll would add its
+    // wake-up latency to every step's end-to-end time), then sleep between polls
+    if (clock::now() - t0 < std::chrono::seconds(1))
       std::this_thread::yield();
     else
-      std::this_thread::sleep_for(std::chrono::microseconds(20));
+      std::this_thread::sleep_for(std::chrono::microseconds(200));
   }
   if (c->err_host && __atomic_load_n(c->err_host, __ATOMIC_SEQ_CST) != 0)
     fail("device-side wait for a peer timed out");
