@@ -819,6 +819,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const float Di = p.D[(long long)head * p.seq + qrow];
       const uint64_t row_idx = ((uint64_t)(p.head_base + head) * p.seq + qrow) * (uint64_t)p.seq + (uint64_t)jb * 128;
       const bool diag = (ib == jb);
+      // the block's 128 keep bits in one 16-byte load, issued before the S wait so its latency hides
+      uint4 mw = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+      if (p.mask != nullptr && p.thresh16)
+        mw = __ldg(reinterpret_cast<const uint4*>(p.mask + ((size_t)head * p.seq + qrow) * (p.seq >> 5)) + jb);
       mbar_wait(smem_u32(s_full), ph);
       tc_fence_after();
       float pr[128];
@@ -908,6 +912,291 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// ---------------------------------------------------------------- backward, one kernel (hd <= 128)
+// attn_bwd2_kernel<HD>: one CTA per (head, 128-key block j), heaviest first, looping over the query
+// blocks i >= j. Per block: S = Q_i K_j^T and dP = dO_i V_j^T in TMEM; the softmax warpgroup forms
+// P (from S, lse and the forward's keep bits) and dS = P~ (dP' - D) into ONE shared smem tile (dS
+// after the dV MMA consumed P); dV += P^T dO_i, dK += dS^T Q_i accumulate in TMEM, and dQ_i's partial
+// dS K_j (in dP's TMEM columns once dP was read) is added into an fp32 dQ accumulator with vector
+// red.global.add — so the dQ pass of attn_bwd_dq_kernel (which recomputed S, dP and the softmax
+// backward) disappears. Q_i / dO_i are double-buffered; S(i+1) is issued as soon as S(i) was read.
+// TMEM: dV [0,128), dK [128,256), S [256,384), dP / dQ partial [384,512).
+template <int HD>
+struct Bwd2Cfg {
+  static constexpr int kChunks = (HD + 63) / 64;
+  static constexpr int kTileBytes = kChunks * 16384;
+  static constexpr int kTBytes = 2 * 16384;  // P / dS tile: 128 x 128 bf16
+  static constexpr int kSmem = 1024 + kTileBytes * 6 + kTBytes + 256;
+  static_assert(HD <= 128, "bwd2 TMEM layout");
+  static_assert(kSmem <= 232448, "bwd2 shared memory");
+};
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    attn_bwd2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
+                     const AttnBwdParams p, float* __restrict__ dq_acc) {
+  using C = Bwd2Cfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sK = smem_u32(smem), sV = sK + C::kTileBytes;
+  const uint32_t sQ0 = sV + C::kTileBytes;           // Q slots 0, 1
+  const uint32_t sO0 = sQ0 + 2 * C::kTileBytes;      // dO slots 0, 1
+  const uint32_t sT = sO0 + 2 * C::kTileBytes;       // P, then dS
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * C::kTileBytes + C::kTBytes);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* qo_full = bars + 1;   // [2]
+  uint64_t* qo_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* s_free = bars + 6;    // 4 softmax warps read S
+  uint64_t* dp_full = bars + 7;
+  uint64_t* p_full = bars + 8;    // 4 warps wrote P
+  uint64_t* pv_done = bars + 9;   // dV MMA consumed P (the tile can take dS)
+  uint64_t* ds_full = bars + 10;  // 4 warps wrote dS
+  uint64_t* mma_done = bars + 11; // dK and dQ-partial MMAs done (tile free, dQ partial in TMEM)
+  uint64_t* dq_free = bars + 12;  // 4 warps drained the dQ partial (dP columns free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int jb = (int)blockIdx.x;  // key block; jb = 0 has the most query blocks (launched first)
+  const int head = blockIdx.y;
+  const int nblk = p.nqb - jb;
+  constexpr uint32_t kDV = 0, kDK = 128, kSC = 256, kDP = 384;
+
+  if (warp == 0 && lane == 0) {
+    for (auto* b : {&tq, &tk, &tv, &tdo}) tma_prefetch_desc(b);
+    for (int i = 0; i < 13; ++i) {
+      const bool four = (bars + i == s_free) || (bars + i == p_full) || (bars + i == ds_full) || (bars + i == dq_free);
+      mbar_init(smem_u32(bars + i), four ? 4 : 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(smem_u32(kv_full), 2 * C::kTileBytes);
+      for (int c = 0; c < C::kChunks; ++c) {
+        tma_load_3d(sK + c * 16384, &tk, smem_u32(kv_full), c * 64, jb * 128, head);
+        tma_load_3d(sV + c * 16384, &tv, smem_u32(kv_full), c * 64, jb * 128, head);
+      }
+      for (int b = 0; b < nblk; ++b) {
+        const int slot = b & 1, ib = jb + b;
+        mbar_wait(smem_u32(qo_empty + slot), ((b >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(smem_u32(qo_full + slot), 2 * C::kTileBytes);
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_load_3d(sQ0 + slot * C::kTileBytes + c * 16384, &tq, smem_u32(qo_full + slot), c * 64, ib * 128, head);
+          tma_load_3d(sO0 + slot * C::kTileBytes + c * 16384, &tdo, smem_u32(qo_full + slot), c * 64, ib * 128, head);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = umma_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t id_acc = umma_idesc_bf16(128, HD, 1, 1);
+      constexpr uint32_t id_dq = umma_idesc_bf16(128, HD, 0, 1);
+      constexpr int kd = HD / 16;
+      auto sQ = [&](int b) { return sQ0 + (b & 1) * C::kTileBytes; };
+      auto sO = [&](int b) { return sO0 + (b & 1) * C::kTileBytes; };
+      auto issue_s = [&](int b) {
+        mma_chain(tmem + kSC, id_s, kd, false, [&](int kk) { return kmaj(sQ(b), kk); },
+                  [&](int kk) { return kmaj(sK, kk); });
+        tc_commit(smem_u32(s_full));
+      };
+      auto issue_dp = [&](int b) {
+        mma_chain(tmem + kDP, id_s, kd, false, [&](int kk) { return kmaj(sO(b), kk); },
+                  [&](int kk) { return kmaj(sV, kk); });
+        tc_commit(smem_u32(dp_full));
+      };
+      mbar_wait(smem_u32(kv_full), 0);
+      mbar_wait(smem_u32(qo_full), 0);
+      tc_fence_after();
+      issue_s(0);
+      issue_dp(0);
+      for (int b = 0; b < nblk; ++b) {
+        const int ph = b & 1;
+        // dV += P^T dO_i
+        mbar_wait(smem_u32(p_full), ph);
+        tc_fence_after();
+        mma_chain(tmem + kDV, id_acc, 8, b > 0, [&](int kk) { return mnmaj(sT, kk); },
+                  [&](int kk) { return mnmaj(sO(b), kk); });
+        tc_commit(smem_u32(pv_done));
+        // S(i+1) as soon as the softmax warps read S(i) (they arrive s_free before writing P)
+        if (b + 1 < nblk) {
+          mbar_wait(smem_u32(qo_full + ((b + 1) & 1)), ((b + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_s(b + 1);
+        }
+        // dK += dS^T Q_i ; dQ partial = dS K_j into dP's columns (dP read before dS was written)
+        mbar_wait(smem_u32(ds_full), ph);
+        tc_fence_after();
+        mma_chain(tmem + kDK, id_acc, 8, b > 0, [&](int kk) { return mnmaj(sT, kk); },
+                  [&](int kk) { return mnmaj(sQ(b), kk); });
+        mma_chain(tmem + kDP, id_dq, 8, false, [&](int kk) { return kmaj(sT, kk); },
+                  [&](int kk) { return mnmaj(sK, kk); });
+        tc_commit(smem_u32(mma_done));
+        tc_commit(smem_u32(qo_empty + (b & 1)));
+        if (b + 1 < nblk) {
+          mbar_wait(smem_u32(dq_free), ph);  // the dQ partial left TMEM
+          tc_fence_after();
+          issue_dp(b + 1);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t quad = warp - 4;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_base = tmem + ((quad * 32) << 16);
+    for (int b = 0; b < nblk; ++b) {
+      const int ib = jb + b, ph = b & 1;
+      const int qrow = ib * 128 + r;
+      const float lse2 = p.lse[(long long)head * p.seq + qrow] * kLog2e;
+      const float Di = p.D[(long long)head * p.seq + qrow];
+      const uint64_t row_idx = ((uint64_t)(p.head_base + head) * p.seq + qrow) * (uint64_t)p.seq + (uint64_t)jb * 128;
+      const bool diag = (ib == jb);
+      // the block's 128 keep bits in one 16-byte load, issued before the S wait so its latency hides
+      uint4 mw = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+      if (p.mask != nullptr && p.thresh16)
+        mw = __ldg(reinterpret_cast<const uint4*>(p.mask + ((size_t)head * p.seq + qrow) * (p.seq >> 5)) + jb);
+      mbar_wait(smem_u32(s_full), ph);
+      tc_fence_after();
+      float pr[128];
+      auto probs = [&](auto diag_tag) {
+        constexpr bool kDiag = decltype(diag_tag)::value;
+#pragma unroll
+        for (int c = 0; c < 4; c += 2) {
+          uint32_t u[64];
+          tmem_ld_32x32b_x32(lane_base + kSC + c * 32, *reinterpret_cast<uint32_t(*)[32]>(u));
+          tmem_ld_32x32b_x32(lane_base + kSC + c * 32 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+          tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < 64; ++t) {
+            const int col = c * 32 + t;
+            pr[col] = (kDiag && col > r) ? 0.f : ex2(__uint_as_float(u[t]) * p.alpha_log2 - lse2);
+          }
+        }
+      };
+      if (diag)
+        probs(std::true_type{});
+      else
+        probs(std::false_type{});
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(s_free));
+      // P (dropped, unscaled) into the tile: the previous block's dK / dQ MMAs are done (its drain waited)
+      uint32_t keep[16];
+      const uint32_t mwa[4] = {mw.x, mw.y, mw.z, mw.w};
+#pragma unroll
+      for (int g = 0; g < 16; ++g) {
+        keep[g] = (p.mask != nullptr || p.thresh16 == 0) ? (mwa[g >> 2] >> ((g & 3) * 8)) & 0xffu
+                                                         : keep8(p.seed, row_idx + g * 8, p.thresh16);
+        float v[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[t] = ((keep[g] >> t) & 1u) ? pr[g * 8 + t] : 0.f;
+        st_shared_v4(sw128_addr(sT + (g >> 3) * 16384, r, g & 7), pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
+                     pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(p_full));
+      // dS = P~ (dP' - D) once dP is in TMEM and the dV MMA has consumed P from the tile
+      mbar_wait(smem_u32(dp_full), ph);
+      mbar_wait(smem_u32(pv_done), ph);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; c += 2) {
+        uint32_t u[64];
+        tmem_ld_32x32b_x32(lane_base + kDP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(u));
+        tmem_ld_32x32b_x32(lane_base + kDP + c * 32 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+        tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const int gg = c * 4 + g;  // 8-column chunk index 0..15
+          float v[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const float dp = ((keep[gg] >> t) & 1u) ? __uint_as_float(u[g * 8 + t]) * p.drop_scale : 0.f;
+            v[t] = pr[gg * 8 + t] * (dp - Di);
+          }
+          st_shared_v4(sw128_addr(sT + (gg >> 3) * 16384, r, gg & 7), pack_bf16x2(v[0], v[1]),
+                       pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(ds_full));
+      // drain dQ_i's partial: TMEM -> registers -> fp32 vector atomics into the accumulator
+      mbar_wait(smem_u32(mma_done), ph);
+      tc_fence_after();
+      float* dst = dq_acc + ((size_t)head * p.seq + qrow) * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t u[32];
+        tmem_ld_32x32b_x32(lane_base + kDP + c * 32, u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          red_add_v4(dst + c * 32 + 4 * v, __uint_as_float(u[4 * v]), __uint_as_float(u[4 * v + 1]),
+                     __uint_as_float(u[4 * v + 2]), __uint_as_float(u[4 * v + 3]));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(dq_free));
+    }
+    // epilogue: dV = scale * acc, dK = alpha * acc -> dqkv (V and K slots) of key rows jb*128 + r
+    __nv_bfloat16* base = p.dq + (long long)(jb * 128 + r) * p.ld_dq + (long long)head * 3 * HD;
+    for (int which = 0; which < 2; ++which) {
+      const float sc = which == 0 ? p.drop_scale : p.alpha;
+      __nv_bfloat16* dst = base + (which == 0 ? 2 * HD : HD);
+      const uint32_t col = which == 0 ? kDV : kDK;
+      for (int c = 0; c * 32 < HD; ++c) {
+        uint32_t u[32];
+        tmem_ld_32x32b_x32(lane_base + col + c * 32, u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          *reinterpret_cast<uint4*>(dst + c * 32 + v * 8) =
+              make_uint4(pack_bf16x2(__uint_as_float(u[8 * v]) * sc, __uint_as_float(u[8 * v + 1]) * sc),
+                         pack_bf16x2(__uint_as_float(u[8 * v + 2]) * sc, __uint_as_float(u[8 * v + 3]) * sc),
+                         pack_bf16x2(__uint_as_float(u[8 * v + 4]) * sc, __uint_as_float(u[8 * v + 5]) * sc),
+                         pack_bf16x2(__uint_as_float(u[8 * v + 6]) * sc, __uint_as_float(u[8 * v + 7]) * sc));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// dQ (bf16, into dqkv's Q slots) = alpha * the fp32 accumulator [heads][seq][HD]; 8 values per thread.
+__global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq, long long ld_dq,
+                                   int hd, int heads, int seq, float alpha) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // 8-value group
+  const long long groups = (long long)heads * seq * (hd / 8);
+  if (i >= groups) return;
+  const int per_row = hd / 8;
+  const long long row = i / per_row;  // head * seq + q
+  const int g = (int)(i - row * per_row);
+  const int h = (int)(row / seq), q = (int)(row - (long long)h * seq);
+  const float4 a = *reinterpret_cast<const float4*>(acc + row * hd + g * 8);
+  const float4 b = *reinterpret_cast<const float4*>(acc + row * hd + g * 8 + 4);
+  *reinterpret_cast<uint4*>(dq + (long long)q * ld_dq + (long long)h * 3 * hd + g * 8) =
+      make_uint4(pack_bf16x2(a.x * alpha, a.y * alpha), pack_bf16x2(a.z * alpha, a.w * alpha),
+                 pack_bf16x2(b.x * alpha, b.y * alpha), pack_bf16x2(b.z * alpha, b.w * alpha));
 }
 
 // dQ for one (head, 128-query block i): loop over key blocks j <= i.
@@ -1162,7 +1451,7 @@ int launch_fwd2(const void* qkv, long long ld_qkv, int heads, int seq, long long
 template <int HD>
 int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* dctx, long long ld_ctx, int heads,
                int seq, long long head_base, float alpha, uint64_t seed, uint32_t thresh16, float drop_scale,
-               const float* lse, float* D, void* dqkv, const uint32_t* mask, cudaStream_t s) {
+               const float* lse, float* D, void* dqkv, const uint32_t* mask, float* dq_acc, cudaStream_t s) {
   using C = BwdCfg<HD>;
   const auto* q = static_cast<const uint16_t*>(qkv);
   CUtensorMap mq, mk, mv, mdo;
@@ -1191,6 +1480,17 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
   p.mask = mask;
   constexpr int kSmemKV = 1024 + 4 * C::kTileBytes + C::kMBytes + 256;
   constexpr int kSmemQ = 1024 + 4 * C::kTileBytes + C::kMBytes + 256;
+  if constexpr (HD <= 128) {
+    if (dq_acc != nullptr) {  // one kernel: dK, dV and dQ (fp32 vector atomics), then the bf16 dQ
+      using C2 = Bwd2Cfg<HD>;
+      if (!set_smem_once<attn_bwd2_kernel<HD>>(C2::kSmem)) return 2;
+      if (cudaMemsetAsync(dq_acc, 0, (size_t)heads * seq * HD * sizeof(float), s) != cudaSuccess) return 2;
+      attn_bwd2_kernel<HD><<<dim3(p.nqb, heads), kAttnThreads, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
+      const long long groups = (long long)heads * seq * (HD / 8);
+      dq_finalize_kernel<<<(unsigned)((groups + 255) / 256), 256, 0, s>>>(dq_acc, p.dq, p.ld_dq, HD, heads, seq, alpha);
+      return cudaGetLastError() == cudaSuccess ? 0 : 2;
+    }
+  }
   if (!set_smem_once<attn_bwd_dkdv_kernel<HD>>(kSmemKV) || !set_smem_once<attn_bwd_dq_kernel<HD>>(kSmemQ)) return 2;
   attn_bwd_dkdv_kernel<HD><<<dim3(p.nqb, heads), kAttnThreads, kSmemKV, s>>>(mq, mk, mv, mdo, p);
   attn_bwd_dq_kernel<HD><<<dim3(p.nqb, heads), kAttnThreads, kSmemQ, s>>>(mq, mk, mv, mdo, p);
@@ -1202,21 +1502,29 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
 // Fused causal attention backward for `heads` heads of one microbatch row: from qkv, the forward's
 // ctx (O), its gradient dctx (dO) and the saved lse, writes dQ, dK, dV into dqkv (same layout as
 // qkv). D is a [heads][seq] fp32 scratch. mask: the forward's dropout keep bits, or nullptr (the
-// kernels re-derive them from the counter-based stream). Returns 0 ok, 1 unsupported shape, 2 CUDA error.
+// kernels re-derive them from the counter-based stream). dq_acc: [heads][seq][hd] fp32 scratch enabling
+// the one-kernel backward for hd <= 128 (nullptr or MT_ATTN_BWD2=0: the dK/dV + dQ kernel pair).
+// Returns 0 ok, 1 unsupported shape, 2 CUDA error.
 int attention_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* dctx, long long ld_ctx, int heads,
                   int seq, int hd, long long head_base, float alpha, uint64_t seed, uint32_t thresh16,
-                  float drop_scale, const float* lse, float* D, void* dqkv, const uint32_t* mask, cudaStream_t s) {
+                  float drop_scale, const float* lse, float* D, void* dqkv, const uint32_t* mask, float* dq_acc,
+                  cudaStream_t s) {
   if (seq % 128 != 0 || seq <= 0) return 1;
+  // MT_ATTN_BWD2=0 selects the deterministic kernel pair (the one-kernel backward adds dQ partials with
+  // fp32 atomics, whose order varies between runs); read per call so tests can switch it
+  const char* bwd2_env = getenv("MT_ATTN_BWD2");
+  const bool one_kernel = !(bwd2_env && bwd2_env[0] == '0');
+  if (!one_kernel) dq_acc = nullptr;
   switch (hd) {
     case 64:
       return launch_bwd<64>(qkv, ld_qkv, ctx, dctx, ld_ctx, heads, seq, head_base, alpha, seed, thresh16, drop_scale,
-                            lse, D, dqkv, mask, s);
+                            lse, D, dqkv, mask, dq_acc, s);
     case 128:
       return launch_bwd<128>(qkv, ld_qkv, ctx, dctx, ld_ctx, heads, seq, head_base, alpha, seed, thresh16, drop_scale,
-                             lse, D, dqkv, mask, s);
+                             lse, D, dqkv, mask, dq_acc, s);
     case 160:
       return launch_bwd<160>(qkv, ld_qkv, ctx, dctx, ld_ctx, heads, seq, head_base, alpha, seed, thresh16, drop_scale,
-                             lse, D, dqkv, mask, s);
+                             lse, D, dqkv, mask, nullptr, s);
     default:
       return 1;
   }

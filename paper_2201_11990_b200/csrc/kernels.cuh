@@ -77,7 +77,8 @@ int attention_fwd(const void* qkv, long long ld_qkv, int heads, int seq, int hd,
                   uint32_t* mask, int* mask_written, cudaStream_t s);
 int attention_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* dctx, long long ld_ctx, int heads,
                   int seq, int hd, long long head_base, float alpha, uint64_t seed, uint32_t thresh16,
-                  float drop_scale, const float* lse, float* D, void* dqkv, const uint32_t* mask, cudaStream_t s);
+                  float drop_scale, const float* lse, float* D, void* dqkv, const uint32_t* mask, float* dq_acc,
+                  cudaStream_t s);
 
 // loss += sum 0.5 (y - t)^2 / n ; dy = (y - t) / n     (n = rows * h)
 // n_total: the element count the mean is over when y/t are one rank's rows of a larger tensor (0 = n)

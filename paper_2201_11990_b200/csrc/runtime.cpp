@@ -697,6 +697,7 @@ extern "C" int mt_layer_create(mt_ctx* c, const mt_layer_desc* d, mt_layer** out
     c->scratch_qkv.ensure(M * l->qkvl * 2);
     c->scratch_attn.ensure(l->fused_attn ? l->heads_local * int64_t{d->seq} * 4
                                          : l->heads_local * int64_t{d->seq} * d->seq * 2);
+    if (l->fused_attn) c->scratch_dq.ensure(l->heads_local * int64_t{d->seq} * l->head_dim * 4);  // fp32 dQ acc
     c->scratch_stats.ensure(l->heads_local * int64_t{d->seq} * ((d->seq + 127) / 128) * 8);
     size_t ws = 0;
     for (int64_t n : {l->h, l->ffl, l->qkvl}) ws = std::max(ws, mt::colsum_workspace_floats((int)M, (int)n));
@@ -1251,7 +1252,8 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, uint64_t 
       const int rc = attention_bwd(q, ld3, sv.ctx.as<uint16_t>() + bb * s * hl, dc, hl, (int)Hl, (int)s, (int)hd,
                                    head_base, alpha, site_attn, th_a, scale_a, sv.lse.as<float>() + bb * Hl * s,
                                    c->scratch_attn.as<float>(), dq,
-                                   sv.mask_valid ? sv.mask.as<uint32_t>() + bb * Hl * s * (s / 32) : nullptr, st);
+                                   sv.mask_valid ? sv.mask.as<uint32_t>() + bb * Hl * s * (s / 32) : nullptr,
+                                   c->scratch_dq.as<float>(), st);
       if (rc != 0) throw RuntimeFailure("attention_bwd failed");
       n += 3;
       mark(c, st, "bwd.flash_attention");

@@ -155,6 +155,7 @@ struct mt_ctx {
   mt::DeviceBuffer scratch_qkv;    // [M, 3h/t] bf16
   mt::DeviceBuffer scratch_attn;   // [heads/t, s, s] bf16
   mt::DeviceBuffer scratch_stats;  // [heads/t, s, s / bn] float2: score-block softmax statistics
+  mt::DeviceBuffer scratch_dq;     // fused attention backward: fp32 dQ accumulator [heads/t, s, hd]
   mt::DeviceBuffer scratch_ws;     // fp32 column-reduction workspace
   mt::DeviceBuffer gemm_ws;        // split-K tail workspace (zeroed counters + partial tiles)
   mt::DeviceBuffer opt_scratch;    // optimizer: squared norms + {norm, clip coefficient}
