@@ -238,6 +238,9 @@ int mt_vocab_zero_grads(mt_vocab* v, void* stream);
 int mt_vocab_embed_forward(mt_vocab* v, const int32_t* tokens, void* x, uint32_t micro_batch, void* stream);
 /* Training step keying the embedding-dropout masks (as mt_layer_set_step). */
 int mt_vocab_set_step(mt_vocab* v, uint64_t step);
+/* Multiplier of mt_vocab_head_loss's loss and gradient (default 1; the stage sets 1 / microbatches so
+ * the iteration's loss is the batch mean). */
+int mt_vocab_set_loss_scale(mt_vocab* v, float scale);
 /* scatter-add of the embedding gradient (dx = gradient w.r.t. the embedding output). */
 int mt_vocab_embed_backward(mt_vocab* v, const int32_t* tokens, const void* dx, uint32_t micro_batch, void* stream);
 /* loss_dev += mean cross-entropy of LN_f(y) E^T against targets; dy = d loss / d y (forward+backward). */
@@ -257,8 +260,9 @@ int mt_stage_layer(mt_stage* st, int32_t i, mt_layer** out);
 /* One training iteration of this rank: zero grads, 1F1B over MB microbatches (first stage reads
  * inputs_host[mb] — host bf16 [b*s*h] per microbatch, copied in-stream; last stage computes the
  * synthetic MSE loss against targets_host), PP send/recv, TP all-reduces inside the layers, then
- * the DP gradient all-reduce (mean). *loss_out = summed loss over microbatches (last stage,
- * DP-averaged), else 0. Host buffers should be pinned. If inputs_host is NULL the stage
+ * the DP gradient all-reduce (mean). The loss is the batch mean — each microbatch's mean loss / MB
+ * (Megatron's convention; gradients scale alike) — DP-averaged; *loss_out holds it on the last stage,
+ * else 0. Host buffers should be pinned. If inputs_host is NULL the stage
  * generates inputs/targets on device from the seed (no host traffic). */
 int mt_stage_train_step(mt_stage* st, const void* inputs_host, const void* targets_host, float* loss_out,
                         void* stream);

@@ -136,6 +136,7 @@ _SIGS = {
     "mt_layer_set_recompute": (C.c_int, [P, I32]),
     "mt_layer_set_step": (C.c_int, [P, U64]),
     "mt_vocab_set_step": (C.c_int, [P, U64]),
+    "mt_vocab_set_loss_scale": (C.c_int, [P, F32]),
     "mt_stage_set_step": (C.c_int, [P, U64]),
     "mt_stage_get_step": (C.c_int, [P, C.POINTER(U64)]),
     "mt_stage_set_recompute": (C.c_int, [P, I32]),

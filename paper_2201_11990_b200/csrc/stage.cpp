@@ -250,7 +250,9 @@ struct Step {
                         s);
         ++launches;
       }
-      mt::mse_loss(y, tgt, y, st->loss.as<float>(), elems(), s, full_elems());  // dy overwrites y in place
+      // the batch mean: each microbatch's mean loss / MB (Megatron's convention), so the loss, the gradients
+      // and the clip norm do not scale with the microbatch count; dy overwrites y in place
+      mt::mse_loss(y, tgt, y, st->loss.as<float>(), elems(), s, full_elems() * st->d.micro_batches);
       ++launches;
     }
   }
@@ -412,7 +414,10 @@ void run_iteration(Step& k, mt_stage* st, void* stream) {
     ok(mt_layer_set_step(l, st->step));
   }
   const bool vocab_here = k.lm() && (k.first() || k.last());
-  if (st->vocab) ok(mt_vocab_set_step(st->vocab, st->step));
+  if (st->vocab) {
+    ok(mt_vocab_set_step(st->vocab, st->step));
+    ok(mt_vocab_set_loss_scale(st->vocab, 1.f / static_cast<float>(MB)));  // the batch mean (Megatron)
+  }
   if (vocab_here) mt::vocab_zero_grads(st->vocab, k.s);
   mt::check_cuda(cudaMemsetAsync(st->loss.ptr, 0, 4, k.s), "memset loss");
   const int warmup = std::min(st->stages - st->stage - 1, MB);

@@ -28,6 +28,7 @@ struct mt_vocab {
   mt_ctx* ctx = nullptr;
   mt_vocab_desc d{};
   uint64_t step = 0;  // training step keying the embedding-dropout masks (curator::step_seed)
+  float loss_scale = 1.f;  // multiplies the head's loss and dlogits (the stage sets 1 / microbatches)
   int64_t vpad = 0, vp = 0, v0 = 0, M = 0, h = 0;
   mt::DeviceBuffer word, pos, lnf_g, lnf_b;        // bf16 params (word: [vp, h])
   mt::DeviceBuffer g_word, g_pos, g_lnf_g, g_lnf_b; // fp32 grads
@@ -346,6 +347,13 @@ extern "C" int mt_vocab_set_step(mt_vocab* v, uint64_t step) {
   });
 }
 
+extern "C" int mt_vocab_set_loss_scale(mt_vocab* v, float scale) {
+  return call([&] {
+    if (!v || !(scale > 0.f)) throw std::invalid_argument("bad loss scale");
+    v->loss_scale = scale;
+  });
+}
+
 extern "C" int mt_vocab_zero_grads(mt_vocab* v, void* stream) {
   return call([&] { mt::vocab_zero_grads(v, (cudaStream_t)stream); });
 }
@@ -400,7 +408,7 @@ extern "C" int mt_vocab_head_loss(mt_vocab* v, const void* y, const int32_t* tar
     ce_sum_kernel<<<(int)M, 256, 0, s>>>(v->logits.as<float>(), vp, v->v0, v->d.vocab, rmax, targets, sums);
     if (tp_active(v)) check_nccl(ncclAllReduce(sums, sums, 2 * M, ncclFloat32, ncclSum, v->ctx->tp, s), "AR sum");
     ce_grad_kernel<<<(int)M, 256, 0, s>>>(v->logits.as<float>(), vp, v->v0, v->d.vocab, rmax, sums, targets,
-                                          (__nv_bfloat16*)v->dlogits.ptr, loss_dev, 1.f / (float)M);
+                                          (__nv_bfloat16*)v->dlogits.ptr, loss_dev, v->loss_scale / (float)M);
     // d LN_f(y) = dlogits E_slice (partial over the vocab slices) -> all-reduce
     gemm(gemm_args(v->dlogits.ptr, vp, false, v->word.ptr, h, true, v->dyn.ptr, h, M, h, vp, MT_EPI_STORE_BF16), s);
     if (tp_active(v))

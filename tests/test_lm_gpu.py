@@ -98,6 +98,7 @@ def test_lm_stage_matches_manual_composition():
     from paper_2201_11990_b200._native import check, lib
     sp = C.c_void_p(s.cuda_stream)
     check(lib().mt_vocab_zero_grads(v2._h, sp))
+    check(lib().mt_vocab_set_loss_scale(v2._h, 1.0 / MB))  # the stage's batch mean
     loss_d = torch.zeros(1, device="cuda")
     acts = [torch.empty(B * S, H, dtype=torch.bfloat16, device="cuda") for _ in range(L + 1)]
     g0, g1 = (torch.empty(B * S, H, dtype=torch.bfloat16, device="cuda") for _ in range(2))
@@ -117,7 +118,7 @@ def test_lm_stage_matches_manual_composition():
     torch.cuda.synchronize()
     want_loss = float(loss_d.item())
     assert abs(loss - want_loss) <= 1e-6 * abs(want_loss), (loss, want_loss)
-    assert 0.9 * np.log(V) < loss / MB < 1.1 * np.log(V)  # ~uniform prediction at init
+    assert 0.9 * np.log(V) < loss < 1.1 * np.log(V)  # batch mean, ~uniform prediction at init
     for i, lay in enumerate(lays):
         for p, (a, b) in enumerate(zip(got_layers[i], layer_grads(lay))):
             assert rel(a, b) < 1e-5, (i, p, rel(a, b))
@@ -174,7 +175,7 @@ def test_lm_training_memorises_a_batch():
     tok_h, tgt_h = torch.from_numpy(tok).pin_memory(), torch.from_numpy(tgt).pin_memory()
     losses = []
     for step in range(1, 31):
-        losses.append(st.train_step(tok_h.data_ptr(), tgt_h.data_ptr(), s) / MB)
+        losses.append(st.train_step(tok_h.data_ptr(), tgt_h.data_ptr(), s))  # batch mean
         norm = st.optimizer_step(adam_defaults(lr=1e-3, step=step, weight_decay=0.0), s)
         assert np.isfinite(norm) and norm > 0
     assert losses[0] > 0.9 * np.log(V)
@@ -224,7 +225,7 @@ def test_lm_stage_consumes_blend_feed_with_batch_ramp(tmp_path):
             feed.fill(1, tok.data_ptr(), tgt.data_ptr(), cap)
             st.set_micro_batches(MB1)
             l1 = st.train_step(tok.data_ptr(), tgt.data_ptr(), s)
-            assert np.isfinite(l1) and 0.9 * np.log(V) < l1 / MB1 < 1.1 * np.log(V)
+            assert np.isfinite(l1) and 0.9 * np.log(V) < l1 < 1.1 * np.log(V)
         st.close()
     assert abs(losses[4] - losses[2]) <= 1e-6 * losses[2], losses  # loss sum uses float atomics
     feed.close()

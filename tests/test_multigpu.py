@@ -368,6 +368,7 @@ def test_pipeline_parallel_1f1b_two_gpus():
     _need(2)
     res = _run("pp")
     loss, grads = _oracle_step([0, 1, 2, 3], range(4))
+    loss, grads = loss / 4, [[g / 4 for g in lg] for lg in grads]  # the batch mean over MB = 4
     assert abs(res[1]["loss"] - loss) / loss < 5e-3, (res[1]["loss"], loss)
     norm = np.sqrt(sum(float((g.astype(np.float64) ** 2).sum()) for lg in grads for g in lg))
     for r in (0, 1):
@@ -382,13 +383,13 @@ def test_pipeline_parallel_1f1b_two_gpus():
 def test_data_parallel_gradient_allreduce_two_gpus():
     _need(2)
     res = _run("dp")
-    loss, grads = _oracle_step([0], range(4))
+    loss, grads = _oracle_step([0], range(4))  # DP = 2 replicas x MB = 2: the mean over all 4 microbatches
     for r in (0, 1):
-        assert abs(res[r]["loss"] - loss / 2) / loss < 5e-3
-        norm = np.sqrt(sum(float(((g / 2).astype(np.float64) ** 2).sum()) for g in grads[0]))
+        assert abs(res[r]["loss"] - loss / 4) / loss < 5e-3
+        norm = np.sqrt(sum(float(((g / 4).astype(np.float64) ** 2).sum()) for g in grads[0]))
         assert abs(res[r]["grad_norm"] - norm) / norm < 2e-2
         for i in range(12):
-            assert rel(res[r]["grads"][0][i], grads[0][i] / 2) < 2e-2, (r, i)
+            assert rel(res[r]["grads"][0][i], grads[0][i] / 4) < 2e-2, (r, i)
 
 
 @pytest.mark.timeout(900)
@@ -442,6 +443,7 @@ def test_tensor_parallel_stage_host_inputs_two_gpus(mode):
     _need(2)
     res = _run(mode)
     loss, _ = _oracle_step([0], range(2))
+    loss /= 2  # the batch mean over MB = 2
     full = 2 * 2 * (B * S * H * 2)  # MB=2 inputs + targets, bf16
     for r in (0, 1):
         assert abs(res[r]["loss"] - loss) / loss < 5e-3, (res[r]["loss"], loss)
@@ -496,8 +498,8 @@ def test_tensor_parallel_layer_four_gpus():
 def test_two_axis_layouts_four_gpus(layout):
     """Every two-axis composition of the 3D layout on 4 GPUs (TPxPP, TPxDP, PPxDP; 2 layers per stage,
     MB=4 per replica): the rank placement is curator::map_topology's (pp slowest, tp fastest), the loss
-    is the DP mean of the oracle's per-replica sums, every rank's gradient shard equals the matching
-    slice of the oracle's DP-mean gradients, and the clip norm is the global one."""
+    is the mean over all DP x MB microbatches of the oracle's losses, every rank's gradient shard equals
+    the matching slice of the oracle's gradients over the same mean, and the clip norm is the global one."""
     _need(4)
     tp, pp, dp = layout
     from paper_2201_11990_b200 import planner as PL
@@ -507,6 +509,7 @@ def test_two_axis_layouts_four_gpus(layout):
         dpi, ppi, tpi = res[r]["place"]
         assert r == (ppi * dp + dpi) * tp + tpi, (r, res[r]["place"])
     loss, grads = _oracle_step(list(range(2 * pp)), range(dp * MB))
+    loss, grads = loss / MB, [[g / MB for g in lg] for lg in grads]  # per-replica batch mean
     norm = np.sqrt(sum(float(((g / dp).astype(np.float64) ** 2).sum()) for lg in grads for g in lg))
     for r in range(4):
         dpi, ppi, tpi = res[r]["place"]
