@@ -137,6 +137,17 @@ __device__ __forceinline__ bool get_work(const GemmParams& p, int w, Work& o) {
   return true;
 }
 
+// The epilogue's hand-back of an accumulator buffer to the pair leader's MMA issuer (TMEM reads
+// completed by tcgen05.wait::ld; no memory is published). MT_GEMM_RELEASE_ARRIVE=1 (compile-time)
+// restores the release-semantics arrive for A/B measurements.
+__device__ __forceinline__ void tmem_release_arrive(uint32_t bar) {
+#if defined(MT_GEMM_RELEASE_ARRIVE) && MT_GEMM_RELEASE_ARRIVE
+  mbar_arrive_cluster(bar, 0);
+#else
+  mbar_arrive_cluster_relaxed(bar, 0);
+#endif
+}
+
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // Epilogue of one 32-row x 32-column piece held by one warp (thread t = row t, r[j] = column j):
@@ -489,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) {
             if (kPair)
-              mbar_arrive_cluster(smem_u32(&bars[2 * C::kStages + 2 + acc]), 0);
+              tmem_release_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
             else
               mbar_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
           }
@@ -681,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         if (kPair)
-          mbar_arrive_cluster(smem_u32(&bars[2 * C::kStages + 2 + acc]), 0);  // the leader's tmem_empty
+          tmem_release_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));  // the leader's tmem_empty
         else
           mbar_arrive(smem_u32(&bars[2 * C::kStages + 2 + acc]));
       }

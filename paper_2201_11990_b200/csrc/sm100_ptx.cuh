@@ -95,6 +95,15 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t local_bar, uint32_t
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_bar), "r"(cta));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+// Remote arrive without memory-release semantics: for hand-offs that publish no memory writes, only
+// the completion of prior tcgen05.ld reads (tcgen05.wait::ld + tcgen05.fence::before_thread_sync
+// precede it). The release form compiles to MEMBAR.ALL.GPU + ERRBAR ahead of the arrive, which
+// ncu showed as the epilogue warps' top stall once per tile (r02_sgemm).
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t local_bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_bar), "r"(cta));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
 
 // smem -> global tile store / reduce-add through a tensor map (bulk-group completion).
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
