@@ -124,7 +124,8 @@ def test_layer_rejects_bad_config():
     ctx.close()
 
 
-@pytest.mark.parametrize("shape", [(1024, 8, 256, 2), (4096, 32, 2048, 2)], ids=["h1024", "h4096_splitk"])
+@pytest.mark.parametrize("shape", [(1024, 8, 256, 2, "auto"), (1024, 8, 256, 2, "2"), (4096, 32, 2048, 2, "auto")],
+                         ids=["h1024", "h1024_split_rows", "h4096_splitk"])
 @pytest.mark.parametrize("fused", [False, True], ids=["unfused_attn", "flash_attn"])
 def test_activation_recompute_is_bit_identical(fused, shape, monkeypatch):
     """with recompute the backward re-runs the forward (same dropout masks) — the
@@ -135,7 +136,8 @@ def test_activation_recompute_is_bit_identical(fused, shape, monkeypatch):
     # the one-kernel fused backward accumulates dQ with fp32 atomics (order varies between runs): the
     # bit-identity check uses the deterministic dK/dV + dQ kernel pair
     monkeypatch.setenv("MT_ATTN_BWD2", "0")
-    hidden, heads, seq, mb = shape
+    hidden, heads, seq, mb, split = shape
+    monkeypatch.setenv("MT_ROWS_SPLIT", split)  # "2": the row kernels split each row over a CTA pair
     out = []
     for rc in (False, True):
         ctx = Context(0)
@@ -202,3 +204,50 @@ def test_dropout_masks_follow_the_training_step():
     assert O.step_seed(SEED, 0) == SEED and O.step_seed(SEED, 3) != SEED
     layer.close()
     ctx.close()
+
+
+@pytest.mark.parametrize("split", ["1", "2"], ids=["whole_rows", "split_rows"])
+def test_row_kernels_whole_and_split_rows_match_oracle(split, monkeypatch):
+    """The LayerNorm / bias-dropout-residual(+LN) / LayerNorm-backward row kernels in both layouts:
+    whole rows per CTA, and each row's columns split over a cluster of two CTAs (the layout of the
+    LayerNorm-carrying kernels at h > 12288, forced here at h = 1024 with MT_ROWS_SPLIT=2), whose LayerNorm statistics combine the
+    halves' (mean, M2) over DSMEM. Both match the oracle; they agree with each other to fp32 rounding of
+    the statistics."""
+    hidden, heads, seq, mb, p = 1024, 8, 128, 2, 0.1
+    params = O.init_params(hidden, SEED, 4)
+    x = O.normal(O.site_seed(SEED, "input", 0, 0), mb * seq, hidden)
+    g = O.normal(O.site_seed(SEED, "grad", 0, 0), mb * seq, hidden, std=1e-2)
+    res = {}
+    for mode in ("1", split):
+        monkeypatch.setenv("MT_ROWS_SPLIT", mode)
+        ctx = Context(0)
+        layer = Layer(ctx, PL.layer_desc(hidden, heads, seq, mb, dropout_hidden=p, dropout_attn=p, seed=SEED,
+                                         layer_index=4))
+        keep = [np.ascontiguousarray(O.to_bf16_bits(prm)) for prm in params]
+        for i, b in enumerate(keep):
+            layer.set_param(i, b.ctypes.data)
+        xd, gd = bf16_tensor(x), bf16_tensor(g)
+        yd, dxd = torch.empty_like(xd), torch.empty_like(xd)
+        s = torch.cuda.current_stream()
+        layer.forward(xd.data_ptr(), yd.data_ptr(), 0, s)
+        layer.backward(gd.data_ptr(), dxd.data_ptr(), 0, s)
+        torch.cuda.synchronize()
+        grads = []
+        for i, prm in enumerate(params):
+            out = np.empty(prm.size, np.float32)
+            layer.get_grad(i, out.ctypes.data)
+            grads.append(out.reshape(prm.shape))
+        res[mode] = (to_np(yd), to_np(dxd), grads)
+        layer.close()
+        ctx.close()
+    y, dx, grads = res[split]
+    ol = O.OracleLayer(hidden, heads, seq, mb, 1, dropout_hidden=p, dropout_attn=p, seed=SEED, layer_index=4,
+                       bf16_emulate=True, params=params)
+    y_ref, dx_ref = ol.forward(x), ol.backward(g)
+    assert rel(y, y_ref) < 5e-3 and rel(dx, dx_ref) < 1e-2
+    for i, name in enumerate(O.PARAM_NAMES):
+        assert rel(grads[i], ol.grads[i]) < 1e-2, name
+    y1, dx1, g1 = res["1"]
+    assert rel(y, y1) < 2e-3 and rel(dx, dx1) < 2e-3
+    for a, b in zip(grads, g1):  # bf16 rounding flips of the LN outputs reach the small bias gradients
+        assert rel(a, b) < 5e-3
