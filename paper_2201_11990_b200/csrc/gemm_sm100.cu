@@ -514,21 +514,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       // fences and warp syncs of 32-column pieces); fp32 outputs and BN = 160 use 32-column pieces
       constexpr bool kWide = (BN % 64) == 0;
       const int c_begin = (kWide && !f32) ? BN / 32 : 0;
+      // Accumulator reads are software-pipelined: the next piece's tcgen05.ld is in flight while this
+      // piece is scaled, packed, staged and stored (the epilogue is one warp per SMSP, latency-bound).
+      #if defined(MT_GEMM_NO_LDPIPE) && MT_GEMM_NO_LDPIPE
+      constexpr bool kLdPipe = false;
+#else
+      constexpr bool kLdPipe = true;
+#endif
       if (kWide && !f32) {
+        uint32_t ra[32], rb[32];
+        if (parts == nullptr) {
+          tmem_ld_32x32b_x32(tmem_row, ra);
+          tmem_ld_32x32b_x32(tmem_row + 32, rb);
+        }
 #pragma unroll 1
         for (int c2 = 0; c2 < BN / 64; ++c2) {
           const int col0 = nb * BN + c2 * 64;
           if (col0 >= p.n) break;
           float x[64];
           if (parts == nullptr) {
-            uint32_t ra[32], rb[32];
-            tmem_ld_32x32b_x32(tmem_row + c2 * 64, ra);
-            tmem_ld_32x32b_x32(tmem_row + c2 * 64 + 32, rb);
+            if (!kLdPipe && c2 > 0) {
+              tmem_ld_32x32b_x32(tmem_row + c2 * 64, ra);
+              tmem_ld_32x32b_x32(tmem_row + c2 * 64 + 32, rb);
+            }
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               x[j] = __uint_as_float(ra[j]);
               x[32 + j] = __uint_as_float(rb[j]);
+            }
+            if (kLdPipe && c2 + 1 < BN / 64 && col0 + 64 < p.n) {
+              tmem_ld_32x32b_x32(tmem_row + (c2 + 1) * 64, ra);
+              tmem_ld_32x32b_x32(tmem_row + (c2 + 1) * 64 + 32, rb);
             }
           } else {
             // split-K tail: the fixed-order sum of every split's published partial (this split's own
@@ -601,17 +618,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           bi = (bi + 1) % C::kEpiBufs;
         }
       }
+      uint32_t rn[32];
+      if (parts == nullptr && c_begin < BN / 32) tmem_ld_32x32b_x32(tmem_row + c_begin * 32, rn);
 #pragma unroll 1
       for (int c = c_begin; c < BN / 32; ++c) {
         const int col0 = nb * BN + c * 32;
         if (col0 >= p.n) break;
         float x[32];
         if (parts == nullptr) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tmem_row + c * 32, r);
+          if (!kLdPipe && c > c_begin) tmem_ld_32x32b_x32(tmem_row + c * 32, rn);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
+          for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(rn[j]);
+          if (kLdPipe && c + 1 < BN / 32 && col0 + 32 < p.n) tmem_ld_32x32b_x32(tmem_row + (c + 1) * 32, rn);
         } else {  // split-K tail: fixed-order sum of all splits' partials (see the 64-column path)
 #pragma unroll
           for (int j = 0; j < 32; ++j) x[j] = 0.f;

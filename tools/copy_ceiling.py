@@ -18,3 +18,13 @@ for mb in (25, 50, 100, 200, 400, 1024):
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1))
     print(f"copy {mb} MB read + {mb} MB write: {best * 1e3:.1f} us = {2 * n * 2 / best / 1e6:.0f} GB/s", flush=True)
+    best = 1e9
+    for _ in range(20):  # write-only stream (what an epilogue-bound GEMM such as the score GEMM does)
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.fill_(0.5)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    print(f"fill {mb} MB: {best * 1e3:.1f} us = {n * 2 / best / 1e6:.0f} GB/s", flush=True)
