@@ -82,8 +82,11 @@ typedef struct mt_gemm_args {
   int32_t block_n;  /* 0 = auto; else 64/128/160/192/256 */
   int32_t max_ctas; /* 0 = one CTA per SM; else cap (leaves SMs free for a concurrent collective) */
   /* Optional zero-initialised device workspace enabling the split-K tail (the last, partial wave of
-   * tiles is split over k and reduced by the last-arriving split). The first 64 KB hold arrival
-   * counters, which the kernel leaves zeroed. NULL disables. MT_GEMM_WORKSPACE_BYTES suggests a size. */
+   * tiles is split over k and reduced by the last-arriving split) and the dynamic tile scheduler (tiles
+   * handed out in raster order from a counter, so the CTAs sharing an operand tile stay in step and
+   * read it from L2 once). The first 64 KB hold counters, which the kernel leaves zeroed. GEMMs that
+   * share a workspace must be stream-ordered. NULL disables both. MT_GEMM_WORKSPACE_BYTES suggests a
+   * size. */
   void* workspace;
   int64_t workspace_bytes;
   mt_gemm_allreduce* allreduce; /* NULL, or the fused TP all-reduce of d (see above) */

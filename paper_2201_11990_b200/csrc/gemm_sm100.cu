@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -56,6 +57,10 @@ struct GemmParams {
   uint32_t* ar_group_cnt;
   int ar_group_cols;
   uint64_t store_policy;  // L2 hint on fp32 output stores (0 = none)
+  // dynamic tile scheduler: ticket counter (nullptr = static round-robin) and the number of tickets
+  // one launch draws (the one drawing the last resets the counter for the next launch)
+  int* tile_ctr;
+  int sched_fetches;
 };
 
 // kPair: 2-CTA (cta_group::2) tiles of 256 x BN — each CTA of the pair holds 128 rows of A and
@@ -72,7 +77,7 @@ struct Cfg {
   static constexpr int kEpiBytes = 4 * kEpiBufs * 4096;  // 4 epilogue warps x buffers x (32 rows x 128 B)
   static constexpr int kStagesRaw = (kSmemBudget - 2048 - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kEpiBytes + 256;
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kEpiBytes + 512;
   static constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256 ? 256 : 512);
   static constexpr uint32_t kAccStride = kTmemCols / 2;  // column offset of accumulator buffer 1
 };
@@ -302,6 +307,65 @@ __global__ void allreduce_wait_kernel(const uint32_t* counter, uint32_t target, 
   bounded_wait_geq<true>(counter, target, err, timeout_ns);
 }
 
+// Dynamic tile scheduler. The pair leader's producer draws work items from a global ticket counter
+// (each pair's first item is its static one) and publishes each into a kSchedDepth-deep ring in both
+// CTAs of the pair: st.async into each CTA's slot completing on that CTA's `full` mbarrier (one
+// arrival = that CTA's producer's expect_tx). Consumers — the MMA issuer, the epilogue warps and the
+// peer's producer — read the slot and hand it back on the leader's `empty` mbarrier. Items are handed
+// out in raster order as units free up, so the CTAs that share an operand tile start it together and
+// read it from L2 once (static round-robin let pairs drift apart over the waves: the fc1 forward read
+// 3.2x its operands from DRAM).
+constexpr int kSchedDepth = 4;
+struct Sched {
+  uint64_t* full;
+  uint64_t* empty;
+  int* slot;
+};
+
+__device__ __forceinline__ uint32_t mapa_cta(uint32_t addr, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ void st_async_s32(uint32_t addr, int v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.s32 [%0], %1, [%2];" ::"r"(addr), "r"(v),
+               "r"(bar)
+               : "memory");
+}
+
+template <bool kPair>
+__device__ __forceinline__ void sched_publish(const Sched& sc, int i, int w) {
+  const int s = i & (kSchedDepth - 1);
+  mbar_wait(smem_u32(&sc.empty[s]), ((i / kSchedDepth) & 1) ^ 1);
+  const uint32_t full = smem_u32(&sc.full[s]), slot = smem_u32(&sc.slot[s]);
+  if (kPair) {
+    mbar_arrive_expect_tx(full, 4);
+    st_async_s32(mapa_cta(slot, 0), w, mapa_cta(full, 0));
+    st_async_s32(mapa_cta(slot, 1), w, mapa_cta(full, 1));
+  } else {
+    *reinterpret_cast<volatile int*>(&sc.slot[s]) = w;
+    mbar_arrive(full);  // release.cta: the slot store is visible to the waiters
+  }
+}
+
+// expect: the peer CTA's producer (the one arrival on its own `full` barrier).
+template <bool kPair>
+__device__ __forceinline__ int sched_take(const Sched& sc, int i, bool expect, uint32_t rank) {
+  const int s = i & (kSchedDepth - 1);
+  const uint32_t full = smem_u32(&sc.full[s]);
+  if (expect) mbar_arrive_expect_tx(full, 4);
+  mbar_wait(full, (i / kSchedDepth) & 1);
+  const int w = *reinterpret_cast<volatile int*>(&sc.slot[s]);
+  if (w != INT_MIN) {  // predicated on the loaded value: the hand-back cannot overtake the read
+    const uint32_t e = smem_u32(&sc.empty[s]);
+    if (!kPair || rank == 0)
+      mbar_arrive(e);
+    else
+      mbar_arrive_cluster_relaxed(e, 0);
+  }
+  return w;
+}
+
 template <int BN, bool kAMN, bool kBMN, bool kPair, bool kAR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
@@ -317,6 +381,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // bars[0..S) full, bars[S..2S) empty, bars[2S..2S+2) tmem_full, bars[2S+2..2S+4) tmem_empty
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4);
   volatile int* split_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  Sched sc;
+  sc.full = bars + 2 * C::kStages + 6;  // after tmem_slot / split_flag (8 bytes)
+  sc.empty = sc.full + kSchedDepth;
+  sc.slot = reinterpret_cast<int*>(sc.empty + kSchedDepth);
+  const bool dyn = p.tile_ctr != nullptr;
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -337,6 +406,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&bars[2 * C::kStages + a]), 1);
       mbar_init(smem_u32(&bars[2 * C::kStages + 2 + a]), kPair ? 8 : 4);  // epilogue warps (of both CTAs)
+    }
+    for (int s = 0; s < kSchedDepth; ++s) {
+      mbar_init(smem_u32(&sc.full[s]), 1);
+      // MMA issuer + 4 epilogue warps (+ the peer's producer and 4 epilogue warps)
+      mbar_init(smem_u32(&sc.empty[s]), kPair ? 10 : 5);
     }
     fence_barrier_init();
   }
@@ -368,7 +442,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_b = !p.hints ? kEvictNormal
                                       : (p.n_fastest ? kEvictLast : (p.hints == 2 ? kEvictNormal : kEvictFirst));
       uint32_t stage = 0, phase = 0;
-      for (int w = t_first; w < p.work_items; w += t_stride) {
+      int ticket = 0;  // the next dynamic ticket, drawn one item ahead
+      for (int i = 0;; ++i) {
+        int w;
+        if (!dyn) {
+          w = t_first + i * t_stride;
+        } else if (leader) {
+          if (i == 0) {
+            w = t_first;
+          } else {
+            w = t_stride + ticket;
+            if (ticket == p.sched_fetches - 1) *reinterpret_cast<volatile int*>(p.tile_ctr) = 0;  // last ticket
+          }
+          sched_publish<kPair>(sc, i, w);
+          if (w < p.work_items) ticket = atomicAdd(p.tile_ctr, 1);
+        } else {
+          w = sched_take<kPair>(sc, i, true, rank);
+        }
+        if (w >= p.work_items) break;
         Work wk;
         if (!get_work<BN, BMT>(p, w, wk)) continue;
         const int b = wk.b, mb = wk.mb, nb = wk.nb;
@@ -410,7 +501,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------------------------------ MMA issuer (pair leader only)
       constexpr uint32_t idesc = umma_idesc_bf16(BMT, BN, kAMN ? 1 : 0, kBMN ? 1 : 0);
       uint32_t stage = 0, phase = 0, it = 0;
-      for (int w = t_first; w < p.work_items; w += t_stride) {
+      for (int i = 0;; ++i) {
+        const int w = dyn ? sched_take<kPair>(sc, i, false, 0) : t_first + i * t_stride;
+        if (w >= p.work_items) break;
         Work wk;
         if (!get_work<BN, BMT>(p, w, wk)) continue;
         const int kb0 = wk.kb0, kb1 = wk.kb1;
@@ -459,7 +552,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t it = 0;
     // fused all-reduce: the previous tile, published once this tile's stores were issued
     int unpublished = -1;
-    for (int w = t_first; w < p.work_items; w += t_stride) {
+    for (int i = 0;; ++i) {
+      int w = t_first + i * t_stride;
+      if (dyn) {
+        int v = 0;
+        if (lane == 0) v = sched_take<kPair>(sc, i, false, rank);
+        w = __shfl_sync(0xffffffffu, v, 0);
+      }
+      if (w >= p.work_items) break;
       Work wk;
       if (!get_work<BN, BMT>(p, w, wk)) continue;
       const int b = wk.b, mb = wk.mb, nb = wk.nb;
@@ -868,7 +968,7 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
     if (full > 0 && tail > 0 && tail * 2 <= units) {
       const int splits = std::min({units / tail, p.kblocks / 4, 8});
       const size_t need = kSplitCounterBytes + (size_t)tail * splits * 2 * 128 * BN * sizeof(float);
-      if (splits >= 2 && (size_t)a.workspace_bytes >= need && tail * 2 * (int)sizeof(int) <= kSplitCounterBytes) {
+      if (splits >= 2 && (size_t)a.workspace_bytes >= need && tail * 2 * (int)sizeof(int) <= kSplitCounterBytes - 64) {
         p.full_tiles = full;
         p.splits = splits;
         p.work_items = full + tail * splits;
@@ -938,14 +1038,26 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
       return 2;
     attr_devices.fetch_or(bit, std::memory_order_release);
   }
+  // dynamic tile scheduler: the ticket counter is the last int of the workspace's counter block
+  static const bool dyn_sched = [] {
+    const char* e = getenv("MT_GEMM_DYNAMIC");
+    return !(e && e[0] == '0');
+  }();
+  auto set_sched = [&](int units) {
+    if (!dyn_sched || a.workspace == nullptr) return;
+    p.tile_ctr = static_cast<int*>(a.workspace) + kSplitCounterBytes / sizeof(int) - 1;
+    p.sched_fetches = std::max(0, p.work_items - units) + std::min(units, p.work_items);
+  };
   if (!kPair) {
     const int cap = a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms();
     const int grid = p.work_items < cap ? p.work_items : cap;
+    set_sched(grid);
     kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, md, maux, p);
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
   }
   const int cap = a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms();
   const int pairs = std::max(1, std::min(p.work_items, cap / 2));
+  set_sched(pairs);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(kThreads);
