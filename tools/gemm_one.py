@@ -25,6 +25,10 @@ SHAPES = {  # name: (m, n, k, a_mn, b_mn, epilogue)
     "wg_mm_f32": (4 * h, h, M, 1, 1, N.EPI_STORE_F32),
     "wg_mm_bf16": (4 * h, h, M, 1, 1, N.EPI_STORE_BF16),
     "wg_kk_bf16": (4 * h, h, M, 0, 0, N.EPI_STORE_BF16),
+    "wg_km_bf16": (4 * h, h, M, 0, 1, N.EPI_STORE_BF16),
+    "wg_mk_bf16": (4 * h, h, M, 1, 0, N.EPI_STORE_BF16),
+    # the forward's shape class with the wgrad's short K (tile count 6x the forward's)
+    "fwd_k2048": (M * 6, 4 * h, M, 0, 0, N.EPI_STORE_BF16),
     # GPT-3 h=12288 at TP=8 / TP=4 (per-GPU shard shapes)
     "g8_proj_fwd": (M, h, h // 8, 0, 0, N.EPI_STORE_BF16),
     "g4_proj_fwd": (M, h, h // 4, 0, 0, N.EPI_STORE_BF16),
