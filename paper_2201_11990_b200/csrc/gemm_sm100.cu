@@ -985,13 +985,19 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
   // wgrad of fc1, M = 4h/t >> N = h, would otherwise re-read its 200 MB A operand per n-block).
   p.n_fastest = (m > n) ? 1 : 0;
   // L2 eviction hints on the operand loads (streamed operand evict_first, re-read one evict_last):
-  // measured 5-10% slower for the m-fastest forward / dgrad GEMMs but ~2% faster for the n-fastest
-  // wgrad GEMMs (tools/gemm_one.py), so by default only the latter use them. MT_GEMM_HINTS=0/1 forces.
+  // ~2% faster for the n-fastest wgrad GEMMs; with the dynamic tile scheduler also 1-2% faster for
+  // the m-fastest GEMMs up to K = 16384 (fc1 / QKV forward at K = 12288) but 2-4% slower at
+  // K = 49152 (tools/hints_dyn_ab.sh), so those keep plain loads. MT_GEMM_HINTS=0/1 forces.
   static const int hints = [] {
     const char* e = getenv("MT_GEMM_HINTS");
     return e ? atoi(e) : -1;
   }();
-  p.hints = hints >= 0 ? hints : (p.n_fastest ? 1 : 0);
+  static const bool shortk_hints = [] {  // MT_GEMM_SHORTK_HINTS=0: plain loads for every m-fastest GEMM (A/B)
+    const char* e = getenv("MT_GEMM_SHORTK_HINTS");
+    return !(e && e[0] == '0');
+  }();
+  const bool short_k = shortk_hints && a.causal == MT_CAUSAL_NONE && p.kblocks <= 256;
+  p.hints = hints >= 0 ? hints : ((p.n_fastest || short_k) ? 1 : 0);
   // (direct register->global fp32 stores were measured 8% slower than smem staging + TMA store)
   p.d_bf16 = static_cast<__nv_bfloat16*>(a.d);
   p.d_f32 = static_cast<float*>(a.d);
