@@ -159,3 +159,42 @@ def test_gemm_split_k_tail(epi, max_ctas):
                            outs[0].view(torch.int16) if o.dtype == torch.bfloat16 else outs[0].view(torch.int32))
 
 
+
+
+def test_gemm_dynamic_scheduler_matches_static():
+    """With a workspace the GEMM hands tiles out dynamically (ticket counter in the workspace, raster
+    order, per-pair mbarrier ring); without one it walks them round-robin. Every tile's arithmetic is
+    the same either way, so for shapes without a split-K tail the outputs are bit-identical. A sequence
+    of launches of different tile counts (fewer tiles than CTA pairs, several waves, causal batched,
+    fp32 n-fastest) sharing one workspace also checks that the counter resets itself after each
+    launch."""
+    g = torch.Generator(device="cuda").manual_seed(7)
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    cases = [
+        dict(m=256, n=512, k=256),                                   # 4 pair tiles < 74 pairs
+        dict(m=2048, n=12288, k=4096),                               # ~5 waves, m-fastest, bf16
+        dict(m=6144, n=1536, k=2048, a_mn=True, b_mn=True, f32=True),  # n-fastest wgrad shape, fp32 out
+        dict(m=1024, n=1024, k=128, batch=6, causal=1),              # causal score GEMM, batched heads
+        dict(m=1024, n=128, k=1024, batch=6, causal=2),              # causal P V GEMM (k-range clipped)
+        dict(m=640, n=4096, k=1024, bn=160),                         # single-CTA (non-pair) tiles
+    ]
+    for rep in range(2):
+        for cs in cases:
+            m, n, k = cs["m"], cs["n"], cs["k"]
+            batch = cs.get("batch", 1)
+            a_mn, b_mn = cs.get("a_mn", False), cs.get("b_mn", False)
+            A = torch.randn(batch, k, m, device="cuda", generator=g).bfloat16() if a_mn else \
+                torch.randn(batch, m, k, device="cuda", generator=g).bfloat16()
+            B = torch.randn(batch, k, n, device="cuda", generator=g).bfloat16() if b_mn else \
+                torch.randn(batch, n, k, device="cuda", generator=g).bfloat16()
+            dt = torch.float32 if cs.get("f32") else torch.bfloat16
+            epi = N.EPI_STORE_F32 if cs.get("f32") else N.EPI_STORE_BF16
+            outs = []
+            for w in (None, ws):
+                D = torch.zeros(batch, m, n, device="cuda", dtype=dt)
+                _gemm(A, B, D, m, n, k, a_mn=a_mn, b_mn=b_mn, batch=batch, abs_=A[0].numel(), bbs=B[0].numel(),
+                      dbs=D[0].numel(), epi=epi, causal=cs.get("causal", 0), bn=cs.get("bn", 0), ws=w)
+                outs.append(D)
+            view = torch.int32 if dt == torch.float32 else torch.int16
+            assert torch.equal(outs[0].view(view), outs[1].view(view)), (rep, cs)
+            assert int(ws[: 64 * 1024].sum()) == 0, (rep, cs)  # the ticket counter reset itself
