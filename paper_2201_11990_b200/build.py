@@ -84,10 +84,16 @@ def build(verbose: bool = False, jobs: int = 8) -> Path:
             _drain(procs)
     _drain(procs)
     newest = max(o.stat().st_mtime for o in objs)
-    if _VARIANT or not LIB.exists() or LIB.stat().st_mtime < newest:
+    # the library records which object set it was linked from, so the default build relinks after an
+    # A/B variant build even when the default objects are older than the variant's library
+    stamp = ROOT / "build" / "libmtnlg.variant"
+    want = " ".join(_VARIANT)
+    linked = stamp.read_text() if stamp.exists() else None
+    if linked != want or not LIB.exists() or LIB.stat().st_mtime < newest:
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs),
               f"-L{NCCL / 'lib'}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={NCCL / 'lib'}",
               "-Xcompiler", "-fopenmp", "-lgomp"])
+        stamp.write_text(want)
     return LIB
 
 

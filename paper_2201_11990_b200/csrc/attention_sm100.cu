@@ -1071,19 +1071,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mw = __ldg(reinterpret_cast<const uint4*>(p.mask + ((size_t)head * p.seq + qrow) * (p.seq >> 5)) + jb);
       mbar_wait(smem_u32(s_full), ph);
       tc_fence_after();
-      float pr[128];
+      // The row's probabilities stay packed as bf16 pairs (64 registers instead of 128 fp32 — the
+      // fp32 row spilled to local memory at 255 registers); P is written to the tile by masking the
+      // packed words with the keep bits, and dS reads them back unpacked.
+      uint32_t pp[64];
       auto probs = [&](auto diag_tag) {
         constexpr bool kDiag = decltype(diag_tag)::value;
 #pragma unroll
-        for (int c = 0; c < 4; c += 2) {
-          uint32_t u[64];
-          tmem_ld_32x32b_x32(lane_base + kSC + c * 32, *reinterpret_cast<uint32_t(*)[32]>(u));
-          tmem_ld_32x32b_x32(lane_base + kSC + c * 32 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+        for (int c = 0; c < 4; ++c) {
+          uint32_t u[32];
+          tmem_ld_32x32b_x32(lane_base + kSC + c * 32, u);
           tmem_ld_wait();
 #pragma unroll
-          for (int t = 0; t < 64; ++t) {
+          for (int t = 0; t < 32; t += 2) {
             const int col = c * 32 + t;
-            pr[col] = (kDiag && col > r) ? 0.f : ex2(__uint_as_float(u[t]) * p.alpha_log2 - lse2);
+            const float a = (kDiag && col > r) ? 0.f : ex2(__uint_as_float(u[t]) * p.alpha_log2 - lse2);
+            const float b = (kDiag && col + 1 > r) ? 0.f : ex2(__uint_as_float(u[t + 1]) * p.alpha_log2 - lse2);
+            pp[col >> 1] = pack_bf16x2(a, b);
           }
         }
       };
@@ -1094,18 +1098,26 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(s_free));
+      // keep bits: byte g of the 16-byte word = the 8 columns of group g (the forward's mask layout)
+      uint32_t kw[4] = {mw.x, mw.y, mw.z, mw.w};
+      if (p.mask == nullptr && p.thresh16 != 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t w = 0;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) w |= keep8(p.seed, row_idx + (4 * q + g) * 8, p.thresh16) << (8 * g);
+          kw[q] = w;
+        }
+      }
       // P (dropped, unscaled) into the tile: the previous block's dK / dQ MMAs are done (its drain waited)
-      uint32_t keep[16];
-      const uint32_t mwa[4] = {mw.x, mw.y, mw.z, mw.w};
 #pragma unroll
       for (int g = 0; g < 16; ++g) {
-        keep[g] = (p.mask != nullptr || p.thresh16 == 0) ? (mwa[g >> 2] >> ((g & 3) * 8)) & 0xffu
-                                                         : keep8(p.seed, row_idx + g * 8, p.thresh16);
-        float v[8];
+        const uint32_t kb = kw[g >> 2] >> ((g & 3) * 8);
+        uint32_t w[4];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) v[t] = ((keep[g] >> t) & 1u) ? pr[g * 8 + t] : 0.f;
-        st_shared_v4(sw128_addr(sT + (g >> 3) * 16384, r, g & 7), pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
-                     pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+        for (int q = 0; q < 4; ++q)
+          w[q] = pp[g * 4 + q] & (((kb >> (2 * q)) & 1u) * 0xffffu | ((kb >> (2 * q + 1)) & 1u) * 0xffff0000u);
+        st_shared_v4(sw128_addr(sT + (g >> 3) * 16384, r, g & 7), w[0], w[1], w[2], w[3]);
       }
       fence_proxy_async_smem();
       tc_fence_before();
@@ -1116,22 +1128,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_wait(smem_u32(pv_done), ph);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 4; c += 2) {
-        uint32_t u[64];
-        tmem_ld_32x32b_x32(lane_base + kDP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(u));
-        tmem_ld_32x32b_x32(lane_base + kDP + c * 32 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+      for (int c = 0; c < 4; ++c) {
+        uint32_t u[32];
+        tmem_ld_32x32b_x32(lane_base + kDP + c * 32, u);
         tmem_ld_wait();
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
+        for (int g = 0; g < 4; ++g) {
           const int gg = c * 4 + g;  // 8-column chunk index 0..15
-          float v[8];
+          const uint32_t kb = kw[gg >> 2] >> ((gg & 3) * 8);
+          uint32_t w[4];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const float dp = ((keep[gg] >> t) & 1u) ? __uint_as_float(u[g * 8 + t]) * p.drop_scale : 0.f;
-            v[t] = pr[gg * 8 + t] * (dp - Di);
+          for (int q = 0; q < 4; ++q) {
+            const float2 pr = unpack_bf16x2(pp[gg * 4 + q]);
+            const float d0 = ((kb >> (2 * q)) & 1u) ? __uint_as_float(u[g * 8 + 2 * q]) * p.drop_scale : 0.f;
+            const float d1 = ((kb >> (2 * q + 1)) & 1u) ? __uint_as_float(u[g * 8 + 2 * q + 1]) * p.drop_scale : 0.f;
+            w[q] = pack_bf16x2(pr.x * (d0 - Di), pr.y * (d1 - Di));
           }
-          st_shared_v4(sw128_addr(sT + (gg >> 3) * 16384, r, gg & 7), pack_bf16x2(v[0], v[1]),
-                       pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+          st_shared_v4(sw128_addr(sT + (gg >> 3) * 16384, r, gg & 7), w[0], w[1], w[2], w[3]);
         }
       }
       fence_proxy_async_smem();
