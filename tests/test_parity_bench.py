@@ -11,13 +11,15 @@ Variant coverage (dispatch points in parentheses):
   * GPT-3 layer, TP=1, h=12288, 96 heads (hd=128), s=2048, b=1, p=0.1, bench seed — the default bench
     line, driven exactly as bench.py does (Stage + mt_layer_init_params + torch.randn inputs/targets
     on cuda with generator seed SEED, mt_stage_train_step_dev): loss and all 12 gradients, plus y and
-    dx through mt_layer_forward / mt_layer_backward of the same layer and microbatch id. Hits
-    softmax_fwd_kernel<8> (kernels.cu MT_VPL_DISPATCH, s=2048), ln_fwd_rows / bdr_ln_rows /
+    dx through mt_layer_forward / mt_layer_backward of the same layer and microbatch id. Hits the
+    default fused attention at s=2048 (attn_fwd2_kernel<128>, attn_bwd2_kernel<128> with its dQ
+    atomics, attention_sm100.cu), ln_fwd_rows / bdr_ln_rows /
     ln_bwd_rows_kernel<3> (rows_sm100.cu, h=12288 -> 1536 vectors / 512 threads), the BN=256 CTA-pair
     GEMM tiles, and the split-K tail (gemm_sm100.cu, K >= 16384: fc2 forward and fc1 dgrad, K=49152).
   * MT-NLG layer, ONE TP=8 shard (bench.py --config mtnlg --shard-of 8): h=20480, 16 local heads of
-    hd=160, s=2048, against the oracle's shard mode (same shard, no all-reduce). Hits the hd=160 score /
-    PV contractions at s=2048 (BN=160 tiles), ln_bwd_rows_kernel<5> (h=20480 -> 2560 vectors), and
+    hd=160, s=2048, against the oracle's shard mode (same shard, no all-reduce). Hits the unfused
+    attention (default at hd=160): the hd=160 score / PV contractions at s=2048 (BN=160 tiles),
+    softmax_fwd_kernel<8> (kernels.cu MT_VPL_DISPATCH, s=2048), ln_bwd_rows_kernel<5> (h=20480 -> 2560 vectors), and
     the TP=8 shard GEMM shapes (K = h/8 = 2560 projection, K = 4h/8 = 10240 fc2).
   * h=8192 PP-slice layer (BASELINE configs[3] shape, 64 heads, hd=128, s=2048), TP=1, with a second
     layer index and microbatch id (different dropout streams): split-K tail at K=32768.
