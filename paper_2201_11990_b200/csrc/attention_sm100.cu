@@ -939,8 +939,8 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
                : "memory");
 }
 
-template <int HD>
-__global__ void __launch_bounds__(kAttnThreads, 1)
+template <int HD, int NH>
+__global__ void __launch_bounds__(128 + 128 * NH, 1)
     attn_bwd2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                      const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
                      const AttnBwdParams p, float* __restrict__ dq_acc) {
@@ -974,7 +974,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     for (auto* b : {&tq, &tk, &tv, &tdo}) tma_prefetch_desc(b);
     for (int i = 0; i < 13; ++i) {
       const bool four = (bars + i == s_free) || (bars + i == p_full) || (bars + i == ds_full) || (bars + i == dq_free);
-      mbar_init(smem_u32(bars + i), four ? 4 : 1);
+      mbar_init(smem_u32(bars + i), four ? 4 * NH : 1);
     }
     fence_barrier_init();
   }
@@ -1023,7 +1023,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_wait(smem_u32(qo_full), 0);
       tc_fence_after();
       issue_s(0);
-      issue_dp(0);
       for (int b = 0; b < nblk; ++b) {
         const int ph = b & 1;
         // dV += P^T dO_i
@@ -1032,12 +1031,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mma_chain(tmem + kDV, id_acc, 8, b > 0, [&](int kk) { return mnmaj(sT, kk); },
                   [&](int kk) { return mnmaj(sO(b), kk); });
         tc_commit(smem_u32(pv_done));
-        // S(i+1) as soon as the softmax warps read S(i) (they arrive s_free before writing P)
+        // S(i+1): the softmax warps read S(i) before they wrote P(i)
         if (b + 1 < nblk) {
           mbar_wait(smem_u32(qo_full + ((b + 1) & 1)), ((b + 1) >> 1) & 1);
           tc_fence_after();
           issue_s(b + 1);
         }
+        // dP(i) once the previous block's dQ partial left the shared columns (drained while dV(i) ran)
+        if (b > 0) {
+          mbar_wait(smem_u32(dq_free), ph ^ 1);
+          tc_fence_after();
+        }
+        issue_dp(b);
         // dK += dS^T Q_i ; dQ partial = dS K_j into dP's columns (dP read before dS was written)
         mbar_wait(smem_u32(ds_full), ph);
         tc_fence_after();
@@ -1047,99 +1052,141 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                   [&](int kk) { return mnmaj(sK, kk); });
         tc_commit(smem_u32(mma_done));
         tc_commit(smem_u32(qo_empty + (b & 1)));
-        if (b + 1 < nblk) {
-          mbar_wait(smem_u32(dq_free), ph);  // the dQ partial left TMEM
-          tc_fence_after();
-          issue_dp(b + 1);
-        }
       }
     }
   } else if (warp >= 4) {
-    const uint32_t quad = warp - 4;
+    // NH column halves: warpgroup hf (warps 4 + 4 hf .. 7 + 4 hf) owns columns [hf * CW, (hf + 1) * CW)
+    // of every block row (the softmax backward has no row reduction: D_i and lse_i are precomputed),
+    // so with NH = 2 two warpgroups share each block's exp / mask / dS work and the dQ drain.
+    constexpr int CW = 128 / NH;          // score columns per thread
+    constexpr int QW = HD / NH;           // dQ / dV / dK columns per thread
+    const uint32_t quad = (warp - 4) & 3;
+    const int hf = (int)(warp - 4) >> 2;
+    const int col0 = hf * CW, g0 = col0 / 8;
     const int r = quad * 32 + lane;
     const uint32_t lane_base = tmem + ((quad * 32) << 16);
-    for (int b = 0; b < nblk; ++b) {
-      const int ib = jb + b, ph = b & 1;
-      const int qrow = ib * 128 + r;
-      const float lse2 = p.lse[(long long)head * p.seq + qrow] * kLog2e;
-      const float Di = p.D[(long long)head * p.seq + qrow];
-      const uint64_t row_idx = ((uint64_t)(p.head_base + head) * p.seq + qrow) * (uint64_t)p.seq + (uint64_t)jb * 128;
-      const bool diag = (ib == jb);
-      // the block's 128 keep bits in one 16-byte load, issued before the S wait so its latency hides
-      uint4 mw = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    // Software-pipelined per block i (the tensor core and the softmax warps overlap):
+    //   write P(i) -> [dV(i) MMA | drain dQ(i-1)] -> dP(i) MMA -> dS(i) -> [dK(i), dQ(i) MMAs | P(i+1) exps]
+    uint32_t pp[CW / 2];  // the row's probabilities, packed bf16 pairs (fp32 spilled at 255 registers)
+    uint4 mw, mw_nx;      // the block's 128 keep bits from the forward (current, next block)
+    float Di = 0.f, D_nx = 0.f, lse_nx = 0.f;
+    // the per-row operands of block b (lse, D, keep bits): issued one block ahead so their L2 latency
+    // is off the softmax warps' critical path
+    auto prefetch = [&](int b) {
+      const int qrow = (jb + b) * 128 + r;
+      lse_nx = p.lse[(long long)head * p.seq + qrow];
+      D_nx = p.D[(long long)head * p.seq + qrow];
+      mw_nx = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
       if (p.mask != nullptr && p.thresh16)
-        mw = __ldg(reinterpret_cast<const uint4*>(p.mask + ((size_t)head * p.seq + qrow) * (p.seq >> 5)) + jb);
-      mbar_wait(smem_u32(s_full), ph);
-      tc_fence_after();
-      // The row's probabilities stay packed as bf16 pairs (64 registers instead of 128 fp32 — the
-      // fp32 row spilled to local memory at 255 registers); P is written to the tile by masking the
-      // packed words with the keep bits, and dS reads them back unpacked.
-      uint32_t pp[64];
-      auto probs = [&](auto diag_tag) {
-        constexpr bool kDiag = decltype(diag_tag)::value;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t u[32];
-          tmem_ld_32x32b_x32(lane_base + kSC + c * 32, u);
-          tmem_ld_wait();
-#pragma unroll
-          for (int t = 0; t < 32; t += 2) {
-            const int col = c * 32 + t;
-            const float a = (kDiag && col > r) ? 0.f : ex2(__uint_as_float(u[t]) * p.alpha_log2 - lse2);
-            const float b = (kDiag && col + 1 > r) ? 0.f : ex2(__uint_as_float(u[t + 1]) * p.alpha_log2 - lse2);
-            pp[col >> 1] = pack_bf16x2(a, b);
-          }
-        }
-      };
-      if (diag)
-        probs(std::true_type{});
-      else
-        probs(std::false_type{});
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(s_free));
-      // keep bits: byte g of the 16-byte word = the 8 columns of group g (the forward's mask layout)
-      uint32_t kw[4] = {mw.x, mw.y, mw.z, mw.w};
+        mw_nx = __ldg(reinterpret_cast<const uint4*>(p.mask + ((size_t)head * p.seq + qrow) * (p.seq >> 5)) + jb);
+    };
+    // exps of block b into pp (S(b) in TMEM), its keep bits and row term (prefetch(b) issued before)
+    auto load_block = [&](int b) {
+      const int ib = jb + b;
+      const int qrow = ib * 128 + r;
+      const float lse2 = lse_nx * kLog2e;
+      Di = D_nx;
+      mw = mw_nx;
       if (p.mask == nullptr && p.thresh16 != 0) {
+        const uint64_t row_idx = ((uint64_t)(p.head_base + head) * p.seq + qrow) * (uint64_t)p.seq + (uint64_t)jb * 128;
+        uint32_t kw[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint32_t w = 0;
 #pragma unroll
-          for (int g = 0; g < 4; ++g) w |= keep8(p.seed, row_idx + (4 * q + g) * 8, p.thresh16) << (8 * g);
+          for (int g = 0; g < 4; ++g)
+            if ((4 * q + g) >= g0 && (4 * q + g) < g0 + CW / 8)
+              w |= keep8(p.seed, row_idx + (4 * q + g) * 8, p.thresh16) << (8 * g);
           kw[q] = w;
         }
+        mw = make_uint4(kw[0], kw[1], kw[2], kw[3]);
       }
-      // P (dropped, unscaled) into the tile: the previous block's dK / dQ MMAs are done (its drain waited)
+      mbar_wait(smem_u32(s_full), b & 1);
+      tc_fence_after();
+      auto probs = [&](auto diag_tag) {
+        constexpr bool kDiag = decltype(diag_tag)::value;
 #pragma unroll
-      for (int g = 0; g < 16; ++g) {
+        for (int c = 0; c < CW / 32; ++c) {
+          uint32_t u[32];
+          tmem_ld_32x32b_x32(lane_base + kSC + col0 + c * 32, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < 32; t += 2) {
+            const int col = col0 + c * 32 + t;
+            const float a = (kDiag && col > r) ? 0.f : ex2(__uint_as_float(u[t]) * p.alpha_log2 - lse2);
+            const float b2 = (kDiag && col + 1 > r) ? 0.f : ex2(__uint_as_float(u[t + 1]) * p.alpha_log2 - lse2);
+            pp[(c * 32 + t) >> 1] = pack_bf16x2(a, b2);
+          }
+        }
+      };
+      if (ib == jb)
+        probs(std::true_type{});
+      else
+        probs(std::false_type{});
+      tc_fence_before();
+    };
+    // TMEM -> registers -> fp32 vector atomics: this half of dQ_i's partial (block b)
+    auto drain = [&](int b) {
+      const int qrow = (jb + b) * 128 + r;
+      float* dst = dq_acc + ((size_t)head * p.seq + qrow) * HD + hf * QW;
+#pragma unroll
+      for (int c = 0; c < QW / 32; ++c) {
+        uint32_t u[32];
+        tmem_ld_32x32b_x32(lane_base + kDP + hf * QW + c * 32, u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          red_add_v4(dst + c * 32 + 4 * v, __uint_as_float(u[4 * v]), __uint_as_float(u[4 * v + 1]),
+                     __uint_as_float(u[4 * v + 2]), __uint_as_float(u[4 * v + 3]));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(dq_free));
+    };
+    prefetch(0);
+    load_block(0);
+    for (int b = 0; b < nblk; ++b) {
+      const int ph = b & 1;
+      const uint32_t kw[4] = {mw.x, mw.y, mw.z, mw.w};  // byte g = keep bits of the 8 columns of group g
+      if (b + 1 < nblk) prefetch(b + 1);
+      // P (dropped, unscaled) into the tile once the previous block's dK / dQ MMAs have read dS from it
+      if (b > 0) mbar_wait(smem_u32(mma_done), ph ^ 1);
+#pragma unroll
+      for (int gl = 0; gl < CW / 8; ++gl) {
+        const int g = g0 + gl;
         const uint32_t kb = kw[g >> 2] >> ((g & 3) * 8);
         uint32_t w[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          w[q] = pp[g * 4 + q] & (((kb >> (2 * q)) & 1u) * 0xffffu | ((kb >> (2 * q + 1)) & 1u) * 0xffff0000u);
+          w[q] = pp[gl * 4 + q] & (((kb >> (2 * q)) & 1u) * 0xffffu | ((kb >> (2 * q + 1)) & 1u) * 0xffff0000u);
         st_shared_v4(sw128_addr(sT + (g >> 3) * 16384, r, g & 7), w[0], w[1], w[2], w[3]);
       }
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(p_full));
+      // the previous block's dQ partial leaves TMEM while the dV MMA runs; dP(i) is issued after it
+      if (b > 0) {
+        tc_fence_after();
+        drain(b - 1);
+      }
       // dS = P~ (dP' - D) once dP is in TMEM and the dV MMA has consumed P from the tile
       mbar_wait(smem_u32(dp_full), ph);
       mbar_wait(smem_u32(pv_done), ph);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < CW / 32; ++c) {
         uint32_t u[32];
-        tmem_ld_32x32b_x32(lane_base + kDP + c * 32, u);
+        tmem_ld_32x32b_x32(lane_base + kDP + col0 + c * 32, u);
         tmem_ld_wait();
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          const int gg = c * 4 + g;  // 8-column chunk index 0..15
+          const int gl = c * 4 + g, gg = g0 + gl;  // 8-column chunk index 0..15
           const uint32_t kb = kw[gg >> 2] >> ((gg & 3) * 8);
           uint32_t w[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float2 pr = unpack_bf16x2(pp[gg * 4 + q]);
+            const float2 pr = unpack_bf16x2(pp[gl * 4 + q]);
             const float d0 = ((kb >> (2 * q)) & 1u) ? __uint_as_float(u[g * 8 + 2 * q]) * p.drop_scale : 0.f;
             const float d1 = ((kb >> (2 * q + 1)) & 1u) ? __uint_as_float(u[g * 8 + 2 * q + 1]) * p.drop_scale : 0.f;
             w[q] = pack_bf16x2(pr.x * (d0 - Di), pr.y * (d1 - Di));
@@ -1151,27 +1198,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(ds_full));
-      // drain dQ_i's partial: TMEM -> registers -> fp32 vector atomics into the accumulator
-      mbar_wait(smem_u32(mma_done), ph);
-      tc_fence_after();
-      float* dst = dq_acc + ((size_t)head * p.seq + qrow) * HD;
-#pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t u[32];
-        tmem_ld_32x32b_x32(lane_base + kDP + c * 32, u);
-        tmem_ld_wait();
-#pragma unroll
-        for (int v = 0; v < 8; ++v)
-          red_add_v4(dst + c * 32 + 4 * v, __uint_as_float(u[4 * v]), __uint_as_float(u[4 * v + 1]),
-                     __uint_as_float(u[4 * v + 2]), __uint_as_float(u[4 * v + 3]));
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(dq_free));
+      // the next block's exps while dK(i) and dQ(i) run on the tensor core
+      if (b + 1 < nblk) load_block(b + 1);
     }
+    mbar_wait(smem_u32(mma_done), (nblk - 1) & 1);
+    tc_fence_after();
+    drain(nblk - 1);
     // epilogue: dV = scale * acc, dK = alpha * acc -> dqkv (V and K slots) of key rows jb*128 + r
+    // (NH = 2: warpgroup 0 writes dV, warpgroup 1 dK)
     __nv_bfloat16* base = p.dq + (long long)(jb * 128 + r) * p.ld_dq + (long long)head * 3 * HD;
-    for (int which = 0; which < 2; ++which) {
+    for (int which = (NH == 2 ? hf : 0); which < (NH == 2 ? hf + 1 : 2); ++which) {
       const float sc = which == 0 ? p.drop_scale : p.alpha;
       __nv_bfloat16* dst = base + (which == 0 ? 2 * HD : HD);
       const uint32_t col = which == 0 ? kDV : kDK;
@@ -1461,6 +1497,15 @@ int launch_fwd2(const void* qkv, long long ld_qkv, int heads, int seq, long long
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
+// Softmax warpgroups of the one-kernel backward (MT_ATTN_BWD_WG, default 2: column halves).
+int bwd2_halves() {
+  static const int v = [] {
+    const char* e = getenv("MT_ATTN_BWD_WG");
+    return (e && e[0] == '1') ? 1 : 2;
+  }();
+  return v;
+}
+
 template <int HD>
 int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* dctx, long long ld_ctx, int heads,
                int seq, long long head_base, float alpha, uint64_t seed, uint32_t thresh16, float drop_scale,
@@ -1496,9 +1541,14 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
   if constexpr (HD <= 128) {
     if (dq_acc != nullptr) {  // one kernel: dK, dV and dQ (fp32 vector atomics), then the bf16 dQ
       using C2 = Bwd2Cfg<HD>;
-      if (!set_smem_once<attn_bwd2_kernel<HD>>(C2::kSmem)) return 2;
       if (cudaMemsetAsync(dq_acc, 0, (size_t)heads * seq * HD * sizeof(float), s) != cudaSuccess) return 2;
-      attn_bwd2_kernel<HD><<<dim3(p.nqb, heads), kAttnThreads, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
+      if (bwd2_halves() == 2) {
+        if (!set_smem_once<attn_bwd2_kernel<HD, 2>>(C2::kSmem)) return 2;
+        attn_bwd2_kernel<HD, 2><<<dim3(p.nqb, heads), 384, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
+      } else {
+        if (!set_smem_once<attn_bwd2_kernel<HD, 1>>(C2::kSmem)) return 2;
+        attn_bwd2_kernel<HD, 1><<<dim3(p.nqb, heads), 256, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
+      }
       const long long groups = (long long)heads * seq * (HD / 8);
       dq_finalize_kernel<<<(unsigned)((groups + 255) / 256), 256, 0, s>>>(dq_acc, p.dq, p.ld_dq, HD, heads, seq, alpha);
       return cudaGetLastError() == cudaSuccess ? 0 : 2;
