@@ -481,7 +481,12 @@ extern "C" int mt_ctx_init_comm(mt_ctx* c, const unsigned char id_bytes[128], in
       // (GPT-3 layer at TP=4: 5.33 vs 5.38 ms/step; neutral at TP=2); MT_TP_NVLS=0/1 overrides
       c->tp_nvls = p.tensor >= 4;
       if (const char* e = getenv("MT_TP_NVLS")) c->tp_nvls = e[0] == '1';
-      if (c->tp_fused || c->tp_nvls) c->tp_symmetric = true;
+      // backward all-reduces over the NVLS kernel: measured no faster than NCCL's (which already runs
+      // its NVLS algorithm on the symmetric windows) beside the wgrad GEMM — TP=4 GPT-3 5.18 / 5.06
+      // (8 CTAs) vs 5.06 ms, profiles/r02_nvls_bwd_ab.log — so opt-in (MT_TP_NVLS_BWD=1)
+      c->tp_nvls_bwd = false;
+      if (const char* e = getenv("MT_TP_NVLS_BWD")) c->tp_nvls_bwd = e[0] == '1';
+      if (c->tp_fused || c->tp_nvls || c->tp_nvls_bwd) c->tp_symmetric = true;
     }
   });
 }
@@ -673,7 +678,7 @@ extern "C" int mt_layer_create(mt_ctx* c, const mt_layer_desc* d, mt_layer** out
     for (auto& b : c->scratch_h) b.ensure(M * l->h * 2);
     if (c->tp_symmetric && d->tp_size > 1 && c->tp && !c->shard_only) {
       for (auto& sb : c->sym_h) ensure_symmetric(c, sb, static_cast<size_t>(M * l->h * 2));
-      if ((c->tp_fused || c->tp_nvls) && !c->fused_ar) {
+      if ((c->tp_fused || c->tp_nvls || c->tp_nvls_bwd) && !c->fused_ar) {
         // all TP ranks must agree on the all-reduce path: fall back to NCCL everywhere if any rank
         // cannot set up the multicast state
         int ok = 1;
@@ -690,7 +695,7 @@ extern "C" int mt_layer_create(mt_ctx* c, const mt_layer_desc* d, mt_layer** out
         if (!ok) {
           if (c->fused_ar) fused_ar_destroy(c, c->fused_ar);
           c->fused_ar = nullptr;
-          c->tp_fused = c->tp_nvls = false;
+          c->tp_fused = c->tp_nvls = c->tp_nvls_bwd = false;
         }
       }
     }
@@ -804,10 +809,17 @@ namespace {
 int tp_allreduce_async(mt_ctx* c, void* buf, int64_t n, cudaStream_t st, const char* what) {
   check_cuda(cudaEventRecord(c->ev_ready, st), "cudaEventRecord");
   check_cuda(cudaStreamWaitEvent(c->comm, c->ev_ready, 0), "cudaStreamWaitEvent");
-  check_nccl(ncclAllReduce(buf, buf, n, ncclBfloat16, ncclSum, c->tp_side, c->comm), what);
-  check_cuda(cudaEventRecord(c->ev_done, c->comm), "cudaEventRecord");
   int sms = 0;
   check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device), "attr");
+  if (c->fused_ar && c->tp_nvls_bwd && buf == c->sym_h[1].ptr) {
+    // NVLink SHARP all-reduce kernel on the side stream (multimem.ld_reduce + multimem.st, bounded
+    // cross-rank waits) instead of NCCL's ring/NVLS kernels
+    nvls_allreduce(c, n, c->comm, 1);
+    check_cuda(cudaEventRecord(c->ev_done, c->comm), "cudaEventRecord");
+    return std::max(2, sms - nvls_bwd_ctas(c));
+  }
+  check_nccl(ncclAllReduce(buf, buf, n, ncclBfloat16, ncclSum, c->tp_side, c->comm), what);
+  check_cuda(cudaEventRecord(c->ev_done, c->comm), "cudaEventRecord");
   return std::max(2, sms - c->comm_sms);
 }
 void tp_allreduce_join(mt_ctx* c, cudaStream_t st) {

@@ -31,7 +31,8 @@ mt_gemm_allreduce* fused_ar_begin(mt_ctx* c);
 void fused_ar_end(mt_ctx* c, cudaStream_t st, void* d, int64_t ldd);
 void fused_ar_prepare(mt_ctx* c, cudaStream_t st);
 int fused_ar_gemm_ctas(mt_ctx* c);
-void nvls_allreduce(mt_ctx* c, int64_t elems, cudaStream_t st);
+void nvls_allreduce(mt_ctx* c, int64_t elems, cudaStream_t st, int which = 0);
+int nvls_bwd_ctas(mt_ctx* c);
 void op_mark(mt_ctx* c, cudaStream_t st, const char* label);  // runtime.cpp (op timing)
 
 // Failed CUDA / NCCL call -> DataError-class status 2.
@@ -144,6 +145,8 @@ struct mt_ctx {
   // implies symmetric buffers); state in tp_fused.cu
   bool tp_fused = false;
   bool tp_nvls = false;  // forward row-parallel all-reduce by nvls_allreduce instead of NCCL (MT_TP_NVLS=1)
+  // backward LN-input-gradient all-reduces by nvls_allreduce on the side stream (MT_TP_NVLS_BWD)
+  bool tp_nvls_bwd = false;
   mt::FusedAllReduce* fused_ar = nullptr;  // PP > 1: first + last stage of the same (dp, tp): tied word-embedding grads
   // compute-only measurement of one TP shard on a single GPU: the layer skips its TP collectives
   // (mt_ctx_shard_only); never set in a real multi-GPU run

@@ -28,31 +28,35 @@ struct FusedAllReduce {
   size_t flags_bytes = 0;
   ncclWindow_t flags_win = nullptr;
   void* z = nullptr;  // the symmetric output buffer the multicast address below belongs to
+  void* z1 = nullptr;   // the second symmetric buffer (LN-input gradients, backward) and its multicast address
+  void* mc1 = nullptr;
   mt_gemm_allreduce desc{};
   uint32_t target = 0;  // cumulative arrivals of all launches: the counter value that means "all done"
   int reducer_ctas = 16;  // reducer CTAs running beside the GEMM (MT_AR_CTAS)
   int nvls_ctas = 0;      // CTAs of the standalone NVLS all-reduce kernel (MT_NVLS_CTAS; 0: reducer_ctas)
   int groups = 6;         // column groups per fused launch (the reduction of group g overlaps groups > g)
+  int bwd_ctas = 16;      // CTAs of the backward NVLS all-reduce beside the wgrad GEMM (MT_NVLS_BWD_CTAS)
 };
 
 namespace {
 
 constexpr int64_t kGroupBase = 64;
 
-__global__ void resolve_kernel(ncclWindow_t zwin, ncclWindow_t fwin, ncclDevComm dc, void** out) {
+__global__ void resolve_kernel(ncclWindow_t zwin, ncclWindow_t fwin, ncclWindow_t z1win, ncclDevComm dc, void** out) {
   out[0] = ncclGetLsaMultimemPointer(zwin, 0, dc);
   out[1] = ncclGetLsaMultimemPointer(fwin, 0, dc);
   out[2] = reinterpret_cast<void*>(static_cast<uintptr_t>(dc.lsaSize));
   out[3] = reinterpret_cast<void*>(static_cast<uintptr_t>(dc.lsaRank));
+  out[4] = z1win ? ncclGetLsaMultimemPointer(z1win, 0, dc) : nullptr;
 }
 
 // Multicast addresses of the current symmetric buffers (collective: every TP rank resolves at the
 // same point because buffer allocation is collective).
 void resolve(mt_ctx* c, FusedAllReduce* f) {
   void** d_out = nullptr;
-  check_cuda(cudaMalloc(&d_out, 4 * sizeof(void*)), "cudaMalloc");
-  resolve_kernel<<<1, 1>>>(c->sym_h[0].win_tp, f->flags_win, f->dev, d_out);
-  void* h[4] = {};
+  check_cuda(cudaMalloc(&d_out, 5 * sizeof(void*)), "cudaMalloc");
+  resolve_kernel<<<1, 1>>>(c->sym_h[0].win_tp, f->flags_win, c->sym_h[1].win_tp, f->dev, d_out);
+  void* h[5] = {};
   check_cuda(cudaMemcpy(h, d_out, sizeof h, cudaMemcpyDeviceToHost), "resolve multicast addresses");
   cudaFree(d_out);
   const int lsa_size = static_cast<int>(reinterpret_cast<uintptr_t>(h[2]));
@@ -60,6 +64,8 @@ void resolve(mt_ctx* c, FusedAllReduce* f) {
   if (lsa_size != c->par.tensor || lsa_rank != c->place.tensor || !h[0] || !h[1])
     throw RuntimeFailure("fused TP all-reduce: the TP group is not one load/store-accessible multicast team");
   f->z = c->sym_h[0].ptr;
+  f->z1 = c->sym_h[1].ptr;
+  f->mc1 = h[4];
   mt_gemm_allreduce& d = f->desc;
   d = mt_gemm_allreduce{};
   d.d_multicast = h[0];
@@ -78,6 +84,7 @@ FusedAllReduce* fused_ar_create(mt_ctx* c) {
   auto f = new FusedAllReduce();
   if (const char* e = getenv("MT_AR_CTAS")) f->reducer_ctas = std::max(1, atoi(e));
   if (const char* e = getenv("MT_NVLS_CTAS")) f->nvls_ctas = std::max(0, atoi(e));
+  if (const char* e = getenv("MT_NVLS_BWD_CTAS")) f->bwd_ctas = std::max(1, atoi(e));
   try {
     ncclDevCommRequirements req{};
     req.lsaMultimem = true;
@@ -260,20 +267,25 @@ __global__ void __launch_bounds__(1024) nvls_allreduce_kernel(__nv_bfloat16* mc,
 }
 }  // namespace
 
-// All-reduce (sum) of `elems` bf16 at offset 0 of the symmetric buffer sym_h[0] over the TP group.
-void nvls_allreduce(mt_ctx* c, int64_t elems, cudaStream_t st) {
+// All-reduce (sum) of `elems` bf16 at offset 0 of the symmetric buffer sym_h[which] over the TP group
+// (0: forward row-parallel outputs, on the compute stream; 1: backward LN-input gradients, on the side
+// stream beside the weight-gradient GEMM). `st` is ordered after every rank's reduction.
+void nvls_allreduce(mt_ctx* c, int64_t elems, cudaStream_t st, int which) {
   FusedAllReduce* f = c->fused_ar;
-  if (f->z != c->sym_h[0].ptr) resolve(c, f);
-  const int ctas = f->nvls_ctas > 0 ? f->nvls_ctas : f->reducer_ctas;
+  if (f->z != c->sym_h[0].ptr || f->z1 != c->sym_h[1].ptr) resolve(c, f);
+  void* mc = which == 0 ? f->desc.d_multicast : f->mc1;
+  if (!mc) throw RuntimeFailure("NVLS all-reduce: no multicast address for the buffer");
+  const int ctas = which == 1 ? f->bwd_ctas : (f->nvls_ctas > 0 ? f->nvls_ctas : f->reducer_ctas);
   const uint32_t entry = f->target + static_cast<uint32_t>(c->par.tensor);
   f->target = entry + static_cast<uint32_t>(c->par.tensor * ctas);
-  nvls_allreduce_kernel<<<ctas, 1024, 0, st>>>(static_cast<__nv_bfloat16*>(f->desc.d_multicast),
-                                               f->desc.counter_multicast, static_cast<const uint32_t*>(f->flags),
-                                               entry, elems, c->place.tensor, c->par.tensor, c->err_dev,
-                                               c->timeout_ns);
+  nvls_allreduce_kernel<<<ctas, 1024, 0, st>>>(static_cast<__nv_bfloat16*>(mc), f->desc.counter_multicast,
+                                               static_cast<const uint32_t*>(f->flags), entry, elems,
+                                               c->place.tensor, c->par.tensor, c->err_dev, c->timeout_ns);
   check_cuda(cudaGetLastError(), "nvls_allreduce");
   if (mt_gemm_allreduce_wait(&f->desc, static_cast<const uint32_t*>(f->flags), f->target, st) != 0)
     throw RuntimeFailure("mt_gemm_allreduce_wait failed");
 }
+
+int nvls_bwd_ctas(mt_ctx* c) { return c->fused_ar ? c->fused_ar->bwd_ctas : 0; }
 
 }  // namespace mt

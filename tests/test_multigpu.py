@@ -128,6 +128,8 @@ def _worker(rank, world, port, mode, q):
             for fused in (0, 1, 2):  # NCCL, fused GEMM + all-reduce, standalone NVLS all-reduce kernel
                 os.environ["MT_TP_FUSED"] = "1" if fused == 1 else "0"
                 os.environ["MT_TP_NVLS"] = "1" if fused == 2 else "0"
+                # the NVLS variant also runs the backward all-reduces through the NVLS kernel
+                os.environ["MT_TP_NVLS_BWD"] = "1" if fused == 2 else "0"
                 c2 = Context(rank)
                 c2.init_comm(ids[fused], world, rank, tensor=world)
                 lay = Layer(c2, d)
@@ -144,6 +146,7 @@ def _worker(rank, world, port, mode, q):
                 c2.close()
             os.environ.pop("MT_TP_FUSED", None)
             os.environ.pop("MT_TP_NVLS", None)
+            os.environ.pop("MT_TP_NVLS_BWD", None)
         elif mode == "peer_hangs":
             # rank 1 builds the same TP=2 stage, then stops taking part (a hung / diverged peer); rank 0's
             # iteration must come back with status 2 within the context's bound (MT_COMM_TIMEOUT_S) —
@@ -452,12 +455,13 @@ def test_tensor_parallel_stage_host_inputs_two_gpus(mode):
 
 @pytest.mark.timeout(600)
 def test_fused_gemm_allreduce_matches_nccl_two_gpus():
-    """Forward row-parallel GEMM + TP all-reduce fused in one kernel (epilogue warps reduce finished
+    """Forward row-parallel GEMM + TP all-reduce fused in one kernel (a reducer kernel reduces finished
     tiles over NVLink SHARP with multimem.ld_reduce / multimem.st) at TP=2 over repeated launches:
     within the oracle tolerance of test_tensor_parallel_layer_two_gpus, within bf16 noise of the
     GEMM + ncclAllReduce path (the two sums differ by one bf16 ulp on rare elements, which the later
     GEMMs spread; measured unbiased), and the TP replicas of the fused result are bit-identical (one
-    owner computes each unit and multicasts it)."""
+    owner computes each unit and multicasts it). The standalone-NVLS variant also runs the two backward
+    LN-input-gradient all-reduces through the NVLS kernel on the side stream (MT_TP_NVLS_BWD=1)."""
     _need(2)
     from oracle import oracle as O
     res = _run("tp_fused")

@@ -12,7 +12,7 @@ from paper_2201_11990_b200.runtime import Context, Layer  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "fwd"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-h, H, s_ = int(os.environ.get("H", 12288)), int(os.environ.get("HEADS", 96)), 2048
+h, H, s_ = int(os.environ.get("H", 12288)), int(os.environ.get("HEADS", 96)), int(os.environ.get("SEQ", 2048))
 ctx = Context(0)
 lay = Layer(ctx, PL.layer_desc(h, H, s_, 1, seed=5))
 st = torch.cuda.current_stream()
