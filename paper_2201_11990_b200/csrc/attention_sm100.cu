@@ -135,8 +135,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int qb = p.nqb - 1 - (int)blockIdx.x;  // heaviest (most kv blocks) first
-  const int head = blockIdx.y;
+  // grid (heads, blocks): the launch order runs every head's heaviest block (most kv blocks) first, so
+  // the last CTAs to start are the light ones (a head-major order left heavy CTAs for the tail)
+  const int qb = p.nqb - 1 - (int)blockIdx.y;
+  const int head = blockIdx.x;
   const int nkv = qb + 1;                       // causal: kv blocks 0..qb
 
   if (warp == 0 && lane == 0) {
@@ -396,8 +398,8 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int pair = p.nqb / 2 - 1 - (int)blockIdx.x;  // heaviest pair first
-  const int head = blockIdx.y;
+  const int pair = p.nqb / 2 - 1 - (int)blockIdx.y;  // heaviest pairs of every head first (grid: heads, pairs)
+  const int head = blockIdx.x;
   const int q_lo = 2 * pair, q_hi = 2 * pair + 1;     // tile a, tile b
   const int nkv = q_hi + 1;                           // kv blocks 0..q_hi (tile a uses 0..q_lo)
 
@@ -737,8 +739,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t* pv_done = bars + 8;  // dV MMA done (P consumed; the tile can take dS)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int jb = p.nqb - 1 - (int)blockIdx.x;  // key block (heaviest = first column of queries: jb = 0)
-  const int head = blockIdx.y;
+  const int jb = (int)blockIdx.y;  // key block; jb = 0 has the most query blocks (grid: heads, key blocks)
+  const int head = blockIdx.x;
   const int i0 = jb, nblk = p.nqb - jb;
   constexpr uint32_t kDV = 0, kDK = C::kHDP, kSC = 2 * C::kHDP;
   // dP gets its own TMEM columns when they fit (head dim <= 128): the dP MMA then runs while the
@@ -965,8 +967,8 @@ __global__ void __launch_bounds__(128 + 128 * NH, 1)
   uint64_t* dq_free = bars + 12;  // 4 warps drained the dQ partial (dP columns free)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int jb = (int)blockIdx.x;  // key block; jb = 0 has the most query blocks (launched first)
-  const int head = blockIdx.y;
+  const int jb = (int)blockIdx.y;  // key block; jb = 0 has the most query blocks: every head's jb = 0
+  const int head = blockIdx.x;     // launches first (grid: heads, key blocks), the light ones last
   const int nblk = p.nqb - jb;
   constexpr uint32_t kDV = 0, kDK = 128, kSC = 256, kDP = 384;
 
@@ -1268,8 +1270,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t* blk_done = bars + 5;  // dQ MMA of the block done (dS smem and TMEM S/dP free)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int ib = p.nqb - 1 - (int)blockIdx.x;
-  const int head = blockIdx.y;
+  const int ib = p.nqb - 1 - (int)blockIdx.y;  // heaviest query blocks of every head first
+  const int head = blockIdx.x;
   const int nblk = ib + 1;
   constexpr uint32_t kDQ = 0, kSC = 256, kDP = 384;
 
@@ -1464,7 +1466,7 @@ int launch_fwd(const void* qkv, long long ld_qkv, int heads, int seq, long long 
   p.out_head_stride = HD;
   p.lse = lse;
   if (!set_smem_once<attn_fwd_kernel<HD>>(C::kSmem)) return 2;
-  attn_fwd_kernel<HD><<<dim3(p.nqb, heads), kAttnThreads, C::kSmem, s>>>(mq, mk, mv, p);
+  attn_fwd_kernel<HD><<<dim3(heads, p.nqb), kAttnThreads, C::kSmem, s>>>(mq, mk, mv, p);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -1493,7 +1495,7 @@ int launch_fwd2(const void* qkv, long long ld_qkv, int heads, int seq, long long
   p.lse = lse;
   p.mask = mask;
   if (!set_smem_once<attn_fwd2_kernel<HD>>(C::kSmem)) return 2;
-  attn_fwd2_kernel<HD><<<dim3(p.nqb / 2, heads), kFwd2Threads, C::kSmem, s>>>(mq, mk, mv, p);
+  attn_fwd2_kernel<HD><<<dim3(heads, p.nqb / 2), kFwd2Threads, C::kSmem, s>>>(mq, mk, mv, p);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -1544,10 +1546,10 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
       if (cudaMemsetAsync(dq_acc, 0, (size_t)heads * seq * HD * sizeof(float), s) != cudaSuccess) return 2;
       if (bwd2_halves() == 2) {
         if (!set_smem_once<attn_bwd2_kernel<HD, 2>>(C2::kSmem)) return 2;
-        attn_bwd2_kernel<HD, 2><<<dim3(p.nqb, heads), 384, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
+        attn_bwd2_kernel<HD, 2><<<dim3(heads, p.nqb), 384, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
       } else {
         if (!set_smem_once<attn_bwd2_kernel<HD, 1>>(C2::kSmem)) return 2;
-        attn_bwd2_kernel<HD, 1><<<dim3(p.nqb, heads), 256, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
+        attn_bwd2_kernel<HD, 1><<<dim3(heads, p.nqb), 256, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
       }
       const long long groups = (long long)heads * seq * (HD / 8);
       dq_finalize_kernel<<<(unsigned)((groups + 255) / 256), 256, 0, s>>>(dq_acc, p.dq, p.ld_dq, HD, heads, seq, alpha);
@@ -1555,8 +1557,8 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
     }
   }
   if (!set_smem_once<attn_bwd_dkdv_kernel<HD>>(kSmemKV) || !set_smem_once<attn_bwd_dq_kernel<HD>>(kSmemQ)) return 2;
-  attn_bwd_dkdv_kernel<HD><<<dim3(p.nqb, heads), kAttnThreads, kSmemKV, s>>>(mq, mk, mv, mdo, p);
-  attn_bwd_dq_kernel<HD><<<dim3(p.nqb, heads), kAttnThreads, kSmemQ, s>>>(mq, mk, mv, mdo, p);
+  attn_bwd_dkdv_kernel<HD><<<dim3(heads, p.nqb), kAttnThreads, kSmemKV, s>>>(mq, mk, mv, mdo, p);
+  attn_bwd_dq_kernel<HD><<<dim3(heads, p.nqb), kAttnThreads, kSmemQ, s>>>(mq, mk, mv, mdo, p);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
