@@ -715,9 +715,10 @@ __device__ __forceinline__ uint64_t mnmaj(uint32_t base, int kk) {
   return umma_desc_sw128(base + kk * 2048, 16384, 1024);
 }
 
-// dK, dV for one (head, 128-key block j): loop over query blocks i >= j.
-template <int HD>
-__global__ void __launch_bounds__(kAttnThreads, 1)
+// dK, dV for one (head, 128-key block j): loop over query blocks i >= j. NH softmax warpgroups split
+// each block row's 128 columns (the backward has no row reduction), NH = 2: 384 threads.
+template <int HD, int NH>
+__global__ void __launch_bounds__(128 + 128 * NH, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                          const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
                          const AttnBwdParams p) {
@@ -750,7 +751,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   if (warp == 0 && lane == 0) {
     for (auto* b : {&tq, &tk, &tv, &tdo}) tma_prefetch_desc(b);
-    for (int i = 0; i < 9; ++i) mbar_init(smem_u32(bars + i), (i == 4 || i == 6) ? 4 : 1);
+    for (int i = 0; i < 9; ++i) mbar_init(smem_u32(bars + i), (i == 4 || i == 6) ? 4 * NH : 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(smem_u32(tmem_slot));
@@ -811,7 +812,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    const uint32_t quad = warp - 4;
+    constexpr int CW = 128 / NH;  // score columns per thread
+    const uint32_t quad = (warp - 4) & 3;
+    const int hf = (int)(warp - 4) >> 2;
+    const int col0 = hf * CW;
     const int r = quad * 32 + lane;
     const uint32_t lane_base = tmem + ((quad * 32) << 16);
     for (int b = 0; b < nblk; ++b) {
@@ -827,18 +831,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mw = __ldg(reinterpret_cast<const uint4*>(p.mask + ((size_t)head * p.seq + qrow) * (p.seq >> 5)) + jb);
       mbar_wait(smem_u32(s_full), ph);
       tc_fence_after();
-      float pr[128];
+      float pr[CW];
       auto probs = [&](auto diag_tag) {  // the causal mask only on the diagonal block (branch-free elsewhere)
         constexpr bool kDiag = decltype(diag_tag)::value;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < CW / 32; ++c) {
           uint32_t u[32];
-          tmem_ld_32x32b_x32(lane_base + kSC + c * 32, u);
+          tmem_ld_32x32b_x32(lane_base + kSC + col0 + c * 32, u);
           tmem_ld_wait();
 #pragma unroll
           for (int t = 0; t < 32; ++t) {
-            const int col = c * 32 + t;
-            pr[col] = (kDiag && col > r) ? 0.f : ex2(__uint_as_float(u[t]) * p.alpha_log2 - lse2);
+            const int col = col0 + c * 32 + t;
+            pr[c * 32 + t] = (kDiag && col > r) ? 0.f : ex2(__uint_as_float(u[t]) * p.alpha_log2 - lse2);
           }
         }
       };
@@ -848,11 +852,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         probs(std::false_type{});
       if (b > 0) mbar_wait(smem_u32(blk_done), ph ^ 1);  // P / dS smem free
 #pragma unroll
-      for (int g = 0; g < 16; ++g) {
+      for (int gl = 0; gl < CW / 8; ++gl) {
+        const int g = col0 / 8 + gl;
         const uint32_t keep = keep8_bwd(p, head, qrow, jb * 128 + g * 8, row_idx + g * 8);
         float v[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) v[t] = ((keep >> t) & 1u) ? pr[g * 8 + t] : 0.f;
+        for (int t = 0; t < 8; ++t) v[t] = ((keep >> t) & 1u) ? pr[gl * 8 + t] : 0.f;
         st_shared_v4(sw128_addr(sP + (g >> 3) * 16384, r, g & 7), pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
                      pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
       }
@@ -864,21 +869,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_wait(smem_u32(pv_done), ph);  // the P tile is free for dS
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < CW / 32; ++c) {
         uint32_t u[32];
-        tmem_ld_32x32b_x32(lane_base + kDPc + c * 32, u);
+        tmem_ld_32x32b_x32(lane_base + kDPc + col0 + c * 32, u);
         tmem_ld_wait();
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          const uint32_t keep = keep8_bwd(p, head, qrow, jb * 128 + c * 32 + g * 8, row_idx + c * 32 + g * 8);
+          const int cc = col0 + c * 32 + g * 8;
+          const uint32_t keep = keep8_bwd(p, head, qrow, jb * 128 + cc, row_idx + cc);
           float v[8];
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
-            const int col = c * 32 + g * 8 + t;
             const float dp = ((keep >> t) & 1u) ? __uint_as_float(u[g * 8 + t]) * p.drop_scale : 0.f;
-            v[t] = pr[col] * (dp - Di);
+            v[t] = pr[c * 32 + g * 8 + t] * (dp - Di);
           }
-          const int gg = c * 4 + g;
+          const int gg = cc / 8;
           st_shared_v4(sw128_addr(sS + (gg >> 3) * 16384, r, gg & 7), pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
                        pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
         }
@@ -892,7 +897,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     mbar_wait(smem_u32(blk_done), (nblk - 1) & 1);
     tc_fence_after();
     __nv_bfloat16* base = p.dq + (long long)(jb * 128 + r) * p.ld_dq + (long long)head * 3 * HD;
-    for (int which = 0; which < 2; ++which) {
+    for (int which = (NH == 2 ? hf : 0); which < (NH == 2 ? hf + 1 : 2); ++which) {
       const float sc = which == 0 ? p.drop_scale : p.alpha;
       __nv_bfloat16* dst = base + (which == 0 ? 2 * HD : HD);
       const uint32_t col = which == 0 ? kDV : kDK;
@@ -1251,8 +1256,8 @@ __global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16*
 }
 
 // dQ for one (head, 128-query block i): loop over key blocks j <= i.
-template <int HD>
-__global__ void __launch_bounds__(kAttnThreads, 1)
+template <int HD, int NH>
+__global__ void __launch_bounds__(128 + 128 * NH, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                        const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
                        const AttnBwdParams p) {
@@ -1277,7 +1282,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   if (warp == 0 && lane == 0) {
     for (auto* b : {&tq, &tk, &tv, &tdo}) tma_prefetch_desc(b);
-    for (int i = 0; i < 6; ++i) mbar_init(smem_u32(bars + i), i == 4 ? 4 : 1);
+    for (int i = 0; i < 6; ++i) mbar_init(smem_u32(bars + i), i == 4 ? 4 * NH : 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(smem_u32(tmem_slot));
@@ -1325,7 +1330,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    const uint32_t quad = warp - 4;
+    constexpr int CW = 128 / NH;  // score columns per thread (NH warpgroups split each block row)
+    const uint32_t quad = (warp - 4) & 3;
+    const int hf = (int)(warp - 4) >> 2;
+    const int col0 = hf * CW;
     const int r = quad * 32 + lane;
     const int qrow = ib * 128 + r;
     const uint32_t lane_base = tmem + ((quad * 32) << 16);
@@ -1341,7 +1349,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       auto dscores = [&](auto diag_tag) {  // the causal mask only on the diagonal block
         constexpr bool kDiag = decltype(diag_tag)::value;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = col0 / 32; c < (col0 + CW) / 32; ++c) {
           uint32_t us[32], ud[32];
           tmem_ld_32x32b_x32(lane_base + kSC + c * 32, us);
           tmem_ld_32x32b_x32(lane_base + kDP + c * 32, ud);
@@ -1376,7 +1384,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     mbar_wait(smem_u32(blk_done), (nblk - 1) & 1);
     tc_fence_after();
     __nv_bfloat16* dst = p.dq + (long long)qrow * p.ld_dq + (long long)head * 3 * HD;
-    for (int c = 0; c * 32 < HD; ++c) {
+    for (int c = hf; c * 32 < HD; c += NH) {
       uint32_t u[32];
       tmem_ld_32x32b_x32(lane_base + kDQ + c * 32, u);
       tmem_ld_wait();
@@ -1556,9 +1564,17 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
       return cudaGetLastError() == cudaSuccess ? 0 : 2;
     }
   }
-  if (!set_smem_once<attn_bwd_dkdv_kernel<HD>>(kSmemKV) || !set_smem_once<attn_bwd_dq_kernel<HD>>(kSmemQ)) return 2;
-  attn_bwd_dkdv_kernel<HD><<<dim3(heads, p.nqb), kAttnThreads, kSmemKV, s>>>(mq, mk, mv, mdo, p);
-  attn_bwd_dq_kernel<HD><<<dim3(heads, p.nqb), kAttnThreads, kSmemQ, s>>>(mq, mk, mv, mdo, p);
+  if (bwd2_halves() == 2) {
+    if (!set_smem_once<attn_bwd_dkdv_kernel<HD, 2>>(kSmemKV) || !set_smem_once<attn_bwd_dq_kernel<HD, 2>>(kSmemQ))
+      return 2;
+    attn_bwd_dkdv_kernel<HD, 2><<<dim3(heads, p.nqb), 384, kSmemKV, s>>>(mq, mk, mv, mdo, p);
+    attn_bwd_dq_kernel<HD, 2><<<dim3(heads, p.nqb), 384, kSmemQ, s>>>(mq, mk, mv, mdo, p);
+  } else {
+    if (!set_smem_once<attn_bwd_dkdv_kernel<HD, 1>>(kSmemKV) || !set_smem_once<attn_bwd_dq_kernel<HD, 1>>(kSmemQ))
+      return 2;
+    attn_bwd_dkdv_kernel<HD, 1><<<dim3(heads, p.nqb), 256, kSmemKV, s>>>(mq, mk, mv, mdo, p);
+    attn_bwd_dq_kernel<HD, 1><<<dim3(heads, p.nqb), 256, kSmemQ, s>>>(mq, mk, mv, mdo, p);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
