@@ -652,13 +652,14 @@ extern "C" int mt_layer_create(mt_ctx* c, const mt_layer_desc* d, mt_layer** out
     l->head_dim = d->hidden / d->heads;
     l->shard = curator::layer_shard(d->hidden, d->heads, d->ffn_mult, d->tp_size, d->tp_rank);
     {
-      // Default: fused flash attention (two-query-tile forward + one-kernel backward) for head_dim <= 128,
-      // measured faster than score GEMM + causal softmax + PV GEMM (GPT-3 layer 18.0-18.3 vs 18.9 ms,
-      // profiles/r02_attn_default_ab.log); at head_dim 160 (MT-NLG) the single-tile flash kernels are
-      // slower (0.64 vs 0.37 ms per TP=8 shard), so the unfused path stays. MT_ATTN_FUSED=0/1 forces.
+      // Default: fused flash attention. head_dim <= 128: two-query-tile forward + one-kernel backward,
+      // faster than score GEMM + causal softmax + PV GEMM (GPT-3 layer 18.0-18.3 vs 18.9 ms,
+      // profiles/r02_attn_default_ab.log); head_dim 160 (MT-NLG): single-tile forward + dK/dV, dQ pair,
+      // a tie in time with the unfused path (0.37 ms per TP=8 shard, profiles/r02_attn_hd160_ab.log)
+      // without the [s x s] score / probability buffers. MT_ATTN_FUSED=0/1 forces.
       const char* e = getenv("MT_ATTN_FUSED");
       const int hd = static_cast<int>(l->head_dim);
-      const bool want = e && e[0] ? e[0] == '1' : hd <= 128;
+      const bool want = e && e[0] ? e[0] == '1' : true;
       l->fused_attn = want && d->seq % 128 == 0 && (hd == 64 || hd == 128 || hd == 160);
     }
     int64_t off = 0;

@@ -17,9 +17,10 @@ Variant coverage (dispatch points in parentheses):
     ln_bwd_rows_kernel<3> (rows_sm100.cu, h=12288 -> 1536 vectors / 512 threads), the BN=256 CTA-pair
     GEMM tiles, and the split-K tail (gemm_sm100.cu, K >= 16384: fc2 forward and fc1 dgrad, K=49152).
   * MT-NLG layer, ONE TP=8 shard (bench.py --config mtnlg --shard-of 8): h=20480, 16 local heads of
-    hd=160, s=2048, against the oracle's shard mode (same shard, no all-reduce). Hits the unfused
-    attention (default at hd=160): the hd=160 score / PV contractions at s=2048 (BN=160 tiles),
-    softmax_fwd_kernel<8> (kernels.cu MT_VPL_DISPATCH, s=2048), ln_bwd_rows_kernel<5> (h=20480 -> 2560 vectors), and
+    hd=160, s=2048, against the oracle's shard mode (same shard, no all-reduce), once with the default
+    fused attention (attn_fwd_kernel<160>, attn_bwd_dkdv_kernel<160, 2>, attn_bwd_dq_kernel<160, 2>)
+    and once unfused (MT_ATTN_FUSED=0: the hd=160 score / PV contractions at s=2048 with BN=160 tiles,
+    softmax_fwd_kernel<8> from kernels.cu MT_VPL_DISPATCH at s=2048); ln_bwd_rows_kernel<5> (h=20480 -> 2560 vectors), and
     the TP=8 shard GEMM shapes (K = h/8 = 2560 projection, K = 4h/8 = 10240 fc2).
   * h=8192 PP-slice layer (BASELINE configs[3] shape, 64 heads, hd=128, s=2048), TP=1, with a second
     layer index and microbatch id (different dropout streams): split-K tail at K=32768.
@@ -147,44 +148,45 @@ def _shard_slices(desc, n):
     return sl
 
 
-def test_mtnlg_tp8_shard_matches_oracle_shard_mode():
+def test_mtnlg_tp8_shard_matches_oracle_shard_mode(monkeypatch):
     h, H, s, t = 20480, 128, 2048, 8
-    ctx = Context(0)
-    ctx.init_comm(bytes(128), 1, 0, 1, 1, 1, 1, 1)
-    check = lib().mt_ctx_shard_only(ctx._h, 1)
-    assert check == 0
-    desc = PL.layer_desc(h, H, s, 1, tp_size=t, tp_rank=0, dropout_hidden=0.1, dropout_attn=0.1, seed=SEED,
-                         layer_index=7)
-    layer = Layer(ctx, desc)
     params = O.init_params(h, SEED, 7, shard=(H, t, 0))  # rank 0's regions (the rest is never read)
-    keep = []
-    for i, p in enumerate(params):
-        b = np.ascontiguousarray(O.to_bf16_bits(p))
-        keep.append(b)
-        layer.set_param(i, b.ctypes.data)
+    keep = [np.ascontiguousarray(O.to_bf16_bits(p)) for p in params]
     x = O.normal(O.site_seed(SEED, "input", 0, 3), s, h)
     g = O.normal(O.site_seed(SEED, "grad", 0, 3), s, h, std=1e-2)
-    xd, gd = bf16_dev(x), bf16_dev(g)
-    yd, dxd = torch.empty_like(xd), torch.empty_like(xd)
-    stream = torch.cuda.current_stream()
-    layer.zero_grads(stream)
-    layer.forward(xd.data_ptr(), yd.data_ptr(), 3, stream)
-    layer.backward(gd.data_ptr(), dxd.data_ptr(), 3, stream)
-    torch.cuda.synchronize()
-    sl = _shard_slices(desc, 12)
-    shapes = [(s_[0].stop - s_[0].start, s_[1].stop - s_[1].start) for s_ in sl]
-    got = layer_grads(layer, shapes)
+    res = {}
+    for fused in ("1", "0"):  # default fused flash attention; the unfused score / softmax / PV path
+        monkeypatch.setenv("MT_ATTN_FUSED", fused)
+        ctx = Context(0)
+        ctx.init_comm(bytes(128), 1, 0, 1, 1, 1, 1, 1)
+        check = lib().mt_ctx_shard_only(ctx._h, 1)
+        assert check == 0
+        desc = PL.layer_desc(h, H, s, 1, tp_size=t, tp_rank=0, dropout_hidden=0.1, dropout_attn=0.1, seed=SEED,
+                             layer_index=7)
+        layer = Layer(ctx, desc)
+        for i, b in enumerate(keep):
+            layer.set_param(i, b.ctypes.data)
+        xd, gd = bf16_dev(x), bf16_dev(g)
+        yd, dxd = torch.empty_like(xd), torch.empty_like(xd)
+        stream = torch.cuda.current_stream()
+        layer.zero_grads(stream)
+        layer.forward(xd.data_ptr(), yd.data_ptr(), 3, stream)
+        layer.backward(gd.data_ptr(), dxd.data_ptr(), 3, stream)
+        torch.cuda.synchronize()
+        sl = _shard_slices(desc, 12)
+        shapes = [(s_[0].stop - s_[0].start, s_[1].stop - s_[1].start) for s_ in sl]
+        res[fused] = (to_np(yd), to_np(dxd), layer_grads(layer, shapes), sl)
+        layer.close()
+        ctx.close()
     ol = O.OracleLayer(h, H, s, 1, t, dropout_hidden=0.1, dropout_attn=0.1, seed=SEED, layer_index=7,
                        bf16_emulate=True, params=params, shard_rank=0)
     y_ref = ol.forward(x, 3)
     dx_ref = ol.backward(g, 3)
-    y, dx = to_np(yd), to_np(dxd)
-    assert rel(y, y_ref) < 5e-3, ("y", rel(y, y_ref))
-    assert rel(dx, dx_ref) < 1e-2, ("dx", rel(dx, dx_ref))
-    check_grads(got, ol.grads, 1e-2, "mtnlg shard", slices=sl)
-    print(f"mtnlg tp8 shard: y rel {rel(y, y_ref):.2e}, dx rel {rel(dx, dx_ref):.2e}")
-    layer.close()
-    ctx.close()
+    for fused, (y, dx, got, sl) in res.items():
+        assert rel(y, y_ref) < 5e-3, (fused, "y", rel(y, y_ref))
+        assert rel(dx, dx_ref) < 1e-2, (fused, "dx", rel(dx, dx_ref))
+        check_grads(got, ol.grads, 1e-2, f"mtnlg shard fused={fused}", slices=sl)
+        print(f"mtnlg tp8 shard (fused attention {fused}): y rel {rel(y, y_ref):.2e}, dx rel {rel(dx, dx_ref):.2e}")
 
 
 def test_h8192_slice_layer_matches_oracle():
