@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(256) colsum_stage1(const uint4* __restrict__ a
                                                      const float* __restrict__ rstd, uint4* __restrict__ out_dz,
                                                      float* __restrict__ ws, int rows, int nvec, int rows_per,
                                                      uint64_t seed, uint32_t thresh16, float scale,
-                                                     uint64_t elem_offset = 0) {
+                                                     uint64_t elem_offset = 0, const uint8_t* __restrict__ keep_in = nullptr) {
   constexpr int NO = OP == kColLnParams ? 2 : 1;
   __shared__ float part[NO][kColTY][32][9];
   const int cv = blockIdx.x * 32 + threadIdx.x;
@@ -291,7 +291,8 @@ __global__ void __launch_bounds__(256) colsum_stage1(const uint4* __restrict__ a
           }
         } else {
           const uint64_t idx = elem_offset + ((uint64_t)r * nvec + cv) * 8;
-          const uint32_t keep = keep_mask8(seed, idx, thresh16);
+          const uint32_t keep = keep_in != nullptr ? (uint32_t)keep_in[(long long)r * nvec + cv]
+                                                   : keep_mask8(seed, idx, thresh16);
           float o[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) o[j] = ((keep >> j) & 1u) ? v[j] * scale : 0.f;
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(256) bias_dropout_residual_kernel(const uint4*
                                                                     const uint4* __restrict__ resid,
                                                                     uint4* __restrict__ out, int nvec_row,
                                                                     uint64_t seed, uint32_t thresh16, float scale,
-                                                                    uint64_t elem_offset) {
+                                                                    uint64_t elem_offset, uint8_t* __restrict__ keep_out) {
   const int cv = blockIdx.x * blockDim.x + threadIdx.x;
   if (cv >= nvec_row) return;
   const size_t v = (size_t)blockIdx.y * nvec_row + cv;
@@ -382,6 +383,7 @@ __global__ void __launch_bounds__(256) bias_dropout_residual_kernel(const uint4*
   unpack8(bias[cv], b);
   unpack8(resid[v], r);
   const uint32_t keep = keep_mask8(seed, elem_offset + (uint64_t)v * 8, thresh16);
+  if (keep_out != nullptr) keep_out[v] = (uint8_t)keep;
 #pragma unroll
   for (int j = 0; j < 8; ++j) o[j] = r[j] + (((keep >> j) & 1u) ? (a[j] + b[j]) * scale : 0.f);
   out[v] = pack8(o);
@@ -662,11 +664,13 @@ int ln_bwd(const void* dy, const void* x, const void* gamma, const float* mean, 
 
 int bias_dropout_residual_ln(const void* z, const void* bias, const void* resid, void* out, const void* gamma,
                               const void* beta, void* y, float* mean, float* rstd, int rows, int h, float eps,
-                              uint64_t seed, uint32_t thresh16, float scale, uint64_t elem_offset, cudaStream_t s) {
+                              uint64_t seed, uint32_t thresh16, float scale, uint64_t elem_offset, cudaStream_t s,
+                              uint8_t* keep_out) {
+  if (thresh16 == 0) keep_out = nullptr;
   if (row_kernels_enabled() && bdr_ln_rows(z, bias, resid, out, gamma, beta, y, mean, rstd, rows, h, eps, seed,
-                                           thresh16, scale, elem_offset, s))
+                                           thresh16, scale, elem_offset, s, keep_out))
     return 1;
-  bias_dropout_residual(z, bias, resid, out, rows, h, seed, thresh16, scale, s, elem_offset);
+  bias_dropout_residual(z, bias, resid, out, rows, h, seed, thresh16, scale, s, elem_offset, keep_out);
   if (gamma != nullptr) ln_fwd(out, gamma, beta, y, mean, rstd, rows, h, eps, s);
   return gamma != nullptr ? 2 : 1;
 }
@@ -690,21 +694,25 @@ void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, floa
 }
 
 void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int h, uint64_t seed, uint32_t thresh16,
-                           float scale, float* ws, bool accumulate, cudaStream_t s, uint64_t elem_offset) {
+                           float scale, float* ws, bool accumulate, cudaStream_t s, uint64_t elem_offset,
+                           const uint8_t* keep_in) {
+  if (thresh16 == 0) keep_in = nullptr;
   const int nvec = h / 8, splits = col_splits(rows);
   dim3 grid((nvec + 31) / 32, splits), block(32, kColTY);
   colsum_stage1<kColDropout><<<grid, block, 0, s>>>((const uint4*)dy, nvec, nullptr, nullptr, nullptr, (uint4*)dz, ws,
                                                     rows, nvec, (rows + splits - 1) / splits, seed, thresh16, scale,
-                                                    elem_offset);
+                                                    elem_offset, keep_in);
   colsum_stage2<<<(h + 31) / 32, dim3(32, 8), 0, s>>>(ws, dbias, nullptr, h, splits, accumulate);
 }
 
 void bias_dropout_residual(const void* z, const void* bias, const void* resid, void* out, int rows, int h,
-                           uint64_t seed, uint32_t thresh16, float scale, cudaStream_t s, uint64_t elem_offset) {
+                           uint64_t seed, uint32_t thresh16, float scale, cudaStream_t s, uint64_t elem_offset,
+                           uint8_t* keep_out) {
   const int nvec_row = h / 8;
   dim3 grid((nvec_row + 255) / 256, rows);
   bias_dropout_residual_kernel<<<grid, 256, 0, s>>>((const uint4*)z, (const uint4*)bias, (const uint4*)resid,
-                                                    (uint4*)out, nvec_row, seed, thresh16, scale, elem_offset);
+                                                    (uint4*)out, nvec_row, seed, thresh16, scale, elem_offset,
+                                                    keep_out);
 }
 
 #define MT_VPL_DISPATCH(SEQ, LAUNCH) \

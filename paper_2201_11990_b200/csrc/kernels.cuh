@@ -22,13 +22,15 @@ void ln_bwd_params(const void* dy, const void* x, const float* mean, const float
                    int rows, int h, float* workspace, bool accumulate, cudaStream_t s);
 
 // out = resid + dropout(z + bias); mask index = elem_offset + (row * h + col) of the rows passed
+// keep_out (optional): the dropout keep bits, one byte per 8 consecutive elements of a row
+// ([rows][h / 8], bit j = element 8 v + j kept), for the backward to read instead of re-hashing
 void bias_dropout_residual(const void* z, const void* bias, const void* resid, void* out, int rows, int h,
                            uint64_t site_seed, uint32_t thresh16, float scale, cudaStream_t s,
-                           uint64_t elem_offset = 0);
-// dz = dropout'(dy) ; dbias (+)= sum_rows dz
+                           uint64_t elem_offset = 0, uint8_t* keep_out = nullptr);
+// dz = dropout'(dy) ; dbias (+)= sum_rows dz   (keep_in: the forward's keep bytes, or nullptr: re-hash)
 void dropout_bwd_bias_grad(const void* dy, void* dz, float* dbias, int rows, int h, uint64_t site_seed,
                            uint32_t thresh16, float scale, float* workspace, bool accumulate, cudaStream_t s,
-                           uint64_t elem_offset = 0);
+                           uint64_t elem_offset = 0, const uint8_t* keep_in = nullptr);
 // dbias (+)= sum_rows x   (x bf16 [rows, n])
 void bias_grad(const void* x, float* dbias, int rows, int n, long long ldx, float* workspace, bool accumulate,
                cudaStream_t s);
@@ -41,7 +43,8 @@ int ln_bwd(const void* dy, const void* x, const void* gamma, const float* mean, 
 // out = resid + dropout(z + bias) and, if gamma != nullptr, y = LN(out) (one pass).
 int bias_dropout_residual_ln(const void* z, const void* bias, const void* resid, void* out, const void* gamma,
                               const void* beta, void* y, float* mean, float* rstd, int rows, int h, float eps,
-                              uint64_t site_seed, uint32_t thresh16, float scale, uint64_t elem_offset, cudaStream_t s);
+                              uint64_t site_seed, uint32_t thresh16, float scale, uint64_t elem_offset, cudaStream_t s,
+                              uint8_t* keep_out = nullptr);
 // dgamma/dbeta (+)= sum over `splits` fp32 partials ws[2][splits][h]
 void colsum_partials(const float* ws, float* out0, float* out1, int n, int splits, bool accumulate, cudaStream_t s);
 // rows_sm100.cu (return false when the shape does not fit; callers then use the per-row kernels)
@@ -50,7 +53,7 @@ bool ln_fwd_rows(const void* x, const void* gamma, const void* beta, void* y, fl
                  float eps, cudaStream_t s);
 bool bdr_ln_rows(const void* z, const void* bias, const void* resid, void* out, const void* gamma, const void* beta,
                  void* y, float* mean, float* rstd, int rows, int h, float eps, uint64_t seed, uint32_t thresh16,
-                 float scale, uint64_t elem_offset, cudaStream_t s);
+                 float scale, uint64_t elem_offset, cudaStream_t s, uint8_t* keep_out = nullptr);
 bool ln_bwd_rows(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
                  const void* resid, void* dx, float* dgamma, float* dbeta, int rows, int h, float* ws, bool accumulate,
                  cudaStream_t s);

@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(T)
                        uint4* __restrict__ out, const uint4* __restrict__ gamma, const uint4* __restrict__ beta,
                        uint4* __restrict__ y, float* __restrict__ mean, float* __restrict__ rstd, int rows, int nvec,
                        float inv_h, float eps, uint64_t seed, uint32_t thresh16, float scale, uint64_t elem_offset,
-                       int stages) {
+                       int stages, uint8_t* __restrict__ keep_out) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float2 red2[32];
   const RowPlace<kSplit> pl(nvec);
@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(T)
         unpack8f(rs_[v], r);
         const uint32_t keep =
             keep_mask8_rows(seed, elem_offset + ((uint64_t)row * nvec + col0 + v) * 8, thresh16);
+        if (keep_out != nullptr) keep_out[row * nvec + col0 + v] = (uint8_t)keep;  // coalesced bytes
 #pragma unroll
         for (int j = 0; j < 8; ++j) o[j] = r[j] + (((keep >> j) & 1u) ? (a[j] + b[j]) * scale : 0.f);
         ob[i] = pack8f(o);
@@ -629,7 +630,7 @@ bool ln_fwd_rows(const void* x, const void* gamma, const void* beta, void* y, fl
 
 bool bdr_ln_rows(const void* z, const void* bias, const void* resid, void* out, const void* gamma, const void* beta,
                  void* y, float* mean, float* rstd, int rows, int h, float eps, uint64_t seed, uint32_t thresh16,
-                 float scale, uint64_t elem_offset, cudaStream_t s) {
+                 float scale, uint64_t elem_offset, cudaStream_t s, uint8_t* keep_out) {
   const int nvec = h / 8;
   const RowLaunch L = fwd_launch(nvec, 2, gamma != nullptr);
   if (h % 8 || nvec > 6 * 512 * L.split) return false;
@@ -641,12 +642,12 @@ bool bdr_ln_rows(const void* z, const void* bias, const void* resid, void* out, 
       units = launch_rows(bdr_ln_rows_kernel<T, V, LNF, 2>, 2, T, L.smem, rows, 1 << 30, s, (const uint4*)z,              \
                           (const uint4*)bias, (const uint4*)resid, (uint4*)out, (const uint4*)gamma,             \
                           (const uint4*)beta, (uint4*)y, mean, rstd, rows, nvec, 1.f / h, eps, seed, thresh16,   \
-                          scale, elem_offset, L.stages);                                                         \
+                          scale, elem_offset, L.stages, keep_out);                                               \
     else                                                                                                         \
       units = launch_rows(bdr_ln_rows_kernel<T, V, LNF, 1>, 1, T, L.smem, rows, 1 << 30, s, (const uint4*)z,              \
                           (const uint4*)bias, (const uint4*)resid, (uint4*)out, (const uint4*)gamma,             \
                           (const uint4*)beta, (uint4*)y, mean, rstd, rows, nvec, 1.f / h, eps, seed, thresh16,   \
-                          scale, elem_offset, L.stages);                                                         \
+                          scale, elem_offset, L.stages, keep_out);                                               \
   } while (0)
 #define BDR_V256(LNF)                \
   switch (L.vpt) {                   \

@@ -904,7 +904,8 @@ struct SeqPar {
 template <class GemmFor>
 void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_t h, int64_t k_dim, GemmFor gemm_rows,
                         void* z, const void* bias, const void* resid, void* out, uint64_t site, uint32_t th,
-                        float scale, const LnOut* ln, cudaStream_t st, int& n, const char* gemm_label) {
+                        float scale, const LnOut* ln, cudaStream_t st, int& n, const char* gemm_label,
+                        uint8_t* keep) {
   if (sp.on) {
     // sequence parallel: reduce-scatter the partial sums to this rank's rows, then the element-wise
     // epilogue on those rows only, and all-gather the LayerNorm output the next GEMM needs in full
@@ -916,7 +917,7 @@ void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_
     n += bias_dropout_residual_ln(rows_of(z, sp.r0, h), bias, resid, out, ln ? ln->gamma : nullptr,
                                   ln ? ln->beta : nullptr, ln ? rows_of(ln->y, sp.r0, h) : nullptr,
                                   ln ? ln->mean : nullptr, ln ? ln->rstd : nullptr, (int)sp.ms, (int)h,
-                                  ln ? ln->eps : 0.f, site, th, scale, static_cast<uint64_t>(sp.r0 * h), st);
+                                  ln ? ln->eps : 0.f, site, th, scale, static_cast<uint64_t>(sp.r0 * h), st, keep);
     mark(c, st, "fwd.bias_dropout_residual_ln");
     if (ln) {
       sp_allgather(c, ln->y, sp.ms * h, st);
@@ -932,7 +933,7 @@ void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_
     n += bias_dropout_residual_ln(row_ptr(z, r0), bias, row_ptr(resid, r0), row_ptr(out, r0), ln ? ln->gamma : nullptr,
                              ln ? ln->beta : nullptr, ln ? row_ptr(ln->y, r0) : nullptr, ln ? ln->mean + r0 : nullptr,
                              ln ? ln->rstd + r0 : nullptr, (int)nr, (int)h, ln ? ln->eps : 0.f, site, th, scale,
-                             static_cast<uint64_t>(r0 * h), st);
+                             static_cast<uint64_t>(r0 * h), st, keep ? keep + r0 * (h / 8) : nullptr);
   };
   if (!tpc) {
     gemm_rows(0, M, 0, nullptr);
@@ -971,6 +972,23 @@ void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_
   mark(c, st, "fwd.bias_dropout_residual_ln");
 }
 
+// The forward's hidden-dropout keep bytes feed the backward's dropout' (MT_HIDDEN_KEEP=0: the backward
+// re-hashes the counter-based mask instead; same bits either way).
+bool hidden_keep_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MT_HIDDEN_KEEP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Keep bytes of hidden-dropout site i (0: attention-out, 1: MLP-out) in the slot (nullptr: no dropout
+// or no buffer; writer and reader then both fall back to the counter-based hash).
+uint8_t* hidden_keep(mt_layer* l, mt_layer::Saved& sv, int i) {
+  if (!(l->d.dropout_hidden > 0.f) || !sv.hmask.ptr || !hidden_keep_enabled()) return nullptr;
+  return sv.hmask.as<uint8_t>() + i * l->M * (l->h / 8);
+}
+
 void ensure_slot_buffers(mt_layer* l, mt_layer::Saved& sv) {
   const int64_t M = l->M, b = l->d.micro_batch, s = l->d.seq, Hl = l->heads_local;
   sv.ln1.ensure(M * l->h * 2);
@@ -988,6 +1006,7 @@ void ensure_slot_buffers(mt_layer* l, mt_layer::Saved& sv) {
   sv.pre.ensure(M * l->ffl * 2);
   sv.act.ensure(M * l->ffl * 2);
   sv.stats.ensure(4 * M * 4);
+  if (l->d.dropout_hidden > 0.f) sv.hmask.ensure(2 * M * (l->h / 8));
 }
 
 // Per-microbatch slot. With activation recompute the slot keeps only the layer
@@ -1124,7 +1143,8 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, uint64_t mse
               .allreduce(ar)
               .run(st, n);
         },
-        z, l->param_ptr(MT_P_PROJ_B), x, sv.x1.ptr, site_out1, th_h, scale_h, &ln2, st, n, "fwd.proj_gemm");
+        z, l->param_ptr(MT_P_PROJ_B), x, sv.x1.ptr, site_out1, th_h, scale_h, &ln2, st, n, "fwd.proj_gemm",
+        hidden_keep(l, sv, 0));
   }
   Gemm(sv.ln2.ptr, h, false, l->param_ptr(MT_P_FC1_W), h, false, sv.act.ptr, ffl, M, ffl, h)
       .epi(MT_EPI_BIAS_GELU)
@@ -1141,7 +1161,8 @@ void forward_into(mt_layer* l, const void* x, void* y, uint32_t mb, uint64_t mse
             .allreduce(ar)
             .run(st, n);
       },
-      z, l->param_ptr(MT_P_FC2_B), sv.x1.ptr, y, site_out2, th_h, scale_h, nullptr, st, n, "fwd.fc2_gemm");
+      z, l->param_ptr(MT_P_FC2_B), sv.x1.ptr, y, site_out2, th_h, scale_h, nullptr, st, n, "fwd.fc2_gemm",
+      hidden_keep(l, sv, 1));
   check_cuda(cudaGetLastError(), "layer forward launch");
   l->fwd_launches = n;
 }
@@ -1210,7 +1231,7 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, uint64_t 
   mark(c, st, "begin");
   // ---- MLP block
   dropout_bwd_bias_grad(dy, rows_of(dm, sp.r0, h), l->grad_ptr(MT_P_FC2_B), (int)sp.ms, (int)h, site_out2, th_h,
-                        scale_h, ws, acc, st, eoff);
+                        scale_h, ws, acc, st, eoff, hidden_keep(l, sv, 1));
   n += 2;
   if (sp.on) {
     sp_allgather(c, dm, sp.ms * h, st);
@@ -1246,7 +1267,7 @@ void backward_from(mt_layer* l, const void* dy, void* dx, uint32_t mb, uint64_t 
   // ---- attention block
   void* dz = dm;
   dropout_bwd_bias_grad(dx1, rows_of(dz, sp.r0, h), l->grad_ptr(MT_P_PROJ_B), (int)sp.ms, (int)h, site_out1, th_h,
-                        scale_h, ws, acc, st, eoff);
+                        scale_h, ws, acc, st, eoff, hidden_keep(l, sv, 0));
   n += 2;
   if (sp.on) {
     sp_allgather(c, dz, sp.ms * h, st);

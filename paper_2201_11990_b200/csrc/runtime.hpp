@@ -207,6 +207,9 @@ struct mt_layer {
     mt::DeviceBuffer ln1, qkv, S, P, lse, ctx, x1, ln2, pre, act, stats;  // stats: mean1,rstd1,mean2,rstd2
     mt::DeviceBuffer mask;      // fused attention: the forward's dropout keep bits [b][heads/t][s][s/32]
     bool mask_valid = false;    // the forward wrote `mask` (the backward reads it instead of re-hashing)
+    // hidden dropout keep bytes of the two bias-dropout-residual sites (attention-out, MLP-out), one
+    // byte per 8 elements [2][rows][h / 8], written by the forward, read by the backward's dropout'
+    mt::DeviceBuffer hmask;
   };
   std::map<uint32_t, std::unique_ptr<Saved>> saved;
   bool recompute = false;           // activation recompute (full-layer checkpointing)
