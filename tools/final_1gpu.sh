@@ -13,9 +13,13 @@ for a in "--config mtnlg --shard-of 8" "--config gpt3 --shard-of 8" "--config mt
   timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu $a > gpurun_out/${R}_bench_$n.json 2>&1; echo "$a rc=$?"
 done
 python bench.py --steps 1 --warmup 1 --no-cpu > /dev/null 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -s 40 -c 40 --csv --log-file gpurun_out/${R}_launches_final.csv \
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/${R}_launches_final.csv \
       python bench.py --steps 1 --warmup 1 --no-cpu > /dev/null 2>&1; echo "ncu launches rc=$?"
 python tools/gemm_one.py fc1_fwd 3 > /dev/null 2>&1 && \
   ncu --set full --import-source on --clock-control none -k regex:gemm_sm100 -s 2 -c 1 -o gpurun_out/${R}_gemm_fc1_fwd \
       python tools/gemm_one.py fc1_fwd 3 > /dev/null 2>&1; echo "ncu gemm rc=$?"
 for f in gpurun_out/${R}_bench_*.json; do echo "== $f"; tail -c 600 $f; echo; done
+# fused attention kernels of the default path (GPT-3 layer shape), full section set
+python tools/attn_one.py bwd 2 > /dev/null 2>&1 && \
+  ncu --set full --import-source on --clock-control none -k regex:"attn_fwd2|attn_bwd2" -s 2 -c 2 -o gpurun_out/${R}_attn_final \
+      python tools/attn_one.py bwd 3 > /dev/null 2>&1; echo "ncu attn rc=$?"
