@@ -56,6 +56,7 @@ struct AttnParams {
   __nv_bfloat16* out;     // ctx: row i, head h at out + i * ld_out + h * out_head_stride
   long long ld_out, out_head_stride;
   float* lse;             // [heads][seq]
+  int group_heads;        // attn_fwd2_kernel: heads per launch-order group (as the one-kernel backward)
   uint32_t* mask;         // optional attention-dropout keep bits [heads][seq][seq / 32] (bit c % 32 of word
                           // c / 32 = score (row, c) kept); written for the causal blocks only
 };
@@ -398,8 +399,13 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int pair = p.nqb / 2 - 1 - (int)blockIdx.y;  // heaviest pairs of every head first (grid: heads, pairs)
-  const int head = blockIdx.x;
+  // 1-D grid in groups of group_heads heads, heaviest pairs of every head of a group first: no tail of
+  // heavy CTAs, and the CTAs in flight share a few heads' K / V blocks in L2
+  const int npair = p.nqb / 2, per_group = p.group_heads * npair;
+  const int grp = (int)blockIdx.x / per_group, within = (int)blockIdx.x - grp * per_group;
+  const int gh = min(p.group_heads, p.heads - grp * p.group_heads);
+  const int pair = npair - 1 - within / gh;
+  const int head = grp * p.group_heads + within % gh;
   const int q_lo = 2 * pair, q_hi = 2 * pair + 1;     // tile a, tile b
   const int nkv = q_hi + 1;                           // kv blocks 0..q_hi (tile a uses 0..q_lo)
 
@@ -666,6 +672,7 @@ struct AttnBwdParams {
   __nv_bfloat16* dq; // dqkv: row i, head h: + i * ld_dq + h * 3hd (+0 Q, +hd K, +2hd V)
   long long ld_dq;
   const uint32_t* mask;  // keep bits written by the forward ([heads][seq][seq/32]); nullptr: re-hash
+  int group_heads;       // one-kernel backward: heads per launch-order group (see attn_bwd2_kernel)
 };
 
 
@@ -972,8 +979,15 @@ __global__ void __launch_bounds__(128 + 128 * NH, 1)
   uint64_t* dq_free = bars + 12;  // 4 warps drained the dQ partial (dP columns free)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int jb = (int)blockIdx.y;  // key block; jb = 0 has the most query blocks: every head's jb = 0
-  const int head = blockIdx.x;     // launches first (grid: heads, key blocks), the light ones last
+  // Launch order (1-D grid): groups of group_heads heads; inside a group every head's heaviest key block
+  // (jb = 0: most query blocks) first, the light ones last. Heavy-first avoids a tail of heavy CTAs;
+  // the grouping keeps the CTAs in flight on a few heads, so the fp32 dQ accumulator rows they add
+  // into (and the heads' Q / dO blocks) stay in L2 instead of spanning all heads at once.
+  const int per_group = p.group_heads * p.nqb;
+  const int grp = (int)blockIdx.x / per_group, within = (int)blockIdx.x - grp * per_group;
+  const int gh = min(p.group_heads, p.heads - grp * p.group_heads);  // heads in this (last) group
+  const int jb = within / gh;
+  const int head = grp * p.group_heads + (within - jb * gh);
   const int nblk = p.nqb - jb;
   constexpr uint32_t kDV = 0, kDK = 128, kSC = 256, kDP = 384;
 
@@ -1503,7 +1517,14 @@ int launch_fwd2(const void* qkv, long long ld_qkv, int heads, int seq, long long
   p.lse = lse;
   p.mask = mask;
   if (!set_smem_once<attn_fwd2_kernel<HD>>(C::kSmem)) return 2;
-  attn_fwd2_kernel<HD><<<dim3(heads, p.nqb / 2), kFwd2Threads, C::kSmem, s>>>(mq, mk, mv, p);
+  {
+    // measured: grouping halves the forward's DRAM reads but its 8 pairs per head leave group tails
+    // (GPT-3 layer 273 us ungrouped vs 286-303 us in groups of 4-12), so one group by default
+    const char* e = getenv("MT_ATTN_FWD_GROUP_HEADS");
+    const int g = e ? atoi(e) : 0;
+    p.group_heads = (g <= 0 || g > heads) ? heads : g;
+  }
+  attn_fwd2_kernel<HD><<<heads * (p.nqb / 2), kFwd2Threads, C::kSmem, s>>>(mq, mk, mv, p);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -1546,6 +1567,12 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
   p.dq = static_cast<__nv_bfloat16*>(dqkv);
   p.ld_dq = ld_qkv;
   p.mask = mask;
+  {
+    // groups of 8 heads: DRAM 1.80 -> 0.50 GB, 582 -> 550 us (GPT-3 layer, profiles/r02_attn_group_ab.log)
+    const char* e = getenv("MT_ATTN_GROUP_HEADS");  // 0: one group (all heads)
+    const int g = e ? atoi(e) : 8;
+    p.group_heads = (g <= 0 || g > heads) ? heads : g;
+  }
   constexpr int kSmemKV = 1024 + 4 * C::kTileBytes + C::kMBytes + 256;
   constexpr int kSmemQ = 1024 + 4 * C::kTileBytes + C::kMBytes + 256;
   if constexpr (HD <= 128) {
@@ -1554,10 +1581,10 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
       if (cudaMemsetAsync(dq_acc, 0, (size_t)heads * seq * HD * sizeof(float), s) != cudaSuccess) return 2;
       if (bwd2_halves() == 2) {
         if (!set_smem_once<attn_bwd2_kernel<HD, 2>>(C2::kSmem)) return 2;
-        attn_bwd2_kernel<HD, 2><<<dim3(heads, p.nqb), 384, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
+        attn_bwd2_kernel<HD, 2><<<heads * p.nqb, 384, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
       } else {
         if (!set_smem_once<attn_bwd2_kernel<HD, 1>>(C2::kSmem)) return 2;
-        attn_bwd2_kernel<HD, 1><<<dim3(heads, p.nqb), 256, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
+        attn_bwd2_kernel<HD, 1><<<heads * p.nqb, 256, C2::kSmem, s>>>(mq, mk, mv, mdo, p, dq_acc);
       }
       const long long groups = (long long)heads * seq * (HD / 8);
       dq_finalize_kernel<<<(unsigned)((groups + 255) / 256), 256, 0, s>>>(dq_acc, p.dq, p.ld_dq, HD, heads, seq, alpha);
