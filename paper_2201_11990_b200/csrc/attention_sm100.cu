@@ -660,6 +660,49 @@ __global__ void attn_bwd_rowdot_kernel(const __nv_bfloat16* __restrict__ dout, c
   if (lane == 0) D[(long long)h * seq + i] = acc;
 }
 
+// Same D with coalesced rows: consecutive threads take consecutive 16-byte chunks of a token row (all
+// heads of row i are contiguous), TPR = hd / 8 lanes per (head, row) reduce with shuffles. hd 64 / 128.
+template <int TPR>
+__global__ void __launch_bounds__(256) attn_bwd_rowdot_vec_kernel(const uint4* __restrict__ dout,
+                                                                  const uint4* __restrict__ out, long long ld_vec,
+                                                                  int heads, int seq, float* __restrict__ D) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per_row = heads * TPR;
+  const long long i = t / per_row;
+  const int c = (int)(t - i * per_row);
+  float acc = 0.f;
+  if (i < seq) {
+    const uint4 x = __ldg(dout + i * ld_vec + c), y = __ldg(out + i * ld_vec + c);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 a = unpack_bf16x2(xs[q]), b = unpack_bf16x2(ys[q]);
+      acc = fmaf(a.x, b.x, fmaf(a.y, b.y, acc));
+    }
+  }
+#pragma unroll
+  for (int o = TPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (i < seq && (c & (TPR - 1)) == 0) D[(long long)(c / TPR) * seq + i] = acc;
+}
+
+// D for every (head, row): the coalesced kernel for hd 64 / 128, the warp-per-row kernel otherwise.
+void launch_rowdot(const void* dout, const void* out, long long ld, int hd, int heads, int seq, float* D,
+                   cudaStream_t s) {
+  const long long threads = (long long)seq * heads * (hd / 8);
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  const bool vec_ok = (ld % 8 == 0) && ((reinterpret_cast<uintptr_t>(dout) | reinterpret_cast<uintptr_t>(out)) % 16 == 0);
+  if (vec_ok && hd == 128)
+    attn_bwd_rowdot_vec_kernel<16><<<blocks, 256, 0, s>>>(static_cast<const uint4*>(dout), static_cast<const uint4*>(out),
+                                                          ld / 8, heads, seq, D);
+  else if (vec_ok && hd == 64)
+    attn_bwd_rowdot_vec_kernel<8><<<blocks, 256, 0, s>>>(static_cast<const uint4*>(dout), static_cast<const uint4*>(out),
+                                                         ld / 8, heads, seq, D);
+  else
+    attn_bwd_rowdot_kernel<<<(heads * seq + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dout),
+                                                                 static_cast<const __nv_bfloat16*>(out), ld, hd, heads,
+                                                                 seq, D);
+}
+
 struct AttnBwdParams {
   int seq, nqb, heads;
   long long head_base;
@@ -1548,10 +1591,7 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
       !head_map(&mv, q + 2 * HD, HD, seq, heads, ld_qkv, 3 * HD) ||
       !head_map(&mdo, dctx, HD, seq, heads, ld_ctx, HD))
     return 1;
-  const int rows = heads * seq;
-  attn_bwd_rowdot_kernel<<<(rows + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dctx),
-                                                         static_cast<const __nv_bfloat16*>(ctx), ld_ctx, HD, heads, seq,
-                                                         D);
+  launch_rowdot(dctx, ctx, ld_ctx, HD, heads, seq, D, s);
   AttnBwdParams p{};
   p.seq = seq;
   p.nqb = seq / 128;
@@ -1674,9 +1714,7 @@ int attention_fwd(const void* qkv, long long ld_qkv, int heads, int seq, int hd,
 
 // D[h][i] = dout_i . out_i per head (the softmax-backward row term; attention_sm100.cu's rowdot kernel)
 void attn_rowdot(const void* dout, const void* out, long long ld, int hd, int heads, int seq, float* D, cudaStream_t s) {
-  const int rows = heads * seq;
-  attn_bwd_rowdot_kernel<<<(rows + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dout),
-                                                         static_cast<const __nv_bfloat16*>(out), ld, hd, heads, seq, D);
+  launch_rowdot(dout, out, ld, hd, heads, seq, D, s);
 }
 
 }  // namespace mt
