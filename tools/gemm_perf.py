@@ -13,6 +13,9 @@ def run(m, n, k, a_mn=False, b_mn=False, bn=0, epi=N.EPI_STORE_BF16, reps=10):
     a.lda = m if a_mn else k; a.ldb = n if b_mn else k; a.ldd = n
     a.a_mn_major, a.b_mn_major = int(a_mn), int(b_mn)
     a.m, a.n, a.k, a.batch, a.alpha, a.epilogue, a.block_n = m, n, k, 1, 1.0, epi, bn
+    # the runtime's workspace (split-K tail counters / partials, dynamic tile scheduler)
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
     s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(3):
