@@ -965,22 +965,7 @@ int launch(const mt_gemm_args& a, cudaStream_t stream) {
       p.kblocks >= split_min_kblocks()) {
     const int units = std::max(1, cap_units);
     const int full = (p.total_tiles / units) * units, tail = p.total_tiles - full;
-    // measurement knob MT_GEMM_SPLIT_ALL=s: split every tile of a GEMM of at most two waves s ways
-    static const int split_all = [] {
-      const char* e = getenv("MT_GEMM_SPLIT_ALL");
-      return e ? atoi(e) : 0;
-    }();
-    if (split_all >= 2 && p.total_tiles <= 2 * units) {
-      const int t = p.total_tiles, splits = std::min(split_all, p.kblocks / 4);
-      const size_t need = kSplitCounterBytes + (size_t)t * splits * 2 * 128 * BN * sizeof(float);
-      if (splits >= 2 && (size_t)a.workspace_bytes >= need && t * 2 * (int)sizeof(int) <= kSplitCounterBytes - 64) {
-        p.full_tiles = 0;
-        p.splits = splits;
-        p.work_items = t * splits;
-        p.split_cnt = static_cast<int*>(a.workspace);
-        p.split_ws = reinterpret_cast<float*>(static_cast<char*>(a.workspace) + kSplitCounterBytes);
-      }
-    } else if (full > 0 && tail > 0 && tail * 2 <= units) {
+    if (full > 0 && tail > 0 && tail * 2 <= units) {
       const int splits = std::min({units / tail, p.kblocks / 4, 8});
       const size_t need = kSplitCounterBytes + (size_t)tail * splits * 2 * 128 * BN * sizeof(float);
       if (splits >= 2 && (size_t)a.workspace_bytes >= need && tail * 2 * (int)sizeof(int) <= kSplitCounterBytes - 64) {
