@@ -1571,13 +1571,11 @@ int launch_fwd2(const void* qkv, long long ld_qkv, int heads, int seq, long long
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
-// Softmax warpgroups of the one-kernel backward (MT_ATTN_BWD_WG, default 2: column halves).
+// Softmax warpgroups of the fused backward kernels (MT_ATTN_BWD_WG, default 2: column halves; read per
+// call so tests can switch it).
 int bwd2_halves() {
-  static const int v = [] {
-    const char* e = getenv("MT_ATTN_BWD_WG");
-    return (e && e[0] == '1') ? 1 : 2;
-  }();
-  return v;
+  const char* e = getenv("MT_ATTN_BWD_WG");
+  return (e && e[0] == '1') ? 1 : 2;
 }
 
 template <int HD>

@@ -974,12 +974,9 @@ void row_parallel_block(mt_ctx* c, bool tpc, const SeqPar& sp, int64_t M, int64_
 
 // The forward's hidden-dropout keep bytes feed the backward's dropout' (MT_HIDDEN_KEEP=0: the backward
 // re-hashes the counter-based mask instead; same bits either way).
-bool hidden_keep_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("MT_HIDDEN_KEEP");
-    return !(e && e[0] == '0');
-  }();
-  return on;
+bool hidden_keep_enabled() {  // read per call so tests can switch it
+  const char* e = getenv("MT_HIDDEN_KEEP");
+  return !(e && e[0] == '0');
 }
 
 // Keep bytes of hidden-dropout site i (0: attention-out, 1: MLP-out) in the slot (nullptr: no dropout

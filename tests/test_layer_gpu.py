@@ -90,6 +90,62 @@ def test_layer_matches_oracle(hidden, heads, seq, mb, p, fused, monkeypatch):
     ctx.close()
 
 
+@pytest.mark.parametrize("env", [{"MT_ATTN_BWD_WG": "1"}, {"MT_HIDDEN_KEEP": "0"}, {"MT_ATTN_GROUP_HEADS": "0"},
+                                 {"MT_ATTN_GROUP_HEADS": "3", "MT_ATTN_FWD_GROUP_HEADS": "3"}],
+                         ids=["one_softmax_warpgroup", "rehash_hidden_dropout", "ungrouped_order", "groups_of_3"])
+def test_runtime_switch_variants_match_oracle(env, monkeypatch):
+    """The non-default variants behind the runtime switches against the oracle: one
+    softmax warpgroup in the fused backward kernels, the backward re-hashing the hidden-dropout mask
+    instead of reading the forward's keep bytes, and other launch-order groupings of the attention
+    kernels (including a last, partial group: 8 heads in groups of 3)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    test_layer_matches_oracle(1024, 8, 256, 1, 0.1, True, monkeypatch)
+
+
+def _layer_outputs(hidden, heads, seq, mb, p):
+    ctx = Context(0)
+    layer = Layer(ctx, PL.layer_desc(hidden, heads, seq, mb, dropout_hidden=p, dropout_attn=p, seed=SEED,
+                                     layer_index=3))
+    for i, prm in enumerate(O.init_params(hidden, SEED, 3)):
+        bits = np.ascontiguousarray(O.to_bf16_bits(prm))
+        layer.set_param(i, bits.ctypes.data)
+    M = mb * seq
+    xd = bf16_tensor(O.normal(O.site_seed(SEED, "input", 0, 0), M, hidden))
+    gd = bf16_tensor(O.normal(O.site_seed(SEED, "grad", 0, 0), M, hidden, std=1e-2))
+    yd, dxd = torch.empty_like(xd), torch.empty_like(xd)
+    s = torch.cuda.current_stream()
+    layer.forward(xd.data_ptr(), yd.data_ptr(), 0, s)
+    layer.backward(gd.data_ptr(), dxd.data_ptr(), 0, s)
+    torch.cuda.synchronize()
+    grads = []
+    for i, shp in enumerate(O.param_shapes(hidden)):
+        out = np.empty(int(np.prod(shp)), np.float32)
+        layer.get_grad(i, out.ctypes.data)
+        grads.append(out)
+    res = (yd.view(torch.int16).cpu().numpy(), dxd.view(torch.int16).cpu().numpy(), grads)
+    layer.close()
+    ctx.close()
+    return res
+
+
+@pytest.mark.parametrize("env", [{"MT_HIDDEN_KEEP": "0"}, {"MT_ATTN_FWD_GROUP_HEADS": "3"}],
+                         ids=["rehashed_hidden_mask", "forward_launch_groups"])
+def test_switch_variants_are_bit_identical(env, monkeypatch):
+    """Variants that must not change a single bit: the backward's hidden-dropout mask read from the
+    forward's keep bytes vs re-hashed from the counter-based stream, and the forward attention's launch
+    order. Deterministic path (MT_ATTN_BWD2=0: no dQ atomics), so every output and gradient is compared
+    bitwise."""
+    monkeypatch.setenv("MT_ATTN_BWD2", "0")
+    base = _layer_outputs(1024, 8, 256, 1, 0.1)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    var = _layer_outputs(1024, 8, 256, 1, 0.1)
+    assert np.array_equal(base[0], var[0]) and np.array_equal(base[1], var[1])
+    for i, (a, b) in enumerate(zip(base[2], var[2])):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), O.PARAM_NAMES[i]
+
+
 def test_device_init_matches_oracle_streams():
     """mt_layer_init_params draws, shard by shard, the same global tensors as the oracle's host
     generator (so TP=t and TP=1 runs start from identical weights)."""
