@@ -183,6 +183,15 @@ int mt_layer_finish_grads(mt_layer* l, void* stream);
  * curator::step_seed(desc.seed, step) (= desc.seed at step 0), so masks differ across iterations; a
  * backward replays the masks of its own forward. The stage driver sets it each iteration. */
 int mt_layer_set_step(mt_layer* l, uint64_t step);
+/* Parity inspection: copy the dropout keep bits the forward of microbatch `mb` saved for its backward
+ * (the microbatch must have activations in flight, i.e. forward done, backward not yet). which = 0:
+ * attention dropout, uint32 words [b][heads/t][s][s/32], bit c % 32 of word c / 32 = score (row, c)
+ * kept — written for the causal 128-column blocks only (fused attention); which = 1 / 2: the hidden
+ * dropout after the attention-out / MLP-out projection, bytes [b*s][h/8], bit j of byte v = element
+ * 8 v + j kept. *bytes_out = bytes copied; status 1 when that mask was not saved (no dropout, the
+ * unfused attention path, activation recompute, or MT_HIDDEN_KEEP=0). Synchronises the device. */
+int mt_layer_dropout_keep_bits(mt_layer* l, uint32_t mb, int32_t which, void* host_out, int64_t capacity,
+                               int64_t* bytes_out);
 /* Kernel launches one forward / backward issues (for the bench's gpu_launches claim). */
 int mt_layer_launch_counts(const mt_layer* l, int32_t* fwd, int32_t* bwd);
 /* Device pointer to the flat fp32 gradient buffer of the layer and its element count. */

@@ -135,6 +135,7 @@ _SIGS = {
     "mt_layer_launch_counts": (C.c_int, [P, PI32, PI32]),
     "mt_layer_set_recompute": (C.c_int, [P, I32]),
     "mt_layer_set_step": (C.c_int, [P, U64]),
+    "mt_layer_dropout_keep_bits": (C.c_int, [P, C.c_uint32, C.c_int32, P, C.c_int64, C.POINTER(C.c_int64)]),
     "mt_vocab_set_step": (C.c_int, [P, U64]),
     "mt_vocab_set_loss_scale": (C.c_int, [P, F32]),
     "mt_stage_set_step": (C.c_int, [P, U64]),

@@ -795,6 +795,37 @@ extern "C" int mt_layer_set_step(mt_layer* l, uint64_t step) {
   });
 }
 
+namespace {
+uint8_t* hidden_keep(mt_layer* l, mt_layer::Saved& sv, int i);  // defined with the forward below
+}  // namespace
+
+extern "C" int mt_layer_dropout_keep_bits(mt_layer* l, uint32_t mb, int32_t which, void* host_out, int64_t capacity,
+                                          int64_t* bytes_out) {
+  return guarded([&] {
+    if (!l || !host_out || !bytes_out || which < 0 || which > 2) throw std::invalid_argument("bad argument");
+    *bytes_out = 0;
+    auto it = l->saved.find(mb);
+    if (it == l->saved.end() || l->recompute) throw std::invalid_argument("no saved activations for this microbatch");
+    mt_layer::Saved& sv = *it->second;
+    const void* src = nullptr;
+    int64_t n = 0;
+    if (which == 0) {
+      if (!l->fused_attn || !sv.mask_valid) throw std::invalid_argument("attention keep bits not saved");
+      src = sv.mask.ptr;
+      n = int64_t{l->d.micro_batch} * l->heads_local * l->d.seq * (l->d.seq / 32) * 4;
+    } else {
+      src = hidden_keep(l, sv, which - 1);
+      if (!src) throw std::invalid_argument("hidden-dropout keep bytes not saved");
+      n = l->M * (l->h / 8);
+    }
+    if (capacity < n) throw std::invalid_argument("host buffer too small");
+    check_cuda(cudaSetDevice(l->ctx->device), "cudaSetDevice");
+    check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    check_cuda(cudaMemcpy(host_out, src, static_cast<size_t>(n), cudaMemcpyDeviceToHost), "D2H keep bits");
+    *bytes_out = n;
+  });
+}
+
 extern "C" int mt_layer_launch_counts(const mt_layer* l, int32_t* f, int32_t* b) {
   return guarded([&] {
     *f = l->fwd_launches;

@@ -123,6 +123,14 @@ class Layer:
         check(lib().mt_layer_launch_counts(self._h, C.byref(f), C.byref(b)))
         return f.value, b.value
 
+    def dropout_keep_bits(self, mb: int, which: int, nbytes: int) -> bytes:
+        """The keep bits the forward of microbatch `mb` saved (which 0: attention words, 1/2: hidden
+        bytes after attention-out / MLP-out); see mt_layer_dropout_keep_bits."""
+        buf = C.create_string_buffer(nbytes)
+        got = C.c_int64()
+        check(lib().mt_layer_dropout_keep_bits(self._h, mb, which, buf, nbytes, C.byref(got)))
+        return buf.raw[: got.value]
+
     def close(self) -> None:
         if self._h:
             lib().mt_layer_destroy(self._h)

@@ -146,6 +146,52 @@ def test_switch_variants_are_bit_identical(env, monkeypatch):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), O.PARAM_NAMES[i]
 
 
+@pytest.mark.parametrize("hidden,heads,seq,mb,attn_saved", [(1024, 8, 256, 1, True), (512, 8, 512, 2, True),
+                                                             (640, 4, 256, 1, False)],
+                         ids=["hd128", "hd64_two_rows", "hd160"])
+def test_saved_dropout_keep_bits_are_bit_exact(hidden, heads, seq, mb, attn_saved):
+    """The keep bits the kernels draw on the device and save for the backward — attention dropout
+    (two-tile fused forward, hd <= 128: one bit per causal score) and both hidden dropouts
+    (bias-dropout-residual kernels: one byte per 8 elements) — equal, bit for bit, the mask definition
+    restated in numpy (tests/test_oracle.py keep_mask, pinned there against the native definition).
+    The hd-160 forward does not save attention bits (its backward re-hashes them)."""
+    from .test_oracle import keep_mask
+    p, mbid, layer_index = 0.1, 5, 3
+    ctx = Context(0)
+    layer = Layer(ctx, PL.layer_desc(hidden, heads, seq, mb, dropout_hidden=p, dropout_attn=p, seed=SEED,
+                                     layer_index=layer_index))
+    layer.init_params(torch.cuda.current_stream())
+    M = mb * seq
+    xd = bf16_tensor(O.normal(O.site_seed(SEED, "input", 0, 0), M, hidden))
+    yd = torch.empty_like(xd)
+    layer.forward(xd.data_ptr(), yd.data_ptr(), mbid, torch.cuda.current_stream())
+    # attention: words [b][heads][s][s / 32]; compare the causal 128-column blocks the forward writes
+    if not attn_saved:
+        with pytest.raises(PL.ConfigError):
+            layer.dropout_keep_bits(mbid, 0, mb * heads * seq * seq // 8)
+    words = np.frombuffer(layer.dropout_keep_bits(mbid, 0, mb * heads * seq * seq // 8), np.uint32) \
+        if attn_saved else None
+    words = words.reshape(mb, heads, seq, seq // 32) if attn_saved else None
+    ref = keep_mask(O.site_seed(SEED, "attn.probs", layer_index, mbid), mb * heads * seq * seq, p)
+    ref_words = np.packbits(ref.reshape(mb, heads, seq, seq // 32, 32)[..., ::-1], axis=-1,
+                            bitorder="big").view(">u4").astype(np.uint32).reshape(mb, heads, seq, seq // 32)
+    for i in range(seq if attn_saved else 0):
+        nw = (i // 128 + 1) * 4  # words of the causal blocks of row i
+        assert np.array_equal(words[:, :, i, :nw], ref_words[:, :, i, :nw]), ("attention row", i)
+    # hidden dropout: bytes [b*s][h/8], bit j of byte v = element 8v + j
+    for which, site in ((1, "attn.out"), (2, "mlp.out")):
+        got = np.frombuffer(layer.dropout_keep_bits(mbid, which, M * hidden // 8), np.uint8)
+        want = np.packbits(keep_mask(O.site_seed(SEED, site, layer_index, mbid), M * hidden, p).reshape(-1, 8),
+                           axis=-1, bitorder="little").reshape(-1)
+        assert np.array_equal(got, want), site
+    gd = torch.zeros_like(xd)
+    dxd = torch.empty_like(xd)
+    layer.backward(gd.data_ptr(), dxd.data_ptr(), mbid, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    layer.close()
+    ctx.close()
+
+
 def test_device_init_matches_oracle_streams():
     """mt_layer_init_params draws, shard by shard, the same global tensors as the oracle's host
     generator (so TP=t and TP=1 runs start from identical weights)."""
