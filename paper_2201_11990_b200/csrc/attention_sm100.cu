@@ -1013,7 +1013,7 @@ __global__ void __launch_bounds__(128 + 128 * NH, 1)
   uint64_t* qo_full = bars + 1;   // [2]
   uint64_t* qo_empty = bars + 3;  // [2]
   uint64_t* s_full = bars + 5;
-  uint64_t* s_free = bars + 6;    // 4 softmax warps read S
+  uint64_t* s_free = bars + 6;    // unused since the pipelined order (p_full(i) implies S(i) was read)
   uint64_t* dp_full = bars + 7;
   uint64_t* p_full = bars + 8;    // 4 warps wrote P
   uint64_t* pv_done = bars + 9;   // dV MMA consumed P (the tile can take dS)
