@@ -192,6 +192,9 @@ def run_reference(args, L: dict) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # rank 0 alone runs the CPU reference: give it every host thread (torchrun exports OMP_NUM_THREADS=1;
+    # the OpenMP runtime reads it when the oracle library loads, which happens below)
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     steps = max(1, min(args.steps, 5))
     warmup = max(1, min(args.warmup, 2))
     cb = cpu_sample(L, steps, warmup)
