@@ -57,6 +57,7 @@ struct AttnParams {
   long long ld_out, out_head_stride;
   float* lse;             // [heads][seq]
   int group_heads;        // attn_fwd2_kernel: heads per launch-order group (as the one-kernel backward)
+  int balanced;           // attn_fwd2_kernel: pair query blocks (p, nqb - 1 - p) instead of (2p, 2p + 1)
   uint32_t* mask;         // optional attention-dropout keep bits [heads][seq][seq / 32] (bit c % 32 of word
                           // c / 32 = score (row, c) kept); written for the causal blocks only
 };
@@ -406,7 +407,11 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
   const int gh = min(p.group_heads, p.heads - grp * p.group_heads);
   const int pair = npair - 1 - within / gh;
   const int head = grp * p.group_heads + within % gh;
-  const int q_lo = 2 * pair, q_hi = 2 * pair + 1;     // tile a, tile b
+  // tile a, tile b: adjacent query blocks (the heaviest pairs first keep a many-wave launch balanced),
+  // or — when the launch is under two waves (e.g. 12 heads at TP=8) and the heaviest adjacent pair
+  // alone would set the kernel's length — a heavy block with a light one, so every CTA carries about
+  // the same number of key blocks
+  const int q_lo = p.balanced ? pair : 2 * pair, q_hi = p.balanced ? p.nqb - 1 - pair : 2 * pair + 1;
   const int nkv = q_hi + 1;                           // kv blocks 0..q_hi (tile a uses 0..q_lo)
 
   if (warp == 0 && lane == 0) {
@@ -437,7 +442,8 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
       mbar_arrive_expect_tx(smem_u32(q_full), 2 * C::kTileBytes);
       for (int x = 0; x < 2; ++x)
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(sQ + x * C::kTileBytes + c * 16384, &tq, smem_u32(q_full), c * 64, (q_lo + x) * 128, head);
+          tma_load_3d(sQ + x * C::kTileBytes + c * 16384, &tq, smem_u32(q_full), c * 64, (x ? q_hi : q_lo) * 128,
+                      head);
       for (int t = 0; t < 2 * nkv; ++t) {  // K_0, V_0, K_1, V_1, ...
         const int slot = t % 3, ph = (t / 3) & 1;
         mbar_wait(smem_u32(r_empty + slot), ph ^ 1);
@@ -507,7 +513,7 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
     const int x = (int)(warp - 4) / 4;  // 0: tile a, 1: tile b
     const uint32_t quad = (warp - 4) & 3;
     const int r = quad * 32 + lane;
-    const int qblk = q_lo + x;
+    const int qblk = x ? q_hi : q_lo;
     const int qrow = qblk * 128 + r;
     const int nblk = qblk + 1;
     const uint32_t lane_base = tmem + ((quad * 32) << 16);
@@ -1535,6 +1541,14 @@ int launch_fwd(const void* qkv, long long ld_qkv, int heads, int seq, long long 
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
+int attn_sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      n <= 0)
+    n = 148;
+  return n;
+}
+
 template <int HD>
 int launch_fwd2(const void* qkv, long long ld_qkv, int heads, int seq, long long head_base, float alpha,
                 uint64_t seed, uint32_t thresh16, float drop_scale, void* out, long long ld_out, float* lse,
@@ -1566,6 +1580,11 @@ int launch_fwd2(const void* qkv, long long ld_qkv, int heads, int seq, long long
     const char* e = getenv("MT_ATTN_FWD_GROUP_HEADS");
     const int g = e ? atoi(e) : 0;
     p.group_heads = (g <= 0 || g > heads) ? heads : g;
+    // MT_ATTN_FWD_BALANCED=0/1 forces the pairing; default: balanced pairs when the CTAs fit one wave
+    // (GPT-3 TP=8, 12 heads: 87.7 -> 74.2 us; from 24 heads on adjacent pairs win: 92 vs 130 us,
+    // profiles/r02_attn_balanced_ab.log)
+    const char* b = getenv("MT_ATTN_FWD_BALANCED");
+    p.balanced = b && b[0] ? (b[0] == '1') : (heads * (p.nqb / 2) <= attn_sm_count());
   }
   attn_fwd2_kernel<HD><<<heads * (p.nqb / 2), kFwd2Threads, C::kSmem, s>>>(mq, mk, mv, p);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;

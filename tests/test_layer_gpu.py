@@ -91,8 +91,10 @@ def test_layer_matches_oracle(hidden, heads, seq, mb, p, fused, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{"MT_ATTN_BWD_WG": "1"}, {"MT_HIDDEN_KEEP": "0"}, {"MT_ATTN_GROUP_HEADS": "0"},
-                                 {"MT_ATTN_GROUP_HEADS": "3", "MT_ATTN_FWD_GROUP_HEADS": "3"}],
-                         ids=["one_softmax_warpgroup", "rehash_hidden_dropout", "ungrouped_order", "groups_of_3"])
+                                 {"MT_ATTN_GROUP_HEADS": "3", "MT_ATTN_FWD_GROUP_HEADS": "3"},
+                                 {"MT_ATTN_FWD_BALANCED": "1"}, {"MT_ATTN_FWD_BALANCED": "0"}],
+                         ids=["one_softmax_warpgroup", "rehash_hidden_dropout", "ungrouped_order", "groups_of_3",
+                              "balanced_pairs", "adjacent_pairs"])
 def test_runtime_switch_variants_match_oracle(env, monkeypatch):
     """The non-default variants behind the runtime switches against the oracle: one
     softmax warpgroup in the fused backward kernels, the backward re-hashing the hidden-dropout mask
@@ -129,14 +131,16 @@ def _layer_outputs(hidden, heads, seq, mb, p):
     return res
 
 
-@pytest.mark.parametrize("env", [{"MT_HIDDEN_KEEP": "0"}, {"MT_ATTN_FWD_GROUP_HEADS": "3"}],
-                         ids=["rehashed_hidden_mask", "forward_launch_groups"])
+@pytest.mark.parametrize("env", [{"MT_HIDDEN_KEEP": "0"}, {"MT_ATTN_FWD_GROUP_HEADS": "3"},
+                                 {"MT_ATTN_FWD_BALANCED": "1"}],
+                         ids=["rehashed_hidden_mask", "forward_launch_groups", "forward_balanced_pairs"])
 def test_switch_variants_are_bit_identical(env, monkeypatch):
     """Variants that must not change a single bit: the backward's hidden-dropout mask read from the
     forward's keep bytes vs re-hashed from the counter-based stream, and the forward attention's launch
     order. Deterministic path (MT_ATTN_BWD2=0: no dQ atomics), so every output and gradient is compared
     bitwise."""
     monkeypatch.setenv("MT_ATTN_BWD2", "0")
+    monkeypatch.setenv("MT_ATTN_FWD_BALANCED", "0")
     base = _layer_outputs(1024, 8, 256, 1, 0.1)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
