@@ -1625,9 +1625,11 @@ int launch_bwd(const void* qkv, long long ld_qkv, const void* ctx, const void* d
   p.ld_dq = ld_qkv;
   p.mask = mask;
   {
-    // groups of 8 heads: DRAM 1.80 -> 0.50 GB, 582 -> 550 us (GPT-3 layer, profiles/r02_attn_group_ab.log)
+    // groups of 8 heads for launches of >= 5 waves: DRAM 1.80 -> 0.50 GB, 582 -> 550 us (GPT-3 layer,
+    // 96 heads; 48 heads 288 -> 284 us); shorter launches get group tails (24 heads: 157 -> 181 us),
+    // so they keep one group (profiles/r02_attn_group_ab.log, r02_attn_group_tp8_ab.log)
     const char* e = getenv("MT_ATTN_GROUP_HEADS");  // 0: one group (all heads)
-    const int g = e ? atoi(e) : 8;
+    const int g = e ? atoi(e) : (heads * p.nqb >= 5 * attn_sm_count() ? 8 : 0);
     p.group_heads = (g <= 0 || g > heads) ? heads : g;
   }
   constexpr int kSmemKV = 1024 + 4 * C::kTileBytes + C::kMBytes + 256;
